@@ -1,0 +1,210 @@
+"""fp64 CPU ORACLE for the VarGrad trajectory-balance loss head (TBA, arXiv 2503.18929).
+
+TEST INFRASTRUCTURE ONLY. Nothing on the product path may import, call or execute this
+module: only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+leg / ``--impl reference`` arm use it. It shares no code with the CUDA path (it imports
+only NumPy and the standard library); inputs come from ``tba_synth`` (which holds no
+arithmetic of the method) or from the tests themselves.
+
+Citations: ``P:L`` = /root/reference/PAPER.md line L (LaTeX source of the paper),
+``S:L`` = SPEC.md line L. Equation numbers are by LaTeX environment count:
+Eq. 2 ``eq:opt_policy`` P:99-102, Eq. 4 ``eq:logZ`` P:122-130, Eq. 5 ``eq:vargrad``
+P:132-141, Eq. 7 ``eq:tba_update`` P:159-176, Appendix A (gradient) P:420-477.
+
+Notation: sequences s = i*K + j (group-major); rows (s, t); z a logits
+row; y the sampled token; mu the response mask; ell_s = log pi_theta(y_s | x);
+rho_s = log pi_ref(y_s | x); r_s = r_phi(y_s; x).
+
+What the method computes is its definition (Eqs. 4-5 and their exact gradient); there is
+no approximation to reproduce, so this file is that definition written out in fp64, in
+the paper's order, with no blocking, fusion or reordering.
+
+Pins (tests/test_oracle.py): worked values of S:52, S:53, S:70, S:133, S:143, S:152;
+the closed form log Z = log(0.5e + 0.5) at pi_theta = pi* (Eq. 2); softmax rows sum to 1
+within 1e-12; shift invariance; scipy's logsumexp; brute-force products of
+probabilities; L = mean within-group population variance; per-group shift invariance;
+the independent Appendix-A advantage form; central finite differences of the loss.
+Every function below is pinned by at least one of them ("parity unpinned": none).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+# ----------------------------------------------------------------------------- a1
+def log_softmax_row(z: np.ndarray) -> tuple[np.ndarray, float]:
+    """log softmax of one logits row in fp64, max-subtracted ("numerically stable").
+
+    Returns (log-probabilities [V], lse). The sum over the vocabulary is NumPy's
+    pairwise summation in fp64 (sequential fp64 could breach the
+    1e-12 row-sum pin at V = 152064). A row with no finite entry has lse = -inf.
+    """
+    z = np.asarray(z, dtype=np.float64)
+    m = np.max(z)
+    if not np.isfinite(m):
+        if m == -np.inf:
+            return np.full(z.shape, np.nan), -np.inf
+        return np.full(z.shape, np.nan), np.nan
+    lse = m + math.log(np.sum(np.exp(z - m)))
+    return z - lse, lse
+
+
+def token_logprob(z: np.ndarray, y: int) -> tuple[float, float]:
+    """log softmax(z)[y] and the row's lse (paper: the per-token factor of
+    log pi_theta(y|x) in Eqs. 4-5)."""
+    V = len(z)
+    if not (0 <= y < V):
+        raise ValueError(f"token {y} out of range [0, {V})")  # S:50 invalid-input
+    lp, lse = log_softmax_row(z)
+    return float(lp[y]), lse
+
+
+# ----------------------------------------------------------------------------- a2
+def seq_logprob(logits: np.ndarray, tokens: np.ndarray, mask: np.ndarray):
+    """ell_s = sum_t mu_{s,t} log softmax(z_{s,t})[y_{s,t}] and n_tok_s = sum_t mu_{s,t}.
+
+    logits [N, T, V] (fp64-convertible), tokens [N, T] int, mask [N, T] 0/1. Tokens at
+    masked positions are ignored (reading R5). The sum over t uses
+    ``math.fsum`` (exact). Returns (ell [N] fp64, n_tok [N] int64, lse [N, T] fp64 with
+    NaN at masked positions)."""
+    N, T = tokens.shape
+    ell = np.zeros(N, dtype=np.float64)
+    ntok = np.zeros(N, dtype=np.int64)
+    lse = np.full((N, T), np.nan)
+    for s in range(N):
+        terms = []
+        for t in range(T):
+            if mask[s, t]:
+                lp, lse[s, t] = token_logprob(logits[s, t], int(tokens[s, t]))
+                terms.append(lp)
+        ell[s] = math.fsum(terms)
+        ntok[s] = len(terms)
+    return ell, ntok, lse
+
+
+# ----------------------------------------------------------------------------- a3
+def _check_config(N: int, beta: float, K: int):
+    if not (math.isfinite(beta) and beta > 0):
+        raise ValueError("invalid-config: beta must be finite and > 0 (S:131)")
+    if K < 2:
+        raise ValueError("invalid-config: K must be >= 2 (S:140)")
+    if N % K:
+        raise ValueError("invalid-arg: N must be a multiple of K")
+
+
+def log_z_hat(ell, ref_logp, log_reward, beta: float, K: int) -> np.ndarray:
+    """Eq. 4: log Z(x_i) = (1/K) sum_j (log pi_ref - log pi_theta + r/beta).
+
+    Inputs are per-sequence in group-major order (s = i*K + j). Returns [B] fp64."""
+    ell = np.asarray(ell, np.float64)
+    _check_config(len(ell), beta, K)
+    delta = np.asarray(ref_logp, np.float64) - ell + np.asarray(log_reward, np.float64) / beta
+    B = len(ell) // K
+    return np.array([math.fsum(delta[i * K:(i + 1) * K]) / K for i in range(B)])
+
+
+def vargrad_tb_loss(ell, ref_logp, log_reward, beta: float, K: int, n_global: int | None = None):
+    """Eq. 5: L = 1/(BK) sum_ij (SG[log Z_i] + log pi_theta - log pi_ref - r/beta)^2.
+
+    Returns (L, log_z [B], eps [N]) with eps_s = log Z_i + ell_s - rho_s - r_s/beta, the
+    residual inside the square. ``n_global`` replaces BK when this batch is one shard
+    of a larger one (reading R2); default BK = len(ell)."""
+    ell = np.asarray(ell, np.float64)
+    N = len(ell)
+    logz = log_z_hat(ell, ref_logp, log_reward, beta, K)
+    eps = np.empty(N)
+    for s in range(N):
+        i = s // K
+        eps[s] = logz[i] + ell[s] - float(ref_logp[s]) - float(log_reward[s]) / beta
+    n = N if n_global is None else n_global
+    loss = math.fsum(eps * eps) / n
+    return loss, logz, eps
+
+
+def advantages(ell, ref_logp, log_reward, beta: float, K: int) -> np.ndarray:
+    """Appendix A: A_ij = (r_ij - rbar_i) - beta (KL_ij - KLbar_i), with
+    KL_ij = log pi_theta - log pi_ref. Independent of ``vargrad_tb_loss``; used to pin the
+    residual through the identity A = -beta * eps."""
+    ell = np.asarray(ell, np.float64)
+    _check_config(len(ell), beta, K)
+    r = np.asarray(log_reward, np.float64)
+    kl = ell - np.asarray(ref_logp, np.float64)
+    A = np.empty_like(ell)
+    for i in range(len(ell) // K):
+        sl = slice(i * K, (i + 1) * K)
+        A[sl] = (r[sl] - r[sl].mean()) - beta * (kl[sl] - kl[sl].mean())
+    return A
+
+
+# ----------------------------------------------------------------------------- a5
+def grad_logprob_row(z: np.ndarray, y: int) -> np.ndarray:
+    """d log softmax(z)[y] / dz = onehot(y) - softmax(z)."""
+    lp, _ = log_softmax_row(z)
+    g = -np.exp(lp)
+    g[y] += 1.0
+    return g
+
+
+def dlogits(logits, tokens, mask, eps, n_global: int, grad_out: float = 1.0) -> np.ndarray:
+    """dL/dz for Eq. 5 (Appendix A: grad L = (1/BK) sum -2(...) grad log pi, the
+    bracket being -eps):  dz_{s,t,v} = mu_{s,t} * (2 eps_s / N) * grad_out * (1[v = y] - p_v).
+
+    Masked rows are exactly 0. Returns fp64 [N, T, V]."""
+    N, T = tokens.shape
+    V = logits.shape[-1]
+    out = np.zeros((N, T, V), dtype=np.float64)
+    for s in range(N):
+        g = 2.0 * float(eps[s]) / n_global * grad_out
+        for t in range(T):
+            if mask[s, t]:
+                out[s, t] = g * grad_logprob_row(logits[s, t], int(tokens[s, t]))
+    return out
+
+
+def dlogits_row(z, y: int, eps_s: float, n_global: int, grad_out: float = 1.0) -> np.ndarray:
+    """One valid row of ``dlogits`` (for sampled-row comparison at full size)."""
+    return 2.0 * eps_s / n_global * grad_out * grad_logprob_row(z, y)
+
+
+# ----------------------------------------------------------------------------- full head
+def vargrad_head(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int,
+                 n_global: int | None = None, grad_out: float = 1.0, want_grad: bool = True):
+    """Steps a1-a5 of SURVEY §8(a) on one (shard of a) batch. Returns a dict with
+    ell, n_tok, log_z, eps, loss (normalised by n_global), partial = [sum eps^2 / n_global,
+    N, B], and dlogits (fp64) if requested."""
+    ell, ntok, lse = seq_logprob(logits, tokens, mask)
+    N = len(ell)
+    n = N if n_global is None else n_global
+    loss, logz, eps = vargrad_tb_loss(ell, ref_logp, log_reward, beta, K, n)
+    out = dict(ell=ell, n_tok=ntok, lse=lse, log_z=logz, eps=eps, loss=loss,
+               partial=np.array([loss, float(N), float(N // K)]))
+    if want_grad:
+        out["dlogits"] = dlogits(logits, tokens, mask, eps, n, grad_out)
+    return out
+
+
+# ----------------------------------------------------------------------------- bf16
+def round_bf16(x) -> np.ndarray:
+    """Round fp64 values to the nearest bf16 value (ties to even), returned as fp64.
+
+    bf16 has 8 significant bits and fp32's exponent range; below 2^-126 the spacing is
+    fixed at 2^-133 (subnormals). Overflow is not handled (|x| < 3e38 assumed)."""
+    x = np.asarray(x, dtype=np.float64)
+    out = np.zeros_like(x)
+    nz = (x != 0) & np.isfinite(x)
+    _, e = np.frexp(x[nz])                 # x = f * 2^e, 0.5 <= |f| < 1
+    e = np.maximum(e, -125)                # subnormal range: fixed ulp 2^-133
+    ulp = np.ldexp(1.0, e - 8)
+    out[nz] = np.rint(x[nz] / ulp) * ulp   # rint = round half to even; /ulp is exact
+    out[~np.isfinite(x)] = x[~np.isfinite(x)]
+    return out
+
+
+def bf16_ulp(x) -> np.ndarray:
+    """Spacing of bf16 values at |x| (for the 1-ulp dlogits tolerance)."""
+    x = np.abs(np.asarray(x, dtype=np.float64))
+    _, e = np.frexp(np.where(x > 0, x, 1.0))
+    e = np.where(x > 0, np.maximum(e, -125), -125)
+    return np.ldexp(1.0, e - 8)

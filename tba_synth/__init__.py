@@ -1,0 +1,246 @@
+"""Seeded synthetic inputs for the VarGrad TB-loss head — shared by the oracle and the CUDA path.
+
+This module is the ONLY code both sides use. It holds no arithmetic of the method
+(no softmax, no log-probabilities, no loss): just an integer counter-based hash,
+the recipe that turns hash bits into logits/tokens/masks/rewards, and the workload
+presets. Its CUDA twin (``tba_synth/csrc/synth.cu`` -> ``libtba_synth.so``) produces
+bit-identical logits on the device for the sizes the host cannot hold.
+
+Recipe (DESIGN.md §"Input recipe"):
+
+* hash: SplitMix64 finaliser, counter-based. ``key(seed, stream)`` selects an
+  independent stream; element ``i`` of a stream is ``mix64(key + (i+1)*GAMMA)``,
+  i.e. the i-th output of a SplitMix64 generator started at ``key``.
+* logits: ``z = (u0+u1+u2+u3 - 131070) * 2^-14`` with ``u_k`` the four 16-bit
+  fields of one hash (Irwin–Hall, ~N(0, 2.31^2), |z| <= 8, exact in fp32); the row's
+  sampled token gets a peak ``z[y] += b``, ``b in {0,4,8,12}`` (fp32 add, exact);
+  bf16 by integer round-to-nearest-even of the fp32 bits. Index = row*V + v, so the
+  content does not depend on the row stride; padding columns hold NaN (0x7FC0 /
+  0x7FC00000) to prove they are never read.
+* tokens: ``y = mulhi(h, V)``; masked positions carry -1 (any value is legal there).
+* masks: prefix masks of length ``L_s`` (full T, or uniform on [lo, hi]).
+* ref_logp: ``e_V * L_s + U(-20, 20)`` with ``e_V = 6 - (ln V + 2.65)``; log_reward per
+  task (binary correctness / reward-model score / sparse red-team log-reward / U(0,1)).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+GAMMA = 0x9E3779B97F4A7C15
+MUL1 = 0xBF58476D1CE4E5B9
+MUL2 = 0x94D049BB133111EB
+STREAM_MUL = 0xD1B54A32D192ED03
+
+# stream ids (must match tba_synth/csrc/synth.cu)
+S_LOGITS, S_TOKENS, S_PEAK, S_LEN, S_REF, S_REWARD, S_BERN = 1, 2, 3, 4, 5, 6, 7
+
+BF16_NAN = 0x7FC0
+F32_NAN_BITS = 0x7FC00000
+
+
+# ----------------------------------------------------------------------------- hash
+def mix64_scalar(z: int) -> int:
+    z &= M64
+    z = ((z ^ (z >> 30)) * MUL1) & M64
+    z = ((z ^ (z >> 27)) * MUL2) & M64
+    return z ^ (z >> 31)
+
+
+def splitmix64_scalar(state: int, i: int) -> int:
+    """i-th (0-based) output of SplitMix64 started at ``state`` (pure-Python ints)."""
+    return mix64_scalar((state + (i + 1) * GAMMA) & M64)
+
+
+def stream_key(seed: int, stream: int) -> int:
+    return mix64_scalar(mix64_scalar((seed + GAMMA) & M64) ^ ((stream * STREAM_MUL) & M64))
+
+
+def _mix64(z: np.ndarray) -> np.ndarray:
+    z = z.astype(np.uint64, copy=True)
+    z ^= z >> np.uint64(30)
+    z *= np.uint64(MUL1)
+    z ^= z >> np.uint64(27)
+    z *= np.uint64(MUL2)
+    z ^= z >> np.uint64(31)
+    return z
+
+
+def hash64(seed: int, stream: int, idx) -> np.ndarray:
+    """Vectorised counter hash: element ``idx`` of stream ``stream`` under ``seed``."""
+    key = np.uint64(stream_key(seed, stream))
+    i = np.asarray(idx, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return _mix64(key + (i + np.uint64(1)) * np.uint64(GAMMA))
+
+
+def mulhi_u64(h: np.ndarray, n: int) -> np.ndarray:
+    """floor(h * n / 2^64) for uint64 h and 0 < n < 2^32, exact."""
+    assert 0 < n < (1 << 32)
+    h = np.asarray(h, dtype=np.uint64)
+    hi = h >> np.uint64(32)
+    lo = h & np.uint64(0xFFFFFFFF)
+    nn = np.uint64(n)
+    return (hi * nn + ((lo * nn) >> np.uint64(32))) >> np.uint64(32)
+
+
+def unit24(h: np.ndarray) -> np.ndarray:
+    """Top 24 bits of the hash as a float64 in [0, 1) (exact in fp32 as well)."""
+    return (np.asarray(h, dtype=np.uint64) >> np.uint64(40)).astype(np.float64) * (2.0 ** -24)
+
+
+# ----------------------------------------------------------------------------- bf16
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16, by integer arithmetic on the bit pattern
+    (finite inputs only)."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = (b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)
+    return r.astype(np.uint16)
+
+
+def bf16_bits_to_f64(b: np.ndarray) -> np.ndarray:
+    return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+# ----------------------------------------------------------------------------- presets
+@dataclasses.dataclass(frozen=True)
+class Workload:
+    name: str
+    B: int               # prompt groups
+    K: int               # samples per prompt
+    T: int               # padded response length
+    V: int               # vocabulary
+    dtype: str           # "bf16" | "fp32" logits (and dlogits)
+    beta: float
+    len_lo: int          # response length L_s ~ U{len_lo..len_hi} (== T for full masks)
+    len_hi: int
+    reward: str          # "binary" | "rm" | "redteam" | "unit"
+    note: str = ""
+
+    @property
+    def N(self) -> int:
+        return self.B * self.K
+
+    def with_groups(self, B: int) -> "Workload":
+        return dataclasses.replace(self, B=B)
+
+
+# BASELINE.json configs; paper anchors in DESIGN.md (§ Input recipe)
+WORKLOADS = {
+    "toy": Workload("toy", 2, 4, 16, 1000, "fp32", 1.0, 16, 16, "unit",
+                    "toy VarGrad TB: 2x4, T=16, V=1000, beta=1, fp32 logits"),
+    "pythia": Workload("pythia", 64, 4, 53, 50304, "bf16", 0.05, 53, 53, "rm",
+                       "Pythia-410M TL;DR: V=50304, 53-token responses, 64x4"),
+    "rhomath": Workload("rhomath", 32, 20, 512, 32000, "bf16", 0.012, 64, 512, "binary",
+                        "RhoMath-1B GSM8K: V=32000, <=512-token responses, 32x20"),
+    "redteam": Workload("redteam", 128, 8, 20, 50257, "bf16", 0.05, 20, 20, "redteam",
+                        "GPT-2 red-teaming: V=50257, 20 tokens, 128x8, sparse log-rewards"),
+    "qwen": Workload("qwen", 64, 8, 1024, 152064, "bf16", 0.005, 1024, 1024, "binary",
+                     "Qwen2.5-7B MATH: V=152064, 1024 tokens, 64x8 (sharded by group over 8 GPUs)"),
+}
+# The per-GPU shard of the Qwen batch at 8xB200 (8 of the 64 groups).
+WORKLOADS["qwen_shard"] = dataclasses.replace(WORKLOADS["qwen"], name="qwen_shard", B=8,
+                                              note="Qwen2.5-7B MATH per-GPU shard: 8 groups x K=8, T=1024, V=152064")
+
+
+# ----------------------------------------------------------------------------- generators
+def seq_lengths(w: Workload, seed: int, seq0: int = 0, n: int | None = None) -> np.ndarray:
+    """Response lengths L_s for global sequences seq0 .. seq0+n-1."""
+    n = w.N if n is None else n
+    s = np.arange(seq0, seq0 + n, dtype=np.uint64)
+    if w.len_lo == w.len_hi:
+        return np.full(n, w.len_hi, dtype=np.int64)
+    span = w.len_hi - w.len_lo + 1
+    return (w.len_lo + mulhi_u64(hash64(seed, S_LEN, s), span)).astype(np.int64)
+
+
+def raw_tokens(seed: int, V: int, rows) -> np.ndarray:
+    """The sampled token of each global row (also where the logit peak sits)."""
+    return mulhi_u64(hash64(seed, S_TOKENS, rows), V).astype(np.int64)
+
+
+def peak_of(seed: int, rows) -> np.ndarray:
+    return (4 * (hash64(seed, S_PEAK, rows) & np.uint64(3))).astype(np.float32)
+
+
+def tokens_and_mask(w: Workload, seed: int, seq0: int = 0, n: int | None = None):
+    """tokens int64 [n, T] (-1 where masked) and mask uint8 [n, T] (prefix masks)."""
+    n = w.N if n is None else n
+    L = seq_lengths(w, seed, seq0, n)
+    t = np.arange(w.T, dtype=np.int64)
+    mask = (t[None, :] < L[:, None]).astype(np.uint8)
+    rows = (np.arange(seq0, seq0 + n, dtype=np.int64)[:, None] * w.T + t[None, :]).astype(np.uint64)
+    tok = raw_tokens(seed, w.V, rows)
+    tok = np.where(mask == 1, tok, -1).astype(np.int64)
+    return tok, mask
+
+
+def logits_rows_f32(seed: int, V: int, rows) -> np.ndarray:
+    """fp32 logits (before any bf16 rounding) for the given global rows: [len(rows), V]."""
+    rows = np.asarray(rows, dtype=np.uint64).reshape(-1)
+    idx = rows[:, None] * np.uint64(V) + np.arange(V, dtype=np.uint64)[None, :]
+    h = hash64(seed, S_LOGITS, idx)
+    acc = np.zeros(h.shape, dtype=np.int64)
+    for k in range(4):
+        acc += ((h >> np.uint64(16 * k)) & np.uint64(0xFFFF)).astype(np.int64)
+    z = ((acc - 131070).astype(np.float64) * (2.0 ** -14)).astype(np.float32)
+    y = raw_tokens(seed, V, rows)
+    b = peak_of(seed, rows)
+    r = np.arange(len(rows))
+    z[r, y] = (z[r, y] + b).astype(np.float32)
+    return z
+
+
+def logits_rows(seed: int, V: int, rows, dtype: str) -> np.ndarray:
+    """Logits rows exactly as stored on the device: uint16 bf16 bits or fp32."""
+    z = logits_rows_f32(seed, V, rows)
+    if dtype == "bf16":
+        return f32_to_bf16_bits(z)
+    return z
+
+
+def logits_rows_f64(seed: int, V: int, rows, dtype: str) -> np.ndarray:
+    """The stored logits converted exactly to fp64 (what the oracle consumes)."""
+    z = logits_rows(seed, V, rows, dtype)
+    if dtype == "bf16":
+        return bf16_bits_to_f64(z)
+    return z.astype(np.float64)
+
+
+def ref_logp(w: Workload, seed: int, seq0: int = 0, n: int | None = None) -> np.ndarray:
+    """Per-sequence reference log-prob: e_V * L_s + U(-20, 20), fp32-representable."""
+    n = w.N if n is None else n
+    L = seq_lengths(w, seed, seq0, n)
+    e_v = 6.0 - (math.log(w.V) + 2.65)
+    u = unit24(hash64(seed, S_REF, np.arange(seq0, seq0 + n, dtype=np.uint64)))
+    return (e_v * L + (-20.0 + 40.0 * u)).astype(np.float32).astype(np.float64)
+
+
+def log_reward(w: Workload, seed: int, seq0: int = 0, n: int | None = None) -> np.ndarray:
+    """Per-sequence r_phi (the log of the tilt exp(r_phi), paper Eq. 2), fp32-representable."""
+    n = w.N if n is None else n
+    s = np.arange(seq0, seq0 + n, dtype=np.uint64)
+    u = unit24(hash64(seed, S_REWARD, s))
+    if w.reward == "binary":          # correctness reward r in {0, 1}
+        r = (hash64(seed, S_BERN, s) >> np.uint64(63)).astype(np.float64)
+    elif w.reward == "rm":            # reward-model score
+        r = -4.0 + 8.0 * u
+    elif w.reward == "redteam":       # sparse log-rewards: 90% U(-12,-4), 10% U(-0.7,0)
+        sel = mulhi_u64(hash64(seed, S_BERN, s), 10) == 0
+        r = np.where(sel, -0.7 + 0.7 * u, -12.0 + 8.0 * u)
+    elif w.reward == "unit":
+        r = u
+    else:
+        raise ValueError(w.reward)
+    return r.astype(np.float32).astype(np.float64)
+
+
+def group_inputs(w: Workload, seed: int, g0: int, ng: int):
+    """Everything except logits for groups g0..g0+ng-1 (global group indices)."""
+    s0, n = g0 * w.K, ng * w.K
+    tok, mask = tokens_and_mask(w, seed, s0, n)
+    return dict(tokens=tok, mask=mask, ref_logp=ref_logp(w, seed, s0, n),
+                log_reward=log_reward(w, seed, s0, n))

@@ -1,0 +1,77 @@
+// CUDA twin of tba_synth (the seeded input generator). Bit-identical to the NumPy twin in
+// tba_synth/__init__.py: same SplitMix64 counter hash, same Irwin-Hall logits, same peak,
+// same integer round-to-nearest-even to bf16. Holds none of the method's arithmetic; it only
+// fills device buffers with synthetic logits so that 20 GB inputs need not cross PCIe.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace {
+
+constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t hash_at(uint64_t key, uint64_t i) { return mix64(key + (i + 1) * GAMMA); }
+
+__device__ __forceinline__ float irwin_hall(uint64_t h) {
+  int64_t acc = (int64_t)(h & 0xFFFF) + (int64_t)((h >> 16) & 0xFFFF) + (int64_t)((h >> 32) & 0xFFFF) +
+                (int64_t)((h >> 48) & 0xFFFF) - 131070;
+  return (float)((double)acc * (1.0 / 16384.0));
+}
+
+__device__ __forceinline__ uint16_t bf16_rne(float x) {
+  uint32_t b = __float_as_uint(x);
+  return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+
+template <bool BF16>
+__global__ void synth_logits_kernel(void* out, uint64_t key_logits, uint64_t key_tok, uint64_t key_peak,
+                                    int64_t row0, int64_t nrows, int64_t V, int64_t row_stride) {
+  for (int64_t r = blockIdx.y; r < nrows; r += gridDim.y) {
+    const uint64_t grow = (uint64_t)(row0 + r);
+    const uint64_t y = __umul64hi(hash_at(key_tok, grow), (uint64_t)V);
+    const float peak = (float)(4 * (int)(hash_at(key_peak, grow) & 3ull));
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < row_stride;
+         c += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t o = r * row_stride + c;
+      if (c >= V) {
+        if (BF16) ((uint16_t*)out)[o] = 0x7FC0u;
+        else ((uint32_t*)out)[o] = 0x7FC00000u;
+        continue;
+      }
+      float z = irwin_hall(hash_at(key_logits, grow * (uint64_t)V + (uint64_t)c));
+      if ((uint64_t)c == y) z = z + peak;
+      if (BF16) ((uint16_t*)out)[o] = bf16_rne(z);
+      else ((float*)out)[o] = z;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// Fill rows [row0, row0+nrows) (global row ids) of a logits buffer laid out as
+// [nrows, row_stride] elements; columns >= V get NaN. dtype 0 = bf16, 1 = fp32.
+// Keys are tba_synth.stream_key(seed, S_LOGITS/S_TOKENS/S_PEAK). Returns 0 or a cudaError_t.
+int tba_synth_logits(void* out, int dtype, uint64_t key_logits, uint64_t key_tok, uint64_t key_peak,
+                     int64_t row0, int64_t nrows, int64_t V, int64_t row_stride, cudaStream_t stream) {
+  if (!out || nrows < 0 || V <= 0 || row_stride < V || (dtype != 0 && dtype != 1)) return 1;
+  if (nrows == 0) return 0;
+  dim3 block(256);
+  int64_t gx = (row_stride + 255) / 256;
+  if (gx > 64) gx = 64;
+  int64_t gy = nrows < 16384 ? nrows : 16384;
+  dim3 grid((unsigned)gx, (unsigned)gy);
+  if (dtype == 0)
+    synth_logits_kernel<true><<<grid, block, 0, stream>>>(out, key_logits, key_tok, key_peak, row0, nrows, V, row_stride);
+  else
+    synth_logits_kernel<false><<<grid, block, 0, stream>>>(out, key_logits, key_tok, key_peak, row0, nrows, V, row_stride);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"
