@@ -1,0 +1,115 @@
+/*
+ * tba.h — C ABI of libtba.so: the VarGrad trajectory-balance loss head of
+ * "Trajectory Balance with Asynchrony" (TBA, arXiv 2503.18929), hand-written CUDA for
+ * B200 (sm_100a).
+ *
+ * Citations: P:L = PAPER.md line L (the paper's LaTeX source), S:L = SPEC.md line L.
+ *   Eq. 4  (eq:logZ,    P:122-130)  log Z(x_i) = 1/K sum_j (log pi_ref - log pi_theta + r_phi/beta)
+ *   Eq. 5  (eq:vargrad)  L = 1/(BK) sum_ij (SG[log Z_i] + log pi_theta - log pi_ref - r_phi/beta)^2
+ *   App. A              grad L = 1/(BK) sum_ij -2(...) grad log pi_theta
+ *   log pi_theta(y|x) = sum_t log softmax(z_t)[y_t]  ("parallel likelihood evaluation of an
+ *   entire sequence through a single forward pass")
+ *
+ * Layout. N = n_seq sequences, group-major: sequence s = i*K + j is sample j
+ * of prompt i (the paper's B queries x K responses). Row (s, t) = s*seq_len + t.
+ *   logits  : row (s,t) starts at logits + ((s*seq_len + t) * row_stride) elements;
+ *             elements [0, vocab) are read, the padding [vocab, row_stride) never is.
+ *   tokens  : int64 [N, seq_len], the sampled token y_{s,t}; ignored where mask == 0
+ *             (may hold -1 / -100 / garbage there).
+ *   mask    : uint8 [N, seq_len], 0/1 response mask mu_{s,t}.
+ * All pointers are caller-owned DEVICE memory unless stated otherwise; the library never
+ * allocates, frees or synchronises. Every call is stream-ordered on `stream` (NULL = the
+ * legacy default stream) and reentrant (no global mutable state; "pure functions").
+ *
+ * Errors. Host-side validation happens before any CUDA call and returns synchronously:
+ *   TBA_ERR_INVALID_ARG    null pointer, negative size, row_stride < vocab, n_seq % K != 0,
+ *                          unknown dtype, misaligned pointer, 64-bit size overflow;
+ *   TBA_ERR_INVALID_CONFIG beta <= 0 or non-finite, K < 2;
+ *   TBA_ERR_CUDA           a launch failed (cudaGetLastError()).
+ * Device-side conditions are reported asynchronously by atomicOr into *dev_status
+ * (nullable): TBA_DEV_TOKEN_RANGE — a token outside [0, vocab) at a valid position (S:50
+ * invalid-input; that row's log-prob becomes NaN); TBA_DEV_NONFINITE_ROW — a valid row with
+ * no finite maximum or a non-finite sum (e.g. all -inf, +inf or NaN logits).
+ */
+#ifndef TBA_H
+#define TBA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tba_stream_t; /* == cudaStream_t */
+
+enum tba_status { TBA_OK = 0, TBA_ERR_INVALID_ARG = 1, TBA_ERR_INVALID_CONFIG = 2, TBA_ERR_CUDA = 3 };
+enum tba_dev_status { TBA_DEV_TOKEN_RANGE = 1, TBA_DEV_NONFINITE_ROW = 2 };
+enum tba_dtype { TBA_BF16 = 0, TBA_FP32 = 1 };
+
+#define TBA_ABI_VERSION 1
+
+/* The rows the head reads. All fields describe caller-owned device memory. */
+typedef struct tba_rows {
+  const void*    logits;      /* [n_seq, seq_len, row_stride] of `dtype`; 2-byte (bf16) / 4-byte aligned */
+  int32_t        dtype;       /* TBA_BF16 or TBA_FP32 */
+  int32_t        _pad;
+  int64_t        n_seq;       /* N >= 0 */
+  int64_t        seq_len;     /* T >= 0 */
+  int64_t        vocab;       /* V >= 1 */
+  int64_t        row_stride;  /* elements between consecutive rows, >= V */
+  const int64_t* tokens;      /* [n_seq, seq_len] */
+  const uint8_t* mask;        /* [n_seq, seq_len] */
+} tba_rows;
+
+int         tba_abi_version(void);
+const char* tba_status_string(int code);
+
+/* Bytes of device workspace the calls below need for N sequences of T rows: per-row
+ * statistics (log2-domain max and log2 of the partition sum, 8 B), per-row log-prob (8 B),
+ * per-group scratch (8 B/sequence) and a counter. Caller allocates; contents need not be
+ * initialised; it must stay alive and unmodified from tba_vargrad_tb_loss_fwd until the
+ * matching tba_vargrad_tb_loss_bwd. 256-byte aligned base required. */
+size_t tba_workspace_bytes(int64_t n_seq, int64_t seq_len);
+
+/* log pi(y_s | x) for every sequence (steps a1+a2; used for pi_theta and for pi_ref).
+ *   seq_logp[s] = sum_{t: mask=1} log softmax(z_{s,t})[y_{s,t}]   (fp64, [N])
+ *   n_tokens[s] = sum_t mask[s,t]                                  (int32, [N])
+ * An all-zero mask row gives 0 and 0 (legal; reading R6). Logits are read once
+ * (2V or 4V bytes per valid row; masked rows are not read). dev_status nullable. */
+int tba_seq_logprob(const tba_rows* x, void* workspace, double* seq_logp, int32_t* n_tokens,
+                    int32_t* dev_status, tba_stream_t stream);
+
+/* Forward of the VarGrad TB loss over this call's groups (steps a1-a3), Eqs. 4-5.
+ *   ref_logp[s]   = log pi_ref(y_s|x)  (fp64, [N]; e.g. from tba_seq_logprob on pi_ref logits)
+ *   log_reward[s] = r_phi(y_s; x)       (fp64, [N]; the paper's r_phi, divided by beta here)
+ *   beta > 0, K >= 2, n_seq % K == 0; n_seq_global = BK of the WHOLE batch (>= n_seq) —
+ *   the 1/(BK) of Eq. 5, so that shards of one batch compose exactly.
+ * Outputs (device, fp64 unless noted):
+ *   seq_logp [N], n_tokens [N] (int32)   as tba_seq_logprob
+ *   log_z    [N/K]  Eq. 4 (detached: STOP-GRAD)
+ *   resid    [N]    eps_s = log_z_i + seq_logp_s - ref_logp_s - log_reward_s/beta (Eq. 5 bracket)
+ *   partial  [3]    { sum_s eps_s^2 / n_seq_global, n_seq, n_seq/K }  — sum over ranks
+ *                   (one allreduce) gives { L, N_global, B_global }.
+ * Deterministic (fixed-order fp64 reductions, no float atomics). */
+int tba_vargrad_tb_loss_fwd(const tba_rows* x, const double* ref_logp, const double* log_reward,
+                            double beta, int32_t K, double n_seq_global, void* workspace,
+                            double* seq_logp, int32_t* n_tokens, double* log_z, double* resid,
+                            double* partial, int32_t* dev_status, tba_stream_t stream);
+
+/* Backward (step a5): dlogits = dL/dz for L of Eq. 5, App. A:
+ *   dz_{s,t,v} = mu_{s,t} * grad_scale * g * resid_s * (1[v = y_{s,t}] - softmax(z_{s,t})_v)
+ * with g = *grad_out (device fp64 scalar; NULL means 1) and grad_scale = 2 / n_seq_global
+ * (host scalar). Reads the row statistics the matching fwd left in `workspace`. Masked rows
+ * are written with +0 and their logits are not read. Columns [vocab, dlogits_row_stride)
+ * are not written. dlogits may alias logits exactly (same pointer, dtype and stride):
+ * every element is read before it is written by the same thread.
+ * dlogits_dtype TBA_BF16 (round-to-nearest-even) or TBA_FP32. */
+int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const double* resid,
+                            double grad_scale, const double* grad_out, void* dlogits,
+                            int32_t dlogits_dtype, int64_t dlogits_row_stride, tba_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TBA_H */

@@ -1,0 +1,13 @@
+"""B200-native VarGrad trajectory-balance loss head (TBA, arXiv 2503.18929).
+
+The compute lives in libtba.so (hand-written sm_100a CUDA, C ABI in include/tba.h);
+this package only marshals PyTorch tensors into it. There is no CPU fallback: the ops
+raise if the extension is missing.
+"""
+from ._lib import TbaError, load as load_library  # noqa: F401
+from .dist import group_range, token_balanced_ranges  # noqa: F401
+from .ops import (VarGradTBLoss, make_rows, seq_logprob, vargrad_bwd, vargrad_fwd,  # noqa: F401
+                  vargrad_tb_loss, workspace_bytes)
+
+__all__ = ["seq_logprob", "vargrad_tb_loss", "VarGradTBLoss", "vargrad_fwd", "vargrad_bwd", "workspace_bytes",
+           "group_range", "token_balanced_ranges", "load_library", "TbaError"]

@@ -1,0 +1,204 @@
+"""PyTorch-facing calls over libtba.so: argument marshalling only.
+
+PyTorch supplies device memory, the current CUDA stream and (optionally) the process
+group; every step of the loss head runs in libtba.so's kernels. Names follow the C ABI
+(include/tba.h) and the paper's notation (Eqs. 4-5).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import _lib
+from ._lib import TBA_BF16, TBA_FP32, TbaRows, check
+
+_DT = {torch.bfloat16: TBA_BF16, torch.float32: TBA_FP32}
+_CHECK = os.environ.get("TBA_CHECK", "0") == "1"
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def make_rows(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor) -> TbaRows:
+    """Describe [N, T, V] logits (any row stride >= V, unit element stride), [N, T] int64
+    tokens and [N, T] uint8/bool mask as a tba_rows struct. Shape/dtype errors raise."""
+    if logits.dim() != 3:
+        raise ValueError("logits must be [N, T, V]")
+    if logits.dtype not in _DT:
+        raise ValueError(f"logits dtype {logits.dtype} unsupported (bf16 or fp32)")
+    if not logits.is_cuda:
+        raise ValueError("logits must be a CUDA tensor (there is no CPU path)")
+    N, T, V = logits.shape
+    if tokens.shape != (N, T) or mask.shape != (N, T):
+        raise ValueError("tokens and mask must be [N, T]")
+    if tokens.dtype != torch.int64 or not tokens.is_contiguous():
+        raise ValueError("tokens must be contiguous int64")
+    if mask.dtype == torch.bool:
+        mask = mask.view(torch.uint8)
+    if mask.dtype != torch.uint8 or not mask.is_contiguous():
+        raise ValueError("mask must be contiguous uint8/bool")
+    if tokens.device != logits.device or mask.device != logits.device:
+        raise ValueError("logits, tokens and mask must be on the same device")
+    if N * T > 0:
+        if logits.stride(2) != 1:
+            raise ValueError("logits must have unit stride over the vocabulary")
+        rs = logits.stride(1) if T > 1 else (logits.stride(0) if N > 1 else V)
+        if N > 1 and logits.stride(0) != T * rs:
+            raise ValueError("logits rows must be uniformly strided ([N, T] must flatten to rows)")
+        if rs < V:
+            raise ValueError("logits rows overlap (row stride < V)")
+    else:
+        rs = V
+    return TbaRows(logits.data_ptr(), _DT[logits.dtype], 0, N, T, V, rs, tokens.data_ptr(),
+                   mask.data_ptr())
+
+
+def workspace_bytes(n_seq: int, seq_len: int) -> int:
+    return int(_lib.load().tba_workspace_bytes(n_seq, seq_len))
+
+
+def _workspace(dev, N, T):
+    return torch.empty(max(workspace_bytes(N, T), 256), dtype=torch.uint8, device=dev)
+
+
+def _status(dev):
+    return torch.zeros(1, dtype=torch.int32, device=dev)
+
+
+def _raise_dev_status(st: torch.Tensor, where: str):
+    v = int(st.item())
+    if v:
+        raise ValueError(f"{where}: device status {v} (1 = token out of range, 2 = non-finite row)")
+
+
+def seq_logprob(logits, tokens, mask, *, check_status: bool = _CHECK):
+    """log pi(y_s | x) and token counts per sequence (tba_seq_logprob).
+
+    Returns (seq_logp fp64 [N], n_tokens int32 [N]). No autograd (use it for pi_ref)."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    N, T = tokens.shape
+    dev = logits.device
+    out = torch.empty(N, dtype=torch.float64, device=dev)
+    ntok = torch.empty(N, dtype=torch.int32, device=dev)
+    ws = _workspace(dev, N, T)
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_seq_logprob(ctypes.byref(x), ws.data_ptr(), out.data_ptr(), ntok.data_ptr(), _ptr(st),
+                                _stream(dev)), "tba_seq_logprob")
+    if st is not None:
+        _raise_dev_status(st, "tba_seq_logprob")
+    return out, ntok
+
+
+class _Fwd:
+    """Outputs of one tba_vargrad_tb_loss_fwd call (device tensors)."""
+
+    def __init__(self, N, K, dev):
+        self.seq_logp = torch.empty(N, dtype=torch.float64, device=dev)
+        self.n_tokens = torch.empty(N, dtype=torch.int32, device=dev)
+        self.log_z = torch.empty(max(N // K, 1), dtype=torch.float64, device=dev)[: N // K]
+        self.resid = torch.empty(N, dtype=torch.float64, device=dev)
+        self.partial = torch.empty(3, dtype=torch.float64, device=dev)
+
+
+def vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
+                workspace=None, out: _Fwd | None = None, check_status: bool = _CHECK):
+    """Raw forward (tba_vargrad_tb_loss_fwd). Returns (_Fwd, workspace)."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    N, T = tokens.shape
+    dev = logits.device
+    for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
+        if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    o = out or _Fwd(N, K, dev)
+    ws = workspace if workspace is not None else _workspace(dev, N, T)
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_vargrad_tb_loss_fwd(ctypes.byref(x), ref_logp.data_ptr(), log_reward.data_ptr(), float(beta),
+                                        int(K), float(n_seq_global), ws.data_ptr(), o.seq_logp.data_ptr(),
+                                        o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None,
+                                        o.resid.data_ptr(), o.partial.data_ptr(), _ptr(st), _stream(dev)),
+              "tba_vargrad_tb_loss_fwd")
+    if st is not None:
+        _raise_dev_status(st, "tba_vargrad_tb_loss_fwd")
+    return o, ws
+
+
+def vargrad_bwd(logits, tokens, mask, workspace, resid, grad_scale: float, grad_out=None, dlogits=None,
+                dlogits_dtype=None):
+    """Raw backward (tba_vargrad_tb_loss_bwd). Returns dlogits (new [N,T,V] unless given)."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    dev = logits.device
+    if dlogits is None:
+        dt = dlogits_dtype or logits.dtype
+        dlogits = torch.empty(logits.shape, dtype=dt, device=dev)
+    if dlogits.shape != logits.shape or dlogits.dtype not in _DT or dlogits.stride(2) != 1:
+        raise ValueError("dlogits must match logits' shape with unit vocab stride (bf16/fp32)")
+    N, T, V = dlogits.shape
+    ors = dlogits.stride(1) if T > 1 else (dlogits.stride(0) if N > 1 else V)
+    if N > 1 and T > 0 and dlogits.stride(0) != T * ors:
+        raise ValueError("dlogits rows must be uniformly strided")
+    if grad_out is not None:
+        grad_out = grad_out.to(device=dev, dtype=torch.float64).contiguous()
+    with torch.cuda.device(dev):
+        check(L.tba_vargrad_tb_loss_bwd(ctypes.byref(x), workspace.data_ptr(), resid.data_ptr(), float(grad_scale),
+                                        _ptr(grad_out), dlogits.data_ptr(), _DT[dlogits.dtype], max(ors, V),
+                                        _stream(dev)), "tba_vargrad_tb_loss_bwd")
+    return dlogits
+
+
+class VarGradTBLoss(torch.autograd.Function):
+    """L = Eq. 5 over the (sharded) batch; backward writes dlogits in one fused pass."""
+
+    @staticmethod
+    def forward(ctx, logits, tokens, mask, ref_logp, log_reward, beta, K, n_global, group, dlogits_dtype, aux):
+        o, ws = vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta, K, n_global)
+        if group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
+        ctx.save_for_backward(logits, tokens, mask, ws, o.resid)
+        ctx.n_global = n_global
+        ctx.dlogits_dtype = dlogits_dtype
+        if aux is not None:
+            aux.update(seq_logp=o.seq_logp, n_tokens=o.n_tokens, log_z=o.log_z, resid=o.resid, partial=o.partial)
+        return o.partial[0]
+
+    @staticmethod
+    def backward(ctx, grad):
+        logits, tokens, mask, ws, resid = ctx.saved_tensors
+        d = vargrad_bwd(logits, tokens, mask, ws, resid, 2.0 / ctx.n_global, grad_out=grad,
+                        dlogits_dtype=ctx.dlogits_dtype)
+        return d, None, None, None, None, None, None, None, None, None, None
+
+
+def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
+                    group=None, dlogits_dtype=None, return_aux: bool = False):
+    """The VarGrad TB loss of Eq. 5, autograd-enabled.
+
+    logits [N, T, V] bf16/fp32 (N = groups*K, group-major); tokens int64 [N, T]; mask
+    uint8/bool [N, T]; ref_logp, log_reward fp64 [N] (log_reward is r_phi). With
+    ``group`` (a torch.distributed process group) each rank passes its own whole groups
+    and the partial sums are all-reduced once; ``n_seq_global`` defaults to N * world.
+    Returns the 0-dim fp64 loss (and an aux dict with seq_logp, n_tokens, log_z, resid,
+    partial when ``return_aux``)."""
+    N = tokens.shape[0]
+    if n_seq_global is None:
+        if group is not None:
+            import torch.distributed as dist
+            n_seq_global = N * dist.get_world_size(group)
+        else:
+            n_seq_global = N
+    aux = {} if return_aux else None
+    loss = VarGradTBLoss.apply(logits, tokens, mask, ref_logp, log_reward, float(beta), int(K),
+                               float(n_seq_global), group, dlogits_dtype, aux)
+    return (loss, aux) if return_aux else loss

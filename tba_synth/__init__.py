@@ -244,3 +244,47 @@ def group_inputs(w: Workload, seed: int, g0: int, ng: int):
     tok, mask = tokens_and_mask(w, seed, s0, n)
     return dict(tokens=tok, mask=mask, ref_logp=ref_logp(w, seed, s0, n),
                 log_reward=log_reward(w, seed, s0, n))
+
+
+# ----------------------------------------------------------------------------- CUDA twin
+_synth_lib = None
+
+
+def _load_cuda_twin():
+    global _synth_lib
+    if _synth_lib is None:
+        import ctypes
+        import os
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtba_synth.so")
+        if not os.path.exists(p):
+            raise ImportError(f"{p} not built (run __graft_entry__.build())")
+        L = ctypes.CDLL(p)
+        L.tba_synth_logits.restype = ctypes.c_int
+        L.tba_synth_logits.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                       ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_void_p]
+        _synth_lib = L
+    return _synth_lib
+
+
+def fill_logits_cuda(out, seed: int, row0: int, V: int, stream: int | None = None):
+    """Fill a CUDA tensor ``out`` viewed as [nrows, row_stride] (bf16 or fp32; last dim
+    unit-stride, rows uniformly strided) with the logits of global rows row0.. on the
+    device. Bit-identical to ``logits_rows`` (columns >= V get NaN)."""
+    import torch
+    dt = {torch.bfloat16: 0, torch.float32: 1}[out.dtype]
+    if out.dim() == 3:
+        nrows = out.shape[0] * out.shape[1]
+        rs = out.stride(1) if out.shape[1] > 1 else out.stride(0)
+    else:
+        nrows, rs = out.shape[0], out.stride(0)
+    if out.shape[-1] != V or out.stride(-1) != 1:
+        raise ValueError("out must be [.., V] with unit stride")
+    # fill the padding too: the storage view covers [nrows, rs]
+    s = torch.cuda.current_stream(out.device).cuda_stream if stream is None else stream
+    rc = _load_cuda_twin().tba_synth_logits(out.data_ptr(), dt, stream_key(seed, S_LOGITS),
+                                            stream_key(seed, S_TOKENS), stream_key(seed, S_PEAK), row0, nrows, V,
+                                            rs, s)
+    if rc:
+        raise RuntimeError(f"tba_synth_logits failed ({rc})")
+    return out

@@ -1,0 +1,120 @@
+"""The C ABI library loads without a GPU, exports every symbol include/tba.h declares, and
+its host-side validation returns the documented status codes before touching CUDA."""
+import ctypes
+import math
+import re
+import os
+
+import pytest
+
+from paper_2503_18929_b200 import _lib
+from paper_2503_18929_b200._lib import TbaRows
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2503_18929_b200 import _build
+    _build.build()
+    return _lib.load()
+
+
+def test_header_declarations_are_exported(L):
+    hdr = open(os.path.join(ROOT, "include", "tba.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(tba_\w+)\s*\(", hdr, re.M))
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name)
+    # nm-level check: the .so really exports them with C linkage
+    out = os.popen(f"nm -D --defined-only {_lib.LIB_PATH}").read()
+    for name in declared:
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_synth_twin_exports():
+    import tba_synth
+    L2 = tba_synth._load_cuda_twin()
+    assert hasattr(L2, "tba_synth_logits")
+
+
+def test_version_and_strings(L):
+    assert L.tba_abi_version() == 1
+    for c in range(4):
+        assert L.tba_status_string(c).startswith(b"TBA_")
+    assert b"unknown" in L.tba_status_string(99)
+
+
+def test_workspace_bytes(L):
+    assert L.tba_workspace_bytes(0, 0) >= 256
+    b = L.tba_workspace_bytes(64, 1024)
+    assert b >= 64 * 1024 * 16 + 64 * 8
+    assert L.tba_workspace_bytes(-1, 4) == 0
+
+
+FAKE = 0x10000  # a non-null, aligned pointer value: validation must fail before any use
+
+
+def _rows(**kw):
+    d = dict(logits=FAKE, dtype=0, _pad=0, n_seq=8, seq_len=4, vocab=100, row_stride=100, tokens=FAKE, mask=FAKE)
+    d.update(kw)
+    return TbaRows(**d)
+
+
+def _fwd(L, x, beta=1.0, K=4, ng=8.0, ptr=FAKE):
+    return L.tba_vargrad_tb_loss_fwd(ctypes.byref(x), ptr, ptr, beta, K, ng, 0x100000, ptr, ptr, ptr, ptr, ptr,
+                                     None, None)
+
+
+def test_fwd_config_errors(L):
+    x = _rows()
+    for beta in (0.0, -1.0, math.nan, math.inf):
+        assert _fwd(L, x, beta=beta) == _lib.TBA_ERR_INVALID_CONFIG
+    for K in (1, 0, -3):
+        assert _fwd(L, x, K=K) == _lib.TBA_ERR_INVALID_CONFIG
+
+
+@pytest.mark.parametrize("kw", [dict(n_seq=-1), dict(seq_len=-2), dict(vocab=0), dict(row_stride=99),
+                                dict(dtype=5), dict(logits=0), dict(tokens=0), dict(mask=0),
+                                dict(logits=FAKE + 1), dict(dtype=1, logits=FAKE + 2), dict(tokens=FAKE + 4),
+                                dict(n_seq=2 ** 40, seq_len=2 ** 30), dict(row_stride=2 ** 62)])
+def test_rows_arg_errors(L, kw):
+    x = _rows(**kw)
+    assert _fwd(L, x) == _lib.TBA_ERR_INVALID_ARG
+    assert L.tba_seq_logprob(ctypes.byref(x), 0x100000, FAKE, FAKE, None, None) == _lib.TBA_ERR_INVALID_ARG
+    assert L.tba_vargrad_tb_loss_bwd(ctypes.byref(x), 0x100000, FAKE, 1.0, None, FAKE, 0, 100, None) == \
+        _lib.TBA_ERR_INVALID_ARG
+
+
+def test_fwd_arg_errors(L):
+    assert _fwd(L, _rows(n_seq=6), K=4, ng=6.0) == _lib.TBA_ERR_INVALID_ARG      # N % K
+    assert _fwd(L, _rows(), ng=4.0) == _lib.TBA_ERR_INVALID_ARG                  # N_global < N
+    assert _fwd(L, _rows(), ng=math.nan) == _lib.TBA_ERR_INVALID_ARG
+    assert _fwd(L, _rows(), ptr=0) == _lib.TBA_ERR_INVALID_ARG                   # null outputs
+    assert L.tba_vargrad_tb_loss_fwd(ctypes.byref(_rows()), FAKE, FAKE, 1.0, 4, 8.0, 0x100010, FAKE, FAKE, FAKE,
+                                     FAKE, FAKE, None, None) == _lib.TBA_ERR_INVALID_ARG  # misaligned workspace
+    assert L.tba_vargrad_tb_loss_fwd(None, FAKE, FAKE, 1.0, 4, 8.0, 0x100000, FAKE, FAKE, FAKE, FAKE, FAKE, None,
+                                     None) == _lib.TBA_ERR_INVALID_ARG
+
+
+def test_bwd_arg_errors(L):
+    x = _rows()
+    bwd = lambda **k: L.tba_vargrad_tb_loss_bwd(ctypes.byref(x), k.get("ws", 0x100000), k.get("resid", FAKE),
+                                               k.get("gs", 1.0), None, k.get("out", FAKE + 0x1000),
+                                               k.get("dt", 0), k.get("ors", 100), None)
+    assert bwd(dt=3) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(ors=99) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(gs=math.inf) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(out=0) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(resid=0) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(ws=0) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(out=FAKE + 1) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(out=FAKE, dt=1) == _lib.TBA_ERR_INVALID_ARG      # aliasing with a different dtype
+    assert bwd(out=FAKE, ors=128) == _lib.TBA_ERR_INVALID_ARG   # aliasing with a different stride
+
+
+def test_empty_batch_is_ok_without_gpu_work(L):
+    # zero rows: seq_logprob has nothing to launch
+    x = _rows(n_seq=0, logits=0, tokens=0, mask=0)
+    assert L.tba_seq_logprob(ctypes.byref(x), 0, 0, 0, None, None) == _lib.TBA_OK
+    assert L.tba_vargrad_tb_loss_bwd(ctypes.byref(x), 0, 0, 1.0, None, 0, 0, 100, None) == _lib.TBA_OK
