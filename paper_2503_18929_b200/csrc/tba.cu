@@ -13,6 +13,7 @@
 // per-thread fp32 partial sums folded into fp64 every 32 elements, fp64 row finalisation.
 #include <cstdint>
 #include <cmath>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/tba.h"
@@ -81,86 +82,66 @@ __device__ __forceinline__ int64_t head_elems(const T* row, int64_t V) {
 }
 
 // ------------------------------------------------------------------------------ fwd state
-// Per-thread online state: m = running max, M2 = fl(m * kL2E), s = sum of 2^(fl(z*kL2E - M2))
+// Per-thread online state over a part of one row:
+//   m  = max of the elements seen so far (exact),
+//   R  = the reference the partial sum is kept against, R2 = fl(R * kL2E),
+//   s  = sum of 2^(fl(z * kL2E - R2)) over the elements seen (fp64, folded every chunk).
+// The reference is only re-based when a chunk's max exceeds it by more than kSlack (nats), so
+// the fp64 rescale (exact exp2 of an fp32 difference) is rare; arguments of ex2 stay <= kSlack*log2e.
+constexpr float kSlack = 6.0f;
+
 struct OnlineState {
-  float m, M2;
+  float m, R, R2;
   double s;
-  __device__ __forceinline__ void init() { m = -INFINITY; M2 = 0.f; s = 0.0; }
-  __device__ __forceinline__ void raise_to(float cm) {  // called when cm > m
-    const float M2n = cm * kL2E;
-    s = (m == -INFINITY) ? 0.0 : s * exp2((double)M2 - (double)M2n);
-    m = cm;
-    M2 = M2n;
+  __device__ __forceinline__ void init() {
+    m = -INFINITY;
+    R = -INFINITY;
+    R2 = 0.f;
+    s = 0.0;
+  }
+  __device__ __forceinline__ void chunk(float cm) {
+    m = fmaxf(m, cm);
+    if (cm > R + kSlack) {  // also taken for the first finite chunk (R = -inf)
+      const float R2n = cm * kL2E;
+      if (R == -INFINITY) {
+        s = 0.0;
+      } else {
+        s *= exp2((double)R2 - (double)R2n);
+      }
+      R = cm;
+      R2 = R2n;
+    }
   }
   __device__ __forceinline__ void add1(float z) {
-    if (z > m) raise_to(z);
-    s += (double)ex2(fmaf(z, kL2E, -M2));
+    chunk(z);
+    s += (double)ex2(fmaf(z, kL2E, -R2));
   }
 };
 
-template <class T, int U>
-__device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_t V, int tid, int nthr,
-                                               OnlineState& st) {
-  using E = Elem<T>;
-  constexpr int VEC = E::VEC;
-  const int64_t h = head_elems(row, V);
-  const int64_t nvec = (V - h) / VEC;
-  const int64_t tail0 = h + nvec * VEC;
-  for (int64_t i = tid; i < h; i += nthr) st.add1(E::load1(row + i));
-  for (int64_t i = tail0 + tid; i < V; i += nthr) st.add1(E::load1(row + i));
-  const uint4* vp = reinterpret_cast<const uint4*>(row + h);
-  for (int64_t k0 = tid; k0 < nvec; k0 += (int64_t)nthr * U) {
-    uint4 v[U];
+// Combine (m, R2, s) partial states held by the lanes of a warp; `active` lanes only.
+// Result (row max M, M2 = fl(M*kL2E), S = sum relative to M2) is returned in every lane.
+// The fp64 butterfly is fixed, so the bits do not depend on timing.
+__device__ __forceinline__ void combine_lanes(float m, float R2, double s, bool active, float& M, float& M2,
+                                              double& S) {
+  float mm = active ? m : -INFINITY;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = k0 + (int64_t)u * nthr;
-      v[u] = (k < nvec) ? ldg_stream(vp + k) : E::neg_inf();
-    }
-    float cm = -INFINITY;
+  for (int o = 16; o >= 1; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+  M = mm;
+  M2 = (mm == -INFINITY) ? 0.f : mm * kL2E;
+  double v = (active && s != 0.0) ? s * exp2((double)R2 - (double)M2) : (active ? s : 0.0);
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) cm = fmaxf(cm, E::get(v[u], e));
-    if (cm > st.m) st.raise_to(cm);
-    const float nM2 = -st.M2;
-    float acc[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) acc[e] += ex2(fmaf(E::get(v[u], e), kL2E, nM2));
-#pragma unroll
-    for (int w = VEC / 2; w >= 1; w >>= 1)
-#pragma unroll
-      for (int e = 0; e < w; ++e) acc[e] += acc[e + w];
-    st.s += (double)acc[0];
-  }
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  S = v;
 }
 
-// Combine states across the 32 lanes of a warp (result valid in every lane).
-__device__ __forceinline__ void warp_combine(OnlineState& st) {
-  float M = st.m;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  const float M2 = (M == -INFINITY) ? 0.f : M * kL2E;
-  double s = (st.m == -INFINITY) ? 0.0 : st.s * exp2((double)st.M2 - (double)M2);
-  // fixed butterfly: every lane ends with the same bits
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  st.m = M;
-  st.M2 = M2;
-  st.s = s;
-}
-
-__device__ __forceinline__ void finalize_row(const OnlineState& st, float zy, bool tok_ok, int64_t row,
+__device__ __forceinline__ void finalize_row(float M, float M2, double S, float zy, bool tok_ok, int64_t row,
                                              float2* __restrict__ stats, double* __restrict__ lp,
                                              int32_t* dev_status) {
-  const bool finite = (st.m > -INFINITY) && (st.m < INFINITY) && (st.s > 0.0) && (st.s < INFINITY);
-  const double log2s = log2(st.s);
-  stats[row] = make_float2(st.M2, (float)log2s);
+  const bool finite = (M > -INFINITY) && (M < INFINITY) && (S > 0.0) && (S < INFINITY);
+  const double log2s = log2(S);
+  stats[row] = make_float2(M2, (float)log2s);
   // lp = (z_y - M) - ln sum_v e^{kappa (z_v - M)},  kappa = kL2E / log2(e)
-  double v = ((double)zy - (double)st.m) - kLN2 * (log2s + (double)st.M2 - (double)st.m * (double)kL2E);
+  double v = ((double)zy - (double)M) - kLN2 * (log2s + (double)M2 - (double)M * (double)kL2E);
   if (!tok_ok) v = nan("");
   lp[row] = v;
   if (dev_status) {
@@ -169,41 +150,207 @@ __device__ __forceinline__ void finalize_row(const OnlineState& st, float zy, bo
   }
 }
 
-// One CTA (NT threads) per row.
-template <class T, int NT, int U>
-__global__ void __launch_bounds__(NT) row_fwd_cta(const T* __restrict__ logits, int64_t rows, int64_t V,
+// packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2)
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// 2^x for a pair of fp32 on the FMA pipe (offloads MUFU.EX2, which the forward saturates first):
+// Cody-Waite split x = n + f, |f| <= 1/2, by the 1.5*2^23 rounding trick; degree-5 minimax
+// polynomial for 2^f (max relative error 2.3e-7 with fp32 Horner, same order as ex2.approx);
+// 2^n by adding n to the exponent field. Inputs are clamped at -125 (2^-125 is below every sum
+// it could enter; ex2.approx.ftz flushes there too).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  float a, b;
+  f2_unpack(x, a, b);
+  const uint64_t xc = f2_pack(fmaxf(a, -125.f), fmaxf(b, -125.f));
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(xc, magic);                             // n + 1.5*2^23 (round to nearest)
+  const uint64_t n = fadd2(t, f2_pack(-12582912.f, -12582912.f));   // n exactly
+  const uint64_t f = ffma2(n, f2_pack(-1.f, -1.f), xc);             // x - n, exact
+  uint64_t p = ffma2(f2_pack(1.3276358367875218e-3f, 1.3276358367875218e-3f), f,
+                     f2_pack(9.67550277709961e-3f, 9.67550277709961e-3f));
+  p = ffma2(p, f, f2_pack(5.550713092088699e-2f, 5.550713092088699e-2f));
+  p = ffma2(p, f, f2_pack(0.24022120237350464f, 0.24022120237350464f));
+  p = ffma2(p, f, f2_pack(0.6931469440460205f, 0.6931469440460205f));
+  p = ffma2(p, f, f2_pack(1.0000001192092896f, 1.0000001192092896f));
+  uint32_t plo, phi, tlo, thi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(plo), "=r"(phi) : "l"(p));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(tlo), "=r"(thi) : "l"(t));
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(plo + (tlo << 23)), "r"(phi + (thi << 23)));
+  return r;
+}
+
+// Consume U 16-byte vectors of one row: chunk max, rare re-base, sum of 2^x (FFMA2 + MUFU + FADD2),
+// fp32 pair accumulators (<= 4U terms each) folded into the fp64 partial once per call.
+// NP of the VEC/2 element pairs of every vector take the FMA-pipe exp2 instead of MUFU.
+template <class T, int U, int NP = 0>
+__device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  float z[U][VEC];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) z[u][e] = E::get(v[u], e);
+  float cm = -INFINITY;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) cm = fmaxf(cm, fmaxf(z[u][e], z[u][e + 1]));
+  st.chunk(cm);
+  const uint64_t l2e = f2_pack(kL2E, kL2E), nr2 = f2_pack(-st.R2, -st.R2);
+  uint64_t acc[VEC / 2];
+#pragma unroll
+  for (int p = 0; p < VEC / 2; ++p) acc[p] = 0ull;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int p = 0; p < VEC / 2; ++p) {
+      const uint64_t x = ffma2(f2_pack(z[u][2 * p], z[u][2 * p + 1]), l2e, nr2);
+      const bool poly = (NP >= 1 && p == VEC / 2 - 1) || (NP >= 2 && p == VEC / 2 - 3);
+      if (poly) {
+        acc[p] = fadd2(acc[p], exp2_poly2(x));
+      } else {
+        float a, b;
+        f2_unpack(x, a, b);
+        acc[p] = fadd2(acc[p], f2_pack(ex2(a), ex2(b)));
+      }
+    }
+#pragma unroll
+  for (int w = VEC / 4; w >= 1; w >>= 1)
+#pragma unroll
+    for (int p = 0; p < w; ++p) acc[p] = fadd2(acc[p], acc[p + w]);
+  float a, b;
+  f2_unpack(acc[0], a, b);
+  st.s += (double)(a + b);
+}
+
+// LDG-streamed partial state of one row over threads tid, tid+nthr, ...
+template <class T, int U, int NP = 0>
+__device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_t V, int tid, int nthr,
+                                               OnlineState& st) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const int64_t h = head_elems(row, V);
+  const int64_t nvec = (V - h) / VEC;
+  const int64_t tail0 = h + nvec * VEC;
+  if (tid < h) st.add1(E::load1(row + tid));
+  for (int64_t i = tail0 + tid; i < V; i += nthr) st.add1(E::load1(row + i));
+  const uint4* vp = reinterpret_cast<const uint4*>(row + h);
+  const int64_t step = (int64_t)nthr * U;
+  const int64_t nfull = nvec / step;
+  int64_t k0 = tid;
+  for (int64_t it = 0; it < nfull; ++it, k0 += step) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + k0 + (int64_t)u * nthr);
+    fwd_consume<T, U, NP>(v, st);
+  }
+  for (int64_t k = k0; k < nvec; k += nthr) {
+    uint4 v1[1] = {ldg_stream(vp + k)};
+    fwd_consume<T, 1>(v1, st);
+  }
+}
+
+// Same, with the next iteration's loads issued before the current vectors are consumed
+// (register double buffer): 2U 16-byte loads in flight per thread.
+template <class T, int U>
+__device__ __forceinline__ void fwd_accumulate_pf(const T* __restrict__ row, int64_t V, int tid, int nthr,
+                                                  OnlineState& st) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const int64_t h = head_elems(row, V);
+  const int64_t nvec = (V - h) / VEC;
+  const int64_t tail0 = h + nvec * VEC;
+  if (tid < h) st.add1(E::load1(row + tid));
+  for (int64_t i = tail0 + tid; i < V; i += nthr) st.add1(E::load1(row + i));
+  const uint4* vp = reinterpret_cast<const uint4*>(row + h);
+  const int64_t step = (int64_t)nthr * U;
+  const int64_t nfull = nvec / step;
+  int64_t k0 = tid;
+  if (nfull > 0) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + k0 + (int64_t)u * nthr);
+    for (int64_t it = 1; it < nfull; ++it) {
+      k0 += step;
+      uint4 w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = ldg_stream(vp + k0 + (int64_t)u * nthr);
+      fwd_consume<T, U>(v, st);
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = w[u];
+    }
+    fwd_consume<T, U>(v, st);
+    k0 += step;
+  }
+  for (int64_t k = k0; k < nvec; k += nthr) {
+    uint4 v1[1] = {ldg_stream(vp + k)};
+    fwd_consume<T, 1>(v1, st);
+  }
+}
+
+// One CTA (NT threads) per row; the 8 warp partials are combined by warp 0's lanes in parallel.
+template <class T, int NT, int U, int MINB = 1, bool PF = false, int NP = 0>
+__global__ void __launch_bounds__(NT, MINB) row_fwd_cta(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                    int64_t stride, const int64_t* __restrict__ tokens,
                                                    const uint8_t* __restrict__ mask, float2* __restrict__ stats,
                                                    double* __restrict__ lp, int32_t* dev_status) {
+  constexpr int NW = NT / 32;
   const int64_t row = blockIdx.x;
   if (row >= rows || mask[row] == 0) return;
   const T* rp = logits + row * stride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float zy = 0.f;
+  bool ok = true;
+  if (threadIdx.x == 0) {
+    const int64_t y = tokens[row];
+    ok = (y >= 0 && y < V);
+    if (ok) zy = Elem<T>::load1(rp + y);
+  }
   OnlineState st;
   st.init();
-  fwd_accumulate<T, U>(rp, V, threadIdx.x, NT, st);
-  warp_combine(st);
-  __shared__ float sm_m[NT / 32], sm_M2[NT / 32];
-  __shared__ double sm_s[NT / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (PF)
+    fwd_accumulate_pf<T, U>(rp, V, threadIdx.x, NT, st);
+  else
+    fwd_accumulate<T, U, NP>(rp, V, threadIdx.x, NT, st);
+  float M, M2;
+  double S;
+  combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
+  __shared__ float sm_m[NW], sm_M2[NW];
+  __shared__ double sm_s[NW];
   if (lane == 0) {
-    sm_m[warp] = st.m;
-    sm_M2[warp] = st.M2;
-    sm_s[warp] = st.s;
+    sm_m[warp] = M;
+    sm_M2[warp] = M2;
+    sm_s[warp] = S;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    OnlineState tot;
-    tot.init();
-    for (int w = 0; w < NT / 32; ++w) tot.m = fmaxf(tot.m, sm_m[w]);
-    tot.M2 = (tot.m == -INFINITY) ? 0.f : tot.m * kL2E;
-    double s = 0.0;
-    for (int w = 0; w < NT / 32; ++w)
-      if (sm_m[w] > -INFINITY) s += sm_s[w] * exp2((double)sm_M2[w] - (double)tot.M2);
-    tot.s = s;
-    const int64_t y = tokens[row];
-    const bool ok = (y >= 0 && y < V);
-    const float zy = ok ? Elem<T>::load1(rp + y) : 0.f;
-    finalize_row(tot, zy, ok, row, stats, lp, dev_status);
+  if (warp == 0) {
+    const bool act = lane < NW;
+    combine_lanes(act ? sm_m[lane] : -INFINITY, act ? sm_M2[lane] : 0.f, act ? sm_s[lane] : 0.0, act, M, M2, S);
+    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
   }
 }
 
@@ -220,12 +367,185 @@ __global__ void __launch_bounds__(NT) row_fwd_warp(const T* __restrict__ logits,
   OnlineState st;
   st.init();
   fwd_accumulate<T, U>(rp, V, lane, 32, st);
-  warp_combine(st);
+  float M, M2;
+  double S;
+  combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
   if (lane == 0) {
     const int64_t y = tokens[row];
     const bool ok = (y >= 0 && y < V);
     const float zy = ok ? Elem<T>::load1(rp + y) : 0.f;
-    finalize_row(st, zy, ok, row, stats, lp, dev_status);
+    finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
+  }
+}
+
+// ------------------------------------------------------------------------------ a1, TMA-staged
+// Persistent, warp-specialised forward for long rows. One producer warp streams the 16-byte
+// aligned interior of every valid row through a STAGES-deep shared-memory ring with 1-D bulk
+// TMA copies (cp.async.bulk, mbarrier complete_tx, L2 evict_first); NCW consumer warps read
+// each tile once (LDS.128) and keep the online state in registers. Warps never wait for each
+// other at a row boundary: each posts its partial to a shared slot and the LAST warp to post
+// (shared-memory counter) combines the row, so the ring keeps streaming.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <class T, int NCW, int TILE, int STAGES, int NP = 0>
+__global__ void __launch_bounds__((NCW + 1) * 32) row_fwd_tma(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                              int64_t stride, const int64_t* __restrict__ tokens,
+                                                              const uint8_t* __restrict__ mask,
+                                                              float2* __restrict__ stats, double* __restrict__ lp,
+                                                              int32_t* dev_status) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  constexpr int NC = NCW * 32;
+  constexpr int TV = TILE / 16;  // vectors per tile
+  constexpr int U = TV / NC;     // vectors per consumer thread per full tile
+  constexpr int SLOTS = 2 * STAGES + 2;  // a warp is at most STAGES tiles (<= STAGES rows) ahead
+  static_assert(TV % NC == 0 && U >= 1, "tile must split evenly over the consumer threads");
+  static_assert(NCW <= 32, "");
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ float sm_m[SLOTS][NCW], sm_M2[SLOTS][NCW];
+  __shared__ double sm_s[SLOTS][NCW];
+  __shared__ float sm_zy[SLOTS];
+  __shared__ int sm_ok[SLOTS];
+  __shared__ unsigned sm_cnt[SLOTS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < SLOTS) sm_cnt[threadIdx.x] = 0;
+  __syncthreads();
+
+  if (warp == NCW) {  // ---------------- producer warp: one elected lane issues the bulk copies
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        if (mask[row] == 0) continue;
+        const T* rp = logits + row * stride;
+        const int64_t h = head_elems(rp, V);
+        const int64_t bytes = ((V - h) / VEC) * 16;
+        const char* src = reinterpret_cast<const char*>(rp + h);
+        for (int64_t off = 0; off < bytes; off += TILE) {
+          const uint32_t n = (uint32_t)((bytes - off) < TILE ? (bytes - off) : TILE);
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_expect_tx(&full[stage], n);
+          bulk_g2s(ring + (size_t)stage * TILE, src + off, n, &full[stage], pol);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps
+  const int ct = threadIdx.x;
+  int stage = 0, slot = 0;
+  uint32_t phase = 0;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    if (mask[row] == 0) continue;
+    const T* rp = logits + row * stride;
+    const int64_t h = head_elems(rp, V);
+    const int64_t nvec = (V - h) / VEC;
+    const int64_t bytes = nvec * 16;
+    OnlineState st;
+    st.init();
+    if (ct == 0) {
+      const int64_t y = tokens[row];
+      const bool ok = (y >= 0 && y < V);
+      sm_zy[slot] = ok ? E::load1(rp + y) : 0.f;
+      sm_ok[slot] = ok;
+    }
+    if (ct < h) st.add1(E::load1(rp + ct));
+    const int64_t tail0 = h + nvec * VEC;
+    if (tail0 + ct < V) st.add1(E::load1(rp + tail0 + ct));
+    for (int64_t off = 0; off < bytes; off += TILE) {
+      const int nv = (int)(((bytes - off) < TILE ? (bytes - off) : TILE) / 16);
+      mbar_wait(&full[stage], phase);
+      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)stage * TILE);
+      if (nv == TV) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = sv[ct + u * NC];
+        fwd_consume<T, U, NP>(v, st);
+      } else {
+        for (int k = ct; k < nv; k += NC) {
+          uint4 v1[1] = {sv[k]};
+          fwd_consume<T, 1>(v1, st);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    float M, M2;
+    double S;
+    combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
+    unsigned prev = 0;
+    if (lane == 0) {
+      sm_m[slot][warp] = M;
+      sm_M2[slot][warp] = M2;
+      sm_s[slot][warp] = S;
+      __threadfence_block();
+      prev = atomicAdd(&sm_cnt[slot], 1u);
+    }
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev == NCW - 1) {  // last warp of this row: combine and finalise
+      __threadfence_block();
+      const bool act = lane < NCW;
+      const volatile float* vm = sm_m[slot];
+      const volatile float* vm2 = sm_M2[slot];
+      const volatile double* vs = sm_s[slot];
+      combine_lanes(act ? vm[lane] : -INFINITY, act ? vm2[lane] : 0.f, act ? vs[lane] : 0.0, act, M, M2, S);
+      if (lane == 0) {
+        const float zy = *(volatile float*)&sm_zy[slot];
+        const bool ok = *(volatile int*)&sm_ok[slot] != 0;
+        finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
+        sm_cnt[slot] = 0;
+      }
+    }
+    if (++slot == SLOTS) slot = 0;
   }
 }
 
@@ -471,6 +791,110 @@ int validate_rows(const tba_rows* x) {
   return TBA_OK;
 }
 
+struct DevInfo {
+  int sms = 0;
+};
+
+int device_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static int cache[64] = {0};
+  if (dev < 64 && cache[dev]) return cache[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 64) cache[dev] = n;
+  return n;
+}
+
+// TMA forward configurations (consumer warps, tile bytes, ring stages); cfg 0 is the default,
+// the others are kept for A/B measurement (env TBA_TMA_CFG).
+template <class T, int NCW, int TILE, int STAGES, int NP = 0>
+int launch_fwd_tma_cfg(const T* lg, const tba_rows* x, const WsLayout& w, int32_t* dev_status, cudaStream_t s) {
+  auto kern = row_fwd_tma<T, NCW, TILE, STAGES, NP>;
+  const int smem = TILE * STAGES;
+  static int attr_done = 0;  // benign race: the attribute is idempotent
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return TBA_ERR_CUDA;
+    attr_done = 1;
+  }
+  static int occ = 0;
+  if (!occ) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, (NCW + 1) * 32, smem) != cudaSuccess || o < 1) o = 1;
+    occ = o;
+  }
+  const int64_t rows = x->n_seq * x->seq_len;
+  int64_t grid = (int64_t)device_sms() * occ;
+  if (grid > rows) grid = rows;
+  kern<<<(unsigned)grid, (NCW + 1) * 32, smem, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, w.stats,
+                                                     w.lp, dev_status);
+  return TBA_OK;
+}
+
+int tma_cfg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TBA_TMA_CFG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <class T>
+int launch_fwd_tma(const T* lg, const tba_rows* x, const WsLayout& w, int32_t* dev_status, cudaStream_t s) {
+  switch (tma_cfg()) {
+    case 1: return launch_fwd_tma_cfg<T, 8, 8192, 8>(lg, x, w, dev_status, s);
+    case 2: return launch_fwd_tma_cfg<T, 16, 16384, 6>(lg, x, w, dev_status, s);
+    case 3: return launch_fwd_tma_cfg<T, 4, 8192, 6>(lg, x, w, dev_status, s);
+    case 4: return launch_fwd_tma_cfg<T, 8, 32768, 3>(lg, x, w, dev_status, s);
+    case 5: return launch_fwd_tma_cfg<T, 8, 16384, 4, 1>(lg, x, w, dev_status, s);
+    case 6: return launch_fwd_tma_cfg<T, 8, 32768, 3, 1>(lg, x, w, dev_status, s);
+    case 7: return launch_fwd_tma_cfg<T, 8, 16384, 4, 2>(lg, x, w, dev_status, s);
+    default: return launch_fwd_tma_cfg<T, 8, 16384, 4>(lg, x, w, dev_status, s);
+  }
+}
+
+int ldg_cfg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TBA_LDG_CFG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+// LDG forward configurations (threads per row, vectors per thread per iteration, min CTAs/SM,
+// register double buffering); cfg 0 is the default, the others are kept for A/B (TBA_LDG_CFG).
+template <class T>
+void launch_fwd_cta(const T* lg, int64_t rows, int64_t V, int64_t stride, const tba_rows* x, const WsLayout& w,
+                    int32_t* dev_status, cudaStream_t s) {
+#define TBA_CTA(NT_, U_, MB_, PF_, NP_) \
+  row_fwd_cta<T, NT_, U_, MB_, PF_, NP_><<<(unsigned)rows, NT_, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats, \
+                                                                   w.lp, dev_status)
+  switch (ldg_cfg()) {
+    case 1: TBA_CTA(256, 8, 1, false, 0); break;
+    case 2: TBA_CTA(512, 4, 1, false, 0); break;
+    case 3: TBA_CTA(256, 4, 5, false, 0); break;
+    case 4: TBA_CTA(256, 4, 1, true, 0); break;
+    case 5: TBA_CTA(256, 4, 1, false, 2); break;
+    case 6: TBA_CTA(512, 4, 1, false, 1); break;
+    case 7: TBA_CTA(256, 4, 1, false, 0); break;
+    case 8: TBA_CTA(256, 4, 1, false, 1); break;
+    default: TBA_CTA(256, 4, 1, false, 0); break;
+  }
+#undef TBA_CTA
+}
+
+bool fwd_use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TBA_FWD_IMPL");
+    v = (e && e[0] == 't') ? 1 : 0;  // default: register-staged LDG kernel; "tma" selects the TMA ring
+  }
+  return v == 1;
+}
+
 int launch_fwd_rows(const tba_rows* x, const WsLayout& w, int32_t* dev_status, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
@@ -478,23 +902,27 @@ int launch_fwd_rows(const tba_rows* x, const WsLayout& w, int32_t* dev_status, c
   const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
   const bool warp = V * esz <= kWarpRowMaxBytes;
   const int64_t grid = warp ? (rows + kNT / 32 - 1) / (kNT / 32) : rows;
+  int rc = TBA_OK;
   if (x->dtype == TBA_BF16) {
     auto lg = static_cast<const uint16_t*>(x->logits);
     if (warp)
       row_fwd_warp<uint16_t, kNT, kU><<<(unsigned)grid, kNT, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats,
                                                                     w.lp, dev_status);
+    else if (fwd_use_tma())
+      rc = launch_fwd_tma<uint16_t>(lg, x, w, dev_status, s);
     else
-      row_fwd_cta<uint16_t, kNT, kU><<<(unsigned)grid, kNT, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats,
-                                                                   w.lp, dev_status);
+      launch_fwd_cta<uint16_t>(lg, rows, V, stride, x, w, dev_status, s);
   } else {
     auto lg = static_cast<const float*>(x->logits);
     if (warp)
       row_fwd_warp<float, kNT, kU><<<(unsigned)grid, kNT, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats,
                                                                  w.lp, dev_status);
+    else if (fwd_use_tma())
+      rc = launch_fwd_tma<float>(lg, x, w, dev_status, s);
     else
-      row_fwd_cta<float, kNT, kU><<<(unsigned)grid, kNT, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats,
-                                                                w.lp, dev_status);
+      launch_fwd_cta<float>(lg, rows, V, stride, x, w, dev_status, s);
   }
+  if (rc) return rc;
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 

@@ -151,12 +151,18 @@ def test_neg_inf_logits_and_empty_sequences():
     _oracle_compare(z, tok, mask, ref, rew, 0.3, 3)
 
 
-def test_duplicate_sequences_in_group():
-    z, tok, mask, ref, rew = _edge_inputs(4, 3, 3001, 4)
+@pytest.mark.parametrize("V", [3008, 50257])
+def test_duplicate_sequences_in_group(V):
+    # identical rows give identical ell when they sit at the same 16-byte alignment (V even
+    # here; for odd V the head/vector split differs per row and ell agrees to rounding)
+    z, tok, mask, ref, rew = _edge_inputs(4, 3, V, 4)
     z[1], tok[1], ref[1], rew[1] = z[0], tok[0], ref[0], rew[0]
     o, _, _ = _oracle_compare(z, tok, mask, ref, rew, 1.0, 4)
     sl = o.seq_logp.cpu().numpy()
-    assert sl[0] == sl[1]
+    if V % 8 == 0:
+        assert sl[0] == sl[1]
+    else:
+        assert abs(sl[0] - sl[1]) <= 1e-9 * abs(sl[0])
 
 
 def test_in_place_dlogits_aliasing():
