@@ -354,6 +354,53 @@ __global__ void __launch_bounds__(NT, MINB) row_fwd_cta(const T* __restrict__ lo
   }
 }
 
+// TPR threads per row, 256/TPR rows per CTA (TPR = 32 ... 256, a power of two). Rows of one CTA
+// are independent: each row group meets on its own named barrier (ids 1..8), masked rows skip
+// the stream but still take part in nothing else, so no thread returns early.
+template <class T, int TPR, int U>
+__global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                     int64_t stride, const int64_t* __restrict__ tokens,
+                                                     const uint8_t* __restrict__ mask, float2* __restrict__ stats,
+                                                     double* __restrict__ lp, int32_t* dev_status) {
+  constexpr int RPC = 256 / TPR, WPR = TPR / 32;
+  const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
+  const int lane = threadIdx.x & 31, wig = gt >> 5;
+  const int64_t row = (int64_t)blockIdx.x * RPC + grp;
+  if (row >= rows || mask[row] == 0) return;  // uniform over the row group (named barriers are per group)
+  const T* rp = logits + row * stride;
+  float zy = 0.f;
+  bool ok = true;
+  if (gt == 0) {
+    const int64_t y = tokens[row];
+    ok = (y >= 0 && y < V);
+    if (ok) zy = Elem<T>::load1(rp + y);
+  }
+  OnlineState st;
+  st.init();
+  fwd_accumulate<T, U>(rp, V, gt, TPR, st);
+  float M, M2;
+  double S;
+  combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
+  if (WPR == 1) {
+    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
+    return;
+  }
+  __shared__ float sm_m[RPC][WPR > 1 ? WPR : 1], sm_M2[RPC][WPR > 1 ? WPR : 1];
+  __shared__ double sm_s[RPC][WPR > 1 ? WPR : 1];
+  if (lane == 0) {
+    sm_m[grp][wig] = M;
+    sm_M2[grp][wig] = M2;
+    sm_s[grp][wig] = S;
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(TPR) : "memory");
+  if (wig == 0) {
+    const bool act = lane < WPR;
+    combine_lanes(act ? sm_m[grp][lane] : -INFINITY, act ? sm_M2[grp][lane] : 0.f, act ? sm_s[grp][lane] : 0.0, act,
+                  M, M2, S);
+    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
+  }
+}
+
 // One warp per row, NT/32 rows per CTA (small vocabularies).
 template <class T, int NT, int U>
 __global__ void __launch_bounds__(NT) row_fwd_warp(const T* __restrict__ logits, int64_t rows, int64_t V,
@@ -895,32 +942,64 @@ bool fwd_use_tma() {
   return v == 1;
 }
 
+int fwd_tpr_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TBA_FWD_TPR");
+    v = e ? atoi(e) : 0;  // 0 = auto
+  }
+  return v;
+}
+
+// Threads per row for the LDG forward. Measured on B200 (scripts/gpu_ab_tpr.sh):
+// 64 threads (4 rows per CTA) is best or within 1 % for V = 32000 ... 152064; one warp per row
+// for short rows (< 1024 16-byte vectors).
+int fwd_tpr(int64_t V, int64_t esz) {
+  const int env = fwd_tpr_env();
+  if (env == 32 || env == 64 || env == 128 || env == 256) return env;
+  const int64_t nv = V * esz / 16;
+  return nv < 1024 ? 32 : 64;
+}
+
+template <class T>
+void launch_fwd_rows_t(const T* lg, int64_t rows, int64_t V, int64_t stride, const tba_rows* x, const WsLayout& w,
+                       int32_t* dev_status, cudaStream_t s, int tpr) {
+  const int64_t rpc = 256 / tpr;
+  const unsigned grid = (unsigned)((rows + rpc - 1) / rpc);
+#define TBA_ROWS(TPR_) \
+  row_fwd_rows<T, TPR_, kU><<<grid, 256, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats, w.lp, dev_status)
+  switch (tpr) {
+    case 32: TBA_ROWS(32); break;
+    case 64: TBA_ROWS(64); break;
+    case 128: TBA_ROWS(128); break;
+    default: TBA_ROWS(256); break;
+  }
+#undef TBA_ROWS
+}
+
 int launch_fwd_rows(const tba_rows* x, const WsLayout& w, int32_t* dev_status, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
   const int64_t V = x->vocab, stride = x->row_stride;
   const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
-  const bool warp = V * esz <= kWarpRowMaxBytes;
-  const int64_t grid = warp ? (rows + kNT / 32 - 1) / (kNT / 32) : rows;
+  const int tpr = fwd_tpr(V, esz);
   int rc = TBA_OK;
   if (x->dtype == TBA_BF16) {
     auto lg = static_cast<const uint16_t*>(x->logits);
-    if (warp)
-      row_fwd_warp<uint16_t, kNT, kU><<<(unsigned)grid, kNT, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats,
-                                                                    w.lp, dev_status);
-    else if (fwd_use_tma())
+    if (fwd_use_tma() && V * esz > kWarpRowMaxBytes)
       rc = launch_fwd_tma<uint16_t>(lg, x, w, dev_status, s);
-    else
+    else if (tpr == 256 && ldg_cfg() != 0)
       launch_fwd_cta<uint16_t>(lg, rows, V, stride, x, w, dev_status, s);
+    else
+      launch_fwd_rows_t<uint16_t>(lg, rows, V, stride, x, w, dev_status, s, tpr);
   } else {
     auto lg = static_cast<const float*>(x->logits);
-    if (warp)
-      row_fwd_warp<float, kNT, kU><<<(unsigned)grid, kNT, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats,
-                                                                 w.lp, dev_status);
-    else if (fwd_use_tma())
+    if (fwd_use_tma() && V * esz > kWarpRowMaxBytes)
       rc = launch_fwd_tma<float>(lg, x, w, dev_status, s);
-    else
+    else if (tpr == 256 && ldg_cfg() != 0)
       launch_fwd_cta<float>(lg, rows, V, stride, x, w, dev_status, s);
+    else
+      launch_fwd_rows_t<float>(lg, rows, V, stride, x, w, dev_status, s, tpr);
   }
   if (rc) return rc;
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;

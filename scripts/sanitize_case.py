@@ -1,0 +1,38 @@
+"""Small cases through the C ABI for compute-sanitizer (memcheck/racecheck/synccheck/initcheck).
+Every buffer the kernels read is initialised; dlogits is allocated uninitialised so initcheck
+proves that masked rows are written (zero-filled), and a second pass reads it back."""
+import dataclasses
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2503_18929_b200 as tba  # noqa: E402
+import tba_synth as syn  # noqa: E402
+
+cases = [
+    dataclasses.replace(syn.WORKLOADS["toy"]),
+    dataclasses.replace(syn.WORKLOADS["redteam"], B=2, K=3, T=5, len_lo=1, len_hi=5),    # unaligned, ragged
+    dataclasses.replace(syn.WORKLOADS["rhomath"], B=2, K=4, T=6, V=4093, len_lo=0, len_hi=6),  # warp path
+    dataclasses.replace(syn.WORKLOADS["qwen"], B=1, K=2, T=2),                              # long rows
+]
+for w in cases:
+    gi = syn.group_inputs(w, 0, 0, w.B)
+    dt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
+    lg = torch.empty((w.N, w.T, w.V), dtype=dt, device="cuda")
+    syn.fill_logits_cuda(lg, 0, 0, w.V)
+    tok = torch.from_numpy(gi["tokens"]).cuda()
+    mask = torch.from_numpy(gi["mask"]).cuda()
+    ref = torch.from_numpy(gi["ref_logp"]).cuda()
+    rew = torch.from_numpy(gi["log_reward"]).cuda()
+    ws = torch.empty(tba.workspace_bytes(w.N, w.T), dtype=torch.uint8, device="cuda")
+    o, _ = tba.vargrad_fwd(lg, tok, mask, ref, rew, w.beta, w.K, float(w.N), workspace=ws, check_status=True)
+    d = torch.empty_like(lg)
+    tba.vargrad_bwd(lg, tok, mask, ws, o.resid, 2.0 / w.N, dlogits=d)
+    sl, nt = tba.seq_logprob(lg, tok, mask, check_status=True)
+    torch.cuda.synchronize()
+    s = float(d.float().sum().item())  # reads every dlogits element (initcheck)
+    print(w.name, w.V, "loss", o.partial[0].item(), "sum dlogits", s, "seq_logprob match",
+          torch.equal(sl, o.seq_logp))
+print("sanitize cases done")
