@@ -143,7 +143,7 @@ def run_reference(args, w):
     line = {"impl": "reference", "metric": "TB-loss fwd+bwd tokens/sec", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "note": w.note, "B_per_rank": w.B, "K": w.K, "T": w.T, "V": w.V},
+            "config": {"workload": w.name, "objective": args.objective, "note": w.note, "B_per_rank": w.B, "K": w.K, "T": w.T, "V": w.V},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -160,6 +160,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--objective", default="vargrad", choices=["vargrad", "tbap"],
+                    help="vargrad: Eq. 5 (the north-star head); tbap: the TBA' token-level rule (Eq. 16)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = syn.WORKLOADS[args.workload]
@@ -197,7 +199,10 @@ def main():
     rew = torch.from_numpy(gi["log_reward"]).to(dev)
     dlogits = torch.empty_like(logits)
     ws = torch.empty(tba.workspace_bytes(N, T), dtype=torch.uint8, device=dev)
-    out = tba.ops._Fwd(N, K, dev)
+    tbap = args.objective == "tbap"
+    out = tba.ops._TbapFwd(N, T, dev) if tbap else tba.ops._Fwd(N, K, dev)
+    gen = torch.from_numpy(syn.gen_logp(w, SEED, g0 * K, N)).to(dev) if tbap else None
+    n_tok_global = float(int(gi["mask"].sum()) * world)
     stream = torch.cuda.current_stream(dev)
 
     valid_rows = int(gi["mask"].sum())
@@ -212,15 +217,22 @@ def main():
     def step(rec=None):
         if rec is not None:
             rec[0].record(stream)
-        tba.vargrad_fwd(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
-                        check_status=False)
+        if tbap:
+            tba.tbap_fwd(logits, tokens, mask, gen, ref, rew, w.beta, K, "clip", 0.0, 8.0, n_tok_global,
+                         workspace=ws, out=out, check_status=False)
+        else:
+            tba.vargrad_fwd(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
+                            check_status=False)
         if rec is not None:
             rec[1].record(stream)
         if group is not None:
             dist.all_reduce(out.partial, group=group)
         if rec is not None:
             rec[2].record(stream)
-        tba.vargrad_bwd(logits, tokens, mask, ws, out.resid, 2.0 / n_global, dlogits=dlogits)
+        if tbap:
+            tba.tbap_bwd(logits, tokens, mask, ws, out.coef, n_tok_global, dlogits=dlogits)
+        else:
+            tba.vargrad_bwd(logits, tokens, mask, ws, out.resid, 2.0 / n_global, dlogits=dlogits)
         if rec is not None:
             rec[3].record(stream)
 
@@ -309,13 +321,13 @@ def main():
         step_gbs = (fwd_bytes + bwd_bytes) / (ms_step / 1e3) / 1e9
         tr = ncu_traffic(w.name, "row_bwd")
         line = {
-            "metric": "TB-loss fwd+bwd tokens/sec",
+            "metric": "TB-loss fwd+bwd tokens/sec" + (" (TBA' Eq. 16 objective)" if tbap else ""),
             "value": tokens_per_step_rank * world / (ms_step / 1e3),
             "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (tba_synth seeded generator, DESIGN.md §6)",
-            "config": {"workload": w.name, "note": w.note, "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
+            "config": {"workload": w.name, "objective": args.objective, "note": w.note, "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
                        "V": V, "beta": w.beta, "logits_dtype": w.dtype, "dlogits_dtype": w.dtype,
                        "valid_tokens_per_rank": valid_rows, "parallelism": f"group-sharded x{world}",
                        "l2": "inputs (%.1f GB logits + dlogits per rank) >> 126 MB L2; no flush needed" %

@@ -109,6 +109,35 @@ int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const doub
                             double grad_scale, const double* grad_out, void* dlogits,
                             int32_t dlogits_dtype, int64_t dlogits_row_stride, tba_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------
+ * TBA' token-level update: Eq. 16 (eq:tbaGrad), the rule
+ * the paper scales to Qwen2.5-7B with PRIME-RL (§6; Table 5):
+ *   grad J = sum_j sum_t sg( w(lambda_t) (r_j - rbar - beta (log Lambda_j - mean log Lambda)) )
+ *            grad log pi_theta(y_t | x, y_<t)
+ *   lambda_t = pi_theta(y_t)/pi_gen(y_t) = exp(lp_t - gen_logp_t)      (per token)
+ *   log Lambda_j = log pi_theta(y_j|x) - log pi_ref(y_j|x) = seq_logp_j - ref_logp_j
+ * IS weight w (is_mode): TBA_IS_NONE w = 1; TBA_IS_CLIP w = clamp(lambda, is_lo, is_hi)
+ * (CISPO bounds 0/8, Table 5); TBA_IS_ICEPOP w = lambda inside [is_lo, is_hi], else 0
+ * (masking; reading R14). Normalisation (the paper's "GRPO-style",
+ * P:708): by the global number of valid tokens n_tok_global (reading R15). The value
+ * returned is the surrogate loss whose gradient is -grad J / n_tok_global:
+ *   partial = { -(1/n_tok_global) sum_{valid t} coef_t * lp_t, n_tok (this call), n_seq }
+ * Outputs: seq_logp [N], n_tokens [N], adv [N] (the bracket A_j), coef [N, T] fp32
+ * (w * A_j, 0 where masked). beta >= 0 (beta = 0 is Dr. GRPO); K >= 2. */
+enum tba_is_mode { TBA_IS_NONE = 0, TBA_IS_CLIP = 1, TBA_IS_ICEPOP = 2 };
+
+int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp /* [N, T] fp32, pi_gen log-probs */,
+                      const double* ref_logp, const double* log_reward, double beta, int32_t K, int32_t is_mode,
+                      double is_lo, double is_hi, double n_tok_global, void* workspace, double* seq_logp,
+                      int32_t* n_tokens, double* adv, float* coef, double* partial, int32_t* dev_status,
+                      tba_stream_t stream);
+
+/* dlogits for the TBA' surrogate: dz_{s,t,v} = mu * grad_scale * g * coef_{s,t} (1[v=y] - softmax_v)
+ * with grad_scale = -1 / n_tok_global; otherwise as tba_vargrad_tb_loss_bwd. */
+int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coef, double grad_scale,
+                      const double* grad_out, void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride,
+                      tba_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

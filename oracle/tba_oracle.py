@@ -24,6 +24,9 @@ the closed form log Z = log(0.5e + 0.5) at pi_theta = pi* (Eq. 2); softmax rows 
 within 1e-12; shift invariance; scipy's logsumexp; brute-force products of
 probabilities; L = mean within-group population variance; per-group shift invariance;
 the independent Appendix-A advantage form; central finite differences of the loss.
+TBA' (Eq. 16) pins (tests/test_oracle_tbap.py): Dr. GRPO equality at beta = 0 on-policy
+(P:616), the Eq. 7 / Eq. 16 link A = -beta*eps, clip/IcePop worked values, the band
+(0, inf) no-op, per-group shift invariance, finite differences with coefficients held fixed.
 Every function below is pinned by at least one of them ("parity unpinned": none).
 """
 from __future__ import annotations
@@ -182,6 +185,73 @@ def vargrad_head(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int
                partial=np.array([loss, float(N), float(N // K)]))
     if want_grad:
         out["dlogits"] = dlogits(logits, tokens, mask, eps, n, grad_out)
+    return out
+
+
+# ----------------------------------------------------------------------------- TBA' (NEXT 1)
+def is_weight(lam: float, mode: str, lo: float, hi: float) -> float:
+    """IS weight of Eq. 16: 'none' -> 1; 'clip' -> min(max(lam, lo), hi) (CISPO bounds 0/8,
+    Table 5; the display's min(lambda, 8)); 'icepop' -> lam inside [lo, hi] else 0
+    (masking the gradient of tokens with large or small ratios; R14)."""
+    if mode == "none":
+        return 1.0
+    if mode == "clip":
+        return min(max(lam, lo), hi)
+    if mode == "icepop":
+        return lam if lo <= lam <= hi else 0.0
+    raise ValueError(mode)
+
+
+def tbap_head(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, K: int, is_mode: str = "clip",
+              is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global: int | None = None, grad_out: float = 1.0,
+              want_grad: bool = True):
+    """TBA' token-level rule, Eq. 16, step by step in the paper's notation:
+      lambda_t = pi_theta(y_t)/pi_gen(y_t)                      per token
+      log Lambda_j = sum_t log(pi_theta(y_t)/pi_ref(y_t)) = ell_j - rho_j
+      A_j = (r_j - rbar) - beta (log Lambda_j - mean_j log Lambda)
+      grad J = sum_j sum_t sg(w(lambda_t) A_j) grad log pi_theta(y_t)
+    normalised by the number of valid tokens (GRPO-style; R15). Returns the
+    surrogate loss L' = -(1/n_tok) sum coef_t lp_t (whose gradient is -grad J / n_tok), ell,
+    n_tok, A, coef [N, T] and, if requested, dlogits = -(coef/n_tok) g (onehot - p)."""
+    if not (math.isfinite(beta) and beta >= 0):
+        raise ValueError("invalid-config: beta must be finite and >= 0")
+    N, T = tokens.shape
+    if K < 2:
+        raise ValueError("invalid-config: K must be >= 2")
+    if N % K:
+        raise ValueError("invalid-arg: N must be a multiple of K")
+    lp = np.zeros((N, T))
+    for s in range(N):
+        for t in range(T):
+            if mask[s, t]:
+                lp[s, t], _ = token_logprob(logits[s, t], int(tokens[s, t]))
+    ell = np.array([math.fsum(lp[s][mask[s] == 1]) for s in range(N)])
+    ntok = mask.sum(1).astype(np.int64)
+    ref = np.asarray(ref_logp, np.float64)
+    r = np.asarray(log_reward, np.float64)
+    A = np.empty(N)
+    for i in range(N // K):
+        sl = slice(i * K, (i + 1) * K)
+        logL = ell[sl] - ref[sl]
+        A[sl] = (r[sl] - r[sl].mean()) - beta * (logL - logL.mean())
+    coef = np.zeros((N, T))
+    for s in range(N):
+        for t in range(T):
+            if mask[s, t]:
+                lam = math.exp(lp[s, t] - float(gen_logp[s, t]))
+                coef[s, t] = is_weight(lam, is_mode, is_lo, is_hi) * A[s]
+    n = int(ntok.sum()) if n_tok_global is None else n_tok_global
+    terms = [coef[s, t] * lp[s, t] for s in range(N) for t in range(T) if mask[s, t]]
+    loss = -math.fsum(terms) / n
+    out = dict(lp=lp, ell=ell, n_tok=ntok, adv=A, coef=coef, loss=loss,
+               partial=np.array([loss, float(ntok.sum()), float(N)]))
+    if want_grad:
+        d = np.zeros(logits.shape)
+        for s in range(N):
+            for t in range(T):
+                if mask[s, t]:
+                    d[s, t] = -(coef[s, t] / n) * grad_out * grad_logprob_row(logits[s, t], int(tokens[s, t]))
+        out["dlogits"] = d
     return out
 
 

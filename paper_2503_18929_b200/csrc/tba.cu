@@ -669,6 +669,114 @@ __global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, c
   }
 }
 
+// ------------------------------------------------------------------------------ TBA' head (Eq. 16)
+// One CTA per group of K sequences. Warps sum token log-probs per sequence (as seq_head), then
+// thread 0 forms A_j = (r_j - rbar) - beta (log Lambda_j - mean log Lambda), log Lambda_j =
+// ell_j - rho_j; then every thread walks the group's valid rows: lambda_t = exp(lp_t - gen_t),
+// w = IS weight (none / clip [lo, hi] / IcePop band), coef_t = w * A_j (stop-gradient: a plain
+// number), and the surrogate term coef_t * lp_t. Fixed-order fp64 sums; last CTA reduces.
+
+__global__ void __launch_bounds__(256) tbap_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
+                                                 const float* __restrict__ gen_logp, int64_t n_seq, int64_t T, int K,
+                                                 const double* __restrict__ ref_logp,
+                                                 const double* __restrict__ log_reward, double beta, int is_mode,
+                                                 double is_lo, double is_hi, double neg_inv_ntok,
+                                                 double* __restrict__ seq_logp, int32_t* __restrict__ n_tokens,
+                                                 double* __restrict__ adv, float* __restrict__ coef,
+                                                 double* __restrict__ group_acc, double* __restrict__ partial,
+                                                 unsigned int* counter) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s0 = (int64_t)blockIdx.x * K;
+  __shared__ int sm_cnt[8];
+  int my_cnt = 0;
+  for (int j = warp; j < K; j += 8) {
+    const int64_t s = s0 + j;
+    double acc = 0.0;
+    int cnt = 0;
+    for (int64_t t = lane; t < T; t += 32) {
+      const int64_t r = s * T + t;
+      if (mask[r]) {
+        acc += lp[r];
+        ++cnt;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane == 0) {
+      seq_logp[s] = acc;
+      n_tokens[s] = cnt;
+    }
+    my_cnt += cnt;
+  }
+  if (lane == 0) sm_cnt[warp] = my_cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double rbar = 0.0, lbar = 0.0;
+    for (int j = 0; j < K; ++j) {
+      rbar += log_reward[s0 + j];
+      lbar += seq_logp[s0 + j] - ref_logp[s0 + j];
+    }
+    rbar /= (double)K;
+    lbar /= (double)K;
+    for (int j = 0; j < K; ++j)
+      adv[s0 + j] = (log_reward[s0 + j] - rbar) - beta * ((seq_logp[s0 + j] - ref_logp[s0 + j]) - lbar);
+  }
+  __syncthreads();
+  // token coefficients and the surrogate sum, rows strided over the CTA in a fixed order
+  double acc = 0.0;
+  const int64_t nr = (int64_t)K * T, r0 = s0 * T;
+  for (int64_t i = threadIdx.x; i < nr; i += 256) {
+    const int64_t r = r0 + i;
+    float cf = 0.f;
+    if (mask[r]) {
+      const double l = lp[r];
+      const double lam = exp(l - (double)gen_logp[r]);
+      double wgt = 1.0;
+      if (is_mode == TBA_IS_CLIP) wgt = fmin(fmax(lam, is_lo), is_hi);
+      else if (is_mode == TBA_IS_ICEPOP) wgt = (lam >= is_lo && lam <= is_hi) ? lam : 0.0;
+      const double c = wgt * adv[r / T];
+      cf = (float)c;
+      acc += c * l;
+    }
+    coef[r] = cf;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double sm_acc[8];
+  __shared__ bool am_last;
+  if (lane == 0) sm_acc[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    int n = 0;
+    for (int w = 0; w < 8; ++w) {
+      g += sm_acc[w];
+      n += sm_cnt[w];
+    }
+    group_acc[2 * blockIdx.x] = g;
+    group_acc[2 * blockIdx.x + 1] = (double)n;
+    __threadfence();
+    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* ga = group_acc;
+    double tot = 0.0, ntok = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) {
+      tot += ga[2 * i];
+      ntok += ga[2 * i + 1];
+    }
+    partial[0] = tot * neg_inv_ntok;
+    partial[1] = ntok;
+    partial[2] = (double)n_seq;
+    *counter = 0u;
+  }
+}
+
 // ------------------------------------------------------------------------------ a5
 template <class TO> struct Out;
 template <> struct Out<uint16_t> {
@@ -760,17 +868,19 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
   }
 }
 
-template <class T, class TO, int NT, int U, bool WARP>
-__global__ void __launch_bounds__(NT) row_bwd(const T* __restrict__ logits, int64_t rows, int64_t T_len, int64_t V,
+// TPR threads per row, 256/TPR rows per CTA. The row coefficient is grad_scale * g * resid[s]
+// (VarGrad TB, per sequence) or grad_scale * g * coef[row] (per-token rules, e.g. TBA', Eq. 16).
+template <class T, class TO, int TPR, int U, bool PER_ROW>
+__global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int64_t rows, int64_t T_len, int64_t V,
                                                int64_t stride, const int64_t* __restrict__ tokens,
                                                const uint8_t* __restrict__ mask, const float2* __restrict__ stats,
-                                               const double* __restrict__ resid, double grad_scale,
-                                               const double* __restrict__ grad_out, TO* __restrict__ dlogits,
-                                               int64_t ostride) {
-  const int64_t row = WARP ? (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5) : (int64_t)blockIdx.x;
+                                               const double* __restrict__ resid, const float* __restrict__ coef,
+                                               double grad_scale, const double* __restrict__ grad_out,
+                                               TO* __restrict__ dlogits, int64_t ostride) {
+  constexpr int RPC = 256 / TPR;
+  const int64_t row = (int64_t)blockIdx.x * RPC + threadIdx.x / TPR;
   if (row >= rows) return;
-  const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x;
-  const int nthr = WARP ? 32 : NT;
+  const int tid = threadIdx.x % TPR;
   const bool valid = mask[row] != 0;
   float M2 = 0.f, L2S = 0.f, c = 0.f;
   int64_t y = -1;
@@ -779,10 +889,10 @@ __global__ void __launch_bounds__(NT) row_bwd(const T* __restrict__ logits, int6
     M2 = st.x;
     L2S = st.y;
     const double g = grad_out ? *grad_out : 1.0;
-    c = (float)(grad_scale * g * resid[row / T_len]);
+    c = PER_ROW ? (float)(grad_scale * g * (double)coef[row]) : (float)(grad_scale * g * resid[row / T_len]);
     y = tokens[row];
   }
-  bwd_row<T, TO, U>(logits + row * stride, dlogits + row * ostride, V, tid, nthr, valid, M2, L2S, c, y);
+  bwd_row<T, TO, U>(logits + row * stride, dlogits + row * ostride, V, tid, TPR, valid, M2, L2S, c, y);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -1005,21 +1115,54 @@ int launch_fwd_rows(const tba_rows* x, const WsLayout& w, int32_t* dev_status, c
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
-template <class T, class TO>
-void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, double gs, const double* go, TO* out,
-                  int64_t ostride, cudaStream_t s) {
+int bwd_tpr_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TBA_BWD_TPR");
+    v = e ? atoi(e) : 0;  // 0 = auto
+  }
+  return v;
+}
+
+int bwd_tpr(int64_t V, int64_t esz) {
+  const int env = bwd_tpr_env();
+  if (env == 32 || env == 64 || env == 128 || env == 256) return env;
+  return V * esz <= kWarpRowMaxBytes ? 32 : 256;
+}
+
+template <class T, class TO, bool PER_ROW>
+void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, const float* coef, double gs,
+                  const double* go, TO* out, int64_t ostride, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
-  const bool warp = x->vocab * (int64_t)sizeof(T) <= kWarpRowMaxBytes;
+  const int tpr = bwd_tpr(x->vocab, (int64_t)sizeof(T));
+  const int64_t rpc = 256 / tpr;
+  const unsigned grid = (unsigned)((rows + rpc - 1) / rpc);
   auto lg = static_cast<const T*>(x->logits);
-  if (warp) {
-    const int64_t grid = (rows + kNT / 32 - 1) / (kNT / 32);
-    row_bwd<T, TO, kNT, kU, true><<<(unsigned)grid, kNT, 0, s>>>(lg, rows, x->seq_len, x->vocab, x->row_stride,
-                                                                 x->tokens, x->mask, w.stats, resid, gs, go, out,
-                                                                 ostride);
+#define TBA_BWD(TPR_)                                                                                              \
+  row_bwd<T, TO, TPR_, kU, PER_ROW><<<grid, 256, 0, s>>>(lg, rows, x->seq_len, x->vocab, x->row_stride, x->tokens, \
+                                                        x->mask, w.stats, resid, coef, gs, go, out, ostride)
+  switch (tpr) {
+    case 32: TBA_BWD(32); break;
+    case 64: TBA_BWD(64); break;
+    case 128: TBA_BWD(128); break;
+    default: TBA_BWD(256); break;
+  }
+#undef TBA_BWD
+}
+
+template <bool PER_ROW>
+void launch_bwd(const tba_rows* x, const WsLayout& w, const double* resid, const float* coef, double gs,
+                const double* go, void* dlogits, int32_t odt, int64_t ostride, cudaStream_t s) {
+  if (x->dtype == TBA_BF16) {
+    if (odt == TBA_BF16)
+      launch_bwd_t<uint16_t, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, static_cast<uint16_t*>(dlogits), ostride, s);
+    else
+      launch_bwd_t<uint16_t, float, PER_ROW>(x, w, resid, coef, gs, go, static_cast<float*>(dlogits), ostride, s);
   } else {
-    row_bwd<T, TO, kNT, kU, false><<<(unsigned)rows, kNT, 0, s>>>(lg, rows, x->seq_len, x->vocab, x->row_stride,
-                                                                  x->tokens, x->mask, w.stats, resid, gs, go, out,
-                                                                  ostride);
+    if (odt == TBA_BF16)
+      launch_bwd_t<float, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, static_cast<uint16_t*>(dlogits), ostride, s);
+    else
+      launch_bwd_t<float, float, PER_ROW>(x, w, resid, coef, gs, go, static_cast<float*>(dlogits), ostride, s);
   }
 }
 
@@ -1111,21 +1254,64 @@ int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const doub
     return TBA_ERR_INVALID_ARG;  // aliasing is only supported element-for-element
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
-  if (x->dtype == TBA_BF16) {
-    if (dlogits_dtype == TBA_BF16)
-      launch_bwd_t<uint16_t, uint16_t>(x, w, resid, grad_scale, grad_out, static_cast<uint16_t*>(dlogits),
-                                       dlogits_row_stride, s);
-    else
-      launch_bwd_t<uint16_t, float>(x, w, resid, grad_scale, grad_out, static_cast<float*>(dlogits),
-                                    dlogits_row_stride, s);
-  } else {
-    if (dlogits_dtype == TBA_BF16)
-      launch_bwd_t<float, uint16_t>(x, w, resid, grad_scale, grad_out, static_cast<uint16_t*>(dlogits),
-                                    dlogits_row_stride, s);
-    else
-      launch_bwd_t<float, float>(x, w, resid, grad_scale, grad_out, static_cast<float*>(dlogits), dlogits_row_stride,
-                                 s);
-  }
+  launch_bwd<false>(x, w, resid, nullptr, grad_scale, grad_out, dlogits, dlogits_dtype, dlogits_row_stride, s);
+  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+
+int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
+                      double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
+                      void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef, double* partial,
+                      int32_t* dev_status, tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta >= 0.0)) return TBA_ERR_INVALID_CONFIG;  // beta = 0 is Dr. GRPO
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  if (is_mode != TBA_IS_NONE && is_mode != TBA_IS_CLIP && is_mode != TBA_IS_ICEPOP) return TBA_ERR_INVALID_CONFIG;
+  if (is_mode != TBA_IS_NONE && !(is_lo >= 0.0 && is_hi >= is_lo && !std::isnan(is_hi)))
+    return TBA_ERR_INVALID_CONFIG;
+  int rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_tok_global) && n_tok_global > 0.0)) return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)  // a rank with zero groups contributes zero partials
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || !gen_logp || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv || !coef)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(gen_logp) % 4 ||
+      reinterpret_cast<uintptr_t>(coef) % 4)
+    return TBA_ERR_INVALID_ARG;
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  rc = launch_fwd_rows(x, w, dev_status, s);
+  if (rc) return rc;
+  const int64_t groups = x->n_seq / K;
+  tbap_head<<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, gen_logp, x->n_seq, x->seq_len, K, ref_logp, log_reward,
+                                            beta, is_mode, is_lo, is_hi, -1.0 / n_tok_global, seq_logp, n_tokens, adv,
+                                            coef, w.group_sq, partial, w.counter);
+  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coef, double grad_scale,
+                      const double* grad_out, void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride,
+                      tba_stream_t stream) {
+  int rc = validate_rows(x);
+  if (rc) return rc;
+  if (dlogits_dtype != TBA_BF16 && dlogits_dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
+  if (dlogits_row_stride < x->vocab) return TBA_ERR_INVALID_ARG;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows == 0) return TBA_OK;
+  const int64_t oesz = dlogits_dtype == TBA_BF16 ? 2 : 4;
+  if (dlogits_row_stride > INT64_MAX / 8 / oesz / rows) return TBA_ERR_INVALID_ARG;
+  if (!workspace || !coef || !dlogits) return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(dlogits) % oesz)
+    return TBA_ERR_INVALID_ARG;
+  if (dlogits == x->logits && (dlogits_dtype != x->dtype || dlogits_row_stride != x->row_stride))
+    return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
+  launch_bwd<true>(x, w, nullptr, coef, grad_scale, grad_out, dlogits, dlogits_dtype, dlogits_row_stride, s);
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 

@@ -202,3 +202,109 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
     loss = VarGradTBLoss.apply(logits, tokens, mask, ref_logp, log_reward, float(beta), int(K),
                                float(n_seq_global), group, dlogits_dtype, aux)
     return (loss, aux) if return_aux else loss
+
+
+# ----------------------------------------------------------------------------- TBA' (Eq. 16)
+_IS = {"none": 0, "clip": 1, "icepop": 2}
+
+
+class _TbapFwd:
+    """Outputs of one tba_tbap_loss_fwd call (device tensors)."""
+
+    def __init__(self, N, T, dev):
+        self.seq_logp = torch.empty(N, dtype=torch.float64, device=dev)
+        self.n_tokens = torch.empty(N, dtype=torch.int32, device=dev)
+        self.adv = torch.empty(N, dtype=torch.float64, device=dev)
+        self.coef = torch.empty((N, T), dtype=torch.float32, device=dev)
+        self.partial = torch.empty(3, dtype=torch.float64, device=dev)
+
+
+def tbap_fwd(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, K: int, is_mode: str = "clip",
+             is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global: float | None = None, workspace=None,
+             out: _TbapFwd | None = None, check_status: bool = _CHECK):
+    """Raw TBA' forward (tba_tbap_loss_fwd, Eq. 16). gen_logp: fp32 [N, T] log-probs of the
+    generating policy. n_tok_global defaults to this call's valid-token count (host sync)."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    N, T = tokens.shape
+    dev = logits.device
+    if gen_logp.shape != (N, T) or gen_logp.dtype != torch.float32 or not gen_logp.is_contiguous():
+        raise ValueError("gen_logp must be a contiguous fp32 [N, T] tensor")
+    for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
+        if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    if n_tok_global is None:
+        n_tok_global = max(int(mask.sum().item()), 1)
+    o = out or _TbapFwd(N, T, dev)
+    ws = workspace if workspace is not None else _workspace(dev, N, T)
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_tbap_loss_fwd(ctypes.byref(x), gen_logp.data_ptr(), ref_logp.data_ptr(), log_reward.data_ptr(),
+                                  float(beta), int(K), _IS[is_mode], float(is_lo), float(is_hi), float(n_tok_global),
+                                  ws.data_ptr(), o.seq_logp.data_ptr(), o.n_tokens.data_ptr(), o.adv.data_ptr(),
+                                  o.coef.data_ptr(), o.partial.data_ptr(), _ptr(st), _stream(dev)),
+              "tba_tbap_loss_fwd")
+    if st is not None:
+        _raise_dev_status(st, "tba_tbap_loss_fwd")
+    return o, ws
+
+
+def tbap_bwd(logits, tokens, mask, workspace, coef, n_tok_global: float, grad_out=None, dlogits=None,
+             dlogits_dtype=None):
+    """Raw TBA' backward (tba_tbap_loss_bwd): dz = -(coef / n_tok_global) * g * (onehot - p)."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    dev = logits.device
+    if dlogits is None:
+        dlogits = torch.empty(logits.shape, dtype=dlogits_dtype or logits.dtype, device=dev)
+    N, T, V = dlogits.shape
+    ors = dlogits.stride(1) if T > 1 else (dlogits.stride(0) if N > 1 else V)
+    if grad_out is not None:
+        grad_out = grad_out.to(device=dev, dtype=torch.float64).contiguous()
+    with torch.cuda.device(dev):
+        check(L.tba_tbap_loss_bwd(ctypes.byref(x), workspace.data_ptr(), coef.data_ptr(), -1.0 / float(n_tok_global),
+                                  _ptr(grad_out), dlogits.data_ptr(), _DT[dlogits.dtype], max(ors, V), _stream(dev)),
+              "tba_tbap_loss_bwd")
+    return dlogits
+
+
+class TBAPrimeLoss(torch.autograd.Function):
+    """Surrogate loss of the TBA' rule (Eq. 16); backward writes dlogits in one fused pass."""
+
+    @staticmethod
+    def forward(ctx, logits, tokens, mask, gen_logp, ref_logp, log_reward, beta, K, is_mode, is_lo, is_hi, n_tok,
+                group, dlogits_dtype, aux):
+        o, ws = tbap_fwd(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta, K, is_mode, is_lo, is_hi, n_tok)
+        if group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
+        ctx.save_for_backward(logits, tokens, mask, ws, o.coef)
+        ctx.n_tok = n_tok
+        ctx.dlogits_dtype = dlogits_dtype
+        if aux is not None:
+            aux.update(seq_logp=o.seq_logp, n_tokens=o.n_tokens, adv=o.adv, coef=o.coef, partial=o.partial)
+        return o.partial[0]
+
+    @staticmethod
+    def backward(ctx, grad):
+        logits, tokens, mask, ws, coef = ctx.saved_tensors
+        d = tbap_bwd(logits, tokens, mask, ws, coef, ctx.n_tok, grad_out=grad, dlogits_dtype=ctx.dlogits_dtype)
+        return (d,) + (None,) * 14
+
+
+def tbap_loss(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, K: int, *, is_mode: str = "clip",
+              is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global=None, group=None, dlogits_dtype=None,
+              return_aux: bool = False):
+    """TBA' (Eq. 16) as an autograd-enabled surrogate loss. Defaults follow Table 5
+    (CISPO IS bounds 0/8). n_tok_global (GRPO-style normaliser) defaults to the valid-token
+    count of all ranks (one host sync + one all-reduce when `group` is given)."""
+    if n_tok_global is None:
+        n = mask.sum().to(torch.float64).reshape(1)
+        if group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(n, group=group)
+        n_tok_global = max(float(n.item()), 1.0)
+    aux = {} if return_aux else None
+    loss = TBAPrimeLoss.apply(logits, tokens, mask, gen_logp, ref_logp, log_reward, float(beta), int(K), is_mode,
+                              float(is_lo), float(is_hi), float(n_tok_global), group, dlogits_dtype, aux)
+    return (loss, aux) if return_aux else loss

@@ -291,3 +291,33 @@ def fill_logits_cuda(out, seed: int, row0: int, V: int, stream: int | None = Non
     if rc:
         raise RuntimeError(f"tba_synth_logits failed ({rc})")
     return out
+
+
+# ----------------------------------------------------------------------------- TBA' inputs
+S_GEN, S_GEN_OUT = 8, 9
+
+
+def gen_logp(w: Workload, seed: int, seq0: int = 0, n: int | None = None) -> np.ndarray:
+    """Per-token log-probs of the GENERATING policy pi_gen (TBA', Eq. 16: lambda_t =
+    pi_theta/pi_gen), fp32 [n, T], 0 where masked. Modelled without any softmax: the stored
+    logit of the sampled token minus the generator's expected log-partition (ln V + 2.65),
+    plus U(-0.2, 0.2) policy drift, and on 2% of tokens a +-3 outlier (lambda ~ 20 or 0.05)
+    so that IS clipping / IcePop masking are exercised."""
+    n = w.N if n is None else n
+    tok, mask = tokens_and_mask(w, seed, seq0, n)
+    rows = (np.arange(seq0, seq0 + n, dtype=np.int64)[:, None] * w.T + np.arange(w.T)[None, :]).reshape(-1)
+    y = raw_tokens(seed, w.V, rows.astype(np.uint64))
+    h = hash64(seed, S_LOGITS, rows.astype(np.uint64) * np.uint64(w.V) + y.astype(np.uint64))
+    acc = np.zeros(h.shape, dtype=np.int64)
+    for k in range(4):
+        acc += ((h >> np.uint64(16 * k)) & np.uint64(0xFFFF)).astype(np.int64)
+    z = ((acc - 131070).astype(np.float64) * (2.0 ** -14)).astype(np.float32)
+    z = (z + peak_of(seed, rows.astype(np.uint64))).astype(np.float32)
+    if w.dtype == "bf16":
+        z = bf16_bits_to_f64(f32_to_bf16_bits(z))
+    u = unit24(hash64(seed, S_GEN, rows.astype(np.uint64)))
+    out_sel = mulhi_u64(hash64(seed, S_GEN_OUT, rows.astype(np.uint64)), 100)
+    drift = -0.2 + 0.4 * u
+    drift = np.where(out_sel == 0, 3.0, np.where(out_sel == 1, -3.0, drift))
+    g = (z.astype(np.float64) - (math.log(w.V) + 2.65) + drift).astype(np.float32).reshape(n, w.T)
+    return np.where(mask == 1, g, np.float32(0.0)).astype(np.float32)
