@@ -24,7 +24,8 @@
  * Errors. Host-side validation happens before any CUDA call and returns synchronously:
  *   TBA_ERR_INVALID_ARG    null pointer, negative size, row_stride < vocab, n_seq % K != 0,
  *                          unknown dtype, misaligned pointer, 64-bit size overflow;
- *   TBA_ERR_INVALID_CONFIG beta <= 0 or non-finite, K < 2;
+ *   TBA_ERR_INVALID_CONFIG beta <= 0 or non-finite, K < 2, bad IS mode or
+ *                          temperature;
  *   TBA_ERR_CUDA           a launch failed (cudaGetLastError()).
  * Device-side conditions are reported asynchronously by atomicOr into *dev_status
  * (nullable): TBA_DEV_TOKEN_RANGE — a token outside [0, vocab) at a valid position (S:50
@@ -108,6 +109,33 @@ int tba_vargrad_tb_loss_fwd(const tba_rows* x, const double* ref_logp, const dou
 int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const double* resid,
                             double grad_scale, const double* grad_out, void* dlogits,
                             int32_t dlogits_dtype, int64_t dlogits_row_stride, tba_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Trajectory-balance head variants. The two calls above are these with
+ * opts = NULL (VarGrad estimate, inv_temp = 1).
+ *   log_z_param = NULL : log Z_i is the VarGrad K-sample estimate of Eq. 4, detached;
+ *   log_z_param != NULL: log Z_i is a learned per-prompt scalar, Eq. 3 (the RT
+ *                        trainer lineage of Lee et al.); resid uses it, log_z echoes it,
+ *                        and tba_tb_loss_bwd returns dL/dlog Z_i = grad_scale * g * sum_j eps.
+ *   inv_temp           : log pi = log softmax(inv_temp * z) (temperature-scaled policy; the
+ *                        generation temperatures of P:511); must be finite and > 0, and
+ *                        the same in the fwd and the matching bwd. 1.0 = the policy itself. */
+typedef struct tba_tb_opts {
+  double        inv_temp;
+  const double* log_z_param; /* [n_seq/K] device fp64 or NULL */
+} tba_tb_opts;
+
+int tba_tb_loss_fwd(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                    const double* log_reward, double beta, int32_t K, double n_seq_global,
+                    void* workspace, double* seq_logp, int32_t* n_tokens, double* log_z,
+                    double* resid, double* partial, int32_t* dev_status, tba_stream_t stream);
+
+/* dz = mu * grad_scale * g * inv_temp * resid_s * (1[v=y] - softmax(inv_temp z)_v); d_log_z
+ * (nullable, [n_seq/K]) receives dL/dlog Z for a learned log Z (K needed only then). */
+int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* workspace,
+                    const double* resid, double grad_scale, const double* grad_out, void* dlogits,
+                    int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z, int32_t K,
+                    tba_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
  * TBA' token-level update: Eq. 16 (eq:tbaGrad), the rule

@@ -173,19 +173,43 @@ def dlogits_row(z, y: int, eps_s: float, n_global: int, grad_out: float = 1.0) -
 
 # ----------------------------------------------------------------------------- full head
 def vargrad_head(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int,
-                 n_global: int | None = None, grad_out: float = 1.0, want_grad: bool = True):
+                 n_global: int | None = None, grad_out: float = 1.0, want_grad: bool = True,
+                 inv_temp: float = 1.0, log_z=None):
     """Steps a1-a5 of SURVEY §8(a) on one (shard of a) batch. Returns a dict with
     ell, n_tok, log_z, eps, loss (normalised by n_global), partial = [sum eps^2 / n_global,
-    N, B], and dlogits (fp64) if requested."""
-    ell, ntok, lse = seq_logprob(logits, tokens, mask)
+    N, B], and dlogits (fp64) if requested.
+
+    Variants: ``inv_temp`` a: log pi = log softmax(a z), so the chain
+    rule gives dz = a (2 eps/N) g (onehot - softmax(a z)); ``log_z`` (length B): a learned
+    log Z(x_i) (Eq. 3) replaces the Eq. 4 estimate, and d_log_z = sum_j 2 eps/N g."""
+    scaled = np.asarray(logits, np.float64) * inv_temp
+    ell, ntok, lse = seq_logprob(scaled, tokens, mask)
     N = len(ell)
     n = N if n_global is None else n_global
-    loss, logz, eps = vargrad_tb_loss(ell, ref_logp, log_reward, beta, K, n)
+    if log_z is None:
+        loss, logz, eps = vargrad_tb_loss(ell, ref_logp, log_reward, beta, K, n)
+    else:
+        loss, logz, eps = tb_learned_z_loss(ell, ref_logp, log_reward, beta, K, log_z, n)
     out = dict(ell=ell, n_tok=ntok, lse=lse, log_z=logz, eps=eps, loss=loss,
                partial=np.array([loss, float(N), float(N // K)]))
+    if log_z is not None:
+        out["d_log_z"] = np.array([2.0 * math.fsum(eps[i * K:(i + 1) * K]) / n * grad_out for i in range(N // K)])
     if want_grad:
-        out["dlogits"] = dlogits(logits, tokens, mask, eps, n, grad_out)
+        out["dlogits"] = inv_temp * dlogits(scaled, tokens, mask, eps, n, grad_out)
     return out
+
+
+def tb_learned_z_loss(ell, ref_logp, log_reward, beta: float, K: int, log_z, n_global: int | None = None):
+    """Eq. 3 with R(y;x) = pi_ref(y|x) exp(r/beta), averaged over the batch
+    like Eq. 5: L = 1/(BK) sum_ij (log Z(x_i) + log pi_theta - log pi_ref - r/beta)^2 with a
+    learned log Z(x_i) (no stop-gradient). Returns (L, log_z, eps)."""
+    ell = np.asarray(ell, np.float64)
+    _check_config(len(ell), beta, K)
+    N = len(ell)
+    lz = np.asarray(log_z, np.float64)
+    eps = np.array([lz[s // K] + ell[s] - float(ref_logp[s]) - float(log_reward[s]) / beta for s in range(N)])
+    n = N if n_global is None else n_global
+    return math.fsum(eps * eps) / n, lz.copy(), eps
 
 
 # ----------------------------------------------------------------------------- TBA' (NEXT 1)

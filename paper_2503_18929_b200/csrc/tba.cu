@@ -1,16 +1,18 @@
-// libtba.so — the VarGrad trajectory-balance loss head (TBA, arXiv 2503.18929) for B200.
+// libtba.so — the trajectory-balance loss head of TBA (arXiv 2503.18929) for B200 (sm_100a).
 //
 // Kernels:
-//   row_fwd   a1  stream each valid logits row from HBM once: online max + sum of
-//                 2^(z*log2e - M2) in one MUFU ex2 per element, gather z[y]; writes per-row
-//                 (M2, log2 S) and the token log-prob (fp64).
-//   seq_head  a2+a3  per-sequence fixed-order fp64 sum of token log-probs (log pi(y|x)),
-//                 token counts, then per group Eq. 4 log Z and the Eq. 5 residuals; the last
-//                 CTA reduces the per-group sums of squares in fixed order (no float atomics).
-//   row_bwd   a5  stream each valid row again: dz = c_s (1[v=y] - 2^(z*log2e - M2 - log2 S)),
-//                 c_s = grad_scale * grad_out * eps_s; masked rows are zero-filled unread.
-// All hot loops use 128-bit loads/stores (ld.global.nc.L1::no_allocate / st.global.cs),
-// per-thread fp32 partial sums folded into fp64 every 32 elements, fp64 row finalisation.
+//   row_fwd_rows  a1   stream each valid logits row from HBM once (TPR threads per row, 128-bit
+//                      loads): online max + sum of 2^(z*sc - R2) with one MUFU ex2 per element
+//                      (packed FFMA2/FADD2), gather z[y]; writes per-row (M2, log2 S) and the
+//                      token log-prob (fp64).
+//   row_fwd_tma   a1   alternative: persistent, warp-specialised, cp.async.bulk + mbarrier ring.
+//   seq_head      a2+a3 per-sequence fixed-order fp64 sums of token log-probs (log pi(y|x)) and
+//                      token counts; per group Eq. 4 log Z (or a learned log Z, Eq. 3) and the
+//                      Eq. 5 residuals; the last CTA reduces the per-group sums of squares.
+//   tbap_head     a2+a3' TBA' (Eq. 16): per-group advantages and per-token IS-weighted coefficients.
+//   row_bwd       a5   stream each valid row again: dz = c (1[v=y] - 2^(z*sc - M2 - log2 S)); c per
+//                      sequence (TB) or per token (TBA'); masked rows zero-filled without a read.
+// No float atomics: every output is bitwise reproducible run to run.
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
@@ -20,8 +22,16 @@
 
 namespace {
 
-constexpr float kL2E = 1.4426950408889634f;  // fp32(log2 e); rows are softmax'd at this exact scale
+constexpr float kL2E = 1.4426950408889634f;  // fp32(log2 e)
 constexpr double kLN2 = 0.69314718055994530942;
+constexpr float kSlack = 6.0f;  // nats a chunk max may exceed the running reference before a re-base
+
+// Row scaling: rows are soft-maxed as 2^(z * sc) with sc = fl(kL2E * inv_temp); slack is kSlack in
+// logit units (kSlack / inv_temp); inv_temp enters the log-prob and the gradient exactly (fp64).
+struct RowScale {
+  float sc, slack;
+  double inv_temp;
+};
 
 // ------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ float ex2(float x) {
@@ -43,24 +53,6 @@ __device__ __forceinline__ void stg_stream(uint4* p, uint4 v) {
                : "memory");
 }
 
-// element traits: 16-byte vector of VEC elements
-template <class T> struct Elem;
-template <> struct Elem<uint16_t> {  // bf16 stored as raw bits
-  static constexpr int VEC = 8;
-  __device__ __forceinline__ static float get(const uint4& v, int e) {
-    const uint32_t w = (&v.x)[e >> 1];
-    return __uint_as_float((e & 1) ? (w & 0xFFFF0000u) : (w << 16));
-  }
-  __device__ __forceinline__ static float load1(const uint16_t* p) { return __uint_as_float(((uint32_t)__ldg(p)) << 16); }
-  __device__ __forceinline__ static uint4 neg_inf() { return make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u); }
-};
-template <> struct Elem<float> {
-  static constexpr int VEC = 4;
-  __device__ __forceinline__ static float get(const uint4& v, int e) { return __uint_as_float((&v.x)[e]); }
-  __device__ __forceinline__ static float load1(const float* p) { return __ldg(p); }
-  __device__ __forceinline__ static uint4 neg_inf() { return make_uint4(0xFF800000u, 0xFF800000u, 0xFF800000u, 0xFF800000u); }
-};
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -71,83 +63,6 @@ __device__ __forceinline__ uint16_t to_bf16(float x) {
   uint16_t r;
   asm("{ .reg .b32 t; cvt.rn.bf16x2.f32 t, %1, %1; mov.b32 {%0, _}, t; }" : "=h"(r) : "f"(x));
   return r;
-}
-
-// row split: [0, head) scalar, [head, head + nvec*VEC) 16-byte vectors, rest scalar tail
-template <class T>
-__device__ __forceinline__ int64_t head_elems(const T* row, int64_t V) {
-  const uint64_t a = reinterpret_cast<uint64_t>(row);
-  int64_t h = (int64_t)(((16u - (a & 15u)) & 15u) / sizeof(T));
-  return h < V ? h : V;
-}
-
-// ------------------------------------------------------------------------------ fwd state
-// Per-thread online state over a part of one row (DESIGN.md §5.1):
-//   m  = max of the elements seen so far (exact),
-//   R  = the reference the partial sum is kept against, R2 = fl(R * kL2E),
-//   s  = sum of 2^(fl(z * kL2E - R2)) over the elements seen (fp64, folded every chunk).
-// The reference is only re-based when a chunk's max exceeds it by more than kSlack (nats), so
-// the fp64 rescale (exact exp2 of an fp32 difference) is rare; arguments of ex2 stay <= kSlack*log2e.
-constexpr float kSlack = 6.0f;
-
-struct OnlineState {
-  float m, R, R2;
-  double s;
-  __device__ __forceinline__ void init() {
-    m = -INFINITY;
-    R = -INFINITY;
-    R2 = 0.f;
-    s = 0.0;
-  }
-  __device__ __forceinline__ void chunk(float cm) {
-    m = fmaxf(m, cm);
-    if (cm > R + kSlack) {  // also taken for the first finite chunk (R = -inf)
-      const float R2n = cm * kL2E;
-      if (R == -INFINITY) {
-        s = 0.0;
-      } else {
-        s *= exp2((double)R2 - (double)R2n);
-      }
-      R = cm;
-      R2 = R2n;
-    }
-  }
-  __device__ __forceinline__ void add1(float z) {
-    chunk(z);
-    s += (double)ex2(fmaf(z, kL2E, -R2));
-  }
-};
-
-// Combine (m, R2, s) partial states held by the lanes of a warp; `active` lanes only.
-// Result (row max M, M2 = fl(M*kL2E), S = sum relative to M2) is returned in every lane.
-// The fp64 butterfly is fixed, so the bits do not depend on timing.
-__device__ __forceinline__ void combine_lanes(float m, float R2, double s, bool active, float& M, float& M2,
-                                              double& S) {
-  float mm = active ? m : -INFINITY;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
-  M = mm;
-  M2 = (mm == -INFINITY) ? 0.f : mm * kL2E;
-  double v = (active && s != 0.0) ? s * exp2((double)R2 - (double)M2) : (active ? s : 0.0);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  S = v;
-}
-
-__device__ __forceinline__ void finalize_row(float M, float M2, double S, float zy, bool tok_ok, int64_t row,
-                                             float2* __restrict__ stats, double* __restrict__ lp,
-                                             int32_t* dev_status) {
-  const bool finite = (M > -INFINITY) && (M < INFINITY) && (S > 0.0) && (S < INFINITY);
-  const double log2s = log2(S);
-  stats[row] = make_float2(M2, (float)log2s);
-  // lp = (z_y - M) - ln sum_v e^{kappa (z_v - M)},  kappa = kL2E / log2(e)
-  double v = ((double)zy - (double)M) - kLN2 * (log2s + (double)M2 - (double)M * (double)kL2E);
-  if (!tok_ok) v = nan("");
-  lp[row] = v;
-  if (dev_status) {
-    int f = (tok_ok ? 0 : TBA_DEV_TOKEN_RANGE) | (finite ? 0 : TBA_DEV_NONFINITE_ROW);
-    if (f) atomicOr(dev_status, f);
-  }
 }
 
 // packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2)
@@ -169,23 +84,16 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
-__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 
 // 2^x for a pair of fp32 on the FMA pipe (offloads MUFU.EX2, which the forward saturates first):
 // Cody-Waite split x = n + f, |f| <= 1/2, by the 1.5*2^23 rounding trick; degree-5 minimax
-// polynomial for 2^f (max relative error 2.3e-7 with fp32 Horner, same order as ex2.approx);
-// 2^n by adding n to the exponent field. Inputs are clamped at -125 (2^-125 is below every sum
-// it could enter; ex2.approx.ftz flushes there too).
+// polynomial for 2^f (max relative error 2.3e-7 with fp32 Horner, the order of ex2.approx);
+// 2^n added to the exponent field. Inputs clamped at -125 (ex2.approx.ftz flushes there too).
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   float a, b;
   f2_unpack(x, a, b);
   const uint64_t xc = f2_pack(fmaxf(a, -125.f), fmaxf(b, -125.f));
-  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
-  const uint64_t t = fadd2(xc, magic);                             // n + 1.5*2^23 (round to nearest)
+  const uint64_t t = fadd2(xc, f2_pack(12582912.f, 12582912.f));    // n + 1.5*2^23 (round to nearest)
   const uint64_t n = fadd2(t, f2_pack(-12582912.f, -12582912.f));   // n exactly
   const uint64_t f = ffma2(n, f2_pack(-1.f, -1.f), xc);             // x - n, exact
   uint64_t p = ffma2(f2_pack(1.3276358367875218e-3f, 1.3276358367875218e-3f), f,
@@ -200,6 +108,97 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(plo + (tlo << 23)), "r"(phi + (thi << 23)));
   return r;
+}
+
+// element traits: 16-byte vector of VEC elements
+template <class T> struct Elem;
+template <> struct Elem<uint16_t> {  // bf16 stored as raw bits
+  static constexpr int VEC = 8;
+  __device__ __forceinline__ static float get(const uint4& v, int e) {
+    const uint32_t w = (&v.x)[e >> 1];
+    return __uint_as_float((e & 1) ? (w & 0xFFFF0000u) : (w << 16));
+  }
+  __device__ __forceinline__ static float load1(const uint16_t* p) { return __uint_as_float(((uint32_t)__ldg(p)) << 16); }
+};
+template <> struct Elem<float> {
+  static constexpr int VEC = 4;
+  __device__ __forceinline__ static float get(const uint4& v, int e) { return __uint_as_float((&v.x)[e]); }
+  __device__ __forceinline__ static float load1(const float* p) { return __ldg(p); }
+};
+
+// row split: [0, head) scalar, [head, head + nvec*VEC) 16-byte vectors, rest scalar tail
+template <class T>
+__device__ __forceinline__ int64_t head_elems(const T* row, int64_t V) {
+  const uint64_t a = reinterpret_cast<uint64_t>(row);
+  int64_t h = (int64_t)(((16u - (a & 15u)) & 15u) / sizeof(T));
+  return h < V ? h : V;
+}
+
+// ------------------------------------------------------------------------------ fwd state
+// Per-thread online state over a part of one row (DESIGN.md §5.1):
+//   m  = max of the elements seen (exact); R = the reference of the partial sum, R2 = fl(R * sc);
+//   s  = sum of 2^(fl(z * sc - R2)) over the elements seen (fp64, folded every chunk).
+// The reference is re-based only when a chunk max exceeds it by more than `slack` (kSlack nats),
+// so the fp64 rescale (exact exp2 of an fp32 difference) is rare and ex2 arguments stay <= 8.7.
+struct OnlineState {
+  float m, R, R2, sc, slack;
+  double s;
+  __device__ __forceinline__ void init(const RowScale& rs) {
+    m = -INFINITY;
+    R = -INFINITY;
+    R2 = 0.f;
+    sc = rs.sc;
+    slack = rs.slack;
+    s = 0.0;
+  }
+  __device__ __forceinline__ void chunk(float cm) {
+    m = fmaxf(m, cm);
+    if (cm > R + slack) {  // also taken for the first finite chunk (R = -inf)
+      const float R2n = cm * sc;
+      if (R == -INFINITY) {
+        s = 0.0;
+      } else {
+        s *= exp2((double)R2 - (double)R2n);
+      }
+      R = cm;
+      R2 = R2n;
+    }
+  }
+  __device__ __forceinline__ void add1(float z) {
+    chunk(z);
+    s += (double)ex2(fmaf(z, sc, -R2));
+  }
+};
+
+// Combine (m, R2, s) partial states held by the lanes of a warp (`active` lanes only). Result
+// (row max M, M2 = fl(M*sc), S = sum relative to M2) in every lane; fixed fp64 butterfly.
+__device__ __forceinline__ void combine_lanes(float m, float R2, double s, bool active, float sc, float& M, float& M2,
+                                              double& S) {
+  float mm = active ? m : -INFINITY;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+  M = mm;
+  M2 = (mm == -INFINITY) ? 0.f : mm * sc;
+  double v = (active && s != 0.0) ? s * exp2((double)R2 - (double)M2) : (active ? s : 0.0);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  S = v;
+}
+
+__device__ __forceinline__ void finalize_row(float M, float M2, double S, float zy, bool tok_ok, int64_t row,
+                                             const RowScale& rs, float2* __restrict__ stats,
+                                             double* __restrict__ lp, int32_t* dev_status) {
+  const bool finite = (M > -INFINITY) && (M < INFINITY) && (S > 0.0) && (S < INFINITY);
+  const double log2s = log2(S);
+  stats[row] = make_float2(M2, (float)log2s);
+  // lp = a (z_y - M) - ln sum_v e^{kappa a (z_v - M)},  a = inv_temp, kappa a = sc / log2(e)  (§5.1)
+  double v = rs.inv_temp * ((double)zy - (double)M) - kLN2 * (log2s + (double)M2 - (double)M * (double)rs.sc);
+  if (!tok_ok) v = nan("");
+  lp[row] = v;
+  if (dev_status) {
+    int f = (tok_ok ? 0 : TBA_DEV_TOKEN_RANGE) | (finite ? 0 : TBA_DEV_NONFINITE_ROW);
+    if (f) atomicOr(dev_status, f);
+  }
 }
 
 // Consume U 16-byte vectors of one row: chunk max, rare re-base, sum of 2^x (FFMA2 + MUFU + FADD2),
@@ -220,7 +219,7 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 #pragma unroll
     for (int e = 0; e < VEC; e += 2) cm = fmaxf(cm, fmaxf(z[u][e], z[u][e + 1]));
   st.chunk(cm);
-  const uint64_t l2e = f2_pack(kL2E, kL2E), nr2 = f2_pack(-st.R2, -st.R2);
+  const uint64_t l2e = f2_pack(st.sc, st.sc), nr2 = f2_pack(-st.R2, -st.R2);
   uint64_t acc[VEC / 2];
 #pragma unroll
   for (int p = 0; p < VEC / 2; ++p) acc[p] = 0ull;
@@ -248,7 +247,7 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 }
 
 // LDG-streamed partial state of one row over threads tid, tid+nthr, ...
-template <class T, int U, int NP = 0>
+template <class T, int U>
 __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_t V, int tid, int nthr,
                                                OnlineState& st) {
   using E = Elem<T>;
@@ -266,45 +265,7 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
     uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + k0 + (int64_t)u * nthr);
-    fwd_consume<T, U, NP>(v, st);
-  }
-  for (int64_t k = k0; k < nvec; k += nthr) {
-    uint4 v1[1] = {ldg_stream(vp + k)};
-    fwd_consume<T, 1>(v1, st);
-  }
-}
-
-// Same, with the next iteration's loads issued before the current vectors are consumed
-// (register double buffer): 2U 16-byte loads in flight per thread.
-template <class T, int U>
-__device__ __forceinline__ void fwd_accumulate_pf(const T* __restrict__ row, int64_t V, int tid, int nthr,
-                                                  OnlineState& st) {
-  using E = Elem<T>;
-  constexpr int VEC = E::VEC;
-  const int64_t h = head_elems(row, V);
-  const int64_t nvec = (V - h) / VEC;
-  const int64_t tail0 = h + nvec * VEC;
-  if (tid < h) st.add1(E::load1(row + tid));
-  for (int64_t i = tail0 + tid; i < V; i += nthr) st.add1(E::load1(row + i));
-  const uint4* vp = reinterpret_cast<const uint4*>(row + h);
-  const int64_t step = (int64_t)nthr * U;
-  const int64_t nfull = nvec / step;
-  int64_t k0 = tid;
-  if (nfull > 0) {
-    uint4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + k0 + (int64_t)u * nthr);
-    for (int64_t it = 1; it < nfull; ++it) {
-      k0 += step;
-      uint4 w[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) w[u] = ldg_stream(vp + k0 + (int64_t)u * nthr);
-      fwd_consume<T, U>(v, st);
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = w[u];
-    }
     fwd_consume<T, U>(v, st);
-    k0 += step;
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {ldg_stream(vp + k)};
@@ -312,61 +273,19 @@ __device__ __forceinline__ void fwd_accumulate_pf(const T* __restrict__ row, int
   }
 }
 
-// One CTA (NT threads) per row; the 8 warp partials are combined by warp 0's lanes in parallel.
-template <class T, int NT, int U, int MINB = 1, bool PF = false, int NP = 0>
-__global__ void __launch_bounds__(NT, MINB) row_fwd_cta(const T* __restrict__ logits, int64_t rows, int64_t V,
-                                                   int64_t stride, const int64_t* __restrict__ tokens,
-                                                   const uint8_t* __restrict__ mask, float2* __restrict__ stats,
-                                                   double* __restrict__ lp, int32_t* dev_status) {
-  constexpr int NW = NT / 32;
-  const int64_t row = blockIdx.x;
-  if (row >= rows || mask[row] == 0) return;
-  const T* rp = logits + row * stride;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float zy = 0.f;
-  bool ok = true;
-  if (threadIdx.x == 0) {
-    const int64_t y = tokens[row];
-    ok = (y >= 0 && y < V);
-    if (ok) zy = Elem<T>::load1(rp + y);
-  }
-  OnlineState st;
-  st.init();
-  if (PF)
-    fwd_accumulate_pf<T, U>(rp, V, threadIdx.x, NT, st);
-  else
-    fwd_accumulate<T, U, NP>(rp, V, threadIdx.x, NT, st);
-  float M, M2;
-  double S;
-  combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
-  __shared__ float sm_m[NW], sm_M2[NW];
-  __shared__ double sm_s[NW];
-  if (lane == 0) {
-    sm_m[warp] = M;
-    sm_M2[warp] = M2;
-    sm_s[warp] = S;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const bool act = lane < NW;
-    combine_lanes(act ? sm_m[lane] : -INFINITY, act ? sm_M2[lane] : 0.f, act ? sm_s[lane] : 0.0, act, M, M2, S);
-    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
-  }
-}
-
-// TPR threads per row, 256/TPR rows per CTA (TPR = 32 ... 256, a power of two). Rows of one CTA
-// are independent: each row group meets on its own named barrier (ids 1..8), masked rows skip
-// the stream but still take part in nothing else, so no thread returns early.
+// TPR threads per row, 256/TPR rows per CTA (TPR = 32 ... 256). Each row group meets on its own
+// named barrier (ids 1..8); a masked row's group exits as a whole.
 template <class T, int TPR, int U>
 __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                      int64_t stride, const int64_t* __restrict__ tokens,
-                                                     const uint8_t* __restrict__ mask, float2* __restrict__ stats,
-                                                     double* __restrict__ lp, int32_t* dev_status) {
+                                                     const uint8_t* __restrict__ mask, RowScale rs,
+                                                     float2* __restrict__ stats, double* __restrict__ lp,
+                                                     int32_t* dev_status) {
   constexpr int RPC = 256 / TPR, WPR = TPR / 32;
   const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
   const int lane = threadIdx.x & 31, wig = gt >> 5;
   const int64_t row = (int64_t)blockIdx.x * RPC + grp;
-  if (row >= rows || mask[row] == 0) return;  // uniform over the row group (named barriers are per group)
+  if (row >= rows || mask[row] == 0) return;
   const T* rp = logits + row * stride;
   float zy = 0.f;
   bool ok = true;
@@ -376,17 +295,17 @@ __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits
     if (ok) zy = Elem<T>::load1(rp + y);
   }
   OnlineState st;
-  st.init();
+  st.init(rs);
   fwd_accumulate<T, U>(rp, V, gt, TPR, st);
   float M, M2;
   double S;
-  combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
+  combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
   if (WPR == 1) {
-    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
+    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
     return;
   }
-  __shared__ float sm_m[RPC][WPR > 1 ? WPR : 1], sm_M2[RPC][WPR > 1 ? WPR : 1];
-  __shared__ double sm_s[RPC][WPR > 1 ? WPR : 1];
+  __shared__ float sm_m[RPC][WPR], sm_M2[RPC][WPR];
+  __shared__ double sm_s[RPC][WPR];
   if (lane == 0) {
     sm_m[grp][wig] = M;
     sm_M2[grp][wig] = M2;
@@ -396,42 +315,17 @@ __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits
   if (wig == 0) {
     const bool act = lane < WPR;
     combine_lanes(act ? sm_m[grp][lane] : -INFINITY, act ? sm_M2[grp][lane] : 0.f, act ? sm_s[grp][lane] : 0.0, act,
-                  M, M2, S);
-    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
-  }
-}
-
-// One warp per row, NT/32 rows per CTA (small vocabularies).
-template <class T, int NT, int U>
-__global__ void __launch_bounds__(NT) row_fwd_warp(const T* __restrict__ logits, int64_t rows, int64_t V,
-                                                    int64_t stride, const int64_t* __restrict__ tokens,
-                                                    const uint8_t* __restrict__ mask, float2* __restrict__ stats,
-                                                    double* __restrict__ lp, int32_t* dev_status) {
-  const int64_t row = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= rows || mask[row] == 0) return;  // warp-uniform
-  const T* rp = logits + row * stride;
-  OnlineState st;
-  st.init();
-  fwd_accumulate<T, U>(rp, V, lane, 32, st);
-  float M, M2;
-  double S;
-  combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
-  if (lane == 0) {
-    const int64_t y = tokens[row];
-    const bool ok = (y >= 0 && y < V);
-    const float zy = ok ? Elem<T>::load1(rp + y) : 0.f;
-    finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
+                  rs.sc, M, M2, S);
+    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
   }
 }
 
 // ------------------------------------------------------------------------------ a1, TMA-staged
-// Persistent, warp-specialised forward for long rows. One producer warp streams the 16-byte
-// aligned interior of every valid row through a STAGES-deep shared-memory ring with 1-D bulk
-// TMA copies (cp.async.bulk, mbarrier complete_tx, L2 evict_first); NCW consumer warps read
-// each tile once (LDS.128) and keep the online state in registers. Warps never wait for each
-// other at a row boundary: each posts its partial to a shared slot and the LAST warp to post
-// (shared-memory counter) combines the row, so the ring keeps streaming.
+// Persistent, warp-specialised forward for long rows (A/B alternative, TBA_FWD_IMPL=tma). One
+// producer lane streams the 16-byte aligned interior of every valid row through a STAGES-deep
+// shared-memory ring with 1-D bulk copies (cp.async.bulk, mbarrier complete_tx, L2 evict_first);
+// NCW consumer warps read each tile once. Warps never wait for each other at a row boundary:
+// each posts its partial to a shared slot and the LAST warp to post combines the row.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -468,14 +362,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 template <class T, int NCW, int TILE, int STAGES, int NP = 0>
 __global__ void __launch_bounds__((NCW + 1) * 32) row_fwd_tma(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                               int64_t stride, const int64_t* __restrict__ tokens,
-                                                              const uint8_t* __restrict__ mask,
+                                                              const uint8_t* __restrict__ mask, RowScale rs,
                                                               float2* __restrict__ stats, double* __restrict__ lp,
                                                               int32_t* dev_status) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   constexpr int NC = NCW * 32;
-  constexpr int TV = TILE / 16;  // vectors per tile
-  constexpr int U = TV / NC;     // vectors per consumer thread per full tile
+  constexpr int TV = TILE / 16;          // vectors per tile
+  constexpr int U = TV / NC;             // vectors per consumer thread per full tile
   constexpr int SLOTS = 2 * STAGES + 2;  // a warp is at most STAGES tiles (<= STAGES rows) ahead
   static_assert(TV % NC == 0 && U >= 1, "tile must split evenly over the consumer threads");
   static_assert(NCW <= 32, "");
@@ -534,7 +428,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) row_fwd_tma(const T* __restric
     const int64_t nvec = (V - h) / VEC;
     const int64_t bytes = nvec * 16;
     OnlineState st;
-    st.init();
+    st.init(rs);
     if (ct == 0) {
       const int64_t y = tokens[row];
       const bool ok = (y >= 0 && y < V);
@@ -568,7 +462,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) row_fwd_tma(const T* __restric
     }
     float M, M2;
     double S;
-    combine_lanes(st.m, st.R2, st.s, true, M, M2, S);
+    combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     unsigned prev = 0;
     if (lane == 0) {
       sm_m[slot][warp] = M;
@@ -584,11 +478,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32) row_fwd_tma(const T* __restric
       const volatile float* vm = sm_m[slot];
       const volatile float* vm2 = sm_M2[slot];
       const volatile double* vs = sm_s[slot];
-      combine_lanes(act ? vm[lane] : -INFINITY, act ? vm2[lane] : 0.f, act ? vs[lane] : 0.0, act, M, M2, S);
+      combine_lanes(act ? vm[lane] : -INFINITY, act ? vm2[lane] : 0.f, act ? vs[lane] : 0.0, act, rs.sc, M, M2, S);
       if (lane == 0) {
         const float zy = *(volatile float*)&sm_zy[slot];
         const bool ok = *(volatile int*)&sm_ok[slot] != 0;
-        finalize_row(M, M2, S, zy, ok, row, stats, lp, dev_status);
+        finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
         sm_cnt[slot] = 0;
       }
     }
@@ -597,19 +491,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32) row_fwd_tma(const T* __restric
 }
 
 // ------------------------------------------------------------------------------ a2 + a3
-// One CTA per group of K sequences (or per 8 sequences when !HEAD). Warps sum the token
-// log-probs of one sequence each in a fixed order (lane-strided fp64 + xor butterfly).
-template <bool HEAD>
-__global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
-                                                int64_t n_seq, int64_t T, int K, const double* __restrict__ ref_logp,
-                                                const double* __restrict__ log_reward, double inv_beta,
-                                                double inv_n_global, double* __restrict__ seq_logp,
-                                                int32_t* __restrict__ n_tokens, double* __restrict__ log_z,
-                                                double* __restrict__ resid, double* __restrict__ group_sq,
-                                                double* __restrict__ partial, unsigned int* counter) {
+// Per-sequence sums: warp w of a CTA takes sequences w, w+8, ... of the CTA's `per` sequences,
+// lane-strided fp64 partial sums over t in a fixed order, then a fixed xor butterfly.
+__device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
+                                         int64_t n_seq, int64_t T, int64_t s0, int per,
+                                         double* __restrict__ seq_logp, int32_t* __restrict__ n_tokens,
+                                         int* my_count) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int per = HEAD ? K : 8;
-  const int64_t s0 = (int64_t)blockIdx.x * per;
+  int tot = 0;
   for (int j = warp; j < per; j += 8) {
     const int64_t s = s0 + j;
     if (s >= n_seq) break;
@@ -631,18 +520,42 @@ __global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, c
       seq_logp[s] = acc;
       n_tokens[s] = cnt;
     }
+    tot += cnt;
   }
+  if (my_count) *my_count = tot;
+}
+
+// One CTA per group of K sequences (HEAD), or per 8 sequences (log-probs only).
+// Eq. 4: log Z_i = 1/K sum_j delta_j (delta = rho - ell + r/beta), or the learned log Z_i of
+// Eq. 3 when log_z_param != NULL; Eq. 5 residual eps = log Z_i - delta. The last CTA (counter)
+// reduces the per-group sums of squares in group order.
+template <bool HEAD>
+__global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
+                                                int64_t n_seq, int64_t T, int K, const double* __restrict__ ref_logp,
+                                                const double* __restrict__ log_reward,
+                                                const double* __restrict__ log_z_param, double inv_beta,
+                                                double inv_n_global, double* __restrict__ seq_logp,
+                                                int32_t* __restrict__ n_tokens, double* __restrict__ log_z,
+                                                double* __restrict__ resid, double* __restrict__ group_sq,
+                                                double* __restrict__ partial, unsigned int* counter) {
+  const int per = HEAD ? K : 8;
+  const int64_t s0 = (int64_t)blockIdx.x * per;
+  seq_sums(lp, mask, n_seq, T, s0, per, seq_logp, n_tokens, nullptr);
   if (!HEAD) return;
   __syncthreads();
   __shared__ bool am_last;
   if (threadIdx.x == 0) {
-    // Eq. 4: log Z_i = 1/K sum_j delta_j, delta = rho - ell + r/beta; Eq. 5 residual eps = log Z - delta
-    double sum = 0.0;
-    for (int j = 0; j < K; ++j) {
-      const int64_t s = s0 + j;
-      sum += ref_logp[s] - seq_logp[s] + log_reward[s] * inv_beta;
+    double lz;
+    if (log_z_param) {
+      lz = log_z_param[blockIdx.x];
+    } else {
+      double sum = 0.0;
+      for (int j = 0; j < K; ++j) {
+        const int64_t s = s0 + j;
+        sum += ref_logp[s] - seq_logp[s] + log_reward[s] * inv_beta;
+      }
+      lz = sum / (double)K;
     }
-    const double lz = sum / (double)K;
     double sq = 0.0;
     for (int j = 0; j < K; ++j) {
       const int64_t s = s0 + j;
@@ -670,12 +583,10 @@ __global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, c
 }
 
 // ------------------------------------------------------------------------------ TBA' head (Eq. 16)
-// One CTA per group of K sequences. Warps sum token log-probs per sequence (as seq_head), then
-// thread 0 forms A_j = (r_j - rbar) - beta (log Lambda_j - mean log Lambda), log Lambda_j =
-// ell_j - rho_j; then every thread walks the group's valid rows: lambda_t = exp(lp_t - gen_t),
-// w = IS weight (none / clip [lo, hi] / IcePop band), coef_t = w * A_j (stop-gradient: a plain
-// number), and the surrogate term coef_t * lp_t. Fixed-order fp64 sums; last CTA reduces.
-
+// One CTA per group: sequence sums as seq_head; thread 0 forms A_j = (r_j - rbar) -
+// beta (log Lambda_j - mean log Lambda) with log Lambda_j = ell_j - rho_j; every thread then
+// walks the group's rows: lambda_t = exp(lp_t - gen_t), IS weight w, coef_t = w * A_j (a
+// stop-gradient constant) and the surrogate term coef_t * lp_t, in a fixed order.
 __global__ void __launch_bounds__(256) tbap_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
                                                  const float* __restrict__ gen_logp, int64_t n_seq, int64_t T, int K,
                                                  const double* __restrict__ ref_logp,
@@ -689,28 +600,7 @@ __global__ void __launch_bounds__(256) tbap_head(const double* __restrict__ lp, 
   const int64_t s0 = (int64_t)blockIdx.x * K;
   __shared__ int sm_cnt[8];
   int my_cnt = 0;
-  for (int j = warp; j < K; j += 8) {
-    const int64_t s = s0 + j;
-    double acc = 0.0;
-    int cnt = 0;
-    for (int64_t t = lane; t < T; t += 32) {
-      const int64_t r = s * T + t;
-      if (mask[r]) {
-        acc += lp[r];
-        ++cnt;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    }
-    if (lane == 0) {
-      seq_logp[s] = acc;
-      n_tokens[s] = cnt;
-    }
-    my_cnt += cnt;
-  }
+  seq_sums(lp, mask, n_seq, T, s0, K, seq_logp, n_tokens, &my_cnt);
   if (lane == 0) sm_cnt[warp] = my_cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -725,7 +615,6 @@ __global__ void __launch_bounds__(256) tbap_head(const double* __restrict__ lp, 
       adv[s0 + j] = (log_reward[s0 + j] - rbar) - beta * ((seq_logp[s0 + j] - ref_logp[s0 + j]) - lbar);
   }
   __syncthreads();
-  // token coefficients and the surrogate sum, rows strided over the CTA in a fixed order
   double acc = 0.0;
   const int64_t nr = (int64_t)K * T, r0 = s0 * T;
   for (int64_t i = threadIdx.x; i < nr; i += 256) {
@@ -777,18 +666,26 @@ __global__ void __launch_bounds__(256) tbap_head(const double* __restrict__ lp, 
   }
 }
 
+// dL/d log Z_i for a learned log Z (Eq. 3): grad_scale * g * sum_j eps_{iK+j}.
+__global__ void dlogz_kernel(const double* __restrict__ resid, int64_t groups, int K, double grad_scale,
+                             const double* __restrict__ grad_out, double* __restrict__ d_log_z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= groups) return;
+  double s = 0.0;
+  for (int j = 0; j < K; ++j) s += resid[i * K + j];
+  d_log_z[i] = grad_scale * (grad_out ? *grad_out : 1.0) * s;
+}
+
 // ------------------------------------------------------------------------------ a5
 template <class TO> struct Out;
 template <> struct Out<uint16_t> {
-  static constexpr int VEC = 8;  // outputs per 16-byte store
   __device__ __forceinline__ static void put1(uint16_t* p, float x) { *p = to_bf16(x); }
 };
 template <> struct Out<float> {
-  static constexpr int VEC = 4;
   __device__ __forceinline__ static void put1(float* p, float x) { __stcs(p, x); }
 };
 
-// store VEC_IN computed values starting at o (16-byte aligned for the first element)
+// store N computed values starting at o (16-byte aligned)
 template <class TO, int N>
 __device__ __forceinline__ void store_vals(TO* o, const float (&d)[N]) {
   if constexpr (sizeof(TO) == 2) {
@@ -812,18 +709,18 @@ __device__ __forceinline__ void store_vals(TO* o, const float (&d)[N]) {
 
 template <class T, class TO, int U>
 __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid, int nthr,
-                                        bool valid, float M2, float L2S, float c, int64_t y) {
+                                        bool valid, float sc, float M2, float L2S, float c, int64_t y) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(rp, V);
-  // vector path needs the output 16-byte aligned at the same element as the input
+  // the vector path needs the output 16-byte aligned at the same element as the input
   const bool vec_ok = ((reinterpret_cast<uint64_t>(op + h) & 15u) == 0);
   const int64_t nvec = vec_ok ? (V - h) / VEC : 0;
   const int64_t vend = h + nvec * VEC;
   auto one = [&](int64_t i) {
     float d = 0.f;
     if (valid) {
-      const float p = ex2(fmaf(E::load1(rp + i), kL2E, -M2) - L2S);
+      const float p = ex2(fmaf(E::load1(rp + i), sc, -M2) - L2S);
       d = (i == y) ? fmaf(-c, p, c) : -c * p;
     }
     Out<TO>::put1(op + i, d);
@@ -855,7 +752,7 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
       if (k < nvec) {
         float d[VEC];
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) d[e] = -c * ex2(fmaf(E::get(v[u], e), kL2E, nM2) - L2S);
+        for (int e = 0; e < VEC; ++e) d[e] = -c * ex2(fmaf(E::get(v[u], e), sc, nM2) - L2S);
         if (k == ky) {
           const int e = (int)((y - h) - k * VEC);
 #pragma unroll
@@ -868,14 +765,14 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
   }
 }
 
-// TPR threads per row, 256/TPR rows per CTA. The row coefficient is grad_scale * g * resid[s]
-// (VarGrad TB, per sequence) or grad_scale * g * coef[row] (per-token rules, e.g. TBA', Eq. 16).
+// TPR threads per row, 256/TPR rows per CTA. Row coefficient c = grad_scale * g * inv_temp *
+// (resid[s] for the TB losses, per sequence | coef[row] for per-token rules such as TBA').
 template <class T, class TO, int TPR, int U, bool PER_ROW>
 __global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int64_t rows, int64_t T_len, int64_t V,
                                                int64_t stride, const int64_t* __restrict__ tokens,
                                                const uint8_t* __restrict__ mask, const float2* __restrict__ stats,
                                                const double* __restrict__ resid, const float* __restrict__ coef,
-                                               double grad_scale, const double* __restrict__ grad_out,
+                                               double grad_scale, const double* __restrict__ grad_out, RowScale rs,
                                                TO* __restrict__ dlogits, int64_t ostride) {
   constexpr int RPC = 256 / TPR;
   const int64_t row = (int64_t)blockIdx.x * RPC + threadIdx.x / TPR;
@@ -888,17 +785,24 @@ __global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int
     const float2 st = stats[row];
     M2 = st.x;
     L2S = st.y;
-    const double g = grad_out ? *grad_out : 1.0;
-    c = PER_ROW ? (float)(grad_scale * g * (double)coef[row]) : (float)(grad_scale * g * resid[row / T_len]);
+    const double g = (grad_out ? *grad_out : 1.0) * grad_scale * rs.inv_temp;
+    c = PER_ROW ? (float)(g * (double)coef[row]) : (float)(g * resid[row / T_len]);
     y = tokens[row];
   }
-  bwd_row<T, TO, U>(logits + row * stride, dlogits + row * ostride, V, tid, TPR, valid, M2, L2S, c, y);
+  bwd_row<T, TO, U>(logits + row * stride, dlogits + row * ostride, V, tid, TPR, valid, rs.sc, M2, L2S, c, y);
 }
 
 // ------------------------------------------------------------------------------ host side
-constexpr int kNT = 256;
 constexpr int kU = 4;
-constexpr int64_t kWarpRowMaxBytes = 8192;  // rows up to 8 KB use one warp per row
+constexpr int64_t kSmallRowBytes = 8192;  // rows up to 8 KB: one warp per row in the backward
+
+RowScale make_scale(double inv_temp) {
+  RowScale r;
+  r.sc = (float)((double)kL2E * inv_temp);
+  r.slack = (float)((double)kSlack / inv_temp);
+  r.inv_temp = inv_temp;
+  return r;
+}
 
 struct WsLayout {
   float2* stats;
@@ -939,7 +843,7 @@ int validate_rows(const tba_rows* x) {
   if (x->n_seq > 0 && x->seq_len > lim / x->n_seq) return TBA_ERR_INVALID_ARG;
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows > 0 && x->row_stride > lim / esz / rows) return TBA_ERR_INVALID_ARG;
-  if (rows > (int64_t)INT32_MAX * 1024) return TBA_ERR_INVALID_ARG;
+  if (rows > (int64_t)INT32_MAX * 64) return TBA_ERR_INVALID_ARG;  // grid limits (256/TPR rows per CTA)
   if (rows > 0) {
     if (!x->logits || !x->tokens || !x->mask) return TBA_ERR_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(x->logits) % esz) return TBA_ERR_INVALID_ARG;
@@ -948,35 +852,77 @@ int validate_rows(const tba_rows* x) {
   return TBA_OK;
 }
 
-struct DevInfo {
-  int sms = 0;
-};
+int validate_out(const tba_rows* x, const void* dlogits, int32_t odt, int64_t ostride) {
+  if (odt != TBA_BF16 && odt != TBA_FP32) return TBA_ERR_INVALID_ARG;
+  if (ostride < x->vocab) return TBA_ERR_INVALID_ARG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows == 0) return TBA_OK;
+  const int64_t oesz = odt == TBA_BF16 ? 2 : 4;
+  if (ostride > INT64_MAX / 8 / oesz / rows) return TBA_ERR_INVALID_ARG;
+  if (!dlogits || reinterpret_cast<uintptr_t>(dlogits) % oesz) return TBA_ERR_INVALID_ARG;
+  if (dlogits == x->logits && (odt != x->dtype || ostride != x->row_stride))
+    return TBA_ERR_INVALID_ARG;  // aliasing is only supported element-for-element
+  return TBA_OK;
+}
 
 int device_sms() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
   static int cache[64] = {0};
-  if (dev < 64 && cache[dev]) return cache[dev];
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
   int n = 148;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  if (dev < 64) cache[dev] = n;
+  if (dev >= 0 && dev < 64) cache[dev] = n;
   return n;
 }
 
-// TMA forward configurations (consumer warps, tile bytes, ring stages); cfg 0 is the default,
-// the others are kept for A/B measurement (env TBA_TMA_CFG).
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// A/B switches (read once): TBA_FWD_IMPL=tma selects the TMA-ring forward, TBA_TMA_CFG its
+// configuration, TBA_FWD_TPR / TBA_BWD_TPR force threads per row. Defaults are the measured best.
+struct Switches {
+  int fwd_tma, tma_cfg, fwd_tpr, bwd_tpr;
+};
+const Switches& switches() {
+  static Switches s = [] {
+    Switches v;
+    const char* e = getenv("TBA_FWD_IMPL");
+    v.fwd_tma = (e && e[0] == 't') ? 1 : 0;
+    v.tma_cfg = env_int("TBA_TMA_CFG", 0);
+    v.fwd_tpr = env_int("TBA_FWD_TPR", 0);
+    v.bwd_tpr = env_int("TBA_BWD_TPR", 0);
+    return v;
+  }();
+  return s;
+}
+
+bool valid_tpr(int t) { return t == 32 || t == 64 || t == 128 || t == 256; }
+
+// Forward threads per row, measured on B200 (scripts/gpu_ab_tpr.sh): 64 threads
+// (4 rows per CTA) is best or within 1 % for V = 32000 ... 152064; one warp for short rows.
+int fwd_tpr(int64_t V, int64_t esz) {
+  if (valid_tpr(switches().fwd_tpr)) return switches().fwd_tpr;
+  return (V * esz / 16) < 1024 ? 32 : 64;
+}
+
+// Backward threads per row (scripts/gpu_ab_bwd.sh): one CTA per long row, one warp per short row.
+int bwd_tpr(int64_t V, int64_t esz) {
+  if (valid_tpr(switches().bwd_tpr)) return switches().bwd_tpr;
+  return V * esz <= kSmallRowBytes ? 32 : 256;
+}
+
 template <class T, int NCW, int TILE, int STAGES, int NP = 0>
-int launch_fwd_tma_cfg(const T* lg, const tba_rows* x, const WsLayout& w, int32_t* dev_status, cudaStream_t s) {
+int launch_fwd_tma_cfg(const T* lg, const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+                       cudaStream_t s) {
   auto kern = row_fwd_tma<T, NCW, TILE, STAGES, NP>;
   const int smem = TILE * STAGES;
-  static int attr_done = 0;  // benign race: the attribute is idempotent
-  if (!attr_done) {
+  static int occ = 0;  // benign race: idempotent
+  if (!occ) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return TBA_ERR_CUDA;
-    attr_done = 1;
-  }
-  static int occ = 0;
-  if (!occ) {
     int o = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, (NCW + 1) * 32, smem) != cudaSuccess || o < 1) o = 1;
     occ = o;
@@ -984,100 +930,31 @@ int launch_fwd_tma_cfg(const T* lg, const tba_rows* x, const WsLayout& w, int32_
   const int64_t rows = x->n_seq * x->seq_len;
   int64_t grid = (int64_t)device_sms() * occ;
   if (grid > rows) grid = rows;
-  kern<<<(unsigned)grid, (NCW + 1) * 32, smem, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, w.stats,
-                                                     w.lp, dev_status);
+  kern<<<(unsigned)grid, (NCW + 1) * 32, smem, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, rs,
+                                                     w.stats, w.lp, dev_status);
   return TBA_OK;
 }
 
-int tma_cfg() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TBA_TMA_CFG");
-    v = e ? atoi(e) : 0;
+template <class T>
+int launch_fwd_tma(const T* lg, const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+                   cudaStream_t s) {
+  switch (switches().tma_cfg) {
+    case 1: return launch_fwd_tma_cfg<T, 8, 8192, 8>(lg, x, w, rs, dev_status, s);
+    case 2: return launch_fwd_tma_cfg<T, 8, 32768, 3>(lg, x, w, rs, dev_status, s);
+    case 3: return launch_fwd_tma_cfg<T, 8, 32768, 3, 1>(lg, x, w, rs, dev_status, s);
+    default: return launch_fwd_tma_cfg<T, 8, 16384, 4>(lg, x, w, rs, dev_status, s);
   }
-  return v;
 }
 
 template <class T>
-int launch_fwd_tma(const T* lg, const tba_rows* x, const WsLayout& w, int32_t* dev_status, cudaStream_t s) {
-  switch (tma_cfg()) {
-    case 1: return launch_fwd_tma_cfg<T, 8, 8192, 8>(lg, x, w, dev_status, s);
-    case 2: return launch_fwd_tma_cfg<T, 16, 16384, 6>(lg, x, w, dev_status, s);
-    case 3: return launch_fwd_tma_cfg<T, 4, 8192, 6>(lg, x, w, dev_status, s);
-    case 4: return launch_fwd_tma_cfg<T, 8, 32768, 3>(lg, x, w, dev_status, s);
-    case 5: return launch_fwd_tma_cfg<T, 8, 16384, 4, 1>(lg, x, w, dev_status, s);
-    case 6: return launch_fwd_tma_cfg<T, 8, 32768, 3, 1>(lg, x, w, dev_status, s);
-    case 7: return launch_fwd_tma_cfg<T, 8, 16384, 4, 2>(lg, x, w, dev_status, s);
-    default: return launch_fwd_tma_cfg<T, 8, 16384, 4>(lg, x, w, dev_status, s);
-  }
-}
-
-int ldg_cfg() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TBA_LDG_CFG");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-// LDG forward configurations (threads per row, vectors per thread per iteration, min CTAs/SM,
-// register double buffering); cfg 0 is the default, the others are kept for A/B (TBA_LDG_CFG).
-template <class T>
-void launch_fwd_cta(const T* lg, int64_t rows, int64_t V, int64_t stride, const tba_rows* x, const WsLayout& w,
-                    int32_t* dev_status, cudaStream_t s) {
-#define TBA_CTA(NT_, U_, MB_, PF_, NP_) \
-  row_fwd_cta<T, NT_, U_, MB_, PF_, NP_><<<(unsigned)rows, NT_, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats, \
-                                                                   w.lp, dev_status)
-  switch (ldg_cfg()) {
-    case 1: TBA_CTA(256, 8, 1, false, 0); break;
-    case 2: TBA_CTA(512, 4, 1, false, 0); break;
-    case 3: TBA_CTA(256, 4, 5, false, 0); break;
-    case 4: TBA_CTA(256, 4, 1, true, 0); break;
-    case 5: TBA_CTA(256, 4, 1, false, 2); break;
-    case 6: TBA_CTA(512, 4, 1, false, 1); break;
-    case 7: TBA_CTA(256, 4, 1, false, 0); break;
-    case 8: TBA_CTA(256, 4, 1, false, 1); break;
-    default: TBA_CTA(256, 4, 1, false, 0); break;
-  }
-#undef TBA_CTA
-}
-
-bool fwd_use_tma() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TBA_FWD_IMPL");
-    v = (e && e[0] == 't') ? 1 : 0;  // default: register-staged LDG kernel; "tma" selects the TMA ring
-  }
-  return v == 1;
-}
-
-int fwd_tpr_env() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TBA_FWD_TPR");
-    v = e ? atoi(e) : 0;  // 0 = auto
-  }
-  return v;
-}
-
-// Threads per row for the LDG forward. Measured on B200 (scripts/gpu_ab_tpr.sh):
-// 64 threads (4 rows per CTA) is best or within 1 % for V = 32000 ... 152064; one warp per row
-// for short rows (< 1024 16-byte vectors).
-int fwd_tpr(int64_t V, int64_t esz) {
-  const int env = fwd_tpr_env();
-  if (env == 32 || env == 64 || env == 128 || env == 256) return env;
-  const int64_t nv = V * esz / 16;
-  return nv < 1024 ? 32 : 64;
-}
-
-template <class T>
-void launch_fwd_rows_t(const T* lg, int64_t rows, int64_t V, int64_t stride, const tba_rows* x, const WsLayout& w,
-                       int32_t* dev_status, cudaStream_t s, int tpr) {
+void launch_fwd_rows_t(const T* lg, const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+                       cudaStream_t s, int tpr) {
+  const int64_t rows = x->n_seq * x->seq_len;
   const int64_t rpc = 256 / tpr;
   const unsigned grid = (unsigned)((rows + rpc - 1) / rpc);
-#define TBA_ROWS(TPR_) \
-  row_fwd_rows<T, TPR_, kU><<<grid, 256, 0, s>>>(lg, rows, V, stride, x->tokens, x->mask, w.stats, w.lp, dev_status)
+#define TBA_ROWS(TPR_)                                                                                               \
+  row_fwd_rows<T, TPR_, kU><<<grid, 256, 0, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, \
+                                                 w.lp, dev_status)
   switch (tpr) {
     case 32: TBA_ROWS(32); break;
     case 64: TBA_ROWS(64); break;
@@ -1087,52 +964,29 @@ void launch_fwd_rows_t(const T* lg, int64_t rows, int64_t V, int64_t stride, con
 #undef TBA_ROWS
 }
 
-int launch_fwd_rows(const tba_rows* x, const WsLayout& w, int32_t* dev_status, cudaStream_t s) {
+int launch_fwd_rows(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
-  const int64_t V = x->vocab, stride = x->row_stride;
   const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
-  const int tpr = fwd_tpr(V, esz);
+  const int tpr = fwd_tpr(x->vocab, esz);
+  const bool tma = switches().fwd_tma && x->vocab * esz > kSmallRowBytes;
   int rc = TBA_OK;
   if (x->dtype == TBA_BF16) {
     auto lg = static_cast<const uint16_t*>(x->logits);
-    if (fwd_use_tma() && V * esz > kWarpRowMaxBytes)
-      rc = launch_fwd_tma<uint16_t>(lg, x, w, dev_status, s);
-    else if (tpr == 256 && ldg_cfg() != 0)
-      launch_fwd_cta<uint16_t>(lg, rows, V, stride, x, w, dev_status, s);
-    else
-      launch_fwd_rows_t<uint16_t>(lg, rows, V, stride, x, w, dev_status, s, tpr);
+    if (tma) rc = launch_fwd_tma<uint16_t>(lg, x, w, rs, dev_status, s);
+    else launch_fwd_rows_t<uint16_t>(lg, x, w, rs, dev_status, s, tpr);
   } else {
     auto lg = static_cast<const float*>(x->logits);
-    if (fwd_use_tma() && V * esz > kWarpRowMaxBytes)
-      rc = launch_fwd_tma<float>(lg, x, w, dev_status, s);
-    else if (tpr == 256 && ldg_cfg() != 0)
-      launch_fwd_cta<float>(lg, rows, V, stride, x, w, dev_status, s);
-    else
-      launch_fwd_rows_t<float>(lg, rows, V, stride, x, w, dev_status, s, tpr);
+    if (tma) rc = launch_fwd_tma<float>(lg, x, w, rs, dev_status, s);
+    else launch_fwd_rows_t<float>(lg, x, w, rs, dev_status, s, tpr);
   }
   if (rc) return rc;
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
-int bwd_tpr_env() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TBA_BWD_TPR");
-    v = e ? atoi(e) : 0;  // 0 = auto
-  }
-  return v;
-}
-
-int bwd_tpr(int64_t V, int64_t esz) {
-  const int env = bwd_tpr_env();
-  if (env == 32 || env == 64 || env == 128 || env == 256) return env;
-  return V * esz <= kWarpRowMaxBytes ? 32 : 256;
-}
-
 template <class T, class TO, bool PER_ROW>
 void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, const float* coef, double gs,
-                  const double* go, TO* out, int64_t ostride, cudaStream_t s) {
+                  const double* go, const RowScale& rs, TO* out, int64_t ostride, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   const int tpr = bwd_tpr(x->vocab, (int64_t)sizeof(T));
   const int64_t rpc = 256 / tpr;
@@ -1140,7 +994,7 @@ void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, con
   auto lg = static_cast<const T*>(x->logits);
 #define TBA_BWD(TPR_)                                                                                              \
   row_bwd<T, TO, TPR_, kU, PER_ROW><<<grid, 256, 0, s>>>(lg, rows, x->seq_len, x->vocab, x->row_stride, x->tokens, \
-                                                        x->mask, w.stats, resid, coef, gs, go, out, ostride)
+                                                        x->mask, w.stats, resid, coef, gs, go, rs, out, ostride)
   switch (tpr) {
     case 32: TBA_BWD(32); break;
     case 64: TBA_BWD(64); break;
@@ -1151,20 +1005,33 @@ void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, con
 }
 
 template <bool PER_ROW>
-void launch_bwd(const tba_rows* x, const WsLayout& w, const double* resid, const float* coef, double gs,
-                const double* go, void* dlogits, int32_t odt, int64_t ostride, cudaStream_t s) {
+int launch_bwd(const tba_rows* x, const void* workspace, const double* resid, const float* coef, double gs,
+               const double* go, const RowScale& rs, void* dlogits, int32_t odt, int64_t ostride, cudaStream_t s) {
+  if (x->n_seq * x->seq_len == 0) return TBA_OK;
+  WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
   if (x->dtype == TBA_BF16) {
     if (odt == TBA_BF16)
-      launch_bwd_t<uint16_t, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, static_cast<uint16_t*>(dlogits), ostride, s);
+      launch_bwd_t<uint16_t, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits),
+                                                ostride, s);
     else
-      launch_bwd_t<uint16_t, float, PER_ROW>(x, w, resid, coef, gs, go, static_cast<float*>(dlogits), ostride, s);
+      launch_bwd_t<uint16_t, float, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
   } else {
     if (odt == TBA_BF16)
-      launch_bwd_t<float, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, static_cast<uint16_t*>(dlogits), ostride, s);
+      launch_bwd_t<float, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits), ostride,
+                                             s);
     else
-      launch_bwd_t<float, float, PER_ROW>(x, w, resid, coef, gs, go, static_cast<float*>(dlogits), ostride, s);
+      launch_bwd_t<float, float, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
   }
+  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
+
+int check_opts(const tba_tb_opts* o) {
+  if (!o) return TBA_OK;
+  if (!(std::isfinite(o->inv_temp) && o->inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  return TBA_OK;
+}
+
+double opt_inv_temp(const tba_tb_opts* o) { return o ? o->inv_temp : 1.0; }
 
 }  // namespace
 
@@ -1177,7 +1044,7 @@ const char* tba_status_string(int code) {
   switch (code) {
     case TBA_OK: return "TBA_OK";
     case TBA_ERR_INVALID_ARG: return "TBA_ERR_INVALID_ARG: invalid argument (null pointer, size, stride, alignment or N % K)";
-    case TBA_ERR_INVALID_CONFIG: return "TBA_ERR_INVALID_CONFIG: invalid configuration (beta must be finite and > 0, K >= 2)";
+    case TBA_ERR_INVALID_CONFIG: return "TBA_ERR_INVALID_CONFIG: invalid configuration (beta, K, IS mode or temperature)";
     case TBA_ERR_CUDA: return "TBA_ERR_CUDA: CUDA launch failed";
     default: return "TBA: unknown status";
   }
@@ -1197,67 +1064,83 @@ int tba_seq_logprob(const tba_rows* x, void* workspace, double* seq_logp, int32_
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
-  rc = launch_fwd_rows(x, w, dev_status, s);
+  rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
   if (rc) return rc;
   const int64_t grid = (x->n_seq + 7) / 8;
-  seq_head<false><<<(unsigned)grid, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, 8, nullptr, nullptr, 0.0, 0.0,
-                                                 seq_logp, n_tokens, nullptr, nullptr, nullptr, nullptr, nullptr);
+  seq_head<false><<<(unsigned)grid, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, 8, nullptr, nullptr, nullptr,
+                                                 0.0, 0.0, seq_logp, n_tokens, nullptr, nullptr, nullptr, nullptr,
+                                                 nullptr);
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
-int tba_vargrad_tb_loss_fwd(const tba_rows* x, const double* ref_logp, const double* log_reward, double beta,
-                            int32_t K, double n_seq_global, void* workspace, double* seq_logp, int32_t* n_tokens,
-                            double* log_z, double* resid, double* partial, int32_t* dev_status,
-                            tba_stream_t stream) {
+int tba_tb_loss_fwd(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
+                    double beta, int32_t K, double n_seq_global, void* workspace, double* seq_logp, int32_t* n_tokens,
+                    double* log_z, double* resid, double* partial, int32_t* dev_status, tba_stream_t stream) {
   if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
   if (K < 2) return TBA_ERR_INVALID_CONFIG;
-  int rc = validate_rows(x);
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
   if (rc) return rc;
   if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
   if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
     return TBA_ERR_INVALID_ARG;
   if (!partial) return TBA_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (x->n_seq == 0) {  // a rank with zero groups contributes zero partials
+  if (x->n_seq == 0)  // a rank with zero groups contributes zero partials
     return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
-  }
   if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
     return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
   if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
-  rc = launch_fwd_rows(x, w, dev_status, s);
+  rc = launch_fwd_rows(x, w, make_scale(opt_inv_temp(opts)), dev_status, s);
   if (rc) return rc;
   const int64_t groups = x->n_seq / K;
   seq_head<true><<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, K, ref_logp, log_reward,
-                                                  1.0 / beta, 1.0 / n_seq_global, seq_logp, n_tokens, log_z, resid,
-                                                  w.group_sq, partial, w.counter);
+                                                  opts ? opts->log_z_param : nullptr, 1.0 / beta, 1.0 / n_seq_global,
+                                                  seq_logp, n_tokens, log_z, resid, w.group_sq, partial, w.counter);
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* workspace, const double* resid,
+                    double grad_scale, const double* grad_out, void* dlogits, int32_t dlogits_dtype,
+                    int64_t dlogits_row_stride, double* d_log_z, int32_t K, tba_stream_t stream) {
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  rc = validate_out(x, dlogits, dlogits_dtype, dlogits_row_stride);
+  if (rc) return rc;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  if (d_log_z && (K < 1 || x->n_seq % K)) return TBA_ERR_INVALID_ARG;
+  if (x->n_seq == 0) return TBA_OK;
+  if (!resid) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (d_log_z) {
+    const int64_t groups = x->n_seq / K;
+    dlogz_kernel<<<(unsigned)((groups + 127) / 128), 128, 0, s>>>(resid, groups, K, grad_scale, grad_out, d_log_z);
+  }
+  if (x->seq_len == 0) return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  return launch_bwd<false>(x, workspace, resid, nullptr, grad_scale, grad_out, make_scale(opt_inv_temp(opts)),
+                           dlogits, dlogits_dtype, dlogits_row_stride, s);
+}
+
+int tba_vargrad_tb_loss_fwd(const tba_rows* x, const double* ref_logp, const double* log_reward, double beta,
+                            int32_t K, double n_seq_global, void* workspace, double* seq_logp, int32_t* n_tokens,
+                            double* log_z, double* resid, double* partial, int32_t* dev_status,
+                            tba_stream_t stream) {
+  return tba_tb_loss_fwd(x, nullptr, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens,
+                         log_z, resid, partial, dev_status, stream);
 }
 
 int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const double* resid, double grad_scale,
                             const double* grad_out, void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride,
                             tba_stream_t stream) {
-  int rc = validate_rows(x);
-  if (rc) return rc;
-  if (dlogits_dtype != TBA_BF16 && dlogits_dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
-  if (dlogits_row_stride < x->vocab) return TBA_ERR_INVALID_ARG;
-  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
-  const int64_t rows = x->n_seq * x->seq_len;
-  if (rows == 0) return TBA_OK;
-  const int64_t oesz = dlogits_dtype == TBA_BF16 ? 2 : 4;
-  if (dlogits_row_stride > INT64_MAX / 8 / oesz / rows) return TBA_ERR_INVALID_ARG;
-  if (!workspace || !resid || !dlogits) return TBA_ERR_INVALID_ARG;
-  if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(dlogits) % oesz)
-    return TBA_ERR_INVALID_ARG;
-  if (dlogits == x->logits && (dlogits_dtype != x->dtype || dlogits_row_stride != x->row_stride))
-    return TBA_ERR_INVALID_ARG;  // aliasing is only supported element-for-element
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
-  launch_bwd<false>(x, w, resid, nullptr, grad_scale, grad_out, dlogits, dlogits_dtype, dlogits_row_stride, s);
-  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  return tba_tb_loss_bwd(x, nullptr, workspace, resid, grad_scale, grad_out, dlogits, dlogits_dtype,
+                         dlogits_row_stride, nullptr, 0, stream);
 }
-
 
 int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
                       double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
@@ -1276,14 +1159,15 @@ int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp, const double* re
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (x->n_seq == 0)  // a rank with zero groups contributes zero partials
     return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
-  if (!workspace || !gen_logp || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv || !coef)
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv || !coef ||
+      (x->seq_len > 0 && !gen_logp))
     return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(gen_logp) % 4 ||
       reinterpret_cast<uintptr_t>(coef) % 4)
     return TBA_ERR_INVALID_ARG;
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
   if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
-  rc = launch_fwd_rows(x, w, dev_status, s);
+  rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
   if (rc) return rc;
   const int64_t groups = x->n_seq / K;
   tbap_head<<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, gen_logp, x->n_seq, x->seq_len, K, ref_logp, log_reward,
@@ -1297,22 +1181,14 @@ int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coe
                       tba_stream_t stream) {
   int rc = validate_rows(x);
   if (rc) return rc;
-  if (dlogits_dtype != TBA_BF16 && dlogits_dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
-  if (dlogits_row_stride < x->vocab) return TBA_ERR_INVALID_ARG;
+  rc = validate_out(x, dlogits, dlogits_dtype, dlogits_row_stride);
+  if (rc) return rc;
   if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
-  const int64_t rows = x->n_seq * x->seq_len;
-  if (rows == 0) return TBA_OK;
-  const int64_t oesz = dlogits_dtype == TBA_BF16 ? 2 : 4;
-  if (dlogits_row_stride > INT64_MAX / 8 / oesz / rows) return TBA_ERR_INVALID_ARG;
-  if (!workspace || !coef || !dlogits) return TBA_ERR_INVALID_ARG;
-  if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(dlogits) % oesz)
-    return TBA_ERR_INVALID_ARG;
-  if (dlogits == x->logits && (dlogits_dtype != x->dtype || dlogits_row_stride != x->row_stride))
-    return TBA_ERR_INVALID_ARG;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
-  launch_bwd<true>(x, w, nullptr, coef, grad_scale, grad_out, dlogits, dlogits_dtype, dlogits_row_stride, s);
-  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (x->n_seq * x->seq_len == 0) return TBA_OK;
+  if (!workspace || !coef) return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  return launch_bwd<true>(x, workspace, nullptr, coef, grad_scale, grad_out, make_scale(1.0), dlogits, dlogits_dtype,
+                          dlogits_row_stride, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -109,9 +109,17 @@ class _Fwd:
         self.partial = torch.empty(3, dtype=torch.float64, device=dev)
 
 
+def _opts(inv_temp: float, log_z_param):
+    if inv_temp == 1.0 and log_z_param is None:
+        return None
+    return _lib.TbaTbOpts(float(inv_temp), None if log_z_param is None else log_z_param.data_ptr())
+
+
 def vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
-                workspace=None, out: _Fwd | None = None, check_status: bool = _CHECK):
-    """Raw forward (tba_vargrad_tb_loss_fwd). Returns (_Fwd, workspace)."""
+                workspace=None, out: _Fwd | None = None, check_status: bool = _CHECK, inv_temp: float = 1.0,
+                log_z_param=None):
+    """Raw TB forward (tba_tb_loss_fwd; tba_vargrad_tb_loss_fwd when inv_temp = 1 and no learned
+    log Z). log_z_param: optional fp64 [N/K] learned log Z(x_i) (Eq. 3). Returns (_Fwd, workspace)."""
     L = _lib.load()
     x = make_rows(logits, tokens, mask)
     N, T = tokens.shape
@@ -119,23 +127,30 @@ def vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int,
     for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
         if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
             raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    if log_z_param is not None and (log_z_param.shape != (N // K,) or log_z_param.dtype != torch.float64
+                                    or not log_z_param.is_contiguous() or log_z_param.device != dev):
+        raise ValueError("log_z_param must be a contiguous fp64 [N/K] tensor on the logits' device")
     o = out or _Fwd(N, K, dev)
     ws = workspace if workspace is not None else _workspace(dev, N, T)
     st = _status(dev) if check_status else None
+    opts = _opts(inv_temp, log_z_param)
     with torch.cuda.device(dev):
-        check(L.tba_vargrad_tb_loss_fwd(ctypes.byref(x), ref_logp.data_ptr(), log_reward.data_ptr(), float(beta),
-                                        int(K), float(n_seq_global), ws.data_ptr(), o.seq_logp.data_ptr(),
-                                        o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None,
-                                        o.resid.data_ptr(), o.partial.data_ptr(), _ptr(st), _stream(dev)),
-              "tba_vargrad_tb_loss_fwd")
+        args = (ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K), float(n_seq_global), ws.data_ptr(),
+                o.seq_logp.data_ptr(), o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None, o.resid.data_ptr(),
+                o.partial.data_ptr(), _ptr(st), _stream(dev))
+        if opts is None:
+            check(L.tba_vargrad_tb_loss_fwd(ctypes.byref(x), *args), "tba_vargrad_tb_loss_fwd")
+        else:
+            check(L.tba_tb_loss_fwd(ctypes.byref(x), ctypes.byref(opts), *args), "tba_tb_loss_fwd")
     if st is not None:
         _raise_dev_status(st, "tba_vargrad_tb_loss_fwd")
     return o, ws
 
 
 def vargrad_bwd(logits, tokens, mask, workspace, resid, grad_scale: float, grad_out=None, dlogits=None,
-                dlogits_dtype=None):
-    """Raw backward (tba_vargrad_tb_loss_bwd). Returns dlogits (new [N,T,V] unless given)."""
+                dlogits_dtype=None, inv_temp: float = 1.0, log_z_param=None, K: int = 0):
+    """Raw TB backward (tba_tb_loss_bwd). Returns dlogits, or (dlogits, d_log_z) when a learned
+    log_z_param is given (then K is required)."""
     L = _lib.load()
     x = make_rows(logits, tokens, mask)
     dev = logits.device
@@ -150,25 +165,41 @@ def vargrad_bwd(logits, tokens, mask, workspace, resid, grad_scale: float, grad_
         raise ValueError("dlogits rows must be uniformly strided")
     if grad_out is not None:
         grad_out = grad_out.to(device=dev, dtype=torch.float64).contiguous()
+    opts = _opts(inv_temp, log_z_param)
+    d_log_z = None
+    if log_z_param is not None:
+        if K < 2:
+            raise ValueError("K is required with a learned log_z_param")
+        d_log_z = torch.empty(N // K, dtype=torch.float64, device=dev)
     with torch.cuda.device(dev):
-        check(L.tba_vargrad_tb_loss_bwd(ctypes.byref(x), workspace.data_ptr(), resid.data_ptr(), float(grad_scale),
-                                        _ptr(grad_out), dlogits.data_ptr(), _DT[dlogits.dtype], max(ors, V),
-                                        _stream(dev)), "tba_vargrad_tb_loss_bwd")
-    return dlogits
+        if opts is None:
+            check(L.tba_vargrad_tb_loss_bwd(ctypes.byref(x), workspace.data_ptr(), resid.data_ptr(),
+                                            float(grad_scale), _ptr(grad_out), dlogits.data_ptr(), _DT[dlogits.dtype],
+                                            max(ors, V), _stream(dev)), "tba_vargrad_tb_loss_bwd")
+        else:
+            check(L.tba_tb_loss_bwd(ctypes.byref(x), ctypes.byref(opts), workspace.data_ptr(), resid.data_ptr(),
+                                    float(grad_scale), _ptr(grad_out), dlogits.data_ptr(), _DT[dlogits.dtype],
+                                    max(ors, V), _ptr(d_log_z), int(K), _stream(dev)), "tba_tb_loss_bwd")
+    return dlogits if d_log_z is None else (dlogits, d_log_z)
 
 
 class VarGradTBLoss(torch.autograd.Function):
-    """L = Eq. 5 over the (sharded) batch; backward writes dlogits in one fused pass."""
+    """L = Eq. 5 (VarGrad log Z, Eq. 4) or Eq. 3 (learned log Z) over the (sharded) batch;
+    backward writes dlogits in one fused pass (and dL/dlog Z for a learned log Z)."""
 
     @staticmethod
-    def forward(ctx, logits, tokens, mask, ref_logp, log_reward, beta, K, n_global, group, dlogits_dtype, aux):
-        o, ws = vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta, K, n_global)
+    def forward(ctx, logits, log_z_param, tokens, mask, ref_logp, log_reward, beta, K, n_global, group,
+                dlogits_dtype, inv_temp, aux):
+        lzp = None if log_z_param is None else log_z_param.detach().contiguous()
+        o, ws = vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta, K, n_global, inv_temp=inv_temp,
+                            log_z_param=lzp)
         if group is not None:
             import torch.distributed as dist
             dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
         ctx.save_for_backward(logits, tokens, mask, ws, o.resid)
-        ctx.n_global = n_global
+        ctx.n_global, ctx.K, ctx.inv_temp = n_global, K, inv_temp
         ctx.dlogits_dtype = dlogits_dtype
+        ctx.lzp = lzp
         if aux is not None:
             aux.update(seq_logp=o.seq_logp, n_tokens=o.n_tokens, log_z=o.log_z, resid=o.resid, partial=o.partial)
         return o.partial[0]
@@ -176,21 +207,24 @@ class VarGradTBLoss(torch.autograd.Function):
     @staticmethod
     def backward(ctx, grad):
         logits, tokens, mask, ws, resid = ctx.saved_tensors
-        d = vargrad_bwd(logits, tokens, mask, ws, resid, 2.0 / ctx.n_global, grad_out=grad,
-                        dlogits_dtype=ctx.dlogits_dtype)
-        return d, None, None, None, None, None, None, None, None, None, None
+        r = vargrad_bwd(logits, tokens, mask, ws, resid, 2.0 / ctx.n_global, grad_out=grad,
+                        dlogits_dtype=ctx.dlogits_dtype, inv_temp=ctx.inv_temp, log_z_param=ctx.lzp, K=ctx.K)
+        d, dz = (r, None) if ctx.lzp is None else r
+        return (d, dz) + (None,) * 11
 
 
 def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
-                    group=None, dlogits_dtype=None, return_aux: bool = False):
-    """The VarGrad TB loss of Eq. 5, autograd-enabled.
+                    group=None, dlogits_dtype=None, return_aux: bool = False, log_z=None, inv_temp: float = 1.0):
+    """The trajectory-balance loss, autograd-enabled.
 
+    Default: the VarGrad loss of Eq. 5 with the detached K-sample log Z of Eq. 4.
+    ``log_z`` (fp64 [N/K] tensor, may require grad): a learned log Z(x_i) instead (Eq. 3,
+    P:114-117). ``inv_temp``: log pi = log softmax(inv_temp * z).
     logits [N, T, V] bf16/fp32 (N = groups*K, group-major); tokens int64 [N, T]; mask
-    uint8/bool [N, T]; ref_logp, log_reward fp64 [N] (log_reward is r_phi). With
-    ``group`` (a torch.distributed process group) each rank passes its own whole groups
-    and the partial sums are all-reduced once; ``n_seq_global`` defaults to N * world.
-    Returns the 0-dim fp64 loss (and an aux dict with seq_logp, n_tokens, log_z, resid,
-    partial when ``return_aux``)."""
+    uint8/bool [N, T]; ref_logp, log_reward fp64 [N] (log_reward is r_phi). With ``group``
+    each rank passes its own whole groups and the partial sums are all-reduced once;
+    ``n_seq_global`` defaults to N * world. Returns the 0-dim fp64 loss (and an aux dict
+    with seq_logp, n_tokens, log_z, resid, partial when ``return_aux``)."""
     N = tokens.shape[0]
     if n_seq_global is None:
         if group is not None:
@@ -199,8 +233,8 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
         else:
             n_seq_global = N
     aux = {} if return_aux else None
-    loss = VarGradTBLoss.apply(logits, tokens, mask, ref_logp, log_reward, float(beta), int(K),
-                               float(n_seq_global), group, dlogits_dtype, aux)
+    loss = VarGradTBLoss.apply(logits, log_z, tokens, mask, ref_logp, log_reward, float(beta), int(K),
+                               float(n_seq_global), group, dlogits_dtype, float(inv_temp), aux)
     return (loss, aux) if return_aux else loss
 
 
