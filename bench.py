@@ -58,8 +58,8 @@ class Clocks:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    def __init__(self, gpu_id: str):
+        self.gpu = gpu_id  # nvidia-smi --id (UUID of the torch device, so CUDA ordering cannot mismatch)
         self.p = None
 
     def __enter__(self):
@@ -160,6 +160,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
+    ap.add_argument("--share-gpu", action="store_true")
     ap.add_argument("--objective", default="vargrad", choices=["vargrad", "tbap"],
                     help="vargrad: Eq. 5 (the north-star head); tbap: the TBA' token-level rule (Eq. 16)")
     args = ap.parse_args()
@@ -176,11 +179,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:  # test mode: all ranks on cuda:0 (needs --dist-backend gloo; NCCL rejects duplicates)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
         group = dist.group.WORLD
     tba.load_library()
 
@@ -243,7 +251,11 @@ def main():
         dist.barrier()
     recs = [[ev() for _ in range(4)] for _ in range(args.steps)]
     t0, t1 = ev(), ev()
-    with Clocks(local) as clk:
+    try:
+        smi_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        smi_id = str(local)
+    with Clocks(smi_id) as clk:
         torch.cuda.synchronize()
         if group is not None:
             dist.barrier()
