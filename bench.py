@@ -160,6 +160,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--schedule", default="two-call", choices=["two-call", "fused"],
+                    help="two-call: tba_vargrad_tb_loss_fwd + _bwd (3 kernels); fused: tba_tb_loss_fused (1 kernel)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
     ap.add_argument("--share-gpu", action="store_true")
@@ -222,10 +224,17 @@ def main():
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    fused = args.schedule == "fused"
+    if fused and tbap:
+        raise SystemExit("--schedule fused implements the TB objectives (Eq. 5 / Eq. 3) only")
+
     def step(rec=None):
         if rec is not None:
             rec[0].record(stream)
-        if tbap:
+        if fused:
+            tba.vargrad_fused(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
+                              dlogits=dlogits, check_status=False)
+        elif tbap:
             tba.tbap_fwd(logits, tokens, mask, gen, ref, rew, w.beta, K, "clip", 0.0, 8.0, n_tok_global,
                          workspace=ws, out=out, check_status=False)
         else:
@@ -237,7 +246,9 @@ def main():
             dist.all_reduce(out.partial, group=group)
         if rec is not None:
             rec[2].record(stream)
-        if tbap:
+        if fused:
+            pass
+        elif tbap:
             tba.tbap_bwd(logits, tokens, mask, ws, out.coef, n_tok_global, dlogits=dlogits)
         else:
             tba.vargrad_bwd(logits, tokens, mask, ws, out.resid, 2.0 / n_global, dlogits=dlogits)
@@ -310,6 +321,13 @@ def main():
             mask_e.copy_(h_mask, non_blocking=True)
             ref_e.copy_(h_ref, non_blocking=True)
             rew_e.copy_(h_rew, non_blocking=True)
+            if fused:
+                tba.vargrad_fused(lg_e, tok_e, mask_e, ref_e, rew_e, w.beta, K, ng_e, workspace=ws, out=out,
+                                  dlogits=dlogits[:nk], check_status=False)
+                if group is not None:
+                    dist.all_reduce(out.partial, group=group)
+                h_loss.copy_(out.partial[:1], non_blocking=True)
+                return
             if tbap:
                 gen_e.copy_(h_gen, non_blocking=True)
                 tba.tbap_fwd(lg_e, tok_e, mask_e, gen_e, ref_e, rew_e, w.beta, K, "clip", 0.0, 8.0, ntok_e,
@@ -361,10 +379,26 @@ def main():
 
     if rank == 0:
         peak, peak_src = peaks()
-        bwd_gbs = bwd_bytes / (bwd_ms / 1e3) / 1e9
+        bwd_gbs = bwd_bytes / (bwd_ms / 1e3) / 1e9 if bwd_ms > 0 else None
         fwd_gbs = fwd_bytes / (fwd_ms / 1e3) / 1e9
         step_gbs = (fwd_bytes + bwd_bytes) / (ms_step / 1e3) / 1e9
-        tr = ncu_traffic(w.name, "row_bwd")
+        if fused:
+            # one kernel; its unique bytes are 2V read + 2V write per valid row (+2V zero-fill per masked
+            # row): the backward re-read is served by L2 when the lookahead window fits
+            fused_bytes = valid_rows * V * 2 * esz + masked_rows * V * esz
+            fgbs = fused_bytes / (fwd_ms / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": "tb_fused (a1-a5 in one launch)", "achieved": fgbs, "peak": peak,
+                    "unit": "GB/s", "frac": fgbs / peak, "traffic": ncu_traffic(w.name, "tb_fused"),
+                    "algorithmic_bytes_per_launch": fused_bytes, "avg_launch_ms": fwd_ms, "peak_source": peak_src,
+                    "bytes_model": "4V per valid token (unique); the two-pass schedule's 6V is in hbm_gbs_step"}
+            kern = {"fused_ms": fwd_ms, "fused_unique_gbs": fgbs}
+        else:
+            tr = ncu_traffic(w.name, "row_bwd")
+            roof = {"bound": "hbm", "kernel": "row_bwd (a5, dominant: 2/3 of bytes)", "achieved": bwd_gbs,
+                    "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak, "traffic": tr,
+                    "algorithmic_bytes_per_launch": bwd_bytes, "avg_launch_ms": bwd_ms, "peak_source": peak_src}
+            kern = {"fwd_ms": fwd_ms, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / peak, "bwd_ms": bwd_ms,
+                    "bwd_gbs": bwd_gbs, "step_frac": step_gbs / peak}
         line = {
             "metric": "TB-loss fwd+bwd tokens/sec" + (" (TBA' Eq. 16 objective)" if tbap else ""),
             "value": tokens_per_step_rank * world / (ms_step / 1e3),
@@ -372,21 +406,19 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (tba_synth seeded generator, DESIGN.md §6)",
-            "config": {"workload": w.name, "objective": args.objective, "note": w.note, "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
+            "config": {"workload": w.name, "objective": args.objective, "schedule": args.schedule, "note": w.note,
+                       "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
                        "V": V, "beta": w.beta, "logits_dtype": w.dtype, "dlogits_dtype": w.dtype,
                        "valid_tokens_per_rank": valid_rows, "parallelism": f"group-sharded x{world}",
                        "l2": "inputs (%.1f GB logits + dlogits per rank) >> 126 MB L2; no flush needed" %
                              ((logits.numel() * esz * 2) / 1e9)},
             "hbm_gbs_step": step_gbs,
-            "roofline": {"bound": "hbm", "kernel": "row_bwd (a5, dominant: 2/3 of bytes)", "achieved": bwd_gbs,
-                         "peak": peak, "unit": "GB/s", "frac": bwd_gbs / peak, "traffic": tr,
-                         "algorithmic_bytes_per_launch": bwd_bytes, "avg_launch_ms": bwd_ms, "peak_source": peak_src},
-            "kernels": {"fwd_ms": fwd_ms, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / peak, "bwd_ms": bwd_ms,
-                        "bwd_gbs": bwd_gbs, "step_frac": step_gbs / peak},
+            "roofline": roof,
+            "kernels": kern,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps * 3,
+            "gpu_launches": args.steps * (1 if fused else 3),
             "loss": loss,
         }
         print(json.dumps(line), flush=True)

@@ -137,6 +137,20 @@ int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* work
                     int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z, int32_t K,
                     tba_stream_t stream);
 
+/* One-launch forward + backward: the outputs of tba_tb_loss_fwd followed
+ * by tba_tb_loss_bwd with grad_scale = 2 g / n_seq_global fixed at call time (g = 1 when the
+ * loss is the training objective). A persistent kernel schedules forward rows, group heads and
+ * gradient rows from one work counter, the backward of group i after the forward of group i+D;
+ * when D groups of logits fit in L2 the backward re-read hits L2. Same results as the two-call
+ * path (bitwise for resid/loss; dlogits identical). d_log_z as in tba_tb_loss_bwd. dlogits may
+ * alias logits. */
+int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                      const double* log_reward, double beta, int32_t K, double n_seq_global,
+                      double grad_scale, void* workspace, double* seq_logp, int32_t* n_tokens,
+                      double* log_z, double* resid, double* partial, void* dlogits,
+                      int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z,
+                      int32_t* dev_status, tba_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * TBA' token-level update: Eq. 16 (eq:tbaGrad), the rule
  * the paper scales to Qwen2.5-7B with PRIME-RL (§6; Table 5):

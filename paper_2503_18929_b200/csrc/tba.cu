@@ -25,6 +25,7 @@ namespace {
 constexpr float kL2E = 1.4426950408889634f;  // fp32(log2 e)
 constexpr double kLN2 = 0.69314718055994530942;
 constexpr float kSlack = 6.0f;  // nats a chunk max may exceed the running reference before a re-base
+constexpr int kFusedU = 4;
 
 // Row scaling: rows are soft-maxed as 2^(z * sc) with sc = fl(kL2E * inv_temp); slack is kSlack in
 // logit units (kSlack / inv_temp); inv_temp enters the log-prob and the gradient exactly (fp64).
@@ -507,7 +508,7 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
     for (int64_t t = lane; t < T; t += 32) {
       const int64_t r = s * T + t;
       if (mask[r]) {
-        acc += lp[r];
+        acc += __ldcg(lp + r);  // L2-coherent: lp may have been written by other CTAs of this grid
         ++cnt;
       }
     }
@@ -792,6 +793,215 @@ __global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int
   bwd_row<T, TO, U>(logits + row * stride, dlogits + row * ostride, V, tid, TPR, valid, rs.sc, M2, L2S, c, y);
 }
 
+// ------------------------------------------------------------------------------ a1-a5 fused (NEXT 2)
+// One persistent launch for the whole VarGrad TB step: forward rows, the group head and the
+// gradient writer, scheduled from one atomic work counter over an item stream in which the
+// forward items of group g+D precede the backward items of group g. The CTA finishing the
+// last forward row of a group computes its head (Eq. 4/5) and publishes a ready flag; backward
+// items of that group wait on it. When D groups of logits fit in L2, the backward re-read of a
+// group hits L2 (6V -> ~4V HBM bytes per token for short-response shapes: Pythia, red-teaming);
+// for large groups (Qwen) it is a single-launch schedule with fwd/bwd overlap.
+struct FusedArgs {
+  const void* logits;
+  void* dlogits;
+  const int64_t* tokens;
+  const uint8_t* mask;
+  const double* ref_logp;
+  const double* log_reward;
+  const double* log_z_param;
+  float2* stats;
+  double* lp;
+  double* seq_logp;
+  int32_t* n_tokens;
+  double* log_z;
+  double* resid;
+  double* group_sq;
+  double* partial;
+  int32_t* dev_status;
+  unsigned int* work;        // [1] item counter
+  unsigned int* groups_done; // [1]
+  unsigned int* rows_done;   // [groups]
+  unsigned int* ready;       // [groups]
+  int64_t rows, T, V, stride, ostride, n_seq;
+  int K, groups, D, nF, nB, RF, RB;
+  double inv_beta, inv_n_global, grad_scale;
+  RowScale rs;
+};
+
+__device__ __forceinline__ void decode_item(const FusedArgs& a, int64_t i, bool& bwd, int& g, int& j) {
+  const int64_t pre = (int64_t)a.D * a.nF;
+  if (i < pre) {
+    bwd = false;
+    g = (int)(i / a.nF);
+    j = (int)(i % a.nF);
+    return;
+  }
+  i -= pre;
+  const int64_t blk = a.nF + a.nB, nfull = a.groups - a.D;
+  if (i < nfull * blk) {
+    const int k = (int)(i / blk), r = (int)(i % blk);
+    if (r < a.nF) {
+      bwd = false;
+      g = k + a.D;
+      j = r;
+    } else {
+      bwd = true;
+      g = k;
+      j = r - a.nF;
+    }
+    return;
+  }
+  i -= nfull * blk;
+  bwd = true;
+  g = (int)(nfull + i / a.nB);
+  j = (int)(i % a.nB);
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <class T, class TO, int TPR_F, int TPR_B>
+__global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
+  constexpr int RF = 256 / TPR_F, WPR = TPR_F / 32, RB = 256 / TPR_B;
+  __shared__ int sh_item;
+  __shared__ bool sh_head;
+  __shared__ float sm_m[RF][WPR], sm_M2[RF][WPR];
+  __shared__ double sm_s[RF][WPR];
+  const int64_t n_items = (int64_t)a.groups * (a.nF + a.nB);
+  const int64_t rows_per_group = (int64_t)a.K * a.T;
+  const T* logits = static_cast<const T*>(a.logits);
+  TO* dlogits = static_cast<TO*>(a.dlogits);
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    if (threadIdx.x == 0) sh_item = (int)atomicAdd(a.work, 1u);
+    __syncthreads();
+    const int64_t item = sh_item;
+    __syncthreads();
+    if (item >= n_items) break;
+    bool bwd;
+    int g, j;
+    decode_item(a, item, bwd, g, j);
+    const int64_t gr0 = (int64_t)g * rows_per_group;
+    if (!bwd) {
+      // ---- forward rows [gr0 + j*RF, +RF) of group g, TPR_F threads per row
+      const int grp = threadIdx.x / TPR_F, gt = threadIdx.x % TPR_F, wig = gt >> 5;
+      const int64_t rin = (int64_t)j * RF + grp;  // row within the group
+      const int64_t row = gr0 + rin;
+      if (rin < rows_per_group && a.mask[row]) {
+        const T* rp = logits + row * a.stride;
+        float zy = 0.f;
+        bool ok = true;
+        if (gt == 0) {
+          const int64_t y = a.tokens[row];
+          ok = (y >= 0 && y < a.V);
+          if (ok) zy = Elem<T>::load1(rp + y);
+        }
+        OnlineState st;
+        st.init(a.rs);
+        fwd_accumulate<T, kFusedU>(rp, a.V, gt, TPR_F, st);
+        float M, M2;
+        double S;
+        combine_lanes(st.m, st.R2, st.s, true, a.rs.sc, M, M2, S);
+        if (WPR == 1) {
+          if (lane == 0) finalize_row(M, M2, S, zy, ok, row, a.rs, a.stats, a.lp, a.dev_status);
+        } else {
+          if (lane == 0) {
+            sm_m[grp][wig] = M;
+            sm_M2[grp][wig] = M2;
+            sm_s[grp][wig] = S;
+          }
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(TPR_F) : "memory");
+          if (wig == 0) {
+            const bool act = lane < WPR;
+            combine_lanes(act ? sm_m[grp][lane] : -INFINITY, act ? sm_M2[grp][lane] : 0.f,
+                          act ? sm_s[grp][lane] : 0.0, act, a.rs.sc, M, M2, S);
+            if (lane == 0) finalize_row(M, M2, S, zy, ok, row, a.rs, a.stats, a.lp, a.dev_status);
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int64_t n = rows_per_group - (int64_t)j * RF;
+        n = n < RF ? n : RF;
+        __threadfence();
+        const unsigned prev = atomicAdd(&a.rows_done[g], (unsigned)n);
+        sh_head = (prev + (unsigned)n == (unsigned)rows_per_group);
+        if (sh_head) __threadfence();
+      }
+      __syncthreads();
+      if (sh_head) {
+        // ---- group head (Eq. 4 / Eq. 3 and Eq. 5) by the CTA that finished the group's last row
+        const int64_t s0 = (int64_t)g * a.K;
+        seq_sums(a.lp, a.mask, a.n_seq, a.T, s0, a.K, a.seq_logp, a.n_tokens, nullptr);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double lz;
+          if (a.log_z_param) {
+            lz = a.log_z_param[g];
+          } else {
+            double sum = 0.0;
+            for (int q = 0; q < a.K; ++q)
+              sum += a.ref_logp[s0 + q] - __ldcg(a.seq_logp + s0 + q) + a.log_reward[s0 + q] * a.inv_beta;
+            lz = sum / (double)a.K;
+          }
+          double sq = 0.0;
+          for (int q = 0; q < a.K; ++q) {
+            const double delta = a.ref_logp[s0 + q] - __ldcg(a.seq_logp + s0 + q) + a.log_reward[s0 + q] * a.inv_beta;
+            const double e = lz - delta;
+            a.resid[s0 + q] = e;
+            sq += e * e;
+          }
+          a.log_z[g] = lz;
+          a.group_sq[g] = sq;
+          __threadfence();
+          st_release(&a.ready[g], 1u);
+          if (atomicAdd(a.groups_done, 1u) == (unsigned)a.groups - 1) {
+            __threadfence();
+            double tot = 0.0;
+            for (int q = 0; q < a.groups; ++q) tot += __ldcg(a.group_sq + q);
+            a.partial[0] = tot * a.inv_n_global;
+            a.partial[1] = (double)a.n_seq;
+            a.partial[2] = (double)a.groups;
+          }
+        }
+      }
+    } else {
+      // ---- backward rows [gr0 + j*RB, +RB) of group g, TPR_B threads per row
+      if (threadIdx.x == 0) {
+        unsigned ns = 32;
+        while (ld_acquire(&a.ready[g]) == 0u) {
+          __nanosleep(ns);
+          ns = ns < 2048 ? 2 * ns : ns;
+        }
+      }
+      __syncthreads();
+      const int grp = threadIdx.x / TPR_B, tid = threadIdx.x % TPR_B;
+      const int64_t rin = (int64_t)j * RB + grp;
+      if (rin < rows_per_group) {
+        const int64_t row = gr0 + rin;
+        const bool valid = a.mask[row] != 0;
+        float M2 = 0.f, L2S = 0.f, c = 0.f;
+        int64_t y = -1;
+        if (valid) {
+          const float2 stt = __ldcg(a.stats + row);
+          M2 = stt.x;
+          L2S = stt.y;
+          c = (float)(a.grad_scale * a.rs.inv_temp * __ldcg(a.resid + row / a.T));
+          y = a.tokens[row];
+        }
+        bwd_row<T, TO, 4>(logits + row * a.stride, dlogits + row * a.ostride, a.V, tid, TPR_B, valid, a.rs.sc, M2,
+                          L2S, c, y);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------ host side
 constexpr int kU = 4;
 constexpr int64_t kSmallRowBytes = 8192;  // rows up to 8 KB: one warp per row in the backward
@@ -809,7 +1019,10 @@ struct WsLayout {
   double* lp;
   double* group_sq;
   unsigned int* counter;
+  unsigned int* fused;
 };
+
+size_t fused_counter_bytes(int64_t n_seq) { return (size_t)(2 + 2 * n_seq) * sizeof(unsigned int); }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -825,13 +1038,15 @@ WsLayout ws_layout(void* ws, int64_t n_seq, int64_t T) {
   l.group_sq = reinterpret_cast<double*>(p + off);
   off = align_up(off + (size_t)n_seq * sizeof(double), 256);
   l.counter = reinterpret_cast<unsigned int*>(p + off);
+  off = align_up(off + 4 * sizeof(unsigned int), 256);
+  l.fused = reinterpret_cast<unsigned int*>(p + off);  // work, groups_done, rows_done[n_seq], ready[n_seq]
   return l;
 }
 
 size_t ws_bytes(int64_t n_seq, int64_t T) {
   const size_t rows = (size_t)n_seq * (size_t)T;
   return align_up(rows * sizeof(float2), 256) + align_up(rows * sizeof(double), 256) +
-         align_up((size_t)n_seq * sizeof(double), 256) + 256;
+         align_up((size_t)n_seq * sizeof(double), 256) + 256 + align_up(fused_counter_bytes(n_seq), 256);
 }
 
 int validate_rows(const tba_rows* x) {
@@ -1025,6 +1240,50 @@ int launch_bwd(const tba_rows* x, const void* workspace, const double* resid, co
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
+int fused_lookahead(int64_t group_bytes, int groups) {
+  const int env = env_int("TBA_FUSED_D", -1);
+  int d;
+  if (env >= 0) {
+    d = env;
+  } else {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
+    d = (int)(0.35 * (double)l2 / (double)(group_bytes > 0 ? group_bytes : 1));
+  }
+  if (d < 1) d = 1;
+  if (d > groups) d = groups;
+  return d;
+}
+
+template <class T, class TO, int TPR_F, int TPR_B>
+int launch_fused_t(FusedArgs& a, cudaStream_t s) {
+  auto kern = tb_fused<T, TO, TPR_F, TPR_B>;
+  static int occ = 0;  // benign race: idempotent
+  if (!occ) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, 0) != cudaSuccess || o < 1) o = 1;
+    occ = o;
+  }
+  a.RF = 256 / TPR_F;
+  a.RB = 256 / TPR_B;
+  const int64_t rpg = (int64_t)a.K * a.T;
+  a.nF = (int)((rpg + a.RF - 1) / a.RF);
+  a.nB = (int)((rpg + a.RB - 1) / a.RB);
+  const int64_t items = (int64_t)a.groups * (a.nF + a.nB);
+  int64_t grid = (int64_t)device_sms() * occ;
+  if (grid > items) grid = items;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 256, 0, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+template <class T, class TO>
+int launch_fused_tpr(FusedArgs& a, int tf, int tb, cudaStream_t s) {
+  if (tf == 32) return tb == 32 ? launch_fused_t<T, TO, 32, 32>(a, s) : launch_fused_t<T, TO, 32, 256>(a, s);
+  return tb == 32 ? launch_fused_t<T, TO, 64, 32>(a, s) : launch_fused_t<T, TO, 64, 256>(a, s);
+}
+
 int check_opts(const tba_tb_opts* o) {
   if (!o) return TBA_OK;
   if (!(std::isfinite(o->inv_temp) && o->inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
@@ -1125,6 +1384,89 @@ int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* work
   if (!workspace || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   return launch_bwd<false>(x, workspace, resid, nullptr, grad_scale, grad_out, make_scale(opt_inv_temp(opts)),
                            dlogits, dlogits_dtype, dlogits_row_stride, s);
+}
+
+int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
+                      double beta, int32_t K, double n_seq_global, double grad_scale, void* workspace,
+                      double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                      void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z,
+                      int32_t* dev_status, tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  rc = validate_out(x, dlogits, dlogits_dtype, dlogits_row_stride);
+  if (rc) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (x->seq_len == 0) {  // no rows: the separate calls already handle this shape
+    rc = tba_tb_loss_fwd(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
+                         resid, partial, dev_status, stream);
+    if (rc) return rc;
+    return tba_tb_loss_bwd(x, opts, workspace, resid, grad_scale, nullptr, dlogits, dlogits_dtype,
+                           dlogits_row_stride, d_log_z, K, stream);
+  }
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.fused, 0, fused_counter_bytes(x->n_seq), s) != cudaSuccess) return TBA_ERR_CUDA;
+  const int64_t groups = x->n_seq / K;
+  const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
+  FusedArgs a;
+  a.logits = x->logits;
+  a.dlogits = dlogits;
+  a.tokens = x->tokens;
+  a.mask = x->mask;
+  a.ref_logp = ref_logp;
+  a.log_reward = log_reward;
+  a.log_z_param = opts ? opts->log_z_param : nullptr;
+  a.stats = w.stats;
+  a.lp = w.lp;
+  a.seq_logp = seq_logp;
+  a.n_tokens = n_tokens;
+  a.log_z = log_z;
+  a.resid = resid;
+  a.group_sq = w.group_sq;
+  a.partial = partial;
+  a.dev_status = dev_status;
+  a.work = w.fused;
+  a.groups_done = w.fused + 1;
+  a.rows_done = w.fused + 2;
+  a.ready = w.fused + 2 + groups;
+  a.rows = x->n_seq * x->seq_len;
+  a.T = x->seq_len;
+  a.V = x->vocab;
+  a.stride = x->row_stride;
+  a.ostride = dlogits_row_stride;
+  a.n_seq = x->n_seq;
+  a.K = K;
+  a.groups = (int)groups;
+  a.D = fused_lookahead((int64_t)K * x->seq_len * x->vocab * esz, (int)groups);
+  a.inv_beta = 1.0 / beta;
+  a.inv_n_global = 1.0 / n_seq_global;
+  a.grad_scale = grad_scale;
+  a.rs = make_scale(opt_inv_temp(opts));
+  const int tf = fwd_tpr(x->vocab, esz) == 32 ? 32 : 64;
+  const int tb = bwd_tpr(x->vocab, esz) == 32 ? 32 : 256;
+  if (x->dtype == TBA_BF16)
+    rc = dlogits_dtype == TBA_BF16 ? launch_fused_tpr<uint16_t, uint16_t>(a, tf, tb, s)
+                                   : launch_fused_tpr<uint16_t, float>(a, tf, tb, s);
+  else
+    rc = dlogits_dtype == TBA_BF16 ? launch_fused_tpr<float, uint16_t>(a, tf, tb, s)
+                                   : launch_fused_tpr<float, float>(a, tf, tb, s);
+  if (rc) return rc;
+  if (d_log_z && a.log_z_param)
+    dlogz_kernel<<<(unsigned)((groups + 127) / 128), 128, 0, s>>>(resid, groups, K, grad_scale, nullptr, d_log_z);
+  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
 int tba_vargrad_tb_loss_fwd(const tba_rows* x, const double* ref_logp, const double* log_reward, double beta,

@@ -238,6 +238,65 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
     return (loss, aux) if return_aux else loss
 
 
+def vargrad_fused(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
+                  grad_scale: float | None = None, workspace=None, out: _Fwd | None = None, dlogits=None,
+                  dlogits_dtype=None, inv_temp: float = 1.0, log_z_param=None, check_status: bool = _CHECK):
+    """One-launch forward + backward (tba_tb_loss_fused). grad_scale defaults to 2/n_seq_global
+    (d loss / d logits with grad_out = 1). Returns (_Fwd, workspace, dlogits, d_log_z or None)."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    N, T = tokens.shape
+    dev = logits.device
+    for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
+        if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    if dlogits is None:
+        dlogits = torch.empty(logits.shape, dtype=dlogits_dtype or logits.dtype, device=dev)
+    Nn, Tt, V = dlogits.shape
+    ors = dlogits.stride(1) if Tt > 1 else (dlogits.stride(0) if Nn > 1 else V)
+    o = out or _Fwd(N, K, dev)
+    ws = workspace if workspace is not None else _workspace(dev, N, T)
+    st = _status(dev) if check_status else None
+    d_log_z = torch.empty(N // K, dtype=torch.float64, device=dev) if log_z_param is not None else None
+    opts = _opts(inv_temp, log_z_param)
+    gs = 2.0 / float(n_seq_global) if grad_scale is None else float(grad_scale)
+    with torch.cuda.device(dev):
+        check(L.tba_tb_loss_fused(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
+                                  ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K), float(n_seq_global),
+                                  gs, ws.data_ptr(), o.seq_logp.data_ptr(), o.n_tokens.data_ptr(),
+                                  o.log_z.data_ptr() if N else None, o.resid.data_ptr(), o.partial.data_ptr(),
+                                  dlogits.data_ptr(), _DT[dlogits.dtype], max(ors, V), _ptr(d_log_z), _ptr(st),
+                                  _stream(dev)), "tba_tb_loss_fused")
+    if st is not None:
+        _raise_dev_status(st, "tba_tb_loss_fused")
+    return o, ws, dlogits, d_log_z
+
+
+def vargrad_tb_loss_and_grad(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
+                             group=None, dlogits=None, dlogits_dtype=None, inv_temp: float = 1.0, log_z=None,
+                             return_aux: bool = False):
+    """Loss AND d loss / d logits in one launch (no autograd): returns (loss, dlogits) or
+    (loss, dlogits, d_log_z) with a learned log_z; aux dict appended when return_aux. The
+    gradient is that of the (all-reduced, when `group` is given) batch loss of Eq. 5 / Eq. 3."""
+    N = tokens.shape[0]
+    if n_seq_global is None:
+        if group is not None:
+            import torch.distributed as dist
+            n_seq_global = N * dist.get_world_size(group)
+        else:
+            n_seq_global = N
+    o, ws, d, dz = vargrad_fused(logits, tokens, mask, ref_logp, log_reward, beta, K, float(n_seq_global),
+                                 dlogits=dlogits, dlogits_dtype=dlogits_dtype, inv_temp=inv_temp,
+                                 log_z_param=None if log_z is None else log_z.detach().contiguous())
+    if group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
+    res = (o.partial[0], d) + ((dz,) if log_z is not None else ())
+    if return_aux:
+        res = res + (dict(seq_logp=o.seq_logp, n_tokens=o.n_tokens, log_z=o.log_z, resid=o.resid, partial=o.partial),)
+    return res
+
+
 # ----------------------------------------------------------------------------- TBA' (Eq. 16)
 _IS = {"none": 0, "clip": 1, "icepop": 2}
 

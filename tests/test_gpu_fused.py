@@ -1,0 +1,107 @@
+"""The one-launch fused schedule (tba_tb_loss_fused) reproduces the
+two-call path bit for bit, for every shape class, lookahead and variant."""
+import dataclasses
+import os
+
+import numpy as np
+import pytest
+
+import tba_synth as syn
+
+from . import _harness as H
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2503_18929_b200 as tba  # noqa: E402
+
+
+def W(name, **kw):
+    return dataclasses.replace(syn.WORKLOADS[name], **kw)
+
+
+CASES = [
+    ("toy", W("toy")),
+    ("rt_ragged_unaligned", W("redteam", B=6, K=4, T=9, len_lo=0, len_hi=9)),
+    ("pythia_full", syn.WORKLOADS["pythia"]),
+    ("rhomath_small_ragged", W("rhomath", B=5, K=4, T=40, len_lo=3, len_hi=40)),
+    ("qwen_small", W("qwen", B=3, K=4, T=8)),
+]
+
+
+def _two_call(inp, w, inv_temp=1.0, lz=None, dl_dtype=None):
+    o, ws = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta,
+                            w.K, w.N, inv_temp=inv_temp, log_z_param=lz)
+    r = tba.vargrad_bwd(inp["logits"], inp["tokens"], inp["mask"], ws, o.resid, 2.0 / w.N, inv_temp=inv_temp,
+                        log_z_param=lz, K=w.K, dlogits_dtype=dl_dtype)
+    d, dz = (r, None) if lz is None else r
+    return o, d, dz
+
+
+@pytest.mark.parametrize("name,w", CASES, ids=[c[0] for c in CASES])
+def test_fused_equals_two_call(name, w):
+    inp = H.device_inputs(w, 7)
+    a, da, _ = _two_call(inp, w)
+    b, ws, db, _ = tba.vargrad_fused(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"],
+                                     w.beta, w.K, float(w.N), check_status=True)
+    torch.cuda.synchronize()
+    for f in ("seq_logp", "n_tokens", "log_z", "resid", "partial"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f
+    assert torch.equal(da.view(torch.int16) if da.dtype == torch.bfloat16 else da,
+                       db.view(torch.int16) if db.dtype == torch.bfloat16 else db)
+
+
+@pytest.mark.parametrize("D", ["1", "2", "64"])
+def test_fused_lookahead_values(D, monkeypatch):
+    # the lookahead only changes the schedule; D is read once per process, so run a subprocess
+    import subprocess
+    import sys
+    code = (
+        "import dataclasses, torch, tba_synth as syn, paper_2503_18929_b200 as tba\n"
+        "from tests import _harness as H\n"
+        "w = dataclasses.replace(syn.WORKLOADS['pythia'], B=12)\n"
+        "inp = H.device_inputs(w, 3)\n"
+        "o, ws = tba.vargrad_fwd(inp['logits'], inp['tokens'], inp['mask'], inp['ref_logp'], inp['log_reward'], w.beta, w.K, w.N)\n"
+        "d = tba.vargrad_bwd(inp['logits'], inp['tokens'], inp['mask'], ws, o.resid, 2.0 / w.N)\n"
+        "b, _, db, _ = tba.vargrad_fused(inp['logits'], inp['tokens'], inp['mask'], inp['ref_logp'], inp['log_reward'], w.beta, w.K, float(w.N))\n"
+        "torch.cuda.synchronize()\n"
+        "assert torch.equal(o.partial, b.partial) and torch.equal(d.view(torch.int16), db.view(torch.int16))\n"
+        "print('ok')\n")
+    env = dict(os.environ, TBA_FUSED_D=D)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_fused_variants_and_fp32_out_and_alias():
+    w = W("pythia", B=3, K=4, T=6, V=5003)
+    inp = H.device_inputs(w, 9)
+    lz = torch.tensor([-20.0, 3.0, 40.0], dtype=torch.float64, device="cuda")
+    a, da, dza = _two_call(inp, w, inv_temp=1 / 0.7, lz=lz, dl_dtype=torch.float32)
+    b, _, db, dzb = tba.vargrad_fused(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"],
+                                      w.beta, w.K, float(w.N), dlogits_dtype=torch.float32, inv_temp=1 / 0.7,
+                                      log_z_param=lz)
+    torch.cuda.synchronize()
+    assert torch.equal(a.resid, b.resid) and torch.equal(da, db) and torch.equal(dza, dzb)
+    # in place: dlogits overwrite the logits they are computed from
+    a2, da2, _ = _two_call(inp, w)
+    lg = inp["logits"].clone()
+    b2, _, db2, _ = tba.vargrad_fused(lg, inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta, w.K,
+                                      float(w.N), dlogits=lg)
+    torch.cuda.synchronize()
+    assert torch.equal(a2.partial, b2.partial) and torch.equal(da2.view(torch.int16), lg.view(torch.int16))
+
+
+def test_loss_and_grad_api():
+    w = W("redteam", B=4, K=8, T=5)
+    inp = H.device_inputs(w, 1)
+    loss, d = tba.vargrad_tb_loss_and_grad(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
+                                           inp["log_reward"], w.beta, w.K)
+    lg = inp["logits"].clone().requires_grad_(True)
+    l2 = tba.vargrad_tb_loss(lg, inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta, w.K)
+    l2.backward()
+    assert loss.item() == l2.item()
+    assert torch.equal(d.view(torch.int16), lg.grad.view(torch.int16))
