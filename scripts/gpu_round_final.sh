@@ -1,0 +1,10 @@
+# Round-end evidence: tests, smoke, profiles, bench lines for every workload, sanitizers.
+TAG=${1:-r01}
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+bash scripts/gpu_profile.sh $TAG > /dev/null 2>&1
+bash scripts/gpu_bench_all.sh $TAG
+timeout 600 python bench.py --objective tbap --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_${TAG}_qwen_shard_tbap.json 2>/dev/null
+tail -c 600 gpurun_out/bench_${TAG}_qwen_shard_tbap.json
+bash scripts/gpu_sanitize.sh
