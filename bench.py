@@ -160,8 +160,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--schedule", default="two-call", choices=["two-call", "fused"],
-                    help="two-call: tba_vargrad_tb_loss_fwd + _bwd (3 kernels); fused: tba_tb_loss_fused (1 kernel)")
+    ap.add_argument("--schedule", default="two-call", choices=["two-call", "fused", "deferred"],
+                    help="two-call: tba_vargrad_tb_loss_fwd + _bwd (3 kernels); fused: tba_tb_loss_fused (1 kernel); "
+                         "deferred: tba_tb_loss_fwd_deferred (unscaled gradient, 4V bytes; NEXT 2 (ii))")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
     ap.add_argument("--share-gpu", action="store_true")
@@ -225,7 +226,8 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     fused = args.schedule == "fused"
-    if fused and tbap:
+    deferred = args.schedule == "deferred"
+    if (fused or deferred) and tbap:
         raise SystemExit("--schedule fused implements the TB objectives (Eq. 5 / Eq. 3) only")
 
     def step(rec=None):
@@ -234,6 +236,9 @@ def main():
         if fused:
             tba.vargrad_fused(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
                               dlogits=dlogits, check_status=False)
+        elif deferred:
+            tba.vargrad_fwd_deferred(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
+                                     grad_unscaled=dlogits, check_status=False)
         elif tbap:
             tba.tbap_fwd(logits, tokens, mask, gen, ref, rew, w.beta, K, "clip", 0.0, 8.0, n_tok_global,
                          workspace=ws, out=out, check_status=False)
@@ -246,7 +251,7 @@ def main():
             dist.all_reduce(out.partial, group=group)
         if rec is not None:
             rec[2].record(stream)
-        if fused:
+        if fused or deferred:
             pass
         elif tbap:
             tba.tbap_bwd(logits, tokens, mask, ws, out.coef, n_tok_global, dlogits=dlogits)
@@ -321,6 +326,13 @@ def main():
             mask_e.copy_(h_mask, non_blocking=True)
             ref_e.copy_(h_ref, non_blocking=True)
             rew_e.copy_(h_rew, non_blocking=True)
+            if deferred:
+                tba.vargrad_fwd_deferred(lg_e, tok_e, mask_e, ref_e, rew_e, w.beta, K, ng_e, workspace=ws, out=out,
+                                         grad_unscaled=dlogits[:nk], check_status=False)
+                if group is not None:
+                    dist.all_reduce(out.partial, group=group)
+                h_loss.copy_(out.partial[:1], non_blocking=True)
+                return
             if fused:
                 tba.vargrad_fused(lg_e, tok_e, mask_e, ref_e, rew_e, w.beta, K, ng_e, workspace=ws, out=out,
                                   dlogits=dlogits[:nk], check_status=False)
@@ -382,12 +394,12 @@ def main():
         bwd_gbs = bwd_bytes / (bwd_ms / 1e3) / 1e9 if bwd_ms > 0 else None
         fwd_gbs = fwd_bytes / (fwd_ms / 1e3) / 1e9
         step_gbs = (fwd_bytes + bwd_bytes) / (ms_step / 1e3) / 1e9
-        if fused:
+        if fused or deferred:
             # one kernel; its unique bytes are 2V read + 2V write per valid row (+2V zero-fill per masked
             # row): the backward re-read is served by L2 when the lookahead window fits
             fused_bytes = valid_rows * V * 2 * esz + masked_rows * V * esz
             fgbs = fused_bytes / (fwd_ms / 1e3) / 1e9
-            roof = {"bound": "hbm", "kernel": "tb_fused (a1-a5 in one launch)", "achieved": fgbs, "peak": peak,
+            roof = {"bound": "hbm", "kernel": "row_single (deferred scale)" if deferred else "tb_fused (a1-a5 in one launch)", "achieved": fgbs, "peak": peak,
                     "unit": "GB/s", "frac": fgbs / peak, "traffic": ncu_traffic(w.name, "tb_fused"),
                     "algorithmic_bytes_per_launch": fused_bytes, "avg_launch_ms": fwd_ms, "peak_source": peak_src,
                     "bytes_model": "4V per valid token (unique); the two-pass schedule's 6V is in hbm_gbs_step"}
@@ -418,7 +430,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps * (1 if fused else 3),
+            "gpu_launches": args.steps * (1 if fused else 2 if deferred else 3),
             "loss": loss,
         }
         print(json.dumps(line), flush=True)

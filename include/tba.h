@@ -151,6 +151,19 @@ int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* 
                       int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z,
                       int32_t* dev_status, tba_stream_t stream);
 
+/* Deferred-scale forward: everything tba_tb_loss_fwd returns, plus
+ * the UNSCALED gradient written in the same pass over the logits:
+ *   grad_unscaled[s,t,v] = mu_{s,t} * inv_temp * (1[v = y] - softmax(inv_temp z)_v)
+ * so that dL/dz = grad_scale * g * resid_s * grad_unscaled with grad_scale = 2 / n_seq_global.
+ * The consumer (the LM-head backward) applies that per-sequence factor as a row scale. Each
+ * valid row is read from HBM once and re-read from L2 (one CTA per SM keeps ~148 rows in
+ * flight): 4V HBM bytes per token instead of 6V. grad_unscaled must not alias logits. */
+int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                             const double* log_reward, double beta, int32_t K, double n_seq_global,
+                             void* workspace, double* seq_logp, int32_t* n_tokens, double* log_z,
+                             double* resid, double* partial, void* grad_unscaled, int32_t g_dtype,
+                             int64_t g_row_stride, int32_t* dev_status, tba_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * TBA' token-level update: Eq. 16 (eq:tbaGrad), the rule
  * the paper scales to Qwen2.5-7B with PRIME-RL (§6; Table 5):

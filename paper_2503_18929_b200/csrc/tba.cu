@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "../../include/tba.h"
@@ -47,6 +48,24 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
+}
+
+// 128-bit load with an explicit L2 eviction policy (createpolicy): evict_last to keep a row
+// resident for a second pass, evict_first for its last read.
+__device__ __forceinline__ uint4 ldg_pol(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint64_t make_policy(bool last) {
+  uint64_t p;
+  if (last)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ void stg_stream(uint4* p, uint4 v) {
@@ -248,9 +267,9 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 }
 
 // LDG-streamed partial state of one row over threads tid, tid+nthr, ...
-template <class T, int U>
+template <class T, int U, bool POL = false>
 __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_t V, int tid, int nthr,
-                                               OnlineState& st) {
+                                               OnlineState& st, uint64_t pol = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(row, V);
@@ -265,11 +284,12 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
   for (int64_t it = 0; it < nfull; ++it, k0 += step) {
     uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + k0 + (int64_t)u * nthr);
+    for (int u = 0; u < U; ++u)
+      v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
     fwd_consume<T, U>(v, st);
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
-    uint4 v1[1] = {ldg_stream(vp + k)};
+    uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
     fwd_consume<T, 1>(v1, st);
   }
 }
@@ -708,9 +728,10 @@ __device__ __forceinline__ void store_vals(TO* o, const float (&d)[N]) {
   }
 }
 
-template <class T, class TO, int U>
+template <class T, class TO, int U, bool POL = false>
 __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid, int nthr,
-                                        bool valid, float sc, float M2, float L2S, float c, int64_t y) {
+                                        bool valid, float sc, float M2, float L2S, float c, int64_t y,
+                                        uint64_t pol = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(rp, V);
@@ -745,7 +766,7 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + (int64_t)u * nthr;
-      if (k < nvec) v[u] = ldg_stream(vp + k);
+      if (k < nvec) v[u] = POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1000,6 +1021,124 @@ __global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
       }
     }
   }
+}
+
+// ------------------------------------------------------------------------------ deferred scale (NEXT 2 (ii))
+// A cluster of CS CTAs (NT threads each) per valid row: pass 1 streams the row from HBM with an
+// L2 evict_last policy (online max/sum); the CTAs of the cluster exchange their (max, sum)
+// partials through distributed shared memory; pass 2 re-reads the row — an L2 hit, because the
+// grid keeps only ~40-60 MB of rows in flight (CS and NT are chosen per row size) — and writes
+// the UNSCALED gradient G = inv_temp (1[v=y] - softmax) once. HBM bytes: 2V read + 2V write per
+// valid row (the 4V floor); the per-sequence factor grad_scale * g * eps_s is applied by the
+// consumer (the LM-head backward, as a row scale), SURVEY §8(f) NEXT 2.
+template <class T, class TO, int NT, int CS, int U2 = 4>
+__device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                int64_t stride, const int64_t* __restrict__ tokens,
+                                                const uint8_t* __restrict__ mask, RowScale rs,
+                                                float2* __restrict__ stats, double* __restrict__ lp,
+                                                int32_t* dev_status, TO* __restrict__ g_out, int64_t ostride) {
+  namespace cg = cooperative_groups;
+  constexpr int NW = NT / 32;
+  const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const int64_t row = (int64_t)blockIdx.x / CS;
+  const int gt = rank * NT + (int)threadIdx.x;  // thread index within the row's cluster
+  __shared__ float sm_m[NW], sm_M2[NW];
+  __shared__ double sm_s[NW];
+  __shared__ float part_m, part_M2;  // this CTA's partial, read by the cluster through DSMEM
+  __shared__ double part_s;
+  __shared__ float sh_M2, sh_L2S;
+  __shared__ int64_t sh_y;
+  const bool live = row < rows;
+  const bool valid = live && mask[row] != 0;  // uniform over the cluster
+  const T* rp = logits + (live ? row : 0) * stride;
+  TO* op = g_out + (live ? row : 0) * ostride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float M = -INFINITY, M2 = 0.f;
+  double S = 0.0;
+  if (valid) {
+    if (threadIdx.x == 0) sh_y = tokens[row];
+    OnlineState st;
+    st.init(rs);
+    fwd_accumulate<T, 4, true>(rp, V, gt, CS * NT, st, make_policy(true));
+    combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
+    if (lane == 0) {
+      sm_m[warp] = M;
+      sm_M2[warp] = M2;
+      sm_s[warp] = S;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const bool act = lane < NW;
+      combine_lanes(act ? sm_m[lane] : -INFINITY, act ? sm_M2[lane] : 0.f, act ? sm_s[lane] : 0.0, act, rs.sc, M,
+                    M2, S);
+      if (lane == 0) {
+        part_m = M;
+        part_M2 = M2;
+        part_s = S;
+      }
+    }
+  }
+  if constexpr (CS > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // partials of every CTA of the row are visible cluster-wide
+    if (valid && warp == 0) {
+      const bool act = lane < CS;
+      float pm = -INFINITY, pm2 = 0.f;
+      double ps = 0.0;
+      if (act) {
+        pm = *cl.map_shared_rank(&part_m, lane);
+        pm2 = *cl.map_shared_rank(&part_M2, lane);
+        ps = *cl.map_shared_rank(&part_s, lane);
+      }
+      combine_lanes(pm, pm2, ps, act, rs.sc, M, M2, S);
+    }
+    cl.sync();  // no CTA leaves (or reuses its shared memory) while a peer still reads it
+  }
+  if (!live) return;
+  if (!valid) {
+    bwd_row<T, TO, 4>(rp, op, V, gt, CS * NT, false, 0.f, 0.f, 0.f, 0.f, -1);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const int64_t y = sh_y;
+    const bool ok = (y >= 0 && y < V);
+    if (rank == 0) {
+      const float zy = ok ? Elem<T>::load1(rp + y) : 0.f;
+      finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+    }
+    sh_M2 = M2;
+    sh_L2S = (float)log2(S);
+  }
+  __syncthreads();
+  bwd_row<T, TO, U2, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
+                           make_policy(false));
+}
+
+template <class T, class TO, int NT, int U2 = 4>
+__global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                  int64_t stride, const int64_t* __restrict__ tokens,
+                                                  const uint8_t* __restrict__ mask, RowScale rs,
+                                                  float2* __restrict__ stats, double* __restrict__ lp,
+                                                  int32_t* dev_status, TO* __restrict__ g_out, int64_t ostride) {
+  row_single_body<T, TO, NT, 1, U2>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out, ostride);
+}
+
+template <class T, class TO, int NT, int U2 = 4>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
+    row_single2(const T* __restrict__ logits, int64_t rows, int64_t V, int64_t stride,
+                const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
+                float2* __restrict__ stats, double* __restrict__ lp, int32_t* dev_status, TO* __restrict__ g_out,
+                int64_t ostride) {
+  row_single_body<T, TO, NT, 2, U2>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out, ostride);
+}
+
+template <class T, class TO, int NT, int U2 = 4>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(NT)
+    row_single4(const T* __restrict__ logits, int64_t rows, int64_t V, int64_t stride,
+                const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
+                float2* __restrict__ stats, double* __restrict__ lp, int32_t* dev_status, TO* __restrict__ g_out,
+                int64_t ostride) {
+  row_single_body<T, TO, NT, 4, U2>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out, ostride);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -1466,6 +1605,76 @@ int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* 
   if (rc) return rc;
   if (d_log_z && a.log_z_param)
     dlogz_kernel<<<(unsigned)((groups + 127) / 128), 128, 0, s>>>(resid, groups, K, grad_scale, nullptr, d_log_z);
+  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                             const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                             double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                             void* grad_unscaled, int32_t g_dtype, int64_t g_row_stride, int32_t* dev_status,
+                             tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  rc = validate_out(x, grad_unscaled, g_dtype, g_row_stride);
+  if (rc) return rc;
+  if (grad_unscaled && grad_unscaled == x->logits) return TBA_ERR_INVALID_ARG;  // pass 2 re-reads the row
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  const int64_t rows = x->n_seq * x->seq_len;
+  const RowScale rs = make_scale(opt_inv_temp(opts));
+  if (rows > 0) {
+    // Rows in flight x row bytes must stay inside L2 for pass 2 to hit it. Measured:
+    // rows <= 128 KB: 256 threads per row (4 CTAs/SM); longer rows: 512 threads (2 CTAs/SM) with 8
+    // vectors per thread in pass 2 — it keeps ~70 % of the re-reads in L2 and overlaps the two passes
+    // across the SM's CTAs, which beats the exact-4V 2-CTA cluster variants (cfg 2/3/5/6).
+    const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
+    int cfg = rb <= 128 * 1024 ? 0 : 4;
+    const int ecfg = env_int("TBA_SINGLE_CFG", -1);
+    if (ecfg >= 0 && ecfg <= 6) cfg = ecfg;
+#define TBA_SINGLE1(KERN_, T_, TO_, NT_, CS_, U2_)                                                             \
+  KERN_<T_, TO_, NT_, U2_><<<(unsigned)(rows * CS_), NT_, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab, \
+                                                             x->row_stride, x->tokens, x->mask, rs, w.stats,      \
+                                                             w.lp, dev_status, static_cast<TO_*>(grad_unscaled),  \
+                                                             g_row_stride)
+#define TBA_SINGLE(T_, TO_)                                          \
+  do {                                                               \
+    if (cfg == 0) TBA_SINGLE1(row_single1, T_, TO_, 256, 1, 4);      \
+    else if (cfg == 1) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 4); \
+    else if (cfg == 2) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 4); \
+    else if (cfg == 3) TBA_SINGLE1(row_single4, T_, TO_, 512, 4, 4); \
+    else if (cfg == 4) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 8); \
+    else if (cfg == 5) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 8); \
+    else TBA_SINGLE1(row_single2, T_, TO_, 256, 2, 4);               \
+  } while (0)
+    if (x->dtype == TBA_BF16) {
+      if (g_dtype == TBA_BF16) TBA_SINGLE(uint16_t, uint16_t);
+      else TBA_SINGLE(uint16_t, float);
+    } else {
+      if (g_dtype == TBA_BF16) TBA_SINGLE(float, uint16_t);
+      else TBA_SINGLE(float, float);
+    }
+#undef TBA_SINGLE
+#undef TBA_SINGLE1
+    if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  }
+  const int64_t groups = x->n_seq / K;
+  seq_head<true><<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, K, ref_logp, log_reward,
+                                                  opts ? opts->log_z_param : nullptr, 1.0 / beta, 1.0 / n_seq_global,
+                                                  seq_logp, n_tokens, log_z, resid, w.group_sq, partial, w.counter);
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 

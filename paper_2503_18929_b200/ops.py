@@ -272,6 +272,41 @@ def vargrad_fused(logits, tokens, mask, ref_logp, log_reward, beta: float, K: in
     return o, ws, dlogits, d_log_z
 
 
+def vargrad_fwd_deferred(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
+                         workspace=None, out: _Fwd | None = None, grad_unscaled=None, g_dtype=None,
+                         inv_temp: float = 1.0, log_z_param=None, check_status: bool = _CHECK):
+    """Deferred-scale forward (tba_tb_loss_fwd_deferred): the forward outputs plus the unscaled
+    gradient G = mu * inv_temp * (onehot - softmax), written in the same pass; the true
+    dlogits are (2 g / n_seq_global) * resid[s] * G (apply as a row scale downstream).
+    Returns (_Fwd, workspace, G)."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    N, T = tokens.shape
+    dev = logits.device
+    for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
+        if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    if grad_unscaled is None:
+        grad_unscaled = torch.empty(logits.shape, dtype=g_dtype or logits.dtype, device=dev)
+    Nn, Tt, V = grad_unscaled.shape
+    ors = grad_unscaled.stride(1) if Tt > 1 else (grad_unscaled.stride(0) if Nn > 1 else V)
+    o = out or _Fwd(N, K, dev)
+    ws = workspace if workspace is not None else _workspace(dev, N, T)
+    st = _status(dev) if check_status else None
+    opts = _opts(inv_temp, log_z_param)
+    with torch.cuda.device(dev):
+        check(L.tba_tb_loss_fwd_deferred(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
+                                         ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K),
+                                         float(n_seq_global), ws.data_ptr(), o.seq_logp.data_ptr(),
+                                         o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None,
+                                         o.resid.data_ptr(), o.partial.data_ptr(), grad_unscaled.data_ptr(),
+                                         _DT[grad_unscaled.dtype], max(ors, V), _ptr(st), _stream(dev)),
+              "tba_tb_loss_fwd_deferred")
+    if st is not None:
+        _raise_dev_status(st, "tba_tb_loss_fwd_deferred")
+    return o, ws, grad_unscaled
+
+
 def vargrad_tb_loss_and_grad(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
                              group=None, dlogits=None, dlogits_dtype=None, inv_temp: float = 1.0, log_z=None,
                              return_aux: bool = False):

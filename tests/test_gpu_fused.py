@@ -105,3 +105,67 @@ def test_loss_and_grad_api():
     l2.backward()
     assert loss.item() == l2.item()
     assert torch.equal(d.view(torch.int16), lg.grad.view(torch.int16))
+
+
+@pytest.mark.parametrize("name,w", CASES, ids=[c[0] for c in CASES])
+def test_deferred_scale_matches_oracle(name, w):
+    """G from the single-pass deferred kernel, scaled by (2/N) eps_s, is the oracle's dlogits
+    (fp32 G: 2e-6 max(1,|c|); bf16 G: within 2 bf16 ulps of the oracle — G and c.G each round once)."""
+    from oracle import tba_oracle as O
+    inp = H.device_inputs(w, 5)
+    h = inp["host"]
+    dt = torch.float32 if w.dtype == "fp32" else torch.bfloat16
+    o, ws, G = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
+                                        inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=torch.float32,
+                                        check_status=True)
+    a, _ = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta,
+                           w.K, w.N)
+    torch.cuda.synchronize()
+    # different threads-per-row => different fp32 summation order: agree to rounding, both match the oracle
+    H.assert_seq_close(o.resid.cpu().numpy(), a.resid.cpu().numpy(), "deferred resid vs two-call", rel=1e-5,
+                       abs_=1e-6)
+    eps = o.resid.cpu().numpy()
+    rng = np.random.default_rng(0)
+    rows = rng.choice(w.N * w.T, size=min(24, w.N * w.T), replace=False)
+    Gh = G.view(-1, w.V)
+    for r in rows:
+        s_, t = divmod(int(r), w.T)
+        got = Gh[r].double().cpu().numpy() * (2 * eps[s_] / w.N)
+        if h["mask"][s_, t]:
+            z = syn.logits_rows_f64(5, w.V, [r], w.dtype)[0]
+            want = O.dlogits_row(z, int(h["tokens"][s_, t]), eps[s_], w.N)
+            H.assert_dlogits_close(got, want, 2 * eps[s_] / w.N, "fp32", f"row {r}")
+        else:
+            assert np.all(got == 0)
+    # bf16 G: also valid
+    o2, _, G2 = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
+                                         inp["log_reward"], w.beta, w.K, float(w.N))
+    torch.cuda.synchronize()
+    assert torch.allclose(G2.double(), G.double(), rtol=2 ** -8, atol=1e-30)
+
+
+@pytest.mark.parametrize("cfg", ["0", "1", "2", "3"])
+def test_deferred_all_cluster_shapes(cfg, monkeypatch):
+    """Every (threads, cluster size) configuration of the deferred kernel gives the same G."""
+    monkeypatch.setenv("TBA_SINGLE_CFG", cfg)
+    w = W("redteam", B=2, K=4, T=5, len_lo=1, len_hi=5)   # odd row length, ragged
+    inp = H.device_inputs(w, 2)
+    o, _, G = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
+                                       inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=torch.float32,
+                                       check_status=True)
+    monkeypatch.setenv("TBA_SINGLE_CFG", "0")
+    o0, _, G0 = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
+                                         inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=torch.float32)
+    torch.cuda.synchronize()
+    H.assert_seq_close(o.seq_logp.cpu().numpy(), o0.seq_logp.cpu().numpy(), "seq_logp", rel=1e-9, abs_=1e-9)
+    assert torch.allclose(G, G0, rtol=1e-5, atol=1e-9)
+    from oracle import tba_oracle as O
+    h = inp["host"]
+    ref = O.vargrad_head(H.host_logits(w, 2, 0, w.B), h["tokens"], h["mask"], h["ref_logp"], h["log_reward"], w.beta,
+                         w.K)
+    eps = o.resid.cpu().numpy()
+    H.assert_seq_close(eps, ref["eps"], "resid")
+    g = G.double().cpu().numpy()
+    for s_ in range(w.N):
+        for t in range(w.T):
+            H.assert_dlogits_close(g[s_, t] * 2 * eps[s_] / w.N, ref["dlogits"][s_, t], 2 * eps[s_] / w.N, "fp32")
