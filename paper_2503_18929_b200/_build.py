@@ -56,6 +56,21 @@ def build(force: bool = False, verbose: bool = False) -> dict:
     return out
 
 
+def build_c_example(out: str | None = None) -> str:
+    """Compile examples/c_abi_example.c against include/tba.h and libtba.so (plain C + CUDA runtime)."""
+    build()
+    cuda = os.path.dirname(os.path.dirname(nvcc()))
+    out = out or os.path.join(ROOT, "examples", "c_abi_example")
+    cmd = ["gcc", "-O2", "-std=c11", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"),
+           os.path.join(ROOT, "examples", "c_abi_example.c"), "-L", PKG, "-ltba", f"-Wl,-rpath,{PKG}",
+           "-L", os.path.join(cuda, "lib64"), "-lcudart", f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-lm",
+           "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"gcc failed: {' '.join(cmd)}\n{r.stderr}")
+    return out
+
+
 if __name__ == "__main__":
     import sys
     print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,60 @@
+"""The C ABI is usable from plain C: examples/c_abi_example.c builds here (CPU) and, on a GPU,
+its printed loss / per-sequence log-probs match the fp64 oracle on the same inputs."""
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import tba_oracle as O
+
+
+def _inputs():
+    N, T, V = 6, 4, 257
+    st = 88172645463325252
+    M = (1 << 64) - 1
+
+    def nxt(x):
+        x ^= (x << 13) & M
+        x ^= x >> 7
+        x ^= (x << 17) & M
+        return x
+
+    logits = np.empty(N * T * V, np.float32)
+    for i in range(N * T * V):
+        st = nxt(st)
+        logits[i] = np.float32((st >> 11) / 9007199254740992.0 * 8.0 - 4.0)
+    tok = np.empty(N * T, np.int64)
+    mask = np.empty(N * T, np.uint8)
+    for i in range(N * T):
+        st = nxt(st)
+        tok[i] = st % V
+        mask[i] = 1 if (i % T) < T - (i // T) % 2 else 0
+    ref = np.array([-20.0 + s for s in range(N)])
+    rew = np.array([float(s % 2) for s in range(N)])
+    return logits.reshape(N, T, V).astype(np.float64), tok.reshape(N, T), mask.reshape(N, T), ref, rew
+
+
+def test_c_example_compiles():
+    from paper_2503_18929_b200 import _build
+    assert _build.build_c_example()
+
+
+@pytest.mark.gpu
+def test_c_example_runs_and_matches_oracle():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_18929_b200 import _build
+    exe = _build.build_c_example()
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    logits, tok, mask, ref, rew = _inputs()
+    r = O.vargrad_head(logits, tok, mask, ref, rew, 0.5, 3)
+    m = re.search(r"status 0 loss (\S+) n_seq 6 n_groups 2", out.stdout)
+    assert m, out.stdout
+    assert abs(float(m.group(1)) - r["loss"]) <= 1e-4 * abs(r["loss"])
+    got = [float(x) for x in re.findall(r"seq \d+ logp (\S+) ntok", out.stdout)]
+    np.testing.assert_allclose(got, r["ell"], rtol=1e-6)
+    cs = float(re.search(r"dlogits_abs_sum (\S+)", out.stdout).group(1))
+    assert abs(cs - np.abs(r["dlogits"]).sum()) <= 1e-5 * np.abs(r["dlogits"]).sum()

@@ -262,3 +262,26 @@ def test_group_reward_shift_invariance():
     H.assert_seq_close(b[0].resid.cpu().numpy(), a[0].resid.cpu().numpy(), "resid shift", rel=1e-9, abs_=1e-9)
     da, db = a[1].float(), b[1].float()
     assert torch.max(torch.abs(da - db)).item() <= 2 * torch.max(torch.abs(da)).item() * 2 ** -8
+
+
+def test_vocab_one_and_two():
+    for V in (1, 2, 3):
+        z, tok, mask, ref, rew = _edge_inputs(4, 3, V, 2, dtype=torch.bfloat16, seed=V)
+        _oracle_compare(z, tok, mask, ref, rew, 0.25, 2)
+
+
+def test_zero_length_responses_shape():
+    """seq_len = 0: every response empty; ell = 0, loss from ref/rewards only, no rows."""
+    N, K = 4, 2
+    z = torch.zeros((N, 0, 7), dtype=torch.bfloat16, device="cuda")
+    tok = torch.zeros((N, 0), dtype=torch.int64, device="cuda")
+    mask = torch.zeros((N, 0), dtype=torch.uint8, device="cuda")
+    ref = torch.tensor([-1.0, -2.0, -3.0, 0.5], dtype=torch.float64, device="cuda")
+    rew = torch.tensor([0.0, 1.0, 1.0, 0.0], dtype=torch.float64, device="cuda")
+    o, ws = tba.vargrad_fwd(z, tok, mask, ref, rew, 0.5, K, N)
+    d = tba.vargrad_bwd(z, tok, mask, ws, o.resid, 2.0 / N)
+    torch.cuda.synchronize()
+    r = O.vargrad_tb_loss(np.zeros(N), ref.cpu().numpy(), rew.cpu().numpy(), 0.5, K)
+    assert o.seq_logp.abs().sum().item() == 0 and o.n_tokens.sum().item() == 0
+    H.assert_seq_close([o.partial[0].item()], [r[0]], "loss")
+    assert d.shape == (N, 0, 7)
