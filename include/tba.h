@@ -187,6 +187,16 @@ int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp /* [N, T] fp32, p
                       int32_t* n_tokens, double* adv, float* coef, double* partial, int32_t* dev_status,
                       tba_stream_t stream);
 
+/* TBA' with the deferred-scale row pass (as tba_tb_loss_fwd_deferred): also writes
+ * grad_unscaled = mu (1[v=y] - softmax) in the same pass; dL'/dz = -(coef_{s,t} / n_tok_global) *
+ * g * grad_unscaled (a per-token row scale applied by the consumer). */
+int tba_tbap_loss_fwd_deferred(const tba_rows* x, const float* gen_logp, const double* ref_logp,
+                               const double* log_reward, double beta, int32_t K, int32_t is_mode,
+                               double is_lo, double is_hi, double n_tok_global, void* workspace,
+                               double* seq_logp, int32_t* n_tokens, double* adv, float* coef,
+                               double* partial, void* grad_unscaled, int32_t g_dtype,
+                               int64_t g_row_stride, int32_t* dev_status, tba_stream_t stream);
+
 /* dlogits for the TBA' surrogate: dz_{s,t,v} = mu * grad_scale * g * coef_{s,t} (1[v=y] - softmax_v)
  * with grad_scale = -1 / n_tok_global; otherwise as tba_vargrad_tb_loss_bwd. */
 int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coef, double grad_scale,

@@ -20,7 +20,7 @@ TBA_BF16, TBA_FP32 = 0, 1
 EXPORTS = ("tba_abi_version", "tba_status_string", "tba_workspace_bytes", "tba_seq_logprob",
            "tba_vargrad_tb_loss_fwd", "tba_vargrad_tb_loss_bwd", "tba_tb_loss_fwd", "tba_tb_loss_bwd", "tba_tb_loss_fused",
            "tba_tb_loss_fwd_deferred",
-           "tba_tbap_loss_fwd", "tba_tbap_loss_bwd")
+           "tba_tbap_loss_fwd", "tba_tbap_loss_bwd", "tba_tbap_loss_fwd_deferred")
 TBA_IS_NONE, TBA_IS_CLIP, TBA_IS_ICEPOP = 0, 1, 2
 
 
@@ -79,6 +79,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         L.tba_tb_loss_fwd_deferred.argtypes = [RP, OP, P, P, D, I32, D, P, P, P, P, P, P, P, I32, I64, P, P]
         L.tba_tbap_loss_fwd.restype = ctypes.c_int
         L.tba_tbap_loss_fwd.argtypes = [RP, P, P, P, D, I32, I32, D, D, D, P, P, P, P, P, P, P, P]
+        L.tba_tbap_loss_fwd_deferred.restype = ctypes.c_int
+        L.tba_tbap_loss_fwd_deferred.argtypes = [RP, P, P, P, D, I32, I32, D, D, D, P, P, P, P, P, P, P, I32, I64, P, P]
         L.tba_tbap_loss_bwd.restype = ctypes.c_int
         L.tba_tbap_loss_bwd.argtypes = [RP, P, P, D, P, P, I32, I64, P]
         if L.tba_abi_version() != 1:

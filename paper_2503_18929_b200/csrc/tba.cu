@@ -1423,6 +1423,48 @@ int launch_fused_tpr(FusedArgs& a, int tf, int tb, cudaStream_t s) {
   return tb == 32 ? launch_fused_t<T, TO, 64, 32>(a, s) : launch_fused_t<T, TO, 64, 256>(a, s);
 }
 
+// deferred-scale row pass (row_single*): configuration by row length, see DESIGN.md §5.4
+int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+                  void* grad_unscaled, int32_t g_dtype, int64_t g_row_stride, cudaStream_t s) {
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows > 0) {
+    // Rows in flight x row bytes must stay inside L2 for pass 2 to hit it (DESIGN.md §5.4). Measured:
+    // rows <= 128 KB: 256 threads per row (4 CTAs/SM); longer rows: 512 threads (2 CTAs/SM) with 8
+    // vectors per thread in pass 2 — it keeps ~70 % of the re-reads in L2 and overlaps the two passes
+    // across the SM's CTAs, which beats the exact-4V 2-CTA cluster variants (cfg 2/3/5/6).
+    const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
+    int cfg = rb <= 128 * 1024 ? 0 : 4;
+    const int ecfg = env_int("TBA_SINGLE_CFG", -1);
+    if (ecfg >= 0 && ecfg <= 6) cfg = ecfg;
+#define TBA_SINGLE1(KERN_, T_, TO_, NT_, CS_, U2_)                                                             \
+  KERN_<T_, TO_, NT_, U2_><<<(unsigned)(rows * CS_), NT_, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab, \
+                                                             x->row_stride, x->tokens, x->mask, rs, w.stats,      \
+                                                             w.lp, dev_status, static_cast<TO_*>(grad_unscaled),  \
+                                                             g_row_stride)
+#define TBA_SINGLE(T_, TO_)                                          \
+  do {                                                               \
+    if (cfg == 0) TBA_SINGLE1(row_single1, T_, TO_, 256, 1, 4);      \
+    else if (cfg == 1) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 4); \
+    else if (cfg == 2) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 4); \
+    else if (cfg == 3) TBA_SINGLE1(row_single4, T_, TO_, 512, 4, 4); \
+    else if (cfg == 4) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 8); \
+    else if (cfg == 5) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 8); \
+    else TBA_SINGLE1(row_single2, T_, TO_, 256, 2, 4);               \
+  } while (0)
+    if (x->dtype == TBA_BF16) {
+      if (g_dtype == TBA_BF16) TBA_SINGLE(uint16_t, uint16_t);
+      else TBA_SINGLE(uint16_t, float);
+    } else {
+      if (g_dtype == TBA_BF16) TBA_SINGLE(float, uint16_t);
+      else TBA_SINGLE(float, float);
+    }
+#undef TBA_SINGLE
+#undef TBA_SINGLE1
+    if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  }
+  return TBA_OK;
+}
+
 int check_opts(const tba_tb_opts* o) {
   if (!o) return TBA_OK;
   if (!(std::isfinite(o->inv_temp) && o->inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
@@ -1634,43 +1676,8 @@ int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const d
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
   if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
-  const int64_t rows = x->n_seq * x->seq_len;
-  const RowScale rs = make_scale(opt_inv_temp(opts));
-  if (rows > 0) {
-    // Rows in flight x row bytes must stay inside L2 for pass 2 to hit it (DESIGN.md §5.4). Measured:
-    // rows <= 128 KB: 256 threads per row (4 CTAs/SM); longer rows: 512 threads (2 CTAs/SM) with 8
-    // vectors per thread in pass 2 — it keeps ~70 % of the re-reads in L2 and overlaps the two passes
-    // across the SM's CTAs, which beats the exact-4V 2-CTA cluster variants (cfg 2/3/5/6).
-    const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
-    int cfg = rb <= 128 * 1024 ? 0 : 4;
-    const int ecfg = env_int("TBA_SINGLE_CFG", -1);
-    if (ecfg >= 0 && ecfg <= 6) cfg = ecfg;
-#define TBA_SINGLE1(KERN_, T_, TO_, NT_, CS_, U2_)                                                             \
-  KERN_<T_, TO_, NT_, U2_><<<(unsigned)(rows * CS_), NT_, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab, \
-                                                             x->row_stride, x->tokens, x->mask, rs, w.stats,      \
-                                                             w.lp, dev_status, static_cast<TO_*>(grad_unscaled),  \
-                                                             g_row_stride)
-#define TBA_SINGLE(T_, TO_)                                          \
-  do {                                                               \
-    if (cfg == 0) TBA_SINGLE1(row_single1, T_, TO_, 256, 1, 4);      \
-    else if (cfg == 1) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 4); \
-    else if (cfg == 2) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 4); \
-    else if (cfg == 3) TBA_SINGLE1(row_single4, T_, TO_, 512, 4, 4); \
-    else if (cfg == 4) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 8); \
-    else if (cfg == 5) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 8); \
-    else TBA_SINGLE1(row_single2, T_, TO_, 256, 2, 4);               \
-  } while (0)
-    if (x->dtype == TBA_BF16) {
-      if (g_dtype == TBA_BF16) TBA_SINGLE(uint16_t, uint16_t);
-      else TBA_SINGLE(uint16_t, float);
-    } else {
-      if (g_dtype == TBA_BF16) TBA_SINGLE(float, uint16_t);
-      else TBA_SINGLE(float, float);
-    }
-#undef TBA_SINGLE
-#undef TBA_SINGLE1
-    if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
-  }
+  rc = launch_single(x, w, make_scale(opt_inv_temp(opts)), dev_status, grad_unscaled, g_dtype, g_row_stride, s);
+  if (rc) return rc;
   const int64_t groups = x->n_seq / K;
   seq_head<true><<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, K, ref_logp, log_reward,
                                                   opts ? opts->log_z_param : nullptr, 1.0 / beta, 1.0 / n_seq_global,
@@ -1693,10 +1700,11 @@ int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const doub
                          dlogits_row_stride, nullptr, 0, stream);
 }
 
-int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
-                      double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
-                      void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef, double* partial,
-                      int32_t* dev_status, tba_stream_t stream) {
+static int tbap_fwd_impl(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
+                         double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
+                         void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef,
+                         double* partial, int32_t* dev_status, void* grad_unscaled, int32_t g_dtype,
+                         int64_t g_row_stride, tba_stream_t stream) {
   if (!(std::isfinite(beta) && beta >= 0.0)) return TBA_ERR_INVALID_CONFIG;  // beta = 0 is Dr. GRPO
   if (K < 2) return TBA_ERR_INVALID_CONFIG;
   if (is_mode != TBA_IS_NONE && is_mode != TBA_IS_CLIP && is_mode != TBA_IS_ICEPOP) return TBA_ERR_INVALID_CONFIG;
@@ -1718,13 +1726,39 @@ int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp, const double* re
     return TBA_ERR_INVALID_ARG;
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
   if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
-  rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
+  if (grad_unscaled) {
+    rc = validate_out(x, grad_unscaled, g_dtype, g_row_stride);
+    if (rc) return rc;
+    if (grad_unscaled == x->logits) return TBA_ERR_INVALID_ARG;
+    rc = launch_single(x, w, make_scale(1.0), dev_status, grad_unscaled, g_dtype, g_row_stride, s);
+  } else {
+    rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
+  }
   if (rc) return rc;
   const int64_t groups = x->n_seq / K;
   tbap_head<<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, gen_logp, x->n_seq, x->seq_len, K, ref_logp, log_reward,
                                             beta, is_mode, is_lo, is_hi, -1.0 / n_tok_global, seq_logp, n_tokens, adv,
                                             coef, w.group_sq, partial, w.counter);
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
+                      double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
+                      void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef, double* partial,
+                      int32_t* dev_status, tba_stream_t stream) {
+  return tbap_fwd_impl(x, gen_logp, ref_logp, log_reward, beta, K, is_mode, is_lo, is_hi, n_tok_global, workspace,
+                       seq_logp, n_tokens, adv, coef, partial, dev_status, nullptr, TBA_BF16, 0, stream);
+}
+
+int tba_tbap_loss_fwd_deferred(const tba_rows* x, const float* gen_logp, const double* ref_logp,
+                               const double* log_reward, double beta, int32_t K, int32_t is_mode, double is_lo,
+                               double is_hi, double n_tok_global, void* workspace, double* seq_logp,
+                               int32_t* n_tokens, double* adv, float* coef, double* partial, void* grad_unscaled,
+                               int32_t g_dtype, int64_t g_row_stride, int32_t* dev_status, tba_stream_t stream) {
+  if (!grad_unscaled && x && x->n_seq * x->seq_len > 0) return TBA_ERR_INVALID_ARG;
+  return tbap_fwd_impl(x, gen_logp, ref_logp, log_reward, beta, K, is_mode, is_lo, is_hi, n_tok_global, workspace,
+                       seq_logp, n_tokens, adv, coef, partial, dev_status, grad_unscaled, g_dtype, g_row_stride,
+                       stream);
 }
 
 int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coef, double grad_scale,

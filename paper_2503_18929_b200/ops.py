@@ -349,7 +349,7 @@ class _TbapFwd:
 
 def tbap_fwd(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, K: int, is_mode: str = "clip",
              is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global: float | None = None, workspace=None,
-             out: _TbapFwd | None = None, check_status: bool = _CHECK):
+             out: _TbapFwd | None = None, check_status: bool = _CHECK, grad_unscaled=None):
     """Raw TBA' forward (tba_tbap_loss_fwd, Eq. 16). gen_logp: fp32 [N, T] log-probs of the
     generating policy. n_tok_global defaults to this call's valid-token count (host sync)."""
     L = _lib.load()
@@ -367,11 +367,17 @@ def tbap_fwd(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, 
     ws = workspace if workspace is not None else _workspace(dev, N, T)
     st = _status(dev) if check_status else None
     with torch.cuda.device(dev):
-        check(L.tba_tbap_loss_fwd(ctypes.byref(x), gen_logp.data_ptr(), ref_logp.data_ptr(), log_reward.data_ptr(),
-                                  float(beta), int(K), _IS[is_mode], float(is_lo), float(is_hi), float(n_tok_global),
-                                  ws.data_ptr(), o.seq_logp.data_ptr(), o.n_tokens.data_ptr(), o.adv.data_ptr(),
-                                  o.coef.data_ptr(), o.partial.data_ptr(), _ptr(st), _stream(dev)),
-              "tba_tbap_loss_fwd")
+        args = (gen_logp.data_ptr(), ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K), _IS[is_mode],
+                float(is_lo), float(is_hi), float(n_tok_global), ws.data_ptr(), o.seq_logp.data_ptr(),
+                o.n_tokens.data_ptr(), o.adv.data_ptr(), o.coef.data_ptr(), o.partial.data_ptr())
+        if grad_unscaled is None:
+            check(L.tba_tbap_loss_fwd(ctypes.byref(x), *args, _ptr(st), _stream(dev)), "tba_tbap_loss_fwd")
+        else:
+            Nn, Tt, V = grad_unscaled.shape
+            ors = grad_unscaled.stride(1) if Tt > 1 else (grad_unscaled.stride(0) if Nn > 1 else V)
+            check(L.tba_tbap_loss_fwd_deferred(ctypes.byref(x), *args, grad_unscaled.data_ptr(),
+                                               _DT[grad_unscaled.dtype], max(ors, V), _ptr(st), _stream(dev)),
+                  "tba_tbap_loss_fwd_deferred")
     if st is not None:
         _raise_dev_status(st, "tba_tbap_loss_fwd")
     return o, ws

@@ -157,8 +157,9 @@ def test_deferred_all_cluster_shapes(cfg, monkeypatch):
     o0, _, G0 = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
                                          inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=torch.float32)
     torch.cuda.synchronize()
-    H.assert_seq_close(o.seq_logp.cpu().numpy(), o0.seq_logp.cpu().numpy(), "seq_logp", rel=1e-9, abs_=1e-9)
-    assert torch.allclose(G, G0, rtol=1e-5, atol=1e-9)
+    # different threads per row => different fp32 partial-sum order: equal to rounding
+    H.assert_seq_close(o.seq_logp.cpu().numpy(), o0.seq_logp.cpu().numpy(), "seq_logp", rel=1e-7, abs_=1e-7)
+    assert torch.allclose(G, G0, rtol=1e-5, atol=1e-8)
     from oracle import tba_oracle as O
     h = inp["host"]
     ref = O.vargrad_head(H.host_logits(w, 2, 0, w.B), h["tokens"], h["mask"], h["ref_logp"], h["log_reward"], w.beta,

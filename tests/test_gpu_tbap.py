@@ -129,3 +129,25 @@ def test_tbap_on_policy_matches_scaled_tb_gradient():
     scale = w.beta * w.N / (2 * ntok)
     np.testing.assert_allclose(o.adv.cpu().numpy(), -w.beta * ot.resid.cpu().numpy(), rtol=1e-6, atol=1e-9)
     assert torch.allclose(dp.double(), scale * dt.double(), rtol=1e-4, atol=1e-9)
+
+
+def test_tbap_deferred_scale_matches_oracle():
+    """TBA' with the deferred-scale row pass: -(coef/n_tok) * G equals the oracle's dlogits."""
+    w = W("qwen", B=2, K=4, T=5)
+    inp = H.device_inputs(w, 8)
+    gen = syn.gen_logp(w, 8)
+    ntok = int(inp["host"]["mask"].sum())
+    G = torch.empty(inp["logits"].shape, dtype=torch.float32, device="cuda")
+    o, ws = tba.tbap_fwd(inp["logits"], inp["tokens"], inp["mask"], torch.from_numpy(gen).cuda(), inp["ref_logp"],
+                         inp["log_reward"], w.beta, w.K, "clip", 0.0, 8.0, ntok, grad_unscaled=G, check_status=True)
+    torch.cuda.synchronize()
+    h = inp["host"]
+    ref = O.tbap_head(H.host_logits(w, 8, 0, w.B), h["tokens"], h["mask"], gen, h["ref_logp"], h["log_reward"],
+                      w.beta, w.K, "clip", 0.0, 8.0)
+    H.assert_seq_close(o.adv.cpu().numpy(), ref["adv"], "adv")
+    coef = o.coef.cpu().numpy().astype(np.float64)
+    g = G.double().cpu().numpy()
+    for s in range(w.N):
+        for t in range(w.T):
+            c = -coef[s, t] / ntok
+            H.assert_dlogits_close(g[s, t] * c, ref["dlogits"][s, t], c, "fp32", f"s={s} t={t}")
