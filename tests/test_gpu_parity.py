@@ -285,3 +285,54 @@ def test_zero_length_responses_shape():
     assert o.seq_logp.abs().sum().item() == 0 and o.n_tokens.sum().item() == 0
     H.assert_seq_close([o.partial[0].item()], [r[0]], "loss")
     assert d.shape == (N, 0, 7)
+
+
+def test_power_of_two_shift_metamorphic():
+    """Adding 16 to every logit of a row (exact in bf16 for half-integer logits) leaves the
+    log-probs and the gradient unchanged (softmax shift invariance)."""
+    g = torch.Generator().manual_seed(3)
+    N, T, V, K = 4, 3, 5000, 2
+    z = (torch.randint(-16, 17, (N, T, V), generator=g).float() / 2).to(torch.bfloat16)
+    zs = (z.float() + 16.0).to(torch.bfloat16)
+    assert torch.equal(zs.float() - 16.0, z.float())            # the shift is exact
+    tok = torch.randint(0, V, (N, T), generator=g).cuda()
+    mask = torch.ones(N, T, dtype=torch.uint8, device="cuda")
+    ref = torch.randn(N, generator=g, dtype=torch.float64).cuda() - 30
+    rew = torch.rand(N, generator=g, dtype=torch.float64).cuda()
+    a, wa = tba.vargrad_fwd(z.cuda(), tok, mask, ref, rew, 0.5, K, N)
+    b, wb = tba.vargrad_fwd(zs.cuda(), tok, mask, ref, rew, 0.5, K, N)
+    da = tba.vargrad_bwd(z.cuda(), tok, mask, wa, a.resid, 2.0 / N)
+    db = tba.vargrad_bwd(zs.cuda(), tok, mask, wb, b.resid, 2.0 / N)
+    torch.cuda.synchronize()
+    H.assert_seq_close(b.seq_logp.cpu().numpy(), a.seq_logp.cpu().numpy(), "shifted seq_logp", rel=1e-6, abs_=1e-6)
+    x, y = da.float(), db.float()
+    assert torch.max(torch.abs(x - y)).item() <= 2 * 2 ** -8 * torch.max(torch.abs(x)).item()
+
+
+def test_sharded_equals_unsharded_on_one_gpu():
+    """Whole-group shards run one after another (what ranks do in parallel): per-sequence outputs
+    and dlogits are bit-identical to the unsharded run, the partials sum to its loss."""
+    w = W("qwen", B=6, K=4, T=3)   # aligned rows: identical per-row arithmetic in every shard
+    full = H.device_inputs(w, 4)
+    N = w.N
+    o, ws = tba.vargrad_fwd(full["logits"], full["tokens"], full["mask"], full["ref_logp"], full["log_reward"], w.beta,
+                            w.K, N)
+    d = tba.vargrad_bwd(full["logits"], full["tokens"], full["mask"], ws, o.resid, 2.0 / N)
+    parts = []
+    for g0, g1 in [tba.group_range(w.B, 4, r) for r in range(4)]:
+        sl = slice(g0 * w.K, g1 * w.K)
+        if g1 == g0:
+            continue
+        lg = full["logits"][sl].contiguous()
+        os_, wss = tba.vargrad_fwd(lg, full["tokens"][sl].contiguous(), full["mask"][sl].contiguous(),
+                                   full["ref_logp"][sl].contiguous(), full["log_reward"][sl].contiguous(), w.beta,
+                                   w.K, N)
+        ds = tba.vargrad_bwd(lg, full["tokens"][sl].contiguous(), full["mask"][sl].contiguous(), wss, os_.resid,
+                             2.0 / N)
+        torch.cuda.synchronize()
+        assert torch.equal(os_.seq_logp, o.seq_logp[sl]) and torch.equal(os_.resid, o.resid[sl])
+        assert torch.equal(ds.view(torch.int16), d[sl].view(torch.int16))
+        parts.append(os_.partial.cpu().numpy())
+    tot = np.sum(parts, axis=0)
+    p = o.partial.cpu().numpy()
+    assert abs(tot[0] - p[0]) <= 1e-12 * p[0] and tot[1] == p[1] and tot[2] == p[2]
