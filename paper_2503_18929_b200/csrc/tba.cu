@@ -1080,7 +1080,8 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   }
   if constexpr (CS > 1) {
     cg::cluster_group cl = cg::this_cluster();
-    cl.sync();  // partials of every CTA of the row are visible cluster-wide
+    // phase 1: every CTA's partial is visible cluster-wide (release/acquire)
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (valid && warp == 0) {
       const bool act = lane < CS;
       float pm = -INFINITY, pm2 = 0.f;
@@ -1092,11 +1093,17 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
       }
       combine_lanes(pm, pm2, ps, act, rs.sc, M, M2, S);
     }
-    cl.sync();  // no CTA leaves (or reuses its shared memory) while a peer still reads it
+    // phase 2 (split): "done reading peers" now, wait only before exiting, so that no CTA's
+    // shared memory disappears while a peer reads it and the barrier latency hides behind pass 2
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   }
-  if (!live) return;
+  if (!live) {
+    if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    return;
+  }
   if (!valid) {
     bwd_row<T, TO, 4>(rp, op, V, gt, CS * NT, false, 0.f, 0.f, 0.f, 0.f, -1);
+    if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     return;
   }
   if (threadIdx.x == 0) {
@@ -1112,6 +1119,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   __syncthreads();
   bwd_row<T, TO, U2, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
                            make_policy(false));
+  if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
 template <class T, class TO, int NT, int U2 = 4>
