@@ -163,6 +163,8 @@ def main():
     ap.add_argument("--schedule", default="two-call", choices=["two-call", "fused", "deferred"],
                     help="two-call: tba_vargrad_tb_loss_fwd + _bwd (3 kernels); fused: tba_tb_loss_fused (1 kernel); "
                          "deferred: tba_tb_loss_fwd_deferred (unscaled gradient, 4V bytes; NEXT 2 (ii))")
+    ap.add_argument("--cuda-graph", action="store_true",
+                    help="replay the step's library calls from CUDA graphs (forward and backward captured separately)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
     ap.add_argument("--share-gpu", action="store_true")
@@ -230,9 +232,7 @@ def main():
     if (fused or deferred) and tbap:
         raise SystemExit("--schedule fused implements the TB objectives (Eq. 5 / Eq. 3) only")
 
-    def step(rec=None):
-        if rec is not None:
-            rec[0].record(stream)
+    def fwd_call():
         if fused:
             tba.vargrad_fused(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
                               dlogits=dlogits, check_status=False)
@@ -245,18 +245,32 @@ def main():
         else:
             tba.vargrad_fwd(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
                             check_status=False)
-        if rec is not None:
-            rec[1].record(stream)
-        if group is not None:
-            dist.all_reduce(out.partial, group=group)
-        if rec is not None:
-            rec[2].record(stream)
+
+    def bwd_call():
         if fused or deferred:
             pass
         elif tbap:
             tba.tbap_bwd(logits, tokens, mask, ws, out.coef, n_tok_global, dlogits=dlogits)
         else:
             tba.vargrad_bwd(logits, tokens, mask, ws, out.resid, 2.0 / n_global, dlogits=dlogits)
+
+    if args.cuda_graph:
+        g_fwd, g_bwd = tba.CapturedStep(fwd_call), tba.CapturedStep(bwd_call)
+        run_fwd, run_bwd = g_fwd.replay, g_bwd.replay
+    else:
+        run_fwd, run_bwd = fwd_call, bwd_call
+
+    def step(rec=None):
+        if rec is not None:
+            rec[0].record(stream)
+        run_fwd()
+        if rec is not None:
+            rec[1].record(stream)
+        if group is not None:
+            dist.all_reduce(out.partial, group=group)
+        if rec is not None:
+            rec[2].record(stream)
+        run_bwd()
         if rec is not None:
             rec[3].record(stream)
 
@@ -418,7 +432,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (tba_synth seeded generator, DESIGN.md §6)",
-            "config": {"workload": w.name, "objective": args.objective, "schedule": args.schedule, "note": w.note,
+            "config": {"workload": w.name, "objective": args.objective, "schedule": args.schedule,
+                       "cuda_graph": bool(args.cuda_graph), "note": w.note,
                        "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
                        "V": V, "beta": w.beta, "logits_dtype": w.dtype, "dlogits_dtype": w.dtype,
                        "valid_tokens_per_rank": valid_rows, "parallelism": f"group-sharded x{world}",

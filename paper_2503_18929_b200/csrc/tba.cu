@@ -1205,7 +1205,7 @@ int validate_rows(const tba_rows* x) {
   if (x->n_seq > 0 && x->seq_len > lim / x->n_seq) return TBA_ERR_INVALID_ARG;
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows > 0 && x->row_stride > lim / esz / rows) return TBA_ERR_INVALID_ARG;
-  if (rows > (int64_t)INT32_MAX * 64) return TBA_ERR_INVALID_ARG;  // grid limits (256/TPR rows per CTA)
+  if (rows > (int64_t)INT32_MAX / 4) return TBA_ERR_INVALID_ARG;  // grid.x limit (up to 4 CTAs per row)
   if (rows > 0) {
     if (!x->logits || !x->tokens || !x->mask) return TBA_ERR_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(x->logits) % esz) return TBA_ERR_INVALID_ARG;

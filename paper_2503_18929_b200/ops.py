@@ -442,3 +442,24 @@ def tbap_loss(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float,
     loss = TBAPrimeLoss.apply(logits, tokens, mask, gen_logp, ref_logp, log_reward, float(beta), int(K), is_mode,
                               float(is_lo), float(is_hi), float(n_tok_global), group, dlogits_dtype, aux)
     return (loss, aux) if return_aux else loss
+
+
+# ----------------------------------------------------------------------------- CUDA graphs
+class CapturedStep:
+    """Capture ``fn`` — a sequence of this library's calls on preallocated tensors (every call
+    is stream-ordered, allocation-free in C and sync-free) — into a CUDA graph once, then
+    ``replay()`` it. Removes the per-launch host overhead that dominates small shapes."""
+
+    def __init__(self, fn, warmup: int = 2):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            fn()
+
+    def replay(self):
+        self.graph.replay()

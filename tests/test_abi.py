@@ -77,7 +77,8 @@ def test_fwd_config_errors(L):
 @pytest.mark.parametrize("kw", [dict(n_seq=-1), dict(seq_len=-2), dict(vocab=0), dict(row_stride=99),
                                 dict(dtype=5), dict(logits=0), dict(tokens=0), dict(mask=0),
                                 dict(logits=FAKE + 1), dict(dtype=1, logits=FAKE + 2), dict(tokens=FAKE + 4),
-                                dict(n_seq=2 ** 40, seq_len=2 ** 30), dict(row_stride=2 ** 62)])
+                                dict(n_seq=2 ** 40, seq_len=2 ** 30), dict(row_stride=2 ** 62),
+                                dict(n_seq=2 ** 20, seq_len=2 ** 10)])
 def test_rows_arg_errors(L, kw):
     x = _rows(**kw)
     assert _fwd(L, x) == _lib.TBA_ERR_INVALID_ARG

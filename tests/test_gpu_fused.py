@@ -170,3 +170,26 @@ def test_deferred_all_cluster_shapes(cfg, monkeypatch):
     for s_ in range(w.N):
         for t in range(w.T):
             H.assert_dlogits_close(g[s_, t] * 2 * eps[s_] / w.N, ref["dlogits"][s_, t], 2 * eps[s_] / w.N, "fp32")
+
+
+def test_cuda_graph_capture_replays_bitwise():
+    w = W("redteam", B=4, K=8, T=5)
+    inp = H.device_inputs(w, 6)
+    ws = torch.empty(tba.workspace_bytes(w.N, w.T), dtype=torch.uint8, device="cuda")
+    out = tba.ops._Fwd(w.N, w.K, torch.device("cuda"))
+    d = torch.empty_like(inp["logits"])
+
+    def step():
+        tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta, w.K,
+                        float(w.N), workspace=ws, out=out, check_status=False)
+        tba.vargrad_bwd(inp["logits"], inp["tokens"], inp["mask"], ws, out.resid, 2.0 / w.N, dlogits=d)
+
+    step()
+    torch.cuda.synchronize()
+    ref_d, ref_p = d.clone(), out.partial.clone()
+    d.zero_()
+    out.partial.zero_()
+    g = tba.CapturedStep(step)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.partial, ref_p) and torch.equal(d.view(torch.int16), ref_d.view(torch.int16))
