@@ -144,7 +144,7 @@ def test_deferred_scale_matches_oracle(name, w):
     assert torch.allclose(G2.double(), G.double(), rtol=2 ** -8, atol=1e-30)
 
 
-@pytest.mark.parametrize("cfg", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("cfg", ["0", "1", "2", "3", "4", "5", "6", "7"])
 def test_deferred_all_cluster_shapes(cfg, monkeypatch):
     """Every (threads, cluster size) configuration of the deferred kernel gives the same G."""
     monkeypatch.setenv("TBA_SINGLE_CFG", cfg)
