@@ -31,8 +31,18 @@ for w in cases:
     d = torch.empty_like(lg)
     tba.vargrad_bwd(lg, tok, mask, ws, o.resid, 2.0 / w.N, dlogits=d)
     sl, nt = tba.seq_logprob(lg, tok, mask, check_status=True)
+    # the other entry points: TBA' (two-call and deferred), fused one-launch, deferred TB
+    gen = torch.from_numpy(syn.gen_logp(w, 0)).cuda()
+    ntok = float(max(int(mask.sum().item()), 1))
+    ob, wsb = tba.tbap_fwd(lg, tok, mask, gen, ref, rew, w.beta, w.K, "icepop", 0.5, 2.0, ntok, check_status=True)
+    db = tba.tbap_bwd(lg, tok, mask, wsb, ob.coef, ntok)
+    G = torch.empty_like(lg)
+    tba.tbap_fwd(lg, tok, mask, gen, ref, rew, w.beta, w.K, "clip", 0.0, 8.0, ntok, grad_unscaled=G)
+    of, _, df, _ = tba.vargrad_fused(lg, tok, mask, ref, rew, w.beta, w.K, float(w.N), check_status=True)
+    od, _, Gd = tba.vargrad_fwd_deferred(lg, tok, mask, ref, rew, w.beta, w.K, float(w.N), check_status=True)
     torch.cuda.synchronize()
+    s2 = float(db.float().sum().item() + G.float().sum().item() + df.float().sum().item() + Gd.float().sum().item())
     s = float(d.float().sum().item())  # reads every dlogits element (initcheck)
     print(w.name, w.V, "loss", o.partial[0].item(), "sum dlogits", s, "seq_logprob match",
-          torch.equal(sl, o.seq_logp))
+          torch.equal(sl, o.seq_logp), "other paths", s2, torch.equal(of.partial, o.partial))
 print("sanitize cases done")
