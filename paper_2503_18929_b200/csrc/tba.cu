@@ -267,7 +267,7 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 }
 
 // LDG-streamed partial state of one row over threads tid, tid+nthr, ...
-template <class T, int U, bool POL = false>
+template <class T, int U, bool POL = false, int NP = 0>
 __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_t V, int tid, int nthr,
                                                OnlineState& st, uint64_t pol = 0) {
   using E = Elem<T>;
@@ -286,7 +286,7 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 #pragma unroll
     for (int u = 0; u < U; ++u)
       v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
-    fwd_consume<T, U>(v, st);
+    fwd_consume<T, U, NP>(v, st);
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
@@ -296,7 +296,7 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 
 // TPR threads per row, 256/TPR rows per CTA (TPR = 32 ... 256). Each row group meets on its own
 // named barrier (ids 1..8); a masked row's group exits as a whole.
-template <class T, int TPR, int U>
+template <class T, int TPR, int U, int NP = 0>
 __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                      int64_t stride, const int64_t* __restrict__ tokens,
                                                      const uint8_t* __restrict__ mask, RowScale rs,
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits
   }
   OnlineState st;
   st.init(rs);
-  fwd_accumulate<T, U>(rp, V, gt, TPR, st);
+  fwd_accumulate<T, U, false, NP>(rp, V, gt, TPR, st);
   float M, M2;
   double S;
   combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
         }
         OnlineState st;
         st.init(a.rs);
-        fwd_accumulate<T, kFusedU>(rp, a.V, gt, TPR_F, st);
+        fwd_accumulate<T, kFusedU, false, (TPR_F == 64 ? 1 : 0)>(rp, a.V, gt, TPR_F, st);  // as the two-call path
         float M, M2;
         double S;
         combine_lanes(st.m, st.R2, st.s, true, a.rs.sc, M, M2, S);
@@ -1421,6 +1421,20 @@ void launch_fwd_rows_t(const T* lg, const tba_rows* x, const WsLayout& w, const 
 #define TBA_ROWS(TPR_)                                                                                               \
   row_fwd_rows<T, TPR_, kU><<<grid, 256, 0, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, \
                                                  w.lp, dev_status)
+  // Pairs per 16-byte vector whose exp2 runs on the FMA pipe (exp2_poly2) instead of MUFU: 1 of 4
+  // relieves the XU pipe (75 % busy) and gives +3 % forward bandwidth on every BASELINE shape
+  // (scripts/gpu_ab_np.sh; 2 of 4 over-loads the FMA/ALU pipes). TBA_FWD_NP overrides (A/B).
+  const int np = env_int("TBA_FWD_NP", 1);
+  if (tpr == 64 && np == 1) {
+    row_fwd_rows<T, 64, kU, 1><<<grid, 256, 0, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, rs,
+                                                    w.stats, w.lp, dev_status);
+    return;
+  }
+  if (tpr == 64 && np == 2) {
+    row_fwd_rows<T, 64, kU, 2><<<grid, 256, 0, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, rs,
+                                                    w.stats, w.lp, dev_status);
+    return;
+  }
   switch (tpr) {
     case 32: TBA_ROWS(32); break;
     case 64: TBA_ROWS(64); break;
