@@ -336,3 +336,27 @@ def test_sharded_equals_unsharded_on_one_gpu():
     tot = np.sum(parts, axis=0)
     p = o.partial.cpu().numpy()
     assert abs(tot[0] - p[0]) <= 1e-12 * p[0] and tot[1] == p[1] and tot[2] == p[2]
+
+
+@pytest.mark.parametrize("V,T,dt", [(262144, 2, "bf16"), (131072, 3, "fp32"), (1000, 8192, "bf16")])
+def test_extreme_shapes(V, T, dt):
+    """Vocabularies past Qwen's (512 KB bf16 / fp32 rows) and very long responses."""
+    w = W("qwen", B=1, K=2, T=T, V=V, dtype=dt, len_lo=T // 2, len_hi=T)
+    compare_full(w, 3) if V * T <= 2 ** 20 else _compare_sampled(w, 3)
+
+
+def _compare_sampled(w, seed):
+    inp = H.device_inputs(w, seed)
+    o, d = run_gpu(inp, w)
+    ref = H.oracle_seq_values(w, seed, 0, w.B)
+    H.assert_seq_close(o.seq_logp.cpu().numpy(), ref["ell"], "seq_logp")
+    loss, logz, eps = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, w.K)
+    H.assert_seq_close(o.resid.cpu().numpy(), eps, "resid")
+    rng = np.random.default_rng(seed)
+    mask = ref["mask"]
+    for r in rng.choice(np.flatnonzero(mask.reshape(-1)), size=8, replace=False):
+        s, t = divmod(int(r), w.T)
+        z = syn.logits_rows_f64(seed, w.V, [r], w.dtype)[0]
+        want = O.dlogits_row(z, int(ref["tokens"][s, t]), eps[s], w.N)
+        got = d[s, t].double().cpu().numpy()
+        H.assert_dlogits_close(got, want, 2 * eps[s] / w.N, "bf16" if d.dtype == torch.bfloat16 else "fp32")
