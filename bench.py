@@ -159,6 +159,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the deferred-scale variant measurement")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--schedule", default="two-call", choices=["two-call", "fused", "deferred"],
                     help="two-call: tba_vargrad_tb_loss_fwd + _bwd (3 kernels); fused: tba_tb_loss_fused (1 kernel); "
@@ -306,6 +307,35 @@ def main():
     ms_step, fwd_ms, bwd_ms = tmax.tolist()
     loss = out.partial[0].item()
 
+    # ---- variant: the deferred-scale schedule on the same inputs
+    variants = {}
+    if not (fused or deferred or tbap) and not args.no_variants:
+        def dstep():
+            tba.vargrad_fwd_deferred(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
+                                     grad_unscaled=dlogits, check_status=False)
+            if group is not None:
+                dist.all_reduce(out.partial, group=group)
+        for _ in range(args.warmup):
+            dstep()
+        torch.cuda.synchronize()
+        if group is not None:
+            dist.barrier()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(args.steps):
+            dstep()
+        b.record(stream)
+        torch.cuda.synchronize()
+        d_ms = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+        if group is not None:
+            dist.all_reduce(d_ms, op=dist.ReduceOp.MAX, group=group)
+        d_ms = d_ms.item()
+        variants["deferred_scale"] = {
+            "ms_per_step": d_ms, "value": tokens_per_step_rank * world / (d_ms / 1e3), "unit": "tokens/s",
+            "what": "tba_tb_loss_fwd_deferred: loss + UNSCALED gradient G in one pass per row; "
+                    "dlogits = (2/N) eps_s G is applied by the consumer (DESIGN.md §5.4)",
+            "gpu_launches_per_step": 2}
+
     # ---- e2e: the same step through the public API from pinned HOST buffers
     e2e = None
     if not args.no_e2e:
@@ -445,6 +475,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "variants": variants,
             "gpu_launches": args.steps * (1 if fused else 2 if deferred else 3),
             "loss": loss,
         }
