@@ -81,6 +81,12 @@ size_t tba_workspace_bytes(int64_t n_seq, int64_t seq_len);
 int tba_seq_logprob(const tba_rows* x, void* workspace, double* seq_logp, int32_t* n_tokens,
                     int32_t* dev_status, tba_stream_t stream);
 
+/* Per-token log-probs (step a1 alone; SPEC's logprob per_token):
+ *   tok_logp[s,t] = mask ? log softmax(inv_temp * z_{s,t})[y_{s,t}] : 0   (fp64, [N, T])
+ * e.g. to record pi_gen log-probs for TBA' or per-token KL terms. inv_temp finite and > 0. */
+int tba_token_logprob(const tba_rows* x, double inv_temp, void* workspace, double* tok_logp,
+                      int32_t* dev_status, tba_stream_t stream);
+
 /* Forward of the VarGrad TB loss over this call's groups (steps a1-a3), Eqs. 4-5.
  *   ref_logp[s]   = log pi_ref(y_s|x)  (fp64, [N]; e.g. from tba_seq_logprob on pi_ref logits)
  *   log_reward[s] = r_phi(y_s; x)       (fp64, [N]; the paper's r_phi, divided by beta here)

@@ -17,7 +17,7 @@ TBA_DEV_TOKEN_RANGE, TBA_DEV_NONFINITE_ROW = 1, 2
 TBA_BF16, TBA_FP32 = 0, 1
 
 # every symbol include/tba.h declares (checked by tests/test_abi.py)
-EXPORTS = ("tba_abi_version", "tba_status_string", "tba_workspace_bytes", "tba_seq_logprob",
+EXPORTS = ("tba_abi_version", "tba_status_string", "tba_workspace_bytes", "tba_seq_logprob", "tba_token_logprob",
            "tba_vargrad_tb_loss_fwd", "tba_vargrad_tb_loss_bwd", "tba_tb_loss_fwd", "tba_tb_loss_bwd", "tba_tb_loss_fused",
            "tba_tb_loss_fwd_deferred",
            "tba_tbap_loss_fwd", "tba_tbap_loss_bwd", "tba_tbap_loss_fwd_deferred")
@@ -64,6 +64,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         L.tba_workspace_bytes.argtypes = [I64, I64]
         L.tba_seq_logprob.restype = ctypes.c_int
         L.tba_seq_logprob.argtypes = [RP, P, P, P, P, P]
+        L.tba_token_logprob.restype = ctypes.c_int
+        L.tba_token_logprob.argtypes = [RP, D, P, P, P, P]
         L.tba_vargrad_tb_loss_fwd.restype = ctypes.c_int
         L.tba_vargrad_tb_loss_fwd.argtypes = [RP, P, P, D, I32, D, P, P, P, P, P, P, P, P]
         L.tba_vargrad_tb_loss_bwd.restype = ctypes.c_int

@@ -687,6 +687,13 @@ __global__ void __launch_bounds__(256) tbap_head(const double* __restrict__ lp, 
   }
 }
 
+// Per-token log-probs out of the workspace: tok_logp[r] = mask ? lp[r] : 0.
+__global__ void token_lp_kernel(const double* __restrict__ lp, const uint8_t* __restrict__ mask, int64_t rows,
+                                double* __restrict__ out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = mask[r] ? lp[r] : 0.0;
+}
+
 // dL/d log Z_i for a learned log Z (Eq. 3): grad_scale * g * sum_j eps_{iK+j}.
 __global__ void dlogz_kernel(const double* __restrict__ resid, int64_t groups, int K, double grad_scale,
                              const double* __restrict__ grad_out, double* __restrict__ d_log_z) {
@@ -1642,6 +1649,23 @@ int tba_seq_logprob(const tba_rows* x, void* workspace, double* seq_logp, int32_
   seq_head<false><<<(unsigned)grid, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, 8, nullptr, nullptr, nullptr,
                                                  0.0, 0.0, seq_logp, n_tokens, nullptr, nullptr, nullptr, nullptr,
                                                  nullptr);
+  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+int tba_token_logprob(const tba_rows* x, double inv_temp, void* workspace, double* tok_logp, int32_t* dev_status,
+                      tba_stream_t stream) {
+  int rc = validate_rows(x);
+  if (rc) return rc;
+  if (!(std::isfinite(inv_temp) && inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows == 0) return TBA_OK;
+  if (!workspace || !tok_logp || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  rc = launch_fwd_rows(x, w, make_scale(inv_temp), dev_status, s);
+  if (rc) return rc;
+  const int64_t blocks = (rows + 255) / 256 < 4096 ? (rows + 255) / 256 : 4096;
+  token_lp_kernel<<<(unsigned)blocks, 256, 0, s>>>(w.lp, x->mask, rows, tok_logp);
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 

@@ -98,6 +98,23 @@ def seq_logprob(logits, tokens, mask, *, check_status: bool = _CHECK):
     return out, ntok
 
 
+def token_logprob(logits, tokens, mask, *, inv_temp: float = 1.0, check_status: bool = _CHECK):
+    """Per-token log softmax(inv_temp * z)[y] (tba_token_logprob), fp64 [N, T], 0 where masked."""
+    L = _lib.load()
+    x = make_rows(logits, tokens, mask)
+    N, T = tokens.shape
+    dev = logits.device
+    out = torch.empty((N, T), dtype=torch.float64, device=dev)
+    ws = _workspace(dev, N, T)
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_token_logprob(ctypes.byref(x), float(inv_temp), ws.data_ptr(), out.data_ptr(), _ptr(st),
+                                  _stream(dev)), "tba_token_logprob")
+    if st is not None:
+        _raise_dev_status(st, "tba_token_logprob")
+    return out
+
+
 class _Fwd:
     """Outputs of one tba_vargrad_tb_loss_fwd call (device tensors)."""
 

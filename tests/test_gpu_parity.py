@@ -360,3 +360,24 @@ def _compare_sampled(w, seed):
         want = O.dlogits_row(z, int(ref["tokens"][s, t]), eps[s], w.N)
         got = d[s, t].double().cpu().numpy()
         H.assert_dlogits_close(got, want, 2 * eps[s] / w.N, "bf16" if d.dtype == torch.bfloat16 else "fp32")
+
+
+@pytest.mark.parametrize("inv_temp", [1.0, 1 / 0.7])
+def test_token_logprob_matches_oracle(inv_temp):
+    w = W("redteam", B=2, K=3, T=6, len_lo=2, len_hi=6)
+    inp = H.device_inputs(w, 9)
+    tl = tba.token_logprob(inp["logits"], inp["tokens"], inp["mask"], inv_temp=inv_temp, check_status=True)
+    torch.cuda.synchronize()
+    lg = H.host_logits(w, 9, 0, w.B) * inv_temp
+    h = inp["host"]
+    got = tl.cpu().numpy()
+    for s in range(w.N):
+        for t in range(w.T):
+            if h["mask"][s, t]:
+                want, _ = O.token_logprob(lg[s, t], int(h["tokens"][s, t]))
+                assert abs(got[s, t] - want) <= 1e-5 * max(1.0, abs(want))
+            else:
+                assert got[s, t] == 0.0
+    sl, _ = tba.seq_logprob(inp["logits"], inp["tokens"], inp["mask"])
+    if inv_temp == 1.0:
+        H.assert_seq_close(tl.sum(1).cpu().numpy(), sl.cpu().numpy(), "sum of token log-probs", rel=1e-9, abs_=1e-9)
