@@ -166,6 +166,8 @@ def main():
                          "deferred: tba_tb_loss_fwd_deferred (unscaled gradient, 4V bytes; NEXT 2 (ii))")
     ap.add_argument("--cuda-graph", action="store_true",
                     help="replay the step's library calls from CUDA graphs (forward and backward captured separately)")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 loss all-reduce: NCCL all_reduce, or fused into the head kernel over peer memory")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
     ap.add_argument("--share-gpu", action="store_true")
@@ -197,6 +199,7 @@ def main():
             dist.init_process_group(args.dist_backend)
         group = dist.group.WORLD
     tba.load_library()
+    peer = tba.PeerReducer(group, dev) if (group is not None and args.collective == "peer") else None
 
     # ---- inputs: this rank's whole groups of the global batch, resident in HBM
     B, K, T, V = w.B, w.K, w.T, w.V
@@ -245,7 +248,7 @@ def main():
                          workspace=ws, out=out, check_status=False)
         else:
             tba.vargrad_fwd(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
-                            check_status=False)
+                            check_status=False, peer=peer)
 
     def bwd_call():
         if fused or deferred:
@@ -255,6 +258,8 @@ def main():
         else:
             tba.vargrad_bwd(logits, tokens, mask, ws, out.resid, 2.0 / n_global, dlogits=dlogits)
 
+    if args.cuda_graph and peer is not None:
+        raise SystemExit("--cuda-graph with --collective peer is not supported (the epoch is a per-call host value)")
     if args.cuda_graph:
         g_fwd, g_bwd = tba.CapturedStep(fwd_call), tba.CapturedStep(bwd_call)
         run_fwd, run_bwd = g_fwd.replay, g_bwd.replay
@@ -267,7 +272,7 @@ def main():
         run_fwd()
         if rec is not None:
             rec[1].record(stream)
-        if group is not None:
+        if group is not None and (peer is None or fused or deferred or tbap):
             dist.all_reduce(out.partial, group=group)
         if rec is not None:
             rec[2].record(stream)
@@ -467,6 +472,7 @@ def main():
                        "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
                        "V": V, "beta": w.beta, "logits_dtype": w.dtype, "dlogits_dtype": w.dtype,
                        "valid_tokens_per_rank": valid_rows, "parallelism": f"group-sharded x{world}",
+                       "collective": (args.collective if world > 1 else None),
                        "l2": "inputs (%.1f GB logits + dlogits per rank) >> 126 MB L2; no flush needed" %
                              ((logits.numel() * esz * 2) / 1e9)},
             "hbm_gbs_step": step_gbs,

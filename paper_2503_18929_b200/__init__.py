@@ -5,7 +5,7 @@ this package only marshals PyTorch tensors into it. There is no CPU fallback: th
 raise if the extension is missing.
 """
 from ._lib import TbaError, load as load_library  # noqa: F401
-from .dist import group_range, token_balanced_ranges  # noqa: F401
+from .dist import PeerReducer, group_range, token_balanced_ranges  # noqa: F401
 from .ops import (CapturedStep, TBAPrimeLoss, VarGradTBLoss, make_rows, seq_logprob, tbap_bwd, tbap_fwd,  # noqa: F401
                   tbap_loss, token_logprob, vargrad_bwd, vargrad_fused, vargrad_fwd, vargrad_fwd_deferred, vargrad_tb_loss,
                   vargrad_tb_loss_and_grad, workspace_bytes)
@@ -13,4 +13,4 @@ from .ops import (CapturedStep, TBAPrimeLoss, VarGradTBLoss, make_rows, seq_logp
 __all__ = ["CapturedStep", "seq_logprob", "token_logprob", "vargrad_tb_loss", "VarGradTBLoss", "vargrad_fwd", "vargrad_bwd", "workspace_bytes",
            "tbap_loss", "TBAPrimeLoss", "tbap_fwd", "tbap_bwd", "vargrad_fused", "vargrad_tb_loss_and_grad",
            "vargrad_fwd_deferred",
-           "group_range", "token_balanced_ranges", "load_library", "TbaError"]
+           "group_range", "token_balanced_ranges", "PeerReducer", "load_library", "TbaError"]

@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -546,6 +547,67 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
   if (my_count) *my_count = tot;
 }
 
+// One-shot all-reduce of the 3 loss partials fused into the head kernel, over peer memory
+// (NVLink P2P stores / loads through CUDA IPC mappings): the last CTA of every rank
+// writes its partial into slot [rank] of every peer's buffer, releases a per-peer flag with the
+// call's epoch, waits (acquire, bounded by a timeout) for all ranks' flags, and sums the slots in
+// rank order — every rank computes bit-identical totals, with no NCCL launch. Slots are double-
+// buffered by epoch parity (a rank cannot get two epochs ahead of a peer that has not read).
+struct PeerArgs {
+  double* const* slots;         // [world] device pointers: rank q's buffer of 2 x world x 4 doubles
+  unsigned int* const* flags;   // [world] device pointers: rank q's [world] epoch flags
+  int rank, world;
+  unsigned int epoch;
+  unsigned long long timeout_ns;
+  int32_t* dev_status;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ void peer_allreduce3(const PeerArgs& pa, const double (&p)[3], double* partial) {
+  const int par = (int)(pa.epoch & 1u);
+  for (int q = 0; q < pa.world; ++q) {
+    double* dst = pa.slots[q] + ((size_t)par * pa.world + pa.rank) * 4;
+    dst[0] = p[0];
+    dst[1] = p[1];
+    dst[2] = p[2];
+  }
+  __threadfence_system();
+  for (int q = 0; q < pa.world; ++q)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pa.flags[q] + pa.rank), "r"(pa.epoch) : "memory");
+  const unsigned int* mine = pa.flags[pa.rank];
+  const unsigned long long t0 = globaltimer_ns();
+  bool timeout = false;
+  for (int q = 0; q < pa.world && !timeout; ++q) {
+    for (;;) {
+      unsigned int v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + q) : "memory");
+      if ((int)(v - pa.epoch) >= 0) break;
+      if (globaltimer_ns() - t0 > pa.timeout_ns) {
+        timeout = true;
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  if (timeout) {
+    if (pa.dev_status) atomicOr(pa.dev_status, TBA_DEV_PEER_TIMEOUT);
+    partial[0] = partial[1] = partial[2] = nan("");
+    return;
+  }
+  const volatile double* my = pa.slots[pa.rank] + (size_t)par * pa.world * 4;
+  double t[3] = {0.0, 0.0, 0.0};
+  for (int q = 0; q < pa.world; ++q)
+    for (int k = 0; k < 3; ++k) t[k] += my[q * 4 + k];
+  partial[0] = t[0];
+  partial[1] = t[1];
+  partial[2] = t[2];
+}
+
 // One CTA per group of K sequences (HEAD), or per 8 sequences (log-probs only).
 // Eq. 4: log Z_i = 1/K sum_j delta_j (delta = rho - ell + r/beta), or the learned log Z_i of
 // Eq. 3 when log_z_param != NULL; Eq. 5 residual eps = log Z_i - delta. The last CTA (counter)
@@ -558,7 +620,8 @@ __global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, c
                                                 double inv_n_global, double* __restrict__ seq_logp,
                                                 int32_t* __restrict__ n_tokens, double* __restrict__ log_z,
                                                 double* __restrict__ resid, double* __restrict__ group_sq,
-                                                double* __restrict__ partial, unsigned int* counter) {
+                                                double* __restrict__ partial, unsigned int* counter,
+                                                PeerArgs pa = PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr}) {
   const int per = HEAD ? K : 8;
   const int64_t s0 = (int64_t)blockIdx.x * per;
   seq_sums(lp, mask, n_seq, T, s0, per, seq_logp, n_tokens, nullptr);
@@ -596,10 +659,15 @@ __global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, c
     const volatile double* gs = group_sq;
     double tot = 0.0;
     for (unsigned i = 0; i < gridDim.x; ++i) tot += gs[i];
-    partial[0] = tot * inv_n_global;
-    partial[1] = (double)n_seq;
-    partial[2] = (double)gridDim.x;
     *counter = 0u;
+    const double p[3] = {tot * inv_n_global, (double)n_seq, (double)gridDim.x};
+    if (pa.world > 0) {
+      peer_allreduce3(pa, p, partial);
+    } else {
+      partial[0] = p[0];
+      partial[1] = p[1];
+      partial[2] = p[2];
+    }
   }
 }
 
@@ -1669,9 +1737,34 @@ int tba_token_logprob(const tba_rows* x, double inv_temp, void* workspace, doubl
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
+static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                            const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                            double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                            int32_t* dev_status, const tba_peer_reduce* pr, tba_stream_t stream);
+
 int tba_tb_loss_fwd(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
                     double beta, int32_t K, double n_seq_global, void* workspace, double* seq_logp, int32_t* n_tokens,
                     double* log_z, double* resid, double* partial, int32_t* dev_status, tba_stream_t stream) {
+  return tb_loss_fwd_impl(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
+                          resid, partial, dev_status, nullptr, stream);
+}
+
+int tba_tb_loss_fwd_peer(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                         const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                         double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                         const tba_peer_reduce* pr, int32_t* dev_status, tba_stream_t stream) {
+  if (!pr || !pr->slots || !pr->flags || pr->world < 1 || pr->rank < 0 || pr->rank >= pr->world || pr->epoch == 0 ||
+      !(pr->timeout_s > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (x && x->n_seq == 0) return TBA_ERR_INVALID_ARG;  // every rank must own >= 1 group to join the reduction
+  return tb_loss_fwd_impl(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
+                          resid, partial, dev_status, pr, stream);
+}
+
+static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                            const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                            double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                            int32_t* dev_status, const tba_peer_reduce* pr, tba_stream_t stream) {
   if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
   if (K < 2) return TBA_ERR_INVALID_CONFIG;
   int rc = check_opts(opts);
@@ -1693,11 +1786,44 @@ int tba_tb_loss_fwd(const tba_rows* x, const tba_tb_opts* opts, const double* re
   rc = launch_fwd_rows(x, w, make_scale(opt_inv_temp(opts)), dev_status, s);
   if (rc) return rc;
   const int64_t groups = x->n_seq / K;
+  PeerArgs pa{nullptr, nullptr, 0, 0, 0u, 0ull, dev_status};
+  if (pr) {
+    pa.slots = pr->slots;
+    pa.flags = pr->flags;
+    pa.rank = pr->rank;
+    pa.world = pr->world;
+    pa.epoch = pr->epoch;
+    pa.timeout_ns = (unsigned long long)(pr->timeout_s * 1e9);
+  }
   seq_head<true><<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, K, ref_logp, log_reward,
                                                   opts ? opts->log_z_param : nullptr, 1.0 / beta, 1.0 / n_seq_global,
-                                                  seq_logp, n_tokens, log_z, resid, w.group_sq, partial, w.counter);
+                                                  seq_logp, n_tokens, log_z, resid, w.group_sq, partial, w.counter,
+                                                  pa);
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
+
+// ---- CUDA IPC helpers for the peer reduction buffers (host-side, not on the hot path)
+int tba_ipc_alloc(size_t bytes, void** dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64 || bytes == 0) return TBA_ERR_INVALID_ARG;
+  if (cudaMalloc(dev_ptr, bytes) != cudaSuccess) return TBA_ERR_CUDA;
+  if (cudaMemset(*dev_ptr, 0, bytes) != cudaSuccess) return TBA_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, *dev_ptr) != cudaSuccess) return TBA_ERR_CUDA;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, sizeof(h));
+  return TBA_OK;
+}
+
+int tba_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return TBA_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+int tba_ipc_close(void* dev_ptr) { return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
+
+int tba_ipc_free(void* dev_ptr) { return cudaFree(dev_ptr) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
 
 int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* workspace, const double* resid,
                     double grad_scale, const double* grad_out, void* dlogits, int32_t dlogits_dtype,

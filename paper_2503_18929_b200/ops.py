@@ -134,7 +134,7 @@ def _opts(inv_temp: float, log_z_param):
 
 def vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
                 workspace=None, out: _Fwd | None = None, check_status: bool = _CHECK, inv_temp: float = 1.0,
-                log_z_param=None):
+                log_z_param=None, peer=None):
     """Raw TB forward (tba_tb_loss_fwd; tba_vargrad_tb_loss_fwd when inv_temp = 1 and no learned
     log Z). log_z_param: optional fp64 [N/K] learned log Z(x_i) (Eq. 3). Returns (_Fwd, workspace)."""
     L = _lib.load()
@@ -155,7 +155,13 @@ def vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int,
         args = (ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K), float(n_seq_global), ws.data_ptr(),
                 o.seq_logp.data_ptr(), o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None, o.resid.data_ptr(),
                 o.partial.data_ptr(), _ptr(st), _stream(dev))
-        if opts is None:
+        if peer is not None:  # dist.PeerReducer: partial becomes the all-reduced global value
+            pr = peer.next_args()
+            a = list(args)
+            st_ptr, stream = a[-2], a[-1]
+            check(L.tba_tb_loss_fwd_peer(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
+                                         *a[:-2], ctypes.byref(pr), st_ptr, stream), "tba_tb_loss_fwd_peer")
+        elif opts is None:
             check(L.tba_vargrad_tb_loss_fwd(ctypes.byref(x), *args), "tba_vargrad_tb_loss_fwd")
         else:
             check(L.tba_tb_loss_fwd(ctypes.byref(x), ctypes.byref(opts), *args), "tba_tb_loss_fwd")
@@ -206,11 +212,11 @@ class VarGradTBLoss(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, logits, log_z_param, tokens, mask, ref_logp, log_reward, beta, K, n_global, group,
-                dlogits_dtype, inv_temp, aux):
+                dlogits_dtype, inv_temp, aux, peer=None):
         lzp = None if log_z_param is None else log_z_param.detach().contiguous()
         o, ws = vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta, K, n_global, inv_temp=inv_temp,
-                            log_z_param=lzp)
-        if group is not None:
+                            log_z_param=lzp, peer=peer)
+        if group is not None and peer is None:
             import torch.distributed as dist
             dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
         ctx.save_for_backward(logits, tokens, mask, ws, o.resid)
@@ -227,11 +233,12 @@ class VarGradTBLoss(torch.autograd.Function):
         r = vargrad_bwd(logits, tokens, mask, ws, resid, 2.0 / ctx.n_global, grad_out=grad,
                         dlogits_dtype=ctx.dlogits_dtype, inv_temp=ctx.inv_temp, log_z_param=ctx.lzp, K=ctx.K)
         d, dz = (r, None) if ctx.lzp is None else r
-        return (d, dz) + (None,) * 11
+        return (d, dz) + (None,) * 12
 
 
 def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
-                    group=None, dlogits_dtype=None, return_aux: bool = False, log_z=None, inv_temp: float = 1.0):
+                    group=None, dlogits_dtype=None, return_aux: bool = False, log_z=None, inv_temp: float = 1.0,
+                    peer=None):
     """The trajectory-balance loss, autograd-enabled.
 
     Default: the VarGrad loss of Eq. 5 with the detached K-sample log Z of Eq. 4.
@@ -240,8 +247,9 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
     logits [N, T, V] bf16/fp32 (N = groups*K, group-major); tokens int64 [N, T]; mask
     uint8/bool [N, T]; ref_logp, log_reward fp64 [N] (log_reward is r_phi). With ``group``
     each rank passes its own whole groups and the partial sums are all-reduced once;
-    ``n_seq_global`` defaults to N * world. Returns the 0-dim fp64 loss (and an aux dict
-    with seq_logp, n_tokens, log_z, resid, partial when ``return_aux``)."""
+    ``n_seq_global`` defaults to N * world. ``peer`` (a ``dist.PeerReducer``) replaces the NCCL
+    all-reduce by the one fused into the head kernel over peer memory. Returns the 0-dim fp64
+    loss (and an aux dict with seq_logp, n_tokens, log_z, resid, partial when ``return_aux``)."""
     N = tokens.shape[0]
     if n_seq_global is None:
         if group is not None:
@@ -251,7 +259,7 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
             n_seq_global = N
     aux = {} if return_aux else None
     loss = VarGradTBLoss.apply(logits, log_z, tokens, mask, ref_logp, log_reward, float(beta), int(K),
-                               float(n_seq_global), group, dlogits_dtype, float(inv_temp), aux)
+                               float(n_seq_global), group, dlogits_dtype, float(inv_temp), aux, peer)
     return (loss, aux) if return_aux else loss
 
 
