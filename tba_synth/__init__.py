@@ -144,6 +144,9 @@ WORKLOADS = {
 # The per-GPU shard of the Qwen batch at 8xB200 (8 of the 64 groups).
 WORKLOADS["qwen_shard"] = dataclasses.replace(WORKLOADS["qwen"], name="qwen_shard", B=8,
                                               note="Qwen2.5-7B MATH per-GPU shard: 8 groups x K=8, T=1024, V=152064")
+# Pythia TL;DR in fp32 logits/dlogits: the paper's PFT runs were fp32 without DeepSpeed.
+WORKLOADS["pythia_fp32"] = dataclasses.replace(WORKLOADS["pythia"], name="pythia_fp32", dtype="fp32",
+                                               note="Pythia-410M TL;DR shape with fp32 logits (PFT precision, P:593)")
 # One Qwen group (8 x 1024 rows, 2.5 GB of logits): the slice `ncu --set full` replays.
 WORKLOADS["qwen_group"] = dataclasses.replace(WORKLOADS["qwen"], name="qwen_group", B=1,
                                               note="one Qwen2.5-7B MATH group: 1 x K=8, T=1024, V=152064 (profiling)")
