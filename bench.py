@@ -33,6 +33,15 @@ SEED = 0
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
+def baseline_metric() -> str:
+    """BASELINE.json's metric string (the value is its tokens/s part; GB/s are in roofline)."""
+    p = os.path.join(ROOT, "BASELINE.json")
+    try:
+        return json.load(open(p))["metric"]
+    except Exception:
+        return "TB-loss fwd+bwd tokens/sec and HBM GB/s vs B200 peak at 1/2/4/8 GPUs"
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -140,7 +149,7 @@ def run_reference(args, w):
         toks += t
     v = toks / secs
     sample = f"{groups} group x K={w.K} x first {tp} positions per step ({toks // args.steps} rows), fwd+bwd a1-a5"
-    line = {"impl": "reference", "metric": "TB-loss fwd+bwd tokens/sec", "value": v, "unit": "tokens/s",
+    line = {"impl": "reference", "metric": baseline_metric(), "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "objective": args.objective, "note": w.note, "B_per_rank": w.B, "K": w.K, "T": w.T, "V": w.V},
@@ -461,7 +470,7 @@ def main():
             kern = {"fwd_ms": fwd_ms, "fwd_gbs": fwd_gbs, "fwd_frac": fwd_gbs / peak, "bwd_ms": bwd_ms,
                     "bwd_gbs": bwd_gbs, "step_frac": step_gbs / peak}
         line = {
-            "metric": "TB-loss fwd+bwd tokens/sec" + (" (TBA' Eq. 16 objective)" if tbap else ""),
+            "metric": baseline_metric() + (" [TBA' Eq. 16 objective]" if tbap else ""),
             "value": tokens_per_step_rank * world / (ms_step / 1e3),
             "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
