@@ -491,7 +491,10 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "variants": variants,
-            "gpu_launches": args.steps * (1 if fused else 2 if deferred else 3),
+            # our kernels per step: fused 1; deferred row_single + seq_head; two-call row_fwd_rows + seq_head
+            # (tbap_head) + row_bwd; 2 with TBA_FUSE_HEAD=1 (row_fwd_head + row_bwd)
+            "gpu_launches": args.steps * (1 if fused else 2 if deferred else
+                                          2 if (not tbap and os.environ.get("TBA_FUSE_HEAD", "0") == "1") else 3),
             "loss": loss,
         }
         print(json.dumps(line), flush=True)

@@ -297,17 +297,16 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 
 // TPR threads per row, 256/TPR rows per CTA (TPR = 32 ... 256). Each row group meets on its own
 // named barrier (ids 1..8); a masked row's group exits as a whole.
-template <class T, int TPR, int U, int NP = 0>
-__global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits, int64_t rows, int64_t V,
-                                                     int64_t stride, const int64_t* __restrict__ tokens,
-                                                     const uint8_t* __restrict__ mask, RowScale rs,
-                                                     float2* __restrict__ stats, double* __restrict__ lp,
-                                                     int32_t* dev_status) {
-  constexpr int RPC = 256 / TPR, WPR = TPR / 32;
-  const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
+// The row work of one TPR-thread row group (called with a valid row only).
+template <class T, int TPR, int U, int NP, bool FENCE = false>
+__device__ __forceinline__ void fwd_row_group(const T* __restrict__ logits, int64_t row, int64_t V, int64_t stride,
+                                              const int64_t* __restrict__ tokens, const RowScale& rs,
+                                              float2* __restrict__ stats, double* __restrict__ lp,
+                                              int32_t* dev_status, float (*sm_m)[TPR / 32 > 0 ? TPR / 32 : 1],
+                                              float (*sm_M2)[TPR / 32 > 0 ? TPR / 32 : 1],
+                                              double (*sm_s)[TPR / 32 > 0 ? TPR / 32 : 1], int grp, int gt) {
+  constexpr int WPR = TPR / 32;
   const int lane = threadIdx.x & 31, wig = gt >> 5;
-  const int64_t row = (int64_t)blockIdx.x * RPC + grp;
-  if (row >= rows || mask[row] == 0) return;
   const T* rp = logits + row * stride;
   float zy = 0.f;
   bool ok = true;
@@ -323,11 +322,12 @@ __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits
   double S;
   combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
   if (WPR == 1) {
-    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+    if (lane == 0) {
+      finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+      if (FENCE) __threadfence();  // publish lp / stats before the unit counters move
+    }
     return;
   }
-  __shared__ float sm_m[RPC][WPR], sm_M2[RPC][WPR];
-  __shared__ double sm_s[RPC][WPR];
   if (lane == 0) {
     sm_m[grp][wig] = M;
     sm_M2[grp][wig] = M2;
@@ -338,8 +338,26 @@ __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits
     const bool act = lane < WPR;
     combine_lanes(act ? sm_m[grp][lane] : -INFINITY, act ? sm_M2[grp][lane] : 0.f, act ? sm_s[grp][lane] : 0.0, act,
                   rs.sc, M, M2, S);
-    if (lane == 0) finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+    if (lane == 0) {
+      finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+      if (FENCE) __threadfence();
+    }
   }
+}
+
+template <class T, int TPR, int U, int NP = 0>
+__global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                     int64_t stride, const int64_t* __restrict__ tokens,
+                                                     const uint8_t* __restrict__ mask, RowScale rs,
+                                                     float2* __restrict__ stats, double* __restrict__ lp,
+                                                     int32_t* dev_status) {
+  constexpr int RPC = 256 / TPR, WPRS = TPR / 32 > 0 ? TPR / 32 : 1;
+  __shared__ float sm_m[RPC][WPRS], sm_M2[RPC][WPRS];
+  __shared__ double sm_s[RPC][WPRS];
+  const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
+  const int64_t row = (int64_t)blockIdx.x * RPC + grp;
+  if (row >= rows || mask[row] == 0) return;
+  fwd_row_group<T, TPR, U, NP>(logits, row, V, stride, tokens, rs, stats, lp, dev_status, sm_m, sm_M2, sm_s, grp, gt);
 }
 
 // ------------------------------------------------------------------------------ a1, TMA-staged
@@ -608,6 +626,47 @@ __device__ void peer_allreduce3(const PeerArgs& pa, const double (&p)[3], double
   partial[2] = t[2];
 }
 
+// Eq. 4 (or the learned log Z of Eq. 3) and the Eq. 5 residuals of group g, by one thread.
+__device__ __forceinline__ void tb_group_head(int64_t g, int K, const double* __restrict__ ref_logp,
+                                              const double* __restrict__ log_reward,
+                                              const double* __restrict__ log_z_param, double inv_beta,
+                                              const double* seq_logp, double* __restrict__ log_z,
+                                              double* __restrict__ resid, double* __restrict__ group_sq) {
+  const int64_t s0 = g * K;
+  double lz;
+  if (log_z_param) {
+    lz = log_z_param[g];
+  } else {
+    double sum = 0.0;
+    for (int j = 0; j < K; ++j) sum += ref_logp[s0 + j] - __ldcg(seq_logp + s0 + j) + log_reward[s0 + j] * inv_beta;
+    lz = sum / (double)K;
+  }
+  double sq = 0.0;
+  for (int j = 0; j < K; ++j) {
+    const double delta = ref_logp[s0 + j] - __ldcg(seq_logp + s0 + j) + log_reward[s0 + j] * inv_beta;
+    const double e = lz - delta;
+    resid[s0 + j] = e;
+    sq += e * e;
+  }
+  log_z[g] = lz;
+  group_sq[g] = sq;
+}
+
+// Final fixed-order reduction of the per-group sums of squares (+ optional fused all-reduce).
+__device__ __forceinline__ void tb_finish(const double* group_sq, int64_t groups, int64_t n_seq, double inv_n_global,
+                                          double* partial, const PeerArgs& pa) {
+  double tot = 0.0;
+  for (int64_t i = 0; i < groups; ++i) tot += __ldcg(group_sq + i);
+  const double p[3] = {tot * inv_n_global, (double)n_seq, (double)groups};
+  if (pa.world > 0) {
+    peer_allreduce3(pa, p, partial);
+  } else {
+    partial[0] = p[0];
+    partial[1] = p[1];
+    partial[2] = p[2];
+  }
+}
+
 // One CTA per group of K sequences (HEAD), or per 8 sequences (log-probs only).
 // Eq. 4: log Z_i = 1/K sum_j delta_j (delta = rho - ell + r/beta), or the learned log Z_i of
 // Eq. 3 when log_z_param != NULL; Eq. 5 residual eps = log Z_i - delta. The last CTA (counter)
@@ -629,44 +688,92 @@ __global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, c
   __syncthreads();
   __shared__ bool am_last;
   if (threadIdx.x == 0) {
-    double lz;
-    if (log_z_param) {
-      lz = log_z_param[blockIdx.x];
-    } else {
-      double sum = 0.0;
-      for (int j = 0; j < K; ++j) {
-        const int64_t s = s0 + j;
-        sum += ref_logp[s] - seq_logp[s] + log_reward[s] * inv_beta;
-      }
-      lz = sum / (double)K;
-    }
-    double sq = 0.0;
-    for (int j = 0; j < K; ++j) {
-      const int64_t s = s0 + j;
-      const double delta = ref_logp[s] - seq_logp[s] + log_reward[s] * inv_beta;
-      const double e = lz - delta;
-      resid[s] = e;
-      sq += e * e;
-    }
-    log_z[blockIdx.x] = lz;
-    group_sq[blockIdx.x] = sq;
+    tb_group_head((int64_t)blockIdx.x, K, ref_logp, log_reward, log_z_param, inv_beta, seq_logp, log_z, resid,
+                  group_sq);
     __threadfence();
     am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
   if (am_last && threadIdx.x == 0) {
     __threadfence();
-    const volatile double* gs = group_sq;
-    double tot = 0.0;
-    for (unsigned i = 0; i < gridDim.x; ++i) tot += gs[i];
     *counter = 0u;
-    const double p[3] = {tot * inv_n_global, (double)n_seq, (double)gridDim.x};
-    if (pa.world > 0) {
-      peer_allreduce3(pa, p, partial);
-    } else {
-      partial[0] = p[0];
-      partial[1] = p[1];
-      partial[2] = p[2];
+    tb_finish(group_sq, (int64_t)gridDim.x, n_seq, inv_n_global, partial, pa);
+  }
+}
+
+// Forward rows + per-sequence sums (+ group head) in ONE kernel: every CTA, after its rows, adds
+// its row counts to per-unit counters (unit = one sequence for log-probs, one group of K
+// sequences for the TB head); the CTA that completes a unit computes that unit's sums (and
+// head), and the CTA completing the last group reduces the loss partials. Saves the separate
+// seq_head launch and its latency.
+struct HeadArgs {
+  int64_t T;
+  int K;             // sequences per unit (1 = log-probs only)
+  int head;          // 1 = TB head per group
+  int64_t n_seq;
+  const double* ref_logp;
+  const double* log_reward;
+  const double* log_z_param;
+  double inv_beta, inv_n_global;
+  double* seq_logp;
+  int32_t* n_tokens;
+  double* log_z;
+  double* resid;
+  double* group_sq;
+  double* partial;
+  unsigned int* units_done;   // [n_units]
+  unsigned int* groups_done;  // [1]
+  PeerArgs pa;
+};
+
+template <class T, int TPR, int U, int NP>
+__global__ void __launch_bounds__(256) row_fwd_head(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                     int64_t stride, const int64_t* __restrict__ tokens,
+                                                     const uint8_t* __restrict__ mask, RowScale rs,
+                                                     float2* __restrict__ stats, double* __restrict__ lp,
+                                                     int32_t* dev_status, HeadArgs ha) {
+  constexpr int RPC = 256 / TPR, WPRS = TPR / 32 > 0 ? TPR / 32 : 1;
+  __shared__ float sm_m[RPC][WPRS], sm_M2[RPC][WPRS];
+  __shared__ double sm_s[RPC][WPRS];
+  __shared__ int64_t sh_done[RPC + 1];
+  __shared__ int sh_ndone;
+  const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
+  const int64_t row0 = (int64_t)blockIdx.x * RPC;
+  const int64_t row = row0 + grp;
+  if (row < rows && mask[row] != 0) {
+    fwd_row_group<T, TPR, U, NP, true>(logits, row, V, stride, tokens, rs, stats, lp, dev_status, sm_m, sm_M2, sm_s,
+                                       grp, gt);
+  }
+  __syncthreads();
+  const int64_t unit_rows = (int64_t)ha.K * ha.T;
+  if (threadIdx.x == 0) {
+    int nd = 0;
+    const int64_t r1 = row0 + RPC < rows ? row0 + RPC : rows;
+    for (int64_t r = row0; r < r1;) {
+      const int64_t u = r / unit_rows;
+      const int64_t ue = (u + 1) * unit_rows < r1 ? (u + 1) * unit_rows : r1;
+      const unsigned cnt = (unsigned)(ue - r);
+      if (atomicAdd(&ha.units_done[u], cnt) + cnt == (unsigned)unit_rows) sh_done[nd++] = u;
+      r = ue;
+    }
+    sh_ndone = nd;
+    if (nd) __threadfence();
+  }
+  __syncthreads();
+  for (int i = 0; i < sh_ndone; ++i) {
+    const int64_t u = sh_done[i];
+    seq_sums(lp, mask, ha.n_seq, ha.T, u * ha.K, ha.K, ha.seq_logp, ha.n_tokens, nullptr);
+    if (!ha.head) continue;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tb_group_head(u, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.seq_logp, ha.log_z,
+                    ha.resid, ha.group_sq);
+      __threadfence();
+      const int64_t groups = ha.n_seq / ha.K;
+      if (atomicAdd(ha.groups_done, 1u) + 1u == (unsigned)groups) {
+        __threadfence();
+        tb_finish(ha.group_sq, groups, ha.n_seq, ha.inv_n_global, ha.partial, ha.pa);
+      }
     }
   }
 }
@@ -1672,6 +1779,44 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
   return TBA_OK;
 }
 
+// Forward rows with the per-unit sums / TB head fused in (row_fwd_head). Returns false when the
+// separate kernels must be used instead (no rows, or the TMA forward selected for A/B).
+bool launch_fwd_head(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, HeadArgs& ha,
+                     cudaStream_t s, int* rc) {
+  const int64_t rows = x->n_seq * x->seq_len;
+  const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
+  if (rows == 0 || (switches().fwd_tma && x->vocab * esz > kSmallRowBytes)) return false;
+  // Off by default: measured on B200 (scripts/gpu_ab_head.sh) the per-row fence + unit counters
+  // cost as much as the separate seq_head launch saves (Qwen 9.305 vs 9.283 ms, RhoMath 7.03 vs
+  // 6.98; only the launch-bound toy gains, 0.056 vs 0.060). TBA_FUSE_HEAD=1 selects it.
+  if (env_int("TBA_FUSE_HEAD", 0) == 0) return false;
+  if (cudaMemsetAsync(w.fused, 0, fused_counter_bytes(x->n_seq), s) != cudaSuccess) {
+    *rc = TBA_ERR_CUDA;
+    return true;
+  }
+  ha.units_done = w.fused + 2;
+  ha.groups_done = w.fused + 1;
+  const int tpr = fwd_tpr(x->vocab, esz);
+  const int np = env_int("TBA_FWD_NP", 1);
+  const unsigned grid = (unsigned)((rows + 256 / tpr - 1) / (256 / tpr));
+#define TBA_HEAD(T_, TPR_, NP_)                                                                                    \
+  row_fwd_head<T_, TPR_, kU, NP_><<<grid, 256, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab,         \
+                                                       x->row_stride, x->tokens, x->mask, rs, w.stats, w.lp,      \
+                                                       dev_status, ha)
+  if (x->dtype == TBA_BF16) {
+    if (tpr == 64 && np == 1) TBA_HEAD(uint16_t, 64, 1);
+    else if (tpr == 64) TBA_HEAD(uint16_t, 64, 0);
+    else TBA_HEAD(uint16_t, 32, 0);
+  } else {
+    if (tpr == 64 && np == 1) TBA_HEAD(float, 64, 1);
+    else if (tpr == 64) TBA_HEAD(float, 64, 0);
+    else TBA_HEAD(float, 32, 0);
+  }
+#undef TBA_HEAD
+  *rc = cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  return true;
+}
+
 int check_opts(const tba_tb_opts* o) {
   if (!o) return TBA_OK;
   if (!(std::isfinite(o->inv_temp) && o->inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
@@ -1711,6 +1856,15 @@ int tba_seq_logprob(const tba_rows* x, void* workspace, double* seq_logp, int32_
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  HeadArgs ha{};
+  ha.T = x->seq_len;
+  ha.K = 1;
+  ha.head = 0;
+  ha.n_seq = x->n_seq;
+  ha.seq_logp = seq_logp;
+  ha.n_tokens = n_tokens;
+  ha.pa = PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, dev_status};
+  if (launch_fwd_head(x, w, make_scale(1.0), dev_status, ha, s, &rc)) return rc;
   rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
   if (rc) return rc;
   const int64_t grid = (x->n_seq + 7) / 8;
@@ -1782,10 +1936,6 @@ static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const do
     return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
-  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
-  rc = launch_fwd_rows(x, w, make_scale(opt_inv_temp(opts)), dev_status, s);
-  if (rc) return rc;
-  const int64_t groups = x->n_seq / K;
   PeerArgs pa{nullptr, nullptr, 0, 0, 0u, 0ull, dev_status};
   if (pr) {
     pa.slots = pr->slots;
@@ -1795,6 +1945,29 @@ static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const do
     pa.epoch = pr->epoch;
     pa.timeout_ns = (unsigned long long)(pr->timeout_s * 1e9);
   }
+  const RowScale rs = make_scale(opt_inv_temp(opts));
+  HeadArgs ha{};
+  ha.T = x->seq_len;
+  ha.K = K;
+  ha.head = 1;
+  ha.n_seq = x->n_seq;
+  ha.ref_logp = ref_logp;
+  ha.log_reward = log_reward;
+  ha.log_z_param = opts ? opts->log_z_param : nullptr;
+  ha.inv_beta = 1.0 / beta;
+  ha.inv_n_global = 1.0 / n_seq_global;
+  ha.seq_logp = seq_logp;
+  ha.n_tokens = n_tokens;
+  ha.log_z = log_z;
+  ha.resid = resid;
+  ha.group_sq = w.group_sq;
+  ha.partial = partial;
+  ha.pa = pa;
+  if (launch_fwd_head(x, w, rs, dev_status, ha, s, &rc)) return rc;
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  rc = launch_fwd_rows(x, w, rs, dev_status, s);
+  if (rc) return rc;
+  const int64_t groups = x->n_seq / K;
   seq_head<true><<<(unsigned)groups, 256, 0, s>>>(w.lp, x->mask, x->n_seq, x->seq_len, K, ref_logp, log_reward,
                                                   opts ? opts->log_z_param : nullptr, 1.0 / beta, 1.0 / n_seq_global,
                                                   seq_logp, n_tokens, log_z, resid, w.group_sq, partial, w.counter,
