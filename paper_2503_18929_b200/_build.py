@@ -1,6 +1,7 @@
 """Build the in-tree shared libraries with nvcc for sm_100a (B200).
 
-libtba.so        — the product: paper_2503_18929_b200/csrc/tba.cu (C ABI in include/tba.h)
+libtba.so        — the product: paper_2503_18929_b200/csrc/*.cu (C ABI in include/tba.h), one
+                   translation unit per kernel family, compiled in parallel and linked once
 libtba_synth.so  — the seeded input generator's CUDA twin: tba_synth/csrc/synth.cu
 
 Both link the CUDA runtime statically so that they dlopen on a machine without a GPU
@@ -8,20 +9,25 @@ Both link the CUDA runtime statically so that they dlopen on a machine without a
 """
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2503_18929_b200")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2", "-cudart", "static",
-         "-Xptxas", "-warn-spills", "-diag-suppress", "177"]
+CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-warn-spills",
+          "-diag-suppress", "177"]
+LDFLAGS = ["-shared", "-cudart", "static"]
+CSRC = os.path.join(PKG, "csrc")
 
 TARGETS = {
-    "tba": (os.path.join(PKG, "csrc", "tba.cu"), os.path.join(PKG, "libtba.so"),
-            [os.path.join(ROOT, "include", "tba.h")]),
-    "tba_synth": (os.path.join(ROOT, "tba_synth", "csrc", "synth.cu"),
+    # name: (translation units, output, extra dependencies)
+    "tba": (sorted(glob.glob(os.path.join(CSRC, "*.cu"))), os.path.join(PKG, "libtba.so"),
+            [os.path.join(ROOT, "include", "tba.h"), *glob.glob(os.path.join(CSRC, "*.cuh"))]),
+    "tba_synth": ([os.path.join(ROOT, "tba_synth", "csrc", "synth.cu")],
                   os.path.join(ROOT, "tba_synth", "libtba_synth.so"), []),
 }
 
@@ -33,24 +39,37 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale(src: str, out: str, deps) -> bool:
+def _stale(srcs, out: str, deps) -> bool:
     if not os.path.exists(out):
         return True
     t = os.path.getmtime(out)
-    return any(os.path.getmtime(p) > t for p in [src, *deps, __file__])
+    return any(os.path.getmtime(p) > t for p in [*srcs, *deps, __file__])
+
+
+def _run(cmd, what: str, verbose: bool) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {what}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if verbose and (r.stdout or r.stderr):
+        print(r.stdout, r.stderr)
 
 
 def build(force: bool = False, verbose: bool = False) -> dict:
-    """Compile every extension that is missing or older than its sources. Returns {name: path}."""
+    """Compile every extension that is missing or older than its sources. Returns {name: path}.
+
+    Each translation unit compiles to an object in parallel (nvcc -c), then one nvcc link makes
+    the shared library (CUDA runtime linked statically)."""
     out = {}
-    for name, (src, lib, deps) in TARGETS.items():
-        if force or _stale(src, lib, deps):
-            cmd = [nvcc(), *ARCH, *FLAGS, "-o", lib + ".tmp", src]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                raise RuntimeError(f"nvcc failed for {name}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-            if verbose and (r.stdout or r.stderr):
-                print(r.stdout, r.stderr)
+    for name, (srcs, lib, deps) in TARGETS.items():
+        if force or _stale(srcs, lib, deps):
+            objdir = os.path.join(os.path.dirname(lib), "build", name)
+            os.makedirs(objdir, exist_ok=True)
+            objs = [os.path.join(objdir, os.path.splitext(os.path.basename(s))[0] + ".o") for s in srcs]
+            jobs = [([nvcc(), *ARCH, *CFLAGS, "-c", "-o", o, s], s) for s, o in zip(srcs, objs)]
+            with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+                for f in [ex.submit(_run, c, w, verbose) for c, w in jobs]:
+                    f.result()
+            _run([nvcc(), *ARCH, *LDFLAGS, "-o", lib + ".tmp", *objs], name + " (link)", verbose)
             os.replace(lib + ".tmp", lib)
         out[name] = lib
     return out

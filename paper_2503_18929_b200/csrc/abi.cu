@@ -1,0 +1,404 @@
+// The C ABI of libtba.so (include/tba.h): argument validation, workspace carving and launch
+// order. Every step of the path runs in the kernels of fwd.cu / head.cu / bwd.cu / fused.cu /
+// deferred.cu; nothing here computes on the host.
+#include "tba_iface.cuh"
+
+using namespace tba;
+
+namespace {
+
+// The Eq. 4/5 group-head arguments shared by the two-call and deferred forwards.
+HeadArgs tb_head_args(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
+                      double beta, int32_t K, double n_seq_global, const WsLayout& w, double* seq_logp,
+                      int32_t* n_tokens, double* log_z, double* resid, double* partial, const PeerArgs& pa) {
+  HeadArgs ha{};
+  ha.T = x->seq_len;
+  ha.K = K;
+  ha.head = 1;
+  ha.n_seq = x->n_seq;
+  ha.ref_logp = ref_logp;
+  ha.log_reward = log_reward;
+  ha.log_z_param = opts ? opts->log_z_param : nullptr;
+  ha.inv_beta = 1.0 / beta;
+  ha.inv_n_global = 1.0 / n_seq_global;
+  ha.seq_logp = seq_logp;
+  ha.n_tokens = n_tokens;
+  ha.log_z = log_z;
+  ha.resid = resid;
+  ha.group_sq = w.group_sq;
+  ha.partial = partial;
+  ha.pa = pa;
+  return ha;
+}
+
+}  // namespace
+
+// ================================================================================ C ABI
+extern "C" {
+
+int tba_abi_version(void) { return TBA_ABI_VERSION; }
+
+const char* tba_status_string(int code) {
+  switch (code) {
+    case TBA_OK: return "TBA_OK";
+    case TBA_ERR_INVALID_ARG: return "TBA_ERR_INVALID_ARG: invalid argument (null pointer, size, stride, alignment or N % K)";
+    case TBA_ERR_INVALID_CONFIG: return "TBA_ERR_INVALID_CONFIG: invalid configuration (beta, K, IS mode or temperature)";
+    case TBA_ERR_CUDA: return "TBA_ERR_CUDA: CUDA launch failed";
+    default: return "TBA: unknown status";
+  }
+}
+
+size_t tba_workspace_bytes(int64_t n_seq, int64_t seq_len) {
+  if (n_seq < 0 || seq_len < 0) return 0;
+  return ws_bytes(n_seq, seq_len);
+}
+
+int tba_seq_logprob(const tba_rows* x, void* workspace, double* seq_logp, int32_t* n_tokens, int32_t* dev_status,
+                    tba_stream_t stream) {
+  int rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq == 0) return TBA_OK;
+  if (!workspace || !seq_logp || !n_tokens) return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  HeadArgs ha{};
+  ha.T = x->seq_len;
+  ha.K = 1;
+  ha.head = 0;
+  ha.n_seq = x->n_seq;
+  ha.seq_logp = seq_logp;
+  ha.n_tokens = n_tokens;
+  ha.pa = PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, dev_status};
+  if (launch_fwd_head(x, w, make_scale(1.0), dev_status, ha, s, &rc)) return rc;
+  rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
+  if (rc) return rc;
+  return launch_seq_head(false, w, x->mask, ha, s);
+}
+
+int tba_token_logprob(const tba_rows* x, double inv_temp, void* workspace, double* tok_logp, int32_t* dev_status,
+                      tba_stream_t stream) {
+  int rc = validate_rows(x);
+  if (rc) return rc;
+  if (!(std::isfinite(inv_temp) && inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows == 0) return TBA_OK;
+  if (!workspace || !tok_logp || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  rc = launch_fwd_rows(x, w, make_scale(inv_temp), dev_status, s);
+  if (rc) return rc;
+  return launch_token_lp(w, x->mask, rows, tok_logp, s);
+}
+
+static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                            const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                            double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                            int32_t* dev_status, const tba_peer_reduce* pr, tba_stream_t stream);
+
+int tba_tb_loss_fwd(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
+                    double beta, int32_t K, double n_seq_global, void* workspace, double* seq_logp, int32_t* n_tokens,
+                    double* log_z, double* resid, double* partial, int32_t* dev_status, tba_stream_t stream) {
+  return tb_loss_fwd_impl(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
+                          resid, partial, dev_status, nullptr, stream);
+}
+
+int tba_tb_loss_fwd_peer(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                         const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                         double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                         const tba_peer_reduce* pr, int32_t* dev_status, tba_stream_t stream) {
+  if (!pr || !pr->slots || !pr->flags || pr->world < 1 || pr->rank < 0 || pr->rank >= pr->world || pr->epoch == 0 ||
+      !(pr->timeout_s > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (x && x->n_seq == 0) return TBA_ERR_INVALID_ARG;  // every rank must own >= 1 group to join the reduction
+  return tb_loss_fwd_impl(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
+                          resid, partial, dev_status, pr, stream);
+}
+
+static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                            const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                            double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                            int32_t* dev_status, const tba_peer_reduce* pr, tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)  // a rank with zero groups contributes zero partials
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  PeerArgs pa{nullptr, nullptr, 0, 0, 0u, 0ull, dev_status};
+  if (pr) {
+    pa.slots = pr->slots;
+    pa.flags = pr->flags;
+    pa.rank = pr->rank;
+    pa.world = pr->world;
+    pa.epoch = pr->epoch;
+    pa.timeout_ns = (unsigned long long)(pr->timeout_s * 1e9);
+  }
+  const RowScale rs = make_scale(opt_inv_temp(opts));
+  HeadArgs ha = tb_head_args(x, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens, log_z, resid,
+                             partial, pa);
+  if (launch_fwd_head(x, w, rs, dev_status, ha, s, &rc)) return rc;
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  rc = launch_fwd_rows(x, w, rs, dev_status, s);
+  if (rc) return rc;
+  return launch_seq_head(true, w, x->mask, ha, s);
+}
+
+// ---- CUDA IPC helpers for the peer reduction buffers (host-side, not on the hot path)
+int tba_ipc_alloc(size_t bytes, void** dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64 || bytes == 0) return TBA_ERR_INVALID_ARG;
+  if (cudaMalloc(dev_ptr, bytes) != cudaSuccess) return TBA_ERR_CUDA;
+  if (cudaMemset(*dev_ptr, 0, bytes) != cudaSuccess) return TBA_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, *dev_ptr) != cudaSuccess) return TBA_ERR_CUDA;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, sizeof(h));
+  return TBA_OK;
+}
+
+int tba_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return TBA_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
+
+int tba_ipc_close(void* dev_ptr) { return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
+
+int tba_ipc_free(void* dev_ptr) { return cudaFree(dev_ptr) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
+
+int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* workspace, const double* resid,
+                    double grad_scale, const double* grad_out, void* dlogits, int32_t dlogits_dtype,
+                    int64_t dlogits_row_stride, double* d_log_z, int32_t K, tba_stream_t stream) {
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  rc = validate_out(x, dlogits, dlogits_dtype, dlogits_row_stride);
+  if (rc) return rc;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  if (d_log_z && (K < 1 || x->n_seq % K)) return TBA_ERR_INVALID_ARG;
+  if (x->n_seq == 0) return TBA_OK;
+  if (!resid) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (d_log_z) {
+    const int64_t groups = x->n_seq / K;
+    rc = launch_dlogz(resid, groups, K, grad_scale, grad_out, d_log_z, s);
+    if (rc) return rc;
+  }
+  if (x->seq_len == 0) return TBA_OK;
+  if (!workspace || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  return launch_bwd(false, x, workspace, resid, nullptr, grad_scale, grad_out, make_scale(opt_inv_temp(opts)),
+                    dlogits, dlogits_dtype, dlogits_row_stride, s);
+}
+
+int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
+                      double beta, int32_t K, double n_seq_global, double grad_scale, void* workspace,
+                      double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                      void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z,
+                      int32_t* dev_status, tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  rc = validate_out(x, dlogits, dlogits_dtype, dlogits_row_stride);
+  if (rc) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (x->seq_len == 0) {  // no rows: the separate calls already handle this shape
+    rc = tba_tb_loss_fwd(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
+                         resid, partial, dev_status, stream);
+    if (rc) return rc;
+    return tba_tb_loss_bwd(x, opts, workspace, resid, grad_scale, nullptr, dlogits, dlogits_dtype,
+                           dlogits_row_stride, d_log_z, K, stream);
+  }
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.fused, 0, fused_counter_bytes(x->n_seq), s) != cudaSuccess) return TBA_ERR_CUDA;
+  const int64_t groups = x->n_seq / K;
+  const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
+  FusedArgs a;
+  a.logits = x->logits;
+  a.dlogits = dlogits;
+  a.tokens = x->tokens;
+  a.mask = x->mask;
+  a.ref_logp = ref_logp;
+  a.log_reward = log_reward;
+  a.log_z_param = opts ? opts->log_z_param : nullptr;
+  a.stats = w.stats;
+  a.lp = w.lp;
+  a.seq_logp = seq_logp;
+  a.n_tokens = n_tokens;
+  a.log_z = log_z;
+  a.resid = resid;
+  a.group_sq = w.group_sq;
+  a.partial = partial;
+  a.dev_status = dev_status;
+  a.work = w.fused;
+  a.groups_done = w.fused + 1;
+  a.rows_done = w.fused + 2;
+  a.ready = w.fused + 2 + groups;
+  a.rows = x->n_seq * x->seq_len;
+  a.T = x->seq_len;
+  a.V = x->vocab;
+  a.stride = x->row_stride;
+  a.ostride = dlogits_row_stride;
+  a.n_seq = x->n_seq;
+  a.K = K;
+  a.groups = (int)groups;
+  a.D = fused_lookahead((int64_t)K * x->seq_len * x->vocab * esz, (int)groups);
+  a.inv_beta = 1.0 / beta;
+  a.inv_n_global = 1.0 / n_seq_global;
+  a.grad_scale = grad_scale;
+  a.rs = make_scale(opt_inv_temp(opts));
+  const int tf = fwd_tpr(x->vocab, esz) == 32 ? 32 : 64;
+  const int tb = bwd_tpr(x->vocab, esz) == 32 ? 32 : 256;
+  rc = launch_fused(a, x->dtype, dlogits_dtype, tf, tb, s);
+  if (rc) return rc;
+  if (d_log_z && a.log_z_param) return launch_dlogz(resid, groups, K, grad_scale, nullptr, d_log_z, s);
+  return TBA_OK;
+}
+
+int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                             const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
+                             double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
+                             void* grad_unscaled, int32_t g_dtype, int64_t g_row_stride, int32_t* dev_status,
+                             tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  rc = validate_out(x, grad_unscaled, g_dtype, g_row_stride);
+  if (rc) return rc;
+  if (grad_unscaled && grad_unscaled == x->logits) return TBA_ERR_INVALID_ARG;  // pass 2 re-reads the row
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  rc = launch_single(x, w, make_scale(opt_inv_temp(opts)), dev_status, grad_unscaled, g_dtype, g_row_stride, s);
+  if (rc) return rc;
+  const HeadArgs ha = tb_head_args(x, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
+                                   log_z, resid, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+  return launch_seq_head(true, w, x->mask, ha, s);
+}
+
+int tba_vargrad_tb_loss_fwd(const tba_rows* x, const double* ref_logp, const double* log_reward, double beta,
+                            int32_t K, double n_seq_global, void* workspace, double* seq_logp, int32_t* n_tokens,
+                            double* log_z, double* resid, double* partial, int32_t* dev_status,
+                            tba_stream_t stream) {
+  return tba_tb_loss_fwd(x, nullptr, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens,
+                         log_z, resid, partial, dev_status, stream);
+}
+
+int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const double* resid, double grad_scale,
+                            const double* grad_out, void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride,
+                            tba_stream_t stream) {
+  return tba_tb_loss_bwd(x, nullptr, workspace, resid, grad_scale, grad_out, dlogits, dlogits_dtype,
+                         dlogits_row_stride, nullptr, 0, stream);
+}
+
+static int tbap_fwd_impl(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
+                         double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
+                         void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef,
+                         double* partial, int32_t* dev_status, void* grad_unscaled, int32_t g_dtype,
+                         int64_t g_row_stride, tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta >= 0.0)) return TBA_ERR_INVALID_CONFIG;  // beta = 0 is Dr. GRPO
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  if (is_mode != TBA_IS_NONE && is_mode != TBA_IS_CLIP && is_mode != TBA_IS_ICEPOP) return TBA_ERR_INVALID_CONFIG;
+  if (is_mode != TBA_IS_NONE && !(is_lo >= 0.0 && is_hi >= is_lo && !std::isnan(is_hi)))
+    return TBA_ERR_INVALID_CONFIG;
+  int rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_tok_global) && n_tok_global > 0.0)) return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)  // a rank with zero groups contributes zero partials
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv || !coef ||
+      (x->seq_len > 0 && !gen_logp))
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(gen_logp) % 4 ||
+      reinterpret_cast<uintptr_t>(coef) % 4)
+    return TBA_ERR_INVALID_ARG;
+  WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  if (grad_unscaled) {
+    rc = validate_out(x, grad_unscaled, g_dtype, g_row_stride);
+    if (rc) return rc;
+    if (grad_unscaled == x->logits) return TBA_ERR_INVALID_ARG;
+    rc = launch_single(x, w, make_scale(1.0), dev_status, grad_unscaled, g_dtype, g_row_stride, s);
+  } else {
+    rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
+  }
+  if (rc) return rc;
+  return launch_tbap_head(w, x->mask, gen_logp, x->n_seq, x->seq_len, K, ref_logp, log_reward, beta, is_mode, is_lo,
+                          is_hi, -1.0 / n_tok_global, seq_logp, n_tokens, adv, coef, partial, s);
+}
+
+int tba_tbap_loss_fwd(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
+                      double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
+                      void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef, double* partial,
+                      int32_t* dev_status, tba_stream_t stream) {
+  return tbap_fwd_impl(x, gen_logp, ref_logp, log_reward, beta, K, is_mode, is_lo, is_hi, n_tok_global, workspace,
+                       seq_logp, n_tokens, adv, coef, partial, dev_status, nullptr, TBA_BF16, 0, stream);
+}
+
+int tba_tbap_loss_fwd_deferred(const tba_rows* x, const float* gen_logp, const double* ref_logp,
+                               const double* log_reward, double beta, int32_t K, int32_t is_mode, double is_lo,
+                               double is_hi, double n_tok_global, void* workspace, double* seq_logp,
+                               int32_t* n_tokens, double* adv, float* coef, double* partial, void* grad_unscaled,
+                               int32_t g_dtype, int64_t g_row_stride, int32_t* dev_status, tba_stream_t stream) {
+  if (!grad_unscaled && x && x->n_seq * x->seq_len > 0) return TBA_ERR_INVALID_ARG;
+  return tbap_fwd_impl(x, gen_logp, ref_logp, log_reward, beta, K, is_mode, is_lo, is_hi, n_tok_global, workspace,
+                       seq_logp, n_tokens, adv, coef, partial, dev_status, grad_unscaled, g_dtype, g_row_stride,
+                       stream);
+}
+
+int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coef, double grad_scale,
+                      const double* grad_out, void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride,
+                      tba_stream_t stream) {
+  int rc = validate_rows(x);
+  if (rc) return rc;
+  rc = validate_out(x, dlogits, dlogits_dtype, dlogits_row_stride);
+  if (rc) return rc;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  if (x->n_seq * x->seq_len == 0) return TBA_OK;
+  if (!workspace || !coef) return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  return launch_bwd(true, x, workspace, nullptr, coef, grad_scale, grad_out, make_scale(1.0), dlogits, dlogits_dtype,
+                    dlogits_row_stride, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

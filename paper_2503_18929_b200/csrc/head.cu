@@ -1,0 +1,277 @@
+// a2 + a3: per-sequence sums and the group heads (VarGrad TB, Eqs. 4-5; TBA', Eq. 16), the
+// forward-with-fused-head variant, and the small helper kernels.
+#include "tba_device.cuh"
+
+namespace tba {
+namespace {
+// One CTA per group of K sequences (HEAD), or per 8 sequences (log-probs only).
+// Eq. 4: log Z_i = 1/K sum_j delta_j (delta = rho - ell + r/beta), or the learned log Z_i of
+// Eq. 3 when log_z_param != NULL; Eq. 5 residual eps = log Z_i - delta. The last CTA (counter)
+// reduces the per-group sums of squares in group order.
+template <bool HEAD>
+__global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
+                                                int64_t n_seq, int64_t T, int K, const double* __restrict__ ref_logp,
+                                                const double* __restrict__ log_reward,
+                                                const double* __restrict__ log_z_param, double inv_beta,
+                                                double inv_n_global, double* __restrict__ seq_logp,
+                                                int32_t* __restrict__ n_tokens, double* __restrict__ log_z,
+                                                double* __restrict__ resid, double* __restrict__ group_sq,
+                                                double* __restrict__ partial, unsigned int* counter,
+                                                PeerArgs pa = PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr}) {
+  const int per = HEAD ? K : 8;
+  const int64_t s0 = (int64_t)blockIdx.x * per;
+  seq_sums(lp, mask, n_seq, T, s0, per, seq_logp, n_tokens, nullptr);
+  if (!HEAD) return;
+  __syncthreads();
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    tb_group_head((int64_t)blockIdx.x, K, ref_logp, log_reward, log_z_param, inv_beta, seq_logp, log_z, resid,
+                  group_sq);
+    __threadfence();
+    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last && threadIdx.x == 0) {
+    __threadfence();
+    *counter = 0u;
+    tb_finish(group_sq, (int64_t)gridDim.x, n_seq, inv_n_global, partial, pa);
+  }
+}
+
+
+// Forward rows + per-sequence sums (+ group head) in ONE kernel: every CTA, after its rows, adds
+// its row counts to per-unit counters (unit = one sequence for log-probs, one group of K
+// sequences for the TB head); the CTA that completes a unit computes that unit's sums (and
+// head), and the CTA completing the last group reduces the loss partials. Saves the separate
+// seq_head launch and its latency.
+template <class T, int TPR, int U, int NP>
+__global__ void __launch_bounds__(256) row_fwd_head(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                     int64_t stride, const int64_t* __restrict__ tokens,
+                                                     const uint8_t* __restrict__ mask, RowScale rs,
+                                                     float2* __restrict__ stats, double* __restrict__ lp,
+                                                     int32_t* dev_status, HeadArgs ha) {
+  constexpr int RPC = 256 / TPR, WPRS = TPR / 32 > 0 ? TPR / 32 : 1;
+  __shared__ float sm_m[RPC][WPRS], sm_M2[RPC][WPRS];
+  __shared__ double sm_s[RPC][WPRS];
+  __shared__ int64_t sh_done[RPC + 1];
+  __shared__ int sh_ndone;
+  const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
+  const int64_t row0 = (int64_t)blockIdx.x * RPC;
+  const int64_t row = row0 + grp;
+  if (row < rows && mask[row] != 0) {
+    fwd_row_group<T, TPR, U, NP, true>(logits, row, V, stride, tokens, rs, stats, lp, dev_status, sm_m, sm_M2, sm_s,
+                                       grp, gt);
+  }
+  __syncthreads();
+  const int64_t unit_rows = (int64_t)ha.K * ha.T;
+  if (threadIdx.x == 0) {
+    int nd = 0;
+    const int64_t r1 = row0 + RPC < rows ? row0 + RPC : rows;
+    for (int64_t r = row0; r < r1;) {
+      const int64_t u = r / unit_rows;
+      const int64_t ue = (u + 1) * unit_rows < r1 ? (u + 1) * unit_rows : r1;
+      const unsigned cnt = (unsigned)(ue - r);
+      if (atomicAdd(&ha.units_done[u], cnt) + cnt == (unsigned)unit_rows) sh_done[nd++] = u;
+      r = ue;
+    }
+    sh_ndone = nd;
+    if (nd) __threadfence();
+  }
+  __syncthreads();
+  for (int i = 0; i < sh_ndone; ++i) {
+    const int64_t u = sh_done[i];
+    seq_sums(lp, mask, ha.n_seq, ha.T, u * ha.K, ha.K, ha.seq_logp, ha.n_tokens, nullptr);
+    if (!ha.head) continue;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tb_group_head(u, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.seq_logp, ha.log_z,
+                    ha.resid, ha.group_sq);
+      __threadfence();
+      const int64_t groups = ha.n_seq / ha.K;
+      if (atomicAdd(ha.groups_done, 1u) + 1u == (unsigned)groups) {
+        __threadfence();
+        tb_finish(ha.group_sq, groups, ha.n_seq, ha.inv_n_global, ha.partial, ha.pa);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ TBA' head (Eq. 16)
+// One CTA per group: sequence sums as seq_head; thread 0 forms A_j = (r_j - rbar) -
+// beta (log Lambda_j - mean log Lambda) with log Lambda_j = ell_j - rho_j; every thread then
+// walks the group's rows: lambda_t = exp(lp_t - gen_t), IS weight w, coef_t = w * A_j (a
+// stop-gradient constant) and the surrogate term coef_t * lp_t, in a fixed order.
+__global__ void __launch_bounds__(256) tbap_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
+                                                 const float* __restrict__ gen_logp, int64_t n_seq, int64_t T, int K,
+                                                 const double* __restrict__ ref_logp,
+                                                 const double* __restrict__ log_reward, double beta, int is_mode,
+                                                 double is_lo, double is_hi, double neg_inv_ntok,
+                                                 double* __restrict__ seq_logp, int32_t* __restrict__ n_tokens,
+                                                 double* __restrict__ adv, float* __restrict__ coef,
+                                                 double* __restrict__ group_acc, double* __restrict__ partial,
+                                                 unsigned int* counter) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s0 = (int64_t)blockIdx.x * K;
+  __shared__ int sm_cnt[8];
+  int my_cnt = 0;
+  seq_sums(lp, mask, n_seq, T, s0, K, seq_logp, n_tokens, &my_cnt);
+  if (lane == 0) sm_cnt[warp] = my_cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double rbar = 0.0, lbar = 0.0;
+    for (int j = 0; j < K; ++j) {
+      rbar += log_reward[s0 + j];
+      lbar += seq_logp[s0 + j] - ref_logp[s0 + j];
+    }
+    rbar /= (double)K;
+    lbar /= (double)K;
+    for (int j = 0; j < K; ++j)
+      adv[s0 + j] = (log_reward[s0 + j] - rbar) - beta * ((seq_logp[s0 + j] - ref_logp[s0 + j]) - lbar);
+  }
+  __syncthreads();
+  double acc = 0.0;
+  const int64_t nr = (int64_t)K * T, r0 = s0 * T;
+  for (int64_t i = threadIdx.x; i < nr; i += 256) {
+    const int64_t r = r0 + i;
+    float cf = 0.f;
+    if (mask[r]) {
+      const double l = lp[r];
+      const double lam = exp(l - (double)gen_logp[r]);
+      double wgt = 1.0;
+      if (is_mode == TBA_IS_CLIP) wgt = fmin(fmax(lam, is_lo), is_hi);
+      else if (is_mode == TBA_IS_ICEPOP) wgt = (lam >= is_lo && lam <= is_hi) ? lam : 0.0;
+      const double c = wgt * adv[r / T];
+      cf = (float)c;
+      acc += c * l;
+    }
+    coef[r] = cf;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double sm_acc[8];
+  __shared__ bool am_last;
+  if (lane == 0) sm_acc[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    int n = 0;
+    for (int w = 0; w < 8; ++w) {
+      g += sm_acc[w];
+      n += sm_cnt[w];
+    }
+    group_acc[2 * blockIdx.x] = g;
+    group_acc[2 * blockIdx.x + 1] = (double)n;
+    __threadfence();
+    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* ga = group_acc;
+    double tot = 0.0, ntok = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) {
+      tot += ga[2 * i];
+      ntok += ga[2 * i + 1];
+    }
+    partial[0] = tot * neg_inv_ntok;
+    partial[1] = ntok;
+    partial[2] = (double)n_seq;
+    *counter = 0u;
+  }
+}
+
+// Per-token log-probs out of the workspace: tok_logp[r] = mask ? lp[r] : 0.
+__global__ void token_lp_kernel(const double* __restrict__ lp, const uint8_t* __restrict__ mask, int64_t rows,
+                                double* __restrict__ out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    out[r] = mask[r] ? lp[r] : 0.0;
+}
+
+// dL/d log Z_i for a learned log Z (Eq. 3): grad_scale * g * sum_j eps_{iK+j}.
+__global__ void dlogz_kernel(const double* __restrict__ resid, int64_t groups, int K, double grad_scale,
+                             const double* __restrict__ grad_out, double* __restrict__ d_log_z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= groups) return;
+  double s = 0.0;
+  for (int j = 0; j < K; ++j) s += resid[i * K + j];
+  d_log_z[i] = grad_scale * (grad_out ? *grad_out : 1.0) * s;
+}
+
+
+// ------------------------------------------------------------------------------ launch
+}  // namespace
+
+// Forward rows with the per-unit sums / TB head fused in (row_fwd_head). Returns false when the
+// separate kernels must be used instead (no rows, or the TMA forward selected for A/B).
+bool launch_fwd_head(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, HeadArgs& ha,
+                     cudaStream_t s, int* rc) {
+  const int64_t rows = x->n_seq * x->seq_len;
+  const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
+  if (rows == 0 || (switches().fwd_tma && x->vocab * esz > kSmallRowBytes)) return false;
+  // Off by default: measured on B200 (scripts/gpu_ab_head.sh) the per-row fence + unit counters
+  // cost as much as the separate seq_head launch saves (Qwen 9.305 vs 9.283 ms, RhoMath 7.03 vs
+  // 6.98; only the launch-bound toy gains, 0.056 vs 0.060). TBA_FUSE_HEAD=1 selects it.
+  if (env_int("TBA_FUSE_HEAD", 0) == 0) return false;
+  if (cudaMemsetAsync(w.fused, 0, fused_counter_bytes(x->n_seq), s) != cudaSuccess) {
+    *rc = TBA_ERR_CUDA;
+    return true;
+  }
+  ha.units_done = w.fused + 2;
+  ha.groups_done = w.fused + 1;
+  const int tpr = fwd_tpr(x->vocab, esz);
+  const int np = env_int("TBA_FWD_NP", 1);
+  const unsigned grid = (unsigned)((rows + 256 / tpr - 1) / (256 / tpr));
+#define TBA_HEAD(T_, TPR_, NP_)                                                                                    \
+  row_fwd_head<T_, TPR_, kU, NP_><<<grid, 256, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab,         \
+                                                       x->row_stride, x->tokens, x->mask, rs, w.stats, w.lp,      \
+                                                       dev_status, ha)
+  if (x->dtype == TBA_BF16) {
+    if (tpr == 64 && np == 1) TBA_HEAD(uint16_t, 64, 1);
+    else if (tpr == 64) TBA_HEAD(uint16_t, 64, 0);
+    else TBA_HEAD(uint16_t, 32, 0);
+  } else {
+    if (tpr == 64 && np == 1) TBA_HEAD(float, 64, 1);
+    else if (tpr == 64) TBA_HEAD(float, 64, 0);
+    else TBA_HEAD(float, 32, 0);
+  }
+#undef TBA_HEAD
+  *rc = cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  return true;
+}
+
+int launch_seq_head(bool head, const WsLayout& w, const uint8_t* mask, const HeadArgs& ha, cudaStream_t s) {
+  if (head) {
+    seq_head<true><<<(unsigned)(ha.n_seq / ha.K), 256, 0, s>>>(
+        w.lp, mask, ha.n_seq, ha.T, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.inv_n_global,
+        ha.seq_logp, ha.n_tokens, ha.log_z, ha.resid, w.group_sq, ha.partial, w.counter, ha.pa);
+  } else {
+    seq_head<false><<<(unsigned)((ha.n_seq + 7) / 8), 256, 0, s>>>(
+        w.lp, mask, ha.n_seq, ha.T, 8, nullptr, nullptr, nullptr, 0.0, 0.0, ha.seq_logp, ha.n_tokens, nullptr,
+        nullptr, nullptr, nullptr, nullptr);
+  }
+  return launch_status();
+}
+
+int launch_tbap_head(const WsLayout& w, const uint8_t* mask, const float* gen_logp, int64_t n_seq, int64_t T, int K,
+                     const double* ref_logp, const double* log_reward, double beta, int is_mode, double is_lo,
+                     double is_hi, double neg_inv_ntok, double* seq_logp, int32_t* n_tokens, double* adv,
+                     float* coef, double* partial, cudaStream_t s) {
+  tbap_head<<<(unsigned)(n_seq / K), 256, 0, s>>>(w.lp, mask, gen_logp, n_seq, T, K, ref_logp, log_reward, beta,
+                                                  is_mode, is_lo, is_hi, neg_inv_ntok, seq_logp, n_tokens, adv, coef,
+                                                  w.group_sq, partial, w.counter);
+  return launch_status();
+}
+
+int launch_token_lp(const WsLayout& w, const uint8_t* mask, int64_t rows, double* tok_logp, cudaStream_t s) {
+  const int64_t blocks = (rows + 255) / 256 < 4096 ? (rows + 255) / 256 : 4096;
+  token_lp_kernel<<<(unsigned)blocks, 256, 0, s>>>(w.lp, mask, rows, tok_logp);
+  return launch_status();
+}
+
+int launch_dlogz(const double* resid, int64_t groups, int K, double grad_scale, const double* grad_out,
+                 double* d_log_z, cudaStream_t s) {
+  dlogz_kernel<<<(unsigned)((groups + 127) / 128), 128, 0, s>>>(resid, groups, K, grad_scale, grad_out, d_log_z);
+  return launch_status();
+}
+
+}  // namespace tba

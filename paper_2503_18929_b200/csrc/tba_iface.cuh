@@ -1,0 +1,310 @@
+// libtba.so — the trajectory-balance loss head of TBA (arXiv 2503.18929) for B200 (sm_100a).
+//
+// Internal interface between the translation units of the library (one TU per kernel family,
+// compiled in parallel; abi.cu holds the extern "C" entry points of include/tba.h and launches
+// nothing itself). Kernels:
+//   fwd.cu       row_fwd_rows  a1   stream each valid logits row from HBM once (TPR threads per
+//                                   row, 128-bit loads): online max + sum of 2^(z*sc - R2), one
+//                                   ex2 per element (packed FFMA2/FADD2; 1 of 4 pairs on the FMA
+//                                   pipe), gather z[y]; writes per-row (M2, log2 S) and the token
+//                                   log-prob (fp64).
+//                row_fwd_tma   a1   alternative: persistent, warp-specialised, cp.async.bulk ring.
+//   head.cu      seq_head      a2+a3 per-sequence fixed-order fp64 sums of token log-probs
+//                                   (log pi(y|x)) and token counts; per group Eq. 4 log Z (or a
+//                                   learned log Z, Eq. 3) and the Eq. 5 residuals; the last CTA
+//                                   reduces the per-group sums of squares (+ peer all-reduce).
+//                tbap_head     a2+a3' TBA' (Eq. 16): per-group advantages, per-token IS-weighted
+//                                   coefficients.
+//                row_fwd_head  a1-a3 forward rows with the head fused in (A/B option).
+//   bwd.cu       row_bwd       a5   stream each valid row again: dz = c (1[v=y] - softmax); c per
+//                                   sequence (TB) or per token (TBA'); masked rows zero-filled.
+//   fused.cu     tb_fused      a1-a5 in one persistent launch (NEXT 2 (i)).
+//   deferred.cu  row_single*   a1 + unscaled a5 in one pass per row (NEXT 2 (ii)).
+// No float atomics: every output is bitwise reproducible run to run.
+#pragma once
+#include <cstdint>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "../../include/tba.h"
+
+namespace tba {
+
+constexpr float kL2E = 1.4426950408889634f;  // fp32(log2 e)
+constexpr double kLN2 = 0.69314718055994530942;
+constexpr float kSlack = 6.0f;  // nats a chunk max may exceed the running reference before a re-base
+constexpr int kFusedU = 4;
+constexpr int kU = 4;
+constexpr int64_t kSmallRowBytes = 8192;  // rows up to 8 KB: one warp per row in the backward
+
+// Row scaling: rows are soft-maxed as 2^(z * sc) with sc = fl(kL2E * inv_temp); slack is kSlack in
+// logit units (kSlack / inv_temp); inv_temp enters the log-prob and the gradient exactly (fp64).
+struct RowScale {
+  float sc, slack;
+  double inv_temp;
+};
+
+// One-shot all-reduce of the 3 loss partials fused into the head kernel, over peer memory
+// (NVLink P2P stores / loads through CUDA IPC mappings): the last CTA of every rank
+// writes its partial into slot [rank] of every peer's buffer, releases a per-peer flag with the
+// call's epoch, waits (acquire, bounded by a timeout) for all ranks' flags, and sums the slots in
+// rank order — every rank computes bit-identical totals, with no NCCL launch. Slots are double-
+// buffered by epoch parity (a rank cannot get two epochs ahead of a peer that has not read).
+struct PeerArgs {
+  double* const* slots;         // [world] device pointers: rank q's buffer of 2 x world x 4 doubles
+  unsigned int* const* flags;   // [world] device pointers: rank q's [world] epoch flags
+  int rank, world;
+  unsigned int epoch;
+  unsigned long long timeout_ns;
+  int32_t* dev_status;
+};
+
+// Forward rows + per-sequence sums (+ group head) in ONE kernel: every CTA, after its rows, adds
+// its row counts to per-unit counters (unit = one sequence for log-probs, one group of K
+// sequences for the TB head); the CTA that completes a unit computes that unit's sums (and
+// head), and the CTA completing the last group reduces the loss partials. Saves the separate
+// seq_head launch and its latency.
+struct HeadArgs {
+  int64_t T;
+  int K;             // sequences per unit (1 = log-probs only)
+  int head;          // 1 = TB head per group
+  int64_t n_seq;
+  const double* ref_logp;
+  const double* log_reward;
+  const double* log_z_param;
+  double inv_beta, inv_n_global;
+  double* seq_logp;
+  int32_t* n_tokens;
+  double* log_z;
+  double* resid;
+  double* group_sq;
+  double* partial;
+  unsigned int* units_done;   // [n_units]
+  unsigned int* groups_done;  // [1]
+  PeerArgs pa;
+};
+
+// One persistent launch for the whole VarGrad TB step: forward rows, the group head and the
+// gradient writer, scheduled from one atomic work counter over an item stream in which the
+// forward items of group g+D precede the backward items of group g. The CTA finishing the
+// last forward row of a group computes its head (Eq. 4/5) and publishes a ready flag; backward
+// items of that group wait on it. When D groups of logits fit in L2, the backward re-read of a
+// group hits L2 (6V -> ~4V HBM bytes per token for short-response shapes: Pythia, red-teaming);
+// for large groups (Qwen) it is a single-launch schedule with fwd/bwd overlap.
+struct FusedArgs {
+  const void* logits;
+  void* dlogits;
+  const int64_t* tokens;
+  const uint8_t* mask;
+  const double* ref_logp;
+  const double* log_reward;
+  const double* log_z_param;
+  float2* stats;
+  double* lp;
+  double* seq_logp;
+  int32_t* n_tokens;
+  double* log_z;
+  double* resid;
+  double* group_sq;
+  double* partial;
+  int32_t* dev_status;
+  unsigned int* work;        // [1] item counter
+  unsigned int* groups_done; // [1]
+  unsigned int* rows_done;   // [groups]
+  unsigned int* ready;       // [groups]
+  int64_t rows, T, V, stride, ostride, n_seq;
+  int K, groups, D, nF, nB, RF, RB;
+  double inv_beta, inv_n_global, grad_scale;
+  RowScale rs;
+};
+
+// ------------------------------------------------------------------------------ host helpers
+inline RowScale make_scale(double inv_temp) {
+  RowScale r;
+  r.sc = (float)((double)kL2E * inv_temp);
+  r.slack = (float)((double)kSlack / inv_temp);
+  r.inv_temp = inv_temp;
+  return r;
+}
+
+// Workspace (tba_workspace_bytes): per-row stats, per-row fp64 log-probs, per-group sums of
+// squares, the last-CTA counter, and the fused/fused-head counters; each block 256-byte aligned.
+struct WsLayout {
+  float2* stats;
+  double* lp;
+  double* group_sq;
+  unsigned int* counter;
+  unsigned int* fused;
+};
+
+inline size_t fused_counter_bytes(int64_t n_seq) { return (size_t)(2 + 2 * n_seq) * sizeof(unsigned int); }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline WsLayout ws_layout(void* ws, int64_t n_seq, int64_t T) {
+  const size_t rows = (size_t)n_seq * (size_t)T;
+  char* p = static_cast<char*>(ws);
+  WsLayout l;
+  size_t off = 0;
+  l.stats = reinterpret_cast<float2*>(p + off);
+  off = align_up(off + rows * sizeof(float2), 256);
+  l.lp = reinterpret_cast<double*>(p + off);
+  off = align_up(off + rows * sizeof(double), 256);
+  l.group_sq = reinterpret_cast<double*>(p + off);
+  off = align_up(off + (size_t)n_seq * sizeof(double), 256);
+  l.counter = reinterpret_cast<unsigned int*>(p + off);
+  off = align_up(off + 4 * sizeof(unsigned int), 256);
+  l.fused = reinterpret_cast<unsigned int*>(p + off);  // work, groups_done, rows_done[n_seq], ready[n_seq]
+  return l;
+}
+
+inline size_t ws_bytes(int64_t n_seq, int64_t T) {
+  const size_t rows = (size_t)n_seq * (size_t)T;
+  return align_up(rows * sizeof(float2), 256) + align_up(rows * sizeof(double), 256) +
+         align_up((size_t)n_seq * sizeof(double), 256) + 256 + align_up(fused_counter_bytes(n_seq), 256);
+}
+
+inline int validate_rows(const tba_rows* x) {
+  if (!x) return TBA_ERR_INVALID_ARG;
+  if (x->dtype != TBA_BF16 && x->dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
+  if (x->n_seq < 0 || x->seq_len < 0 || x->vocab < 1 || x->row_stride < x->vocab) return TBA_ERR_INVALID_ARG;
+  const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
+  const int64_t lim = INT64_MAX / 8;
+  if (x->n_seq > 0 && x->seq_len > lim / x->n_seq) return TBA_ERR_INVALID_ARG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows > 0 && x->row_stride > lim / esz / rows) return TBA_ERR_INVALID_ARG;
+  if (rows > (int64_t)INT32_MAX / 4) return TBA_ERR_INVALID_ARG;  // grid.x limit (up to 4 CTAs per row)
+  if (rows > 0) {
+    if (!x->logits || !x->tokens || !x->mask) return TBA_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(x->logits) % esz) return TBA_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(x->tokens) % 8) return TBA_ERR_INVALID_ARG;
+  }
+  return TBA_OK;
+}
+
+inline int validate_out(const tba_rows* x, const void* dlogits, int32_t odt, int64_t ostride) {
+  if (odt != TBA_BF16 && odt != TBA_FP32) return TBA_ERR_INVALID_ARG;
+  if (ostride < x->vocab) return TBA_ERR_INVALID_ARG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows == 0) return TBA_OK;
+  const int64_t oesz = odt == TBA_BF16 ? 2 : 4;
+  if (ostride > INT64_MAX / 8 / oesz / rows) return TBA_ERR_INVALID_ARG;
+  if (!dlogits || reinterpret_cast<uintptr_t>(dlogits) % oesz) return TBA_ERR_INVALID_ARG;
+  if (dlogits == x->logits && (odt != x->dtype || ostride != x->row_stride))
+    return TBA_ERR_INVALID_ARG;  // aliasing is only supported element-for-element
+  return TBA_OK;
+}
+
+inline int device_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static int cache[64] = {0};
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev] = n;
+  return n;
+}
+
+inline int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// A/B switches (read once): TBA_FWD_IMPL=tma selects the TMA-ring forward, TBA_TMA_CFG its
+// configuration, TBA_FWD_TPR / TBA_BWD_TPR force threads per row. Defaults are the measured best.
+struct Switches {
+  int fwd_tma, tma_cfg, fwd_tpr, bwd_tpr;
+};
+inline const Switches& switches() {
+  static Switches s = [] {
+    Switches v;
+    const char* e = getenv("TBA_FWD_IMPL");
+    v.fwd_tma = (e && e[0] == 't') ? 1 : 0;
+    v.tma_cfg = env_int("TBA_TMA_CFG", 0);
+    v.fwd_tpr = env_int("TBA_FWD_TPR", 0);
+    v.bwd_tpr = env_int("TBA_BWD_TPR", 0);
+    return v;
+  }();
+  return s;
+}
+
+inline bool valid_tpr(int t) { return t == 32 || t == 64 || t == 128 || t == 256; }
+
+// Forward threads per row, measured on B200 (scripts/gpu_ab_tpr.sh): 64 threads
+// (4 rows per CTA) is best or within 1 % for V = 32000 ... 152064; one warp for short rows.
+inline int fwd_tpr(int64_t V, int64_t esz) {
+  if (valid_tpr(switches().fwd_tpr)) return switches().fwd_tpr;
+  return (V * esz / 16) < 1024 ? 32 : 64;
+}
+
+// Backward threads per row (scripts/gpu_ab_bwd.sh): one CTA per long row, one warp per short row.
+inline int bwd_tpr(int64_t V, int64_t esz) {
+  if (valid_tpr(switches().bwd_tpr)) return switches().bwd_tpr;
+  return V * esz <= kSmallRowBytes ? 32 : 256;
+}
+
+// Groups of look-ahead in the fused schedule: as many groups of logits as fit in ~35 % of L2.
+inline int fused_lookahead(int64_t group_bytes, int groups) {
+  const int env = env_int("TBA_FUSED_D", -1);
+  int d;
+  if (env >= 0) {
+    d = env;
+  } else {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
+    d = (int)(0.35 * (double)l2 / (double)(group_bytes > 0 ? group_bytes : 1));
+  }
+  if (d < 1) d = 1;
+  if (d > groups) d = groups;
+  return d;
+}
+
+inline int check_opts(const tba_tb_opts* o) {
+  if (!o) return TBA_OK;
+  if (!(std::isfinite(o->inv_temp) && o->inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  return TBA_OK;
+}
+
+inline double opt_inv_temp(const tba_tb_opts* o) { return o ? o->inv_temp : 1.0; }
+
+inline int launch_status() { return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
+
+// ------------------------------------------------------------------------------ launchers
+// Defined in the kernel TUs; each returns a TBA_* status (launch errors included).
+
+// fwd.cu — a1 over every row of x: per-row stats + fp64 token log-probs into the workspace.
+int launch_fwd_rows(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, cudaStream_t s);
+
+// head.cu
+// Forward rows with the sums / TB head fused in (row_fwd_head, TBA_FUSE_HEAD=1). Returns false
+// when the separate kernels must be used instead; otherwise *rc holds the status.
+bool launch_fwd_head(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, HeadArgs& ha,
+                     cudaStream_t s, int* rc);
+// seq_head: HEAD = false -> log pi(y|x) and counts only (ha.K ignored); true -> + Eq. 4/5 head.
+int launch_seq_head(bool head, const WsLayout& w, const uint8_t* mask, const HeadArgs& ha, cudaStream_t s);
+int launch_tbap_head(const WsLayout& w, const uint8_t* mask, const float* gen_logp, int64_t n_seq, int64_t T, int K,
+                     const double* ref_logp, const double* log_reward, double beta, int is_mode, double is_lo,
+                     double is_hi, double neg_inv_ntok, double* seq_logp, int32_t* n_tokens, double* adv,
+                     float* coef, double* partial, cudaStream_t s);
+int launch_token_lp(const WsLayout& w, const uint8_t* mask, int64_t rows, double* tok_logp, cudaStream_t s);
+int launch_dlogz(const double* resid, int64_t groups, int K, double grad_scale, const double* grad_out,
+                 double* d_log_z, cudaStream_t s);
+
+// bwd.cu — a5: per_row = false: c = resid[s] (TB); true: c = coef[row] (TBA').
+int launch_bwd(bool per_row, const tba_rows* x, const void* workspace, const double* resid, const float* coef,
+               double gs, const double* go, const RowScale& rs, void* dlogits, int32_t odt, int64_t ostride,
+               cudaStream_t s);
+
+// fused.cu — the whole VarGrad TB step (a.* filled except nF/nB/RF/RB, set here).
+int launch_fused(FusedArgs& a, int32_t in_dtype, int32_t out_dtype, int tpr_f, int tpr_b, cudaStream_t s);
+
+// deferred.cu — a1 + the unscaled gradient in one pass per row.
+int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+                  void* grad_unscaled, int32_t g_dtype, int64_t g_row_stride, cudaStream_t s);
+
+}  // namespace tba

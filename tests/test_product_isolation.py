@@ -24,8 +24,11 @@ def test_product_package_never_imports_oracle_or_generator():
         if f.endswith(".py"):
             imps = _imports(os.path.join(PKG, f))
             assert "oracle" not in imps and "tba_synth" not in imps, f
-    src = open(os.path.join(PKG, "csrc", "tba.cu")).read()
-    assert "oracle" not in src.lower()
+    csrc = os.path.join(PKG, "csrc")
+    srcs = [f for f in os.listdir(csrc) if f.endswith((".cu", ".cuh"))]
+    assert "abi.cu" in srcs and "tba_device.cuh" in srcs
+    for f in srcs:
+        assert "oracle" not in open(os.path.join(csrc, f)).read().lower(), f
 
 
 def test_oracle_imports_nothing_from_the_product():
