@@ -170,9 +170,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the deferred-scale variant measurement")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--schedule", default="two-call", choices=["two-call", "fused", "deferred"],
+    ap.add_argument("--schedule", default="two-call", choices=["two-call", "fused", "deferred", "pipelined"],
                     help="two-call: tba_vargrad_tb_loss_fwd + _bwd (3 kernels); fused: tba_tb_loss_fused (1 kernel); "
-                         "deferred: tba_tb_loss_fwd_deferred (unscaled gradient, 4V bytes; NEXT 2 (ii))")
+                         "deferred: tba_tb_loss_fwd_deferred (unscaled gradient, 4V bytes; NEXT 2 (ii)); "
+                         "pipelined: tba_tb_loss_pipelined (group chunks, writer of chunk c-1 beside the forward "
+                         "of chunk c on a second stream)")
+    ap.add_argument("--pipe-groups", type=int, default=0,
+                    help="groups per chunk for --schedule pipelined (0 = ~L2/4 of logits per chunk)")
     ap.add_argument("--cuda-graph", action="store_true",
                     help="replay the step's library calls from CUDA graphs (forward and backward captured separately)")
     ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
@@ -240,13 +244,22 @@ def main():
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    fused = args.schedule == "fused"
+    pipelined = args.schedule == "pipelined"
+    fused = args.schedule == "fused" or pipelined  # one call per step (fwd + bwd)
     deferred = args.schedule == "deferred"
     if (fused or deferred) and tbap:
-        raise SystemExit("--schedule fused implements the TB objectives (Eq. 5 / Eq. 3) only")
+        raise SystemExit("--schedule fused/pipelined/deferred implement the TB objectives (Eq. 5 / Eq. 3) only")
+    gpc = args.pipe_groups if args.pipe_groups > 0 else int(os.environ.get("TBA_PIPE_GROUPS", "0"))
+    if gpc <= 0:
+        gpc = int(0.25 * torch.cuda.get_device_properties(dev).L2_cache_size // max(1, K * T * V * esz))
+    gpc = max(1, min(B, gpc))
+    n_chunks = -(-B // gpc)
 
     def fwd_call():
-        if fused:
+        if pipelined:
+            tba.vargrad_pipelined(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
+                                  dlogits=dlogits, groups_per_chunk=gpc, check_status=False)
+        elif fused:
             tba.vargrad_fused(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
                               dlogits=dlogits, check_status=False)
         elif deferred:
@@ -391,6 +404,13 @@ def main():
                     dist.all_reduce(out.partial, group=group)
                 h_loss.copy_(out.partial[:1], non_blocking=True)
                 return
+            if pipelined:
+                tba.vargrad_pipelined(lg_e, tok_e, mask_e, ref_e, rew_e, w.beta, K, ng_e, workspace=ws, out=out,
+                                      dlogits=dlogits[:nk], groups_per_chunk=gpc, check_status=False)
+                if group is not None:
+                    dist.all_reduce(out.partial, group=group)
+                h_loss.copy_(out.partial[:1], non_blocking=True)
+                return
             if fused:
                 tba.vargrad_fused(lg_e, tok_e, mask_e, ref_e, rew_e, w.beta, K, ng_e, workspace=ws, out=out,
                                   dlogits=dlogits[:nk], check_status=False)
@@ -457,8 +477,11 @@ def main():
             # row): the backward re-read is served by L2 when the lookahead window fits
             fused_bytes = valid_rows * V * 2 * esz + masked_rows * V * esz
             fgbs = fused_bytes / (fwd_ms / 1e3) / 1e9
-            roof = {"bound": "hbm", "kernel": "row_single (deferred scale)" if deferred else "tb_fused (a1-a5 in one launch)", "achieved": fgbs, "peak": peak,
-                    "unit": "GB/s", "frac": fgbs / peak, "traffic": ncu_traffic(w.name, "tb_fused"),
+            kname = ("row_single (deferred scale)" if deferred else
+                     f"pipelined step (row_fwd_rows + seq_head + row_bwd per chunk of {gpc} groups)" if pipelined
+                     else "tb_fused (a1-a5 in one launch)")
+            roof = {"bound": "hbm", "kernel": kname, "achieved": fgbs, "peak": peak,
+                    "unit": "GB/s", "frac": fgbs / peak, "traffic": ncu_traffic(w.name, "row_single" if deferred else "pipelined" if pipelined else "tb_fused"),
                     "algorithmic_bytes_per_launch": fused_bytes, "avg_launch_ms": fwd_ms, "peak_source": peak_src,
                     "bytes_model": "4V per valid token (unique); the two-pass schedule's 6V is in hbm_gbs_step"}
             kern = {"fused_ms": fwd_ms, "fused_unique_gbs": fgbs}
@@ -477,6 +500,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (tba_synth seeded generator, DESIGN.md §6)",
             "config": {"workload": w.name, "objective": args.objective, "schedule": args.schedule,
+                       **({"groups_per_chunk": gpc, "chunks": n_chunks} if pipelined else {}),
                        "cuda_graph": bool(args.cuda_graph), "note": w.note,
                        "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
                        "V": V, "beta": w.beta, "logits_dtype": w.dtype, "dlogits_dtype": w.dtype,
@@ -491,9 +515,10 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "variants": variants,
-            # our kernels per step: fused 1; deferred row_single + seq_head; two-call row_fwd_rows + seq_head
+            # our kernels per step: pipelined 3 per chunk + the finisher; fused 1; deferred row_single + seq_head;
+            # two-call row_fwd_rows + seq_head
             # (tbap_head) + row_bwd; 2 with TBA_FUSE_HEAD=1 (row_fwd_head + row_bwd)
-            "gpu_launches": args.steps * (1 if fused else 2 if deferred else
+            "gpu_launches": args.steps * ((3 * n_chunks + 1) if pipelined else 1 if fused else 2 if deferred else
                                           2 if (not tbap and os.environ.get("TBA_FUSE_HEAD", "0") == "1") else 3),
             "loss": loss,
         }

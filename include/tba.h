@@ -187,6 +187,27 @@ int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* 
                       int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z,
                       int32_t* dev_status, tba_stream_t stream);
 
+/* Group-chunked, two-stream forward + backward (stream-level form):
+ * the same outputs as tba_tb_loss_fwd + tba_tb_loss_bwd (bitwise: every row, head and the
+ * final fixed-order reduction run the same arithmetic), scheduled in chunks of
+ * groups_per_chunk whole groups (<= 0: as many groups as fit in ~1/4 of L2, at least 1).
+ * For chunk c, `stream` runs the forward rows and the Eq. 4/5 head of c while `aux_stream`
+ * runs the gradient writer of chunk c-1; the forward of chunk c+1 waits for the writer of
+ * chunk c-1. When a chunk fits in L2, the writer's re-read of its logits hits L2 (4V instead
+ * of 6V HBM bytes per token for groups of <= ~30 MB: the Pythia and red-teaming shapes).
+ * Measured on B200 it is not faster than the two calls: small chunks pay
+ * ~10 us of launch + cross-stream latency per chunk, large ones gain no reuse.
+ * On return all work, including aux_stream's, is ordered before later work on `stream`
+ * (capturable in a CUDA graph). aux_stream may equal stream (no overlap). d_log_z as in
+ * tba_tb_loss_bwd (learned log Z only). dlogits may alias logits element-for-element (the
+ * writer of chunk c-1 and the forward of chunk c touch disjoint rows). */
+int tba_tb_loss_pipelined(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                          const double* log_reward, double beta, int32_t K, double n_seq_global,
+                          double grad_scale, int32_t groups_per_chunk, void* workspace, double* seq_logp,
+                          int32_t* n_tokens, double* log_z, double* resid, double* partial, void* dlogits,
+                          int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z,
+                          int32_t* dev_status, tba_stream_t stream, tba_stream_t aux_stream);
+
 /* Deferred-scale forward: everything tba_tb_loss_fwd returns, plus
  * the UNSCALED gradient written in the same pass over the logits:
  *   grad_unscaled[s,t,v] = mu_{s,t} * inv_temp * (1[v = y] - softmax(inv_temp z)_v)

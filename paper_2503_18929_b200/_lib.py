@@ -19,7 +19,7 @@ TBA_BF16, TBA_FP32 = 0, 1
 # every symbol include/tba.h declares (checked by tests/test_abi.py)
 EXPORTS = ("tba_abi_version", "tba_status_string", "tba_workspace_bytes", "tba_seq_logprob", "tba_token_logprob",
            "tba_vargrad_tb_loss_fwd", "tba_vargrad_tb_loss_bwd", "tba_tb_loss_fwd", "tba_tb_loss_bwd", "tba_tb_loss_fused",
-           "tba_tb_loss_fwd_deferred",
+           "tba_tb_loss_pipelined", "tba_tb_loss_fwd_deferred",
            "tba_tbap_loss_fwd", "tba_tbap_loss_bwd", "tba_tbap_loss_fwd_deferred", "tba_tb_loss_fwd_peer",
            "tba_ipc_alloc", "tba_ipc_open", "tba_ipc_close", "tba_ipc_free")
 TBA_DEV_PEER_TIMEOUT = 4
@@ -84,6 +84,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
         L.tba_tb_loss_bwd.argtypes = [RP, OP, P, P, D, P, P, I32, I64, P, I32, P]
         L.tba_tb_loss_fused.restype = ctypes.c_int
         L.tba_tb_loss_fused.argtypes = [RP, OP, P, P, D, I32, D, D, P, P, P, P, P, P, P, I32, I64, P, P, P]
+        L.tba_tb_loss_pipelined.restype = ctypes.c_int
+        L.tba_tb_loss_pipelined.argtypes = [RP, OP, P, P, D, I32, D, D, I32, P, P, P, P, P, P, P, I32, I64, P, P, P, P]
         L.tba_tb_loss_fwd_deferred.restype = ctypes.c_int
         L.tba_tb_loss_fwd_deferred.argtypes = [RP, OP, P, P, D, I32, D, P, P, P, P, P, P, P, I32, I64, P, P]
         PP = ctypes.POINTER(TbaPeerReduce)

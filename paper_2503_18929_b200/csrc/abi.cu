@@ -31,6 +31,19 @@ HeadArgs tb_head_args(const tba_rows* x, const tba_tb_opts* opts, const double* 
   return ha;
 }
 
+// Four timing-free events per (host thread, device) for the pipelined schedule, created on first
+// use and reused: a wait always refers to the latest record issued before it, so reuse across
+// calls is safe, and thread-local storage keeps concurrent callers on other threads apart.
+cudaEvent_t* pipe_events() {
+  thread_local cudaEvent_t ev[64][4] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!ev[dev][0])
+    for (int i = 0; i < 4; ++i)
+      if (cudaEventCreateWithFlags(&ev[dev][i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  return ev[dev];
+}
+
 }  // namespace
 
 // ================================================================================ C ABI
@@ -199,7 +212,8 @@ int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* work
   }
   if (x->seq_len == 0) return TBA_OK;
   if (!workspace || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
-  return launch_bwd(false, x, workspace, resid, nullptr, grad_scale, grad_out, make_scale(opt_inv_temp(opts)),
+  const WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
+  return launch_bwd(false, x, w.stats, resid, nullptr, grad_scale, grad_out, make_scale(opt_inv_temp(opts)),
                     dlogits, dlogits_dtype, dlogits_row_stride, s);
 }
 
@@ -278,6 +292,85 @@ int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* 
   if (rc) return rc;
   if (d_log_z && a.log_z_param) return launch_dlogz(resid, groups, K, grad_scale, nullptr, d_log_z, s);
   return TBA_OK;
+}
+
+int tba_tb_loss_pipelined(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
+                          const double* log_reward, double beta, int32_t K, double n_seq_global,
+                          double grad_scale, int32_t groups_per_chunk, void* workspace, double* seq_logp,
+                          int32_t* n_tokens, double* log_z, double* resid, double* partial, void* dlogits,
+                          int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z,
+                          int32_t* dev_status, tba_stream_t stream, tba_stream_t aux_stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_rows(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  rc = validate_out(x, dlogits, dlogits_dtype, dlogits_row_stride);
+  if (rc) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t sb = reinterpret_cast<cudaStream_t>(aux_stream);
+  if (x->n_seq == 0)
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (x->seq_len == 0) {  // no rows: the separate calls already handle this shape
+    rc = tba_tb_loss_fwd(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
+                         resid, partial, dev_status, stream);
+    if (rc) return rc;
+    return tba_tb_loss_bwd(x, opts, workspace, resid, grad_scale, nullptr, dlogits, dlogits_dtype,
+                           dlogits_row_stride, d_log_z, K, stream);
+  }
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  const WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  const RowScale rs = make_scale(opt_inv_temp(opts));
+  const int64_t groups = x->n_seq / K, T = x->seq_len;
+  const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4, oesz = dlogits_dtype == TBA_BF16 ? 2 : 4;
+  const int64_t gpc = groups_per_chunk > 0 ? (groups_per_chunk < groups ? groups_per_chunk : groups)
+                                           : pipe_groups((int64_t)K * T * x->vocab * esz, groups);
+  const int64_t nchunks = (groups + gpc - 1) / gpc;
+  const bool two = sb != s;
+  cudaEvent_t* ev = two ? pipe_events() : nullptr;
+  if (two && !ev) return TBA_ERR_CUDA;
+  cudaEvent_t* evF = two ? ev : nullptr;
+  cudaEvent_t* evB = two ? ev + 2 : nullptr;
+  for (int64_t c = 0; c < nchunks && rc == TBA_OK; ++c) {
+    const int64_t g0 = c * gpc, gc = (g0 + gpc <= groups) ? gpc : groups - g0;
+    const int64_t s0 = g0 * K, r0 = s0 * T;
+    tba_rows xc = *x;
+    xc.logits = static_cast<const char*>(x->logits) + r0 * x->row_stride * esz;
+    xc.tokens = x->tokens + r0;
+    xc.mask = x->mask + r0;
+    xc.n_seq = gc * K;
+    const WsLayout wc{w.stats + r0, w.lp + r0, w.group_sq + g0, nullptr, nullptr};
+    // forward of chunk c after the writer of chunk c-2: at most two chunks of logits live in L2
+    if (two && c >= 2 && cudaStreamWaitEvent(s, evB[c % 2], 0) != cudaSuccess) rc = TBA_ERR_CUDA;
+    if (!rc) rc = launch_fwd_rows(&xc, wc, rs, dev_status, s);
+    if (rc) break;
+    HeadArgs ha = tb_head_args(&xc, opts, ref_logp + s0, log_reward + s0, beta, K, n_seq_global, wc, seq_logp + s0,
+                               n_tokens + s0, log_z + g0, resid + s0, partial,
+                               PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+    if (ha.log_z_param) ha.log_z_param += g0;
+    rc = launch_seq_head(true, wc, xc.mask, ha, s);  // wc.counter == NULL: no per-chunk reduction
+    if (rc) break;
+    if (two && (cudaEventRecord(evF[c % 2], s) != cudaSuccess || cudaStreamWaitEvent(sb, evF[c % 2], 0) != cudaSuccess))
+      rc = TBA_ERR_CUDA;
+    if (!rc)
+      rc = launch_bwd(false, &xc, wc.stats, resid + s0, nullptr, grad_scale, nullptr, rs,
+                      static_cast<char*>(dlogits) + r0 * dlogits_row_stride * oesz, dlogits_dtype, dlogits_row_stride,
+                      two ? sb : s);
+    if (!rc && two && cudaEventRecord(evB[c % 2], sb) != cudaSuccess) rc = TBA_ERR_CUDA;
+  }
+  // join: the aux stream's last writer (and, in stream order, all before it) precedes the tail
+  if (two && cudaStreamWaitEvent(s, evB[(nchunks - 1) % 2], 0) != cudaSuccess && !rc) rc = TBA_ERR_CUDA;
+  if (!rc) rc = launch_tb_finish(w.group_sq, groups, x->n_seq, 1.0 / n_seq_global, partial, s);
+  if (!rc && d_log_z && opts && opts->log_z_param) rc = launch_dlogz(resid, groups, K, grad_scale, nullptr, d_log_z, s);
+  return rc;
 }
 
 int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
@@ -397,7 +490,8 @@ int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coe
   if (x->n_seq * x->seq_len == 0) return TBA_OK;
   if (!workspace || !coef) return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
-  return launch_bwd(true, x, workspace, nullptr, coef, grad_scale, grad_out, make_scale(1.0), dlogits, dlogits_dtype,
+  const WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
+  return launch_bwd(true, x, w.stats, nullptr, coef, grad_scale, grad_out, make_scale(1.0), dlogits, dlogits_dtype,
                     dlogits_row_stride, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int
 
 // ------------------------------------------------------------------------------ launch
 template <class T, class TO, bool PER_ROW>
-void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, const float* coef, double gs,
+void launch_bwd_t(const tba_rows* x, const float2* stats, const double* resid, const float* coef, double gs,
                   const double* go, const RowScale& rs, TO* out, int64_t ostride, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   const int tpr = bwd_tpr(x->vocab, (int64_t)sizeof(T));
@@ -42,7 +42,7 @@ void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, con
   auto lg = static_cast<const T*>(x->logits);
 #define TBA_BWD(TPR_)                                                                                              \
   row_bwd<T, TO, TPR_, kU, PER_ROW><<<grid, 256, 0, s>>>(lg, rows, x->seq_len, x->vocab, x->row_stride, x->tokens, \
-                                                        x->mask, w.stats, resid, coef, gs, go, rs, out, ostride)
+                                                        x->mask, stats, resid, coef, gs, go, rs, out, ostride)
   switch (tpr) {
     case 32: TBA_BWD(32); break;
     case 64: TBA_BWD(64); break;
@@ -53,32 +53,32 @@ void launch_bwd_t(const tba_rows* x, const WsLayout& w, const double* resid, con
 }
 
 template <bool PER_ROW>
-int launch_bwd_dt(const tba_rows* x, const void* workspace, const double* resid, const float* coef, double gs,
+int launch_bwd_dt(const tba_rows* x, const float2* stats, const double* resid, const float* coef, double gs,
                   const double* go, const RowScale& rs, void* dlogits, int32_t odt, int64_t ostride, cudaStream_t s) {
   if (x->n_seq * x->seq_len == 0) return TBA_OK;
-  WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
   if (x->dtype == TBA_BF16) {
     if (odt == TBA_BF16)
-      launch_bwd_t<uint16_t, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits),
+      launch_bwd_t<uint16_t, uint16_t, PER_ROW>(x, stats, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits),
                                                 ostride, s);
     else
-      launch_bwd_t<uint16_t, float, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
+      launch_bwd_t<uint16_t, float, PER_ROW>(x, stats, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
   } else {
     if (odt == TBA_BF16)
-      launch_bwd_t<float, uint16_t, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits), ostride,
+      launch_bwd_t<float, uint16_t, PER_ROW>(x, stats, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits), ostride,
                                              s);
     else
-      launch_bwd_t<float, float, PER_ROW>(x, w, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
+      launch_bwd_t<float, float, PER_ROW>(x, stats, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
   }
   return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
 }  // namespace
 
-int launch_bwd(bool per_row, const tba_rows* x, const void* workspace, const double* resid, const float* coef, double gs,
-               const double* go, const RowScale& rs, void* dlogits, int32_t odt, int64_t ostride, cudaStream_t s) {
-  return per_row ? launch_bwd_dt<true>(x, workspace, resid, coef, gs, go, rs, dlogits, odt, ostride, s)
-                 : launch_bwd_dt<false>(x, workspace, resid, coef, gs, go, rs, dlogits, odt, ostride, s);
+int launch_bwd(bool per_row, const tba_rows* x, const float2* stats, const double* resid, const float* coef,
+               double gs, const double* go, const RowScale& rs, void* dlogits, int32_t odt, int64_t ostride,
+               cudaStream_t s) {
+  return per_row ? launch_bwd_dt<true>(x, stats, resid, coef, gs, go, rs, dlogits, odt, ostride, s)
+                 : launch_bwd_dt<false>(x, stats, resid, coef, gs, go, rs, dlogits, odt, ostride, s);
 }
 
 }  // namespace tba

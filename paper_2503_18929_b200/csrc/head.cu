@@ -27,8 +27,11 @@ __global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, c
   if (threadIdx.x == 0) {
     tb_group_head((int64_t)blockIdx.x, K, ref_logp, log_reward, log_z_param, inv_beta, seq_logp, log_z, resid,
                   group_sq);
-    __threadfence();
-    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    am_last = false;
+    if (counter) {  // counter == NULL: a chunk of a larger batch; tb_finish_kernel reduces later
+      __threadfence();
+      am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    }
   }
   __syncthreads();
   if (am_last && threadIdx.x == 0) {
@@ -198,6 +201,14 @@ __global__ void dlogz_kernel(const double* __restrict__ resid, int64_t groups, i
 }
 
 
+// The final fixed-order reduction of a chunked step (tba_tb_loss_pipelined): the same
+// arithmetic as seq_head's last CTA over all groups of the call.
+__global__ void tb_finish_kernel(const double* __restrict__ group_sq, int64_t groups, int64_t n_seq,
+                                 double inv_n_global, double* __restrict__ partial) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    tb_finish(group_sq, groups, n_seq, inv_n_global, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+}
+
 // ------------------------------------------------------------------------------ launch
 }  // namespace
 
@@ -271,6 +282,12 @@ int launch_token_lp(const WsLayout& w, const uint8_t* mask, int64_t rows, double
 int launch_dlogz(const double* resid, int64_t groups, int K, double grad_scale, const double* grad_out,
                  double* d_log_z, cudaStream_t s) {
   dlogz_kernel<<<(unsigned)((groups + 127) / 128), 128, 0, s>>>(resid, groups, K, grad_scale, grad_out, d_log_z);
+  return launch_status();
+}
+
+int launch_tb_finish(const double* group_sq, int64_t groups, int64_t n_seq, double inv_n_global, double* partial,
+                     cudaStream_t s) {
+  tb_finish_kernel<<<1, 32, 0, s>>>(group_sq, groups, n_seq, inv_n_global, partial);
   return launch_status();
 }
 

@@ -264,6 +264,21 @@ inline int fused_lookahead(int64_t group_bytes, int groups) {
   return d;
 }
 
+// Groups per chunk of the pipelined schedule: chunks of <= ~1/4 of L2, so that chunk c (being
+// re-read by the gradient writer) and chunk c+1 (being read by the forward) both stay resident.
+inline int pipe_groups(int64_t group_bytes, int64_t groups) {
+  int d = env_int("TBA_PIPE_GROUPS", 0);
+  if (d <= 0) {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
+    d = (int)(0.25 * (double)l2 / (double)(group_bytes > 0 ? group_bytes : 1));
+  }
+  if (d < 1) d = 1;
+  if (d > groups) d = (int)groups;
+  return d;
+}
+
 inline int check_opts(const tba_tb_opts* o) {
   if (!o) return TBA_OK;
   if (!(std::isfinite(o->inv_temp) && o->inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
@@ -292,11 +307,14 @@ int launch_tbap_head(const WsLayout& w, const uint8_t* mask, const float* gen_lo
                      double is_hi, double neg_inv_ntok, double* seq_logp, int32_t* n_tokens, double* adv,
                      float* coef, double* partial, cudaStream_t s);
 int launch_token_lp(const WsLayout& w, const uint8_t* mask, int64_t rows, double* tok_logp, cudaStream_t s);
+// The final fixed-order loss reduction over group_sq[0, groups) (a chunked step's tail).
+int launch_tb_finish(const double* group_sq, int64_t groups, int64_t n_seq, double inv_n_global, double* partial,
+                     cudaStream_t s);
 int launch_dlogz(const double* resid, int64_t groups, int K, double grad_scale, const double* grad_out,
                  double* d_log_z, cudaStream_t s);
 
 // bwd.cu — a5: per_row = false: c = resid[s] (TB); true: c = coef[row] (TBA').
-int launch_bwd(bool per_row, const tba_rows* x, const void* workspace, const double* resid, const float* coef,
+int launch_bwd(bool per_row, const tba_rows* x, const float2* stats, const double* resid, const float* coef,
                double gs, const double* go, const RowScale& rs, void* dlogits, int32_t odt, int64_t ostride,
                cudaStream_t s);
 

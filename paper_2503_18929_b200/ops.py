@@ -263,11 +263,20 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
     return (loss, aux) if return_aux else loss
 
 
-def vargrad_fused(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
-                  grad_scale: float | None = None, workspace=None, out: _Fwd | None = None, dlogits=None,
-                  dlogits_dtype=None, inv_temp: float = 1.0, log_z_param=None, check_status: bool = _CHECK):
-    """One-launch forward + backward (tba_tb_loss_fused). grad_scale defaults to 2/n_seq_global
-    (d loss / d logits with grad_out = 1). Returns (_Fwd, workspace, dlogits, d_log_z or None)."""
+_AUX_STREAMS: dict = {}
+
+
+def _aux_stream(dev: torch.device) -> int:
+    """A second stream per device for the pipelined schedule (created once, reused)."""
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _AUX_STREAMS:
+        _AUX_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _AUX_STREAMS[key].cuda_stream
+
+
+def _fwd_bwd_one_call(entry: str, logits, tokens, mask, ref_logp, log_reward, beta, K, n_seq_global, grad_scale,
+                      workspace, out, dlogits, dlogits_dtype, inv_temp, log_z_param, check_status, extra_mid=(),
+                      extra_tail=()):
     L = _lib.load()
     x = make_rows(logits, tokens, mask)
     N, T = tokens.shape
@@ -286,15 +295,39 @@ def vargrad_fused(logits, tokens, mask, ref_logp, log_reward, beta: float, K: in
     opts = _opts(inv_temp, log_z_param)
     gs = 2.0 / float(n_seq_global) if grad_scale is None else float(grad_scale)
     with torch.cuda.device(dev):
-        check(L.tba_tb_loss_fused(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
-                                  ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K), float(n_seq_global),
-                                  gs, ws.data_ptr(), o.seq_logp.data_ptr(), o.n_tokens.data_ptr(),
-                                  o.log_z.data_ptr() if N else None, o.resid.data_ptr(), o.partial.data_ptr(),
-                                  dlogits.data_ptr(), _DT[dlogits.dtype], max(ors, V), _ptr(d_log_z), _ptr(st),
-                                  _stream(dev)), "tba_tb_loss_fused")
+        check(getattr(L, entry)(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
+                                ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K), float(n_seq_global),
+                                gs, *extra_mid, ws.data_ptr(), o.seq_logp.data_ptr(), o.n_tokens.data_ptr(),
+                                o.log_z.data_ptr() if N else None, o.resid.data_ptr(), o.partial.data_ptr(),
+                                dlogits.data_ptr(), _DT[dlogits.dtype], max(ors, V), _ptr(d_log_z), _ptr(st),
+                                _stream(dev), *extra_tail), entry)
     if st is not None:
-        _raise_dev_status(st, "tba_tb_loss_fused")
+        _raise_dev_status(st, entry)
     return o, ws, dlogits, d_log_z
+
+
+def vargrad_fused(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
+                  grad_scale: float | None = None, workspace=None, out: _Fwd | None = None, dlogits=None,
+                  dlogits_dtype=None, inv_temp: float = 1.0, log_z_param=None, check_status: bool = _CHECK):
+    """One-launch forward + backward (tba_tb_loss_fused). grad_scale defaults to 2/n_seq_global
+    (d loss / d logits with grad_out = 1). Returns (_Fwd, workspace, dlogits, d_log_z or None)."""
+    return _fwd_bwd_one_call("tba_tb_loss_fused", logits, tokens, mask, ref_logp, log_reward, beta, K, n_seq_global,
+                             grad_scale, workspace, out, dlogits, dlogits_dtype, inv_temp, log_z_param, check_status)
+
+
+def vargrad_pipelined(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
+                      grad_scale: float | None = None, workspace=None, out: _Fwd | None = None, dlogits=None,
+                      dlogits_dtype=None, inv_temp: float = 1.0, log_z_param=None, groups_per_chunk: int = 0,
+                      aux_stream: bool = True, check_status: bool = _CHECK):
+    """Forward + backward in group chunks on two streams (tba_tb_loss_pipelined): the gradient
+    writer of chunk c-1 runs beside the forward of chunk c, so small groups are re-read from L2.
+    Same results as vargrad_fwd + vargrad_bwd, bitwise. groups_per_chunk <= 0 picks ~L2/4 of
+    logits per chunk. Returns (_Fwd, workspace, dlogits, d_log_z or None)."""
+    dev = logits.device
+    aux = _aux_stream(dev) if aux_stream else _stream(dev)
+    return _fwd_bwd_one_call("tba_tb_loss_pipelined", logits, tokens, mask, ref_logp, log_reward, beta, K,
+                             n_seq_global, grad_scale, workspace, out, dlogits, dlogits_dtype, inv_temp, log_z_param,
+                             check_status, extra_mid=(int(groups_per_chunk),), extra_tail=(aux,))
 
 
 def vargrad_fwd_deferred(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
@@ -334,7 +367,7 @@ def vargrad_fwd_deferred(logits, tokens, mask, ref_logp, log_reward, beta: float
 
 def vargrad_tb_loss_and_grad(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
                              group=None, dlogits=None, dlogits_dtype=None, inv_temp: float = 1.0, log_z=None,
-                             return_aux: bool = False):
+                             return_aux: bool = False, schedule: str = "fused"):
     """Loss AND d loss / d logits in one launch (no autograd): returns (loss, dlogits) or
     (loss, dlogits, d_log_z) with a learned log_z; aux dict appended when return_aux. The
     gradient is that of the (all-reduced, when `group` is given) batch loss of Eq. 5 / Eq. 3."""
@@ -345,9 +378,12 @@ def vargrad_tb_loss_and_grad(logits, tokens, mask, ref_logp, log_reward, beta: f
             n_seq_global = N * dist.get_world_size(group)
         else:
             n_seq_global = N
-    o, ws, d, dz = vargrad_fused(logits, tokens, mask, ref_logp, log_reward, beta, K, float(n_seq_global),
-                                 dlogits=dlogits, dlogits_dtype=dlogits_dtype, inv_temp=inv_temp,
-                                 log_z_param=None if log_z is None else log_z.detach().contiguous())
+    if schedule not in ("fused", "pipelined"):
+        raise ValueError("schedule must be 'fused' or 'pipelined'")
+    call = vargrad_fused if schedule == "fused" else vargrad_pipelined
+    o, ws, d, dz = call(logits, tokens, mask, ref_logp, log_reward, beta, K, float(n_seq_global),
+                        dlogits=dlogits, dlogits_dtype=dlogits_dtype, inv_temp=inv_temp,
+                        log_z_param=None if log_z is None else log_z.detach().contiguous())
     if group is not None:
         import torch.distributed as dist
         dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
