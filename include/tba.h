@@ -260,6 +260,50 @@ int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coe
                       const double* grad_out, void* dlogits, int32_t dlogits_dtype, int64_t dlogits_row_stride,
                       tba_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------
+ * LM-head-fused head, forward: the same log pi(y|x) and Eq. 4/5
+ * outputs, computed from the final hidden states and the LM-head weight WITHOUT writing
+ * the logits. "Parallel likelihood evaluation of an entire sequence through a single
+ * forward pass" ends in z_{s,t} = W h_{s,t}; here that contraction runs on the
+ * tcgen05 tensor cores (bf16 operands, fp32 accumulation in TMEM) and its epilogue folds
+ * each 128 x 256 logit tile into the row's online log-sum-exp and gathers z[y], so the
+ * [N, T, V] logits (20 GB at the Qwen shard) never reach HBM.
+ *   hidden : bf16, row (s, t) at hidden + (s*seq_len + t) * hidden_stride elements, d used
+ *   weight : bf16 [vocab, d], row v at weight + v * weight_stride elements (no bias)
+ *   z_{s,t,v} = sum_i hidden[s,t,i] * weight[v,i]   (fp32 accumulation, any order)
+ * Requirements (TBA_ERR_INVALID_ARG otherwise): d >= 8, d and both strides multiples of 8
+ * elements, hidden/weight 16-byte aligned, n_seq*seq_len <= 2^31 - 1, vocab <= 2^31 - 1.
+ * tokens / mask as in tba_rows. Numerics: the logits carry the fp32 accumulation error of
+ * a d-term dot product; the softmax epilogue is as accurate as the row
+ * kernels'. Backward (dL/dhidden, dL/dW) is not provided: use the logits path for training
+ * steps that need it. */
+typedef struct tba_lmhead {
+  const void*    hidden;         /* bf16 */
+  const void*    weight;         /* bf16 */
+  int64_t        n_seq;          /* N >= 0 */
+  int64_t        seq_len;        /* T >= 0 */
+  int64_t        d;              /* hidden size */
+  int64_t        vocab;          /* V >= 1 */
+  int64_t        hidden_stride;  /* elements between consecutive hidden rows, >= d */
+  int64_t        weight_stride;  /* elements between consecutive weight rows, >= d */
+  const int64_t* tokens;         /* [n_seq, seq_len] */
+  const uint8_t* mask;           /* [n_seq, seq_len] */
+} tba_lmhead;
+
+/* Workspace for the two calls below: tba_workspace_bytes(n_seq, seq_len) plus the per-(row,
+ * vocab group of 1024) partial {max, sum} and the gathered logit (256-B aligned base). */
+size_t tba_lmhead_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t vocab);
+
+/* tba_seq_logprob from hidden states: seq_logp[s] = sum_t mask * log softmax(inv_temp z)[y]. */
+int tba_lmhead_seq_logprob(const tba_lmhead* x, double inv_temp, void* workspace, double* seq_logp,
+                           int32_t* n_tokens, int32_t* dev_status, tba_stream_t stream);
+
+/* tba_tb_loss_fwd from hidden states (Eqs. 4-5 / Eq. 3; opts as there). */
+int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const double* ref_logp,
+                           const double* log_reward, double beta, int32_t K, double n_seq_global,
+                           void* workspace, double* seq_logp, int32_t* n_tokens, double* log_z,
+                           double* resid, double* partial, int32_t* dev_status, tba_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

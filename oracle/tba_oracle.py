@@ -27,6 +27,9 @@ the independent Appendix-A advantage form; central finite differences of the los
 TBA' (Eq. 16) pins (tests/test_oracle_tbap.py): Dr. GRPO equality at beta = 0 on-policy
 (P:616), the Eq. 7 / Eq. 16 link A = -beta*eps, clip/IcePop worked values, the band
 (0, inf) no-op, per-group shift invariance, finite differences with coefficients held fixed.
+LM-head pins (tests/test_oracle_lmhead.py): brute-force triple loops on tiny inputs, equal
+weight rows (lp = -ln V for any hidden state), one-hot weight rows (closed form), invariance
+to adding a common vector to every weight row, temperature = scaling the weight.
 Every function below is pinned by at least one of them ("parity unpinned": none).
 """
 from __future__ import annotations
@@ -302,3 +305,41 @@ def bf16_ulp(x) -> np.ndarray:
     _, e = np.frexp(np.where(x > 0, x, 1.0))
     e = np.where(x > 0, np.maximum(e, -125), -125)
     return np.ldexp(1.0, e - 8)
+
+
+# ----------------------------------------------------------------------------- NEXT 3: from hidden states
+def lmhead_logits(hidden: np.ndarray, weight: np.ndarray) -> np.ndarray:
+    """z_{r,v} = sum_i h_{r,i} W_{v,i}: the LM-head contraction that ends the "single forward
+    pass" of P:202 (the logits every a1 step consumes), in fp64 (a library matmul of the
+    exact fp64 values of the bf16 inputs). hidden [R, d], weight [V, d] -> [R, V]."""
+    return np.asarray(hidden, np.float64) @ np.asarray(weight, np.float64).T
+
+
+def lmhead_token_logprob(hidden: np.ndarray, weight: np.ndarray, tokens, inv_temp: float = 1.0,
+                         chunk: int = 8192) -> np.ndarray:
+    """log softmax(inv_temp * W h_r)[y_r] for every row r of hidden [R, d] (tokens [R]), fp64.
+    The weight may be a callable ``weight(v0, v1) -> [v1 - v0, d]`` (rows generated on demand,
+    for vocabularies too large to hold in fp64); the logits are then built chunk by chunk
+    (the chunking only splits the matmul's output columns; every z is the same dot product)."""
+    hidden = np.asarray(hidden, np.float64)
+    if callable(weight):
+        V = weight.vocab
+        parts = []
+        for v0 in range(0, V, chunk):
+            parts.append(lmhead_logits(hidden, weight(v0, min(V, v0 + chunk))))
+        z = np.concatenate(parts, axis=1)
+    else:
+        z = lmhead_logits(hidden, weight)
+    out = np.empty(len(hidden))
+    for r in range(len(hidden)):
+        out[r] = token_logprob(inv_temp * z[r], int(tokens[r]))[0]
+    return out
+
+
+def lmhead_seq_logprob(hidden: np.ndarray, weight: np.ndarray, tokens: np.ndarray, mask: np.ndarray,
+                       inv_temp: float = 1.0):
+    """seq_logprob of the logits z = inv_temp * W h (hidden [N, T, d]); returns (ell, n_tok)."""
+    N, T, d = np.shape(hidden)
+    z = inv_temp * lmhead_logits(np.reshape(hidden, (N * T, d)), weight).reshape(N, T, -1)
+    ell, ntok, _ = seq_logprob(z, tokens, mask)
+    return ell, ntok

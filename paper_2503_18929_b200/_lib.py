@@ -21,7 +21,8 @@ EXPORTS = ("tba_abi_version", "tba_status_string", "tba_workspace_bytes", "tba_s
            "tba_vargrad_tb_loss_fwd", "tba_vargrad_tb_loss_bwd", "tba_tb_loss_fwd", "tba_tb_loss_bwd", "tba_tb_loss_fused",
            "tba_tb_loss_pipelined", "tba_tb_loss_fwd_deferred",
            "tba_tbap_loss_fwd", "tba_tbap_loss_bwd", "tba_tbap_loss_fwd_deferred", "tba_tb_loss_fwd_peer",
-           "tba_ipc_alloc", "tba_ipc_open", "tba_ipc_close", "tba_ipc_free")
+           "tba_ipc_alloc", "tba_ipc_open", "tba_ipc_close", "tba_ipc_free",
+           "tba_lmhead_workspace_bytes", "tba_lmhead_seq_logprob", "tba_lmhead_tb_loss_fwd")
 TBA_DEV_PEER_TIMEOUT = 4
 TBA_IS_NONE, TBA_IS_CLIP, TBA_IS_ICEPOP = 0, 1, 2
 
@@ -30,6 +31,13 @@ class TbaRows(ctypes.Structure):
     _fields_ = [("logits", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("_pad", ctypes.c_int32),
                 ("n_seq", ctypes.c_int64), ("seq_len", ctypes.c_int64), ("vocab", ctypes.c_int64),
                 ("row_stride", ctypes.c_int64), ("tokens", ctypes.c_void_p), ("mask", ctypes.c_void_p)]
+
+
+class TbaLmhead(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_void_p), ("weight", ctypes.c_void_p), ("n_seq", ctypes.c_int64),
+                ("seq_len", ctypes.c_int64), ("d", ctypes.c_int64), ("vocab", ctypes.c_int64),
+                ("hidden_stride", ctypes.c_int64), ("weight_stride", ctypes.c_int64), ("tokens", ctypes.c_void_p),
+                ("mask", ctypes.c_void_p)]
 
 
 class TbaTbOpts(ctypes.Structure):
@@ -91,6 +99,13 @@ def load(path: str | None = None) -> ctypes.CDLL:
         PP = ctypes.POINTER(TbaPeerReduce)
         L.tba_tb_loss_fwd_peer.restype = ctypes.c_int
         L.tba_tb_loss_fwd_peer.argtypes = [RP, OP, P, P, D, I32, D, P, P, P, P, P, P, PP, P, P]
+        LP = ctypes.POINTER(TbaLmhead)
+        L.tba_lmhead_workspace_bytes.restype = SZ
+        L.tba_lmhead_workspace_bytes.argtypes = [I64, I64, I64]
+        L.tba_lmhead_seq_logprob.restype = ctypes.c_int
+        L.tba_lmhead_seq_logprob.argtypes = [LP, D, P, P, P, P, P]
+        L.tba_lmhead_tb_loss_fwd.restype = ctypes.c_int
+        L.tba_lmhead_tb_loss_fwd.argtypes = [LP, OP, P, P, D, I32, D, P, P, P, P, P, P, P, P]
         L.tba_ipc_alloc.restype = ctypes.c_int
         L.tba_ipc_alloc.argtypes = [SZ, ctypes.POINTER(ctypes.c_void_p), P]
         L.tba_ipc_open.restype = ctypes.c_int

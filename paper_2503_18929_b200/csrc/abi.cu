@@ -495,4 +495,65 @@ int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coe
                     dlogits_row_stride, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// ---- LM-head-fused head (NEXT 3)
+size_t tba_lmhead_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t vocab) {
+  if (n_seq < 0 || seq_len < 0 || vocab < 1) return 0;
+  return ws_bytes(n_seq, seq_len) + lmhead_partial_bytes(n_seq * seq_len, vocab);
+}
+
+int tba_lmhead_seq_logprob(const tba_lmhead* x, double inv_temp, void* workspace, double* seq_logp,
+                           int32_t* n_tokens, int32_t* dev_status, tba_stream_t stream) {
+  int rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (!(std::isfinite(inv_temp) && inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (x->n_seq == 0) return TBA_OK;
+  if (!workspace || !seq_logp || !n_tokens || reinterpret_cast<uintptr_t>(workspace) % 256)
+    return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  rc = launch_lmhead_rows(x, static_cast<char*>(workspace) + ws_bytes(x->n_seq, x->seq_len), w,
+                          make_scale(inv_temp), dev_status, s);
+  if (rc) return rc;
+  HeadArgs ha{};
+  ha.T = x->seq_len;
+  ha.K = 1;
+  ha.n_seq = x->n_seq;
+  ha.seq_logp = seq_logp;
+  ha.n_tokens = n_tokens;
+  return launch_seq_head(false, w, x->mask, ha, s);
+}
+
+int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const double* ref_logp,
+                           const double* log_reward, double beta, int32_t K, double n_seq_global,
+                           void* workspace, double* seq_logp, int32_t* n_tokens, double* log_z,
+                           double* resid, double* partial, int32_t* dev_status, tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  const WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  rc = launch_lmhead_rows(x, static_cast<char*>(workspace) + ws_bytes(x->n_seq, x->seq_len), w,
+                          make_scale(opt_inv_temp(opts)), dev_status, s);
+  if (rc) return rc;
+  tba_rows xr{};
+  xr.n_seq = x->n_seq;
+  xr.seq_len = x->seq_len;
+  const HeadArgs ha = tb_head_args(&xr, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
+                                   log_z, resid, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+  return launch_seq_head(true, w, x->mask, ha, s);
+}
+
 }  // extern "C"

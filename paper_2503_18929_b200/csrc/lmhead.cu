@@ -1,0 +1,374 @@
+// NEXT 3: the LM-head contraction z = W h on the tcgen05 tensor cores with the
+// online log-softmax in its epilogue, so the [rows, V] logits never reach HBM.
+//
+// lmhead_fwd — persistent, warp-specialised, one CTA per SM (192 threads):
+//   warp 0      TMA producer: 128 x 64 hidden tile (A) + 256 x 64 weight tile (B) per stage,
+//               SWIZZLE_128B, into a LM_STAGES-deep shared-memory ring (mbarrier complete_tx);
+//   warp 1      owns 512 TMEM columns (two 128 x 256 fp32 accumulators); lane 0 issues
+//               tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16; bf16 in, fp32 out)
+//               and tcgen05.commit's the stage back to the producer / the tile to the epilogue;
+//   warps 2-5   epilogue: each thread owns one row (TMEM lane), tcgen05.ld's its 256 logits in
+//               32-column chunks, folds them into an online (max, sum 2^x) state in log2 units
+//               and gathers z[y]; releases the accumulator for the next tile.
+// Work item = (row block of 128, group of LM_G vocab tiles); items are rasterised in super-rows
+// of LM_RB_SWZ row blocks (vocab groups outer, row blocks inner) so the CTAs running at one
+// time share a few hidden blocks and weight groups in L2. Each item writes a per-(row, group)
+// partial {max, sum}; lmhead_combine reduces the groups of a row in a fixed order (fp64) and
+// writes the same per-row log-prob (fp64) as the logits path, so seq_head runs unchanged.
+#include <cudaTypedefs.h>
+
+#include "tba_device.cuh"
+
+namespace tba {
+namespace {
+
+constexpr int LM_BM = 128, LM_BN = 256, LM_BK = 64, LM_STAGES = 4, LM_G = 4, LM_RB_SWZ = 16;
+constexpr int LM_A_BYTES = LM_BM * LM_BK * 2;  // 16 KB
+constexpr int LM_B_BYTES = LM_BN * LM_BK * 2;  // 32 KB
+constexpr int LM_STAGE_BYTES = LM_A_BYTES + LM_B_BYTES;
+constexpr int LM_THREADS = 192;
+// instruction descriptor: f32 accumulate (bit 4), bf16 A (bits 7-9) and B (10-12), both K-major,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t LM_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
+                              ((uint32_t)(LM_BM >> 4) << 24);
+constexpr size_t LM_SMEM = 1024 + (size_t)LM_STAGES * LM_STAGE_BYTES + 256;
+
+// K-major operand, 128-byte swizzle (rows of 64 bf16 = 128 B, 8-row atoms of 1024 B): start
+// address >> 4, leading offset 1 (unused when swizzled), stride 1024 B between 8-row groups,
+// descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(LM_IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 consecutive fp32 accumulator columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct LmGrid {
+  int64_t rows, V;
+  int n_rb, n_tiles, n_groups, nkb;
+  int64_t n_items;
+};
+
+// item -> (row block, vocab group): super-rows of LM_RB_SWZ row blocks, groups outer.
+__device__ __forceinline__ void lm_item(const LmGrid& g, int64_t item, int& rb, int& grp) {
+  const int64_t per_super = (int64_t)LM_RB_SWZ * g.n_groups;
+  const int sup = (int)(item / per_super);
+  const int64_t w = item - (int64_t)sup * per_super;
+  const int rb0 = sup * LM_RB_SWZ;
+  const int nrb = (g.n_rb - rb0) < LM_RB_SWZ ? (g.n_rb - rb0) : LM_RB_SWZ;
+  grp = (int)(w / nrb);
+  rb = rb0 + (int)(w % nrb);
+}
+
+__global__ void __launch_bounds__(LM_THREADS, 1)
+    lmhead_fwd(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
+               const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
+               float2* __restrict__ part, float* __restrict__ zy_out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + LM_STAGES * LM_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + LM_STAGES * LM_STAGE_BYTES);
+  uint64_t* empty = full + LM_STAGES;
+  uint64_t* tfull = empty + LM_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+      uint64_t pol_w, pol_h;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_w));
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_h));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = blockIdx.x; it < g.n_items; it += gridDim.x) {
+        int rb, grp;
+        lm_item(g, it, rb, grp);
+        const int t0 = grp * LM_G, t1 = min(g.n_tiles, t0 + LM_G);
+        for (int t = t0; t < t1; ++t) {
+          for (int kb = 0; kb < g.nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_expect_tx(&full[stage], LM_STAGE_BYTES);
+            tma_load_2d(smem_u32(sA + stage * LM_A_BYTES), &tmH, kb * LM_BK, rb * LM_BM, smem_u32(&full[stage]),
+                        pol_h);
+            tma_load_2d(smem_u32(sB + stage * LM_B_BYTES), &tmW, kb * LM_BK, t * LM_BN, smem_u32(&full[stage]),
+                        pol_w);
+            if (++stage == LM_STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t j = 0;  // accumulator tile counter
+      for (int64_t it = blockIdx.x; it < g.n_items; it += gridDim.x) {
+        int rb, grp;
+        lm_item(g, it, rb, grp);
+        const int t0 = grp * LM_G, t1 = min(g.n_tiles, t0 + LM_G);
+        for (int t = t0; t < t1; ++t, ++j) {
+          const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+          mbar_wait(&tempty[acc], aph ^ 1u);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + acc * LM_BN;
+          for (int kb = 0; kb < g.nkb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * LM_A_BYTES));
+            const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * LM_B_BYTES));
+#pragma unroll
+            for (int k = 0; k < LM_BK / 16; ++k)  // K = 16 per MMA: +32 bytes = +2 in the address field
+              umma_bf16(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+            umma_commit(&empty[stage]);
+            if (++stage == LM_STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          umma_commit(&tfull[acc]);
+        }
+      }
+    }
+  } else {  // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+    const int q = warp & 3;
+    const int row_in = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const float sc = rs.sc;
+    uint32_t j = 0;
+    for (int64_t it = blockIdx.x; it < g.n_items; it += gridDim.x) {
+      int rb, grp;
+      lm_item(g, it, rb, grp);
+      const int t0 = grp * LM_G, t1 = min(g.n_tiles, t0 + LM_G);
+      const int64_t row = (int64_t)rb * LM_BM + row_in;
+      const bool in_rows = row < g.rows;
+      const int64_t y = in_rows ? tokens[row] : -1;
+      float R = -INFINITY;  // reference in logit units (a running max, moved only by > slack)
+      double S = 0.0;       // sum of 2^((z - R) * sc)
+      float zy = 0.f;
+      bool found = false;
+      for (int t = t0; t < t1; ++t, ++j) {
+        const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const int64_t nb = (int64_t)t * LM_BN;
+#pragma unroll 1
+        for (int c = 0; c < LM_BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(tmem + lane_addr + acc * LM_BN + c * 32, v);
+          const int64_t n0 = nb + c * 32;
+          const int64_t lim = g.V - n0;  // columns [0, lim) of this chunk are in the vocabulary
+          const int64_t dy = y - n0;
+          float cm = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (dy == i) {
+              zy = v[i];
+              found = true;
+            }
+            v[i] = (i < lim) ? v[i] : -INFINITY;
+            cm = fmaxf(cm, v[i]);
+          }
+          if (cm > R + rs.slack) {  // re-base (rare): exact fp64 rescale of the running sum
+            S = (R == -INFINITY) ? 0.0 : S * exp2(((double)R - (double)cm) * (double)sc);
+            R = cm;
+          }
+          // 2^((z - R) sc): the difference is exact for the terms that matter, so the scale's
+          // rounding never multiplies the row's full log-sum-exp. Pairwise sum (~5 ulp) -> fp64.
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = ex2((v[i] - R) * sc);
+#pragma unroll
+          for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; ++i) v[i] += v[i + w];
+          S += (double)v[0];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+      if (in_rows) {
+        part[(int64_t)grp * g.rows + row] = make_float2(R, (float)S);
+        if (found) zy_out[row] = zy;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// Per valid row: fixed-order fp64 reduction of the group partials, then the same stats / log-prob
+// outputs as the logits path (finalize_row's contract): stats = {M2, log2 S}, lp fp64.
+__global__ void lmhead_combine(const float2* __restrict__ part, const float* __restrict__ zy_in, int64_t rows,
+                               int n_groups, int64_t V, const int64_t* __restrict__ tokens,
+                               const uint8_t* __restrict__ mask, RowScale rs, float2* __restrict__ stats,
+                               double* __restrict__ lp, int32_t* dev_status) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    if (!mask[r]) continue;
+    float M = -INFINITY;  // logit units
+    for (int k = 0; k < n_groups; ++k) M = fmaxf(M, part[(int64_t)k * rows + r].x);
+    double S = 0.0;  // sum over the vocabulary of 2^((z - M) sc)
+    for (int k = 0; k < n_groups; ++k) {
+      const float2 p = part[(int64_t)k * rows + r];
+      S += (double)p.y * exp2(((double)p.x - (double)M) * (double)rs.sc);
+    }
+    const double l2s = log2(S);
+    const int64_t y = tokens[r];
+    double out;
+    if (y < 0 || y >= V) {
+      out = __longlong_as_double(0x7ff8000000000000ll);
+      if (dev_status) atomicOr(dev_status, TBA_DEV_TOKEN_RANGE);
+    } else {
+      // log softmax(inv_temp z)[y] = inv_temp (z_y - M) - ln 2 log2 sum 2^((z - M) sc)
+      out = rs.inv_temp * ((double)zy_in[r] - (double)M) - kLN2 * l2s;
+    }
+    if (!(isfinite(M) && isfinite(l2s))) {
+      out = __longlong_as_double(0x7ff8000000000000ll);
+      if (dev_status) atomicOr(dev_status, TBA_DEV_NONFINITE_ROW);
+    }
+    // row statistics in the logits path's convention: M2 = M sc (log2 units), log2 S
+    stats[r] = make_float2((float)((double)M * (double)rs.sc), (float)l2s);
+    lp[r] = out;
+  }
+}
+
+using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D bf16 tensor map over [n_rows, d] (row stride `stride` elements), box 64 x box_rows, 128B swizzle.
+bool make_map(CUtensorMap* m, const void* base, int64_t n_rows, int64_t d, int64_t stride, int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)stride * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)LM_BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t lmhead_partial_bytes(int64_t rows, int64_t V) {
+  const int64_t groups = ((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G;
+  return align_up((size_t)groups * (size_t)rows * sizeof(float2), 256) + align_up((size_t)rows * sizeof(float), 256);
+}
+
+int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+                       cudaStream_t s) {
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows == 0) return TBA_OK;
+  LmGrid g;
+  g.rows = rows;
+  g.V = x->vocab;
+  g.n_rb = (int)((rows + LM_BM - 1) / LM_BM);
+  g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
+  g.n_groups = (g.n_tiles + LM_G - 1) / LM_G;
+  g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
+  g.n_items = (int64_t)g.n_rb * g.n_groups;
+  CUtensorMap mh, mw;
+  if (!make_map(&mh, x->hidden, rows, x->d, x->hidden_stride, LM_BM) ||
+      !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN))
+    return TBA_ERR_CUDA;
+  float2* part = static_cast<float2*>(part_ws);
+  float* zy = reinterpret_cast<float*>(static_cast<char*>(part_ws) +
+                                       align_up((size_t)g.n_groups * (size_t)rows * sizeof(float2), 256));
+  static bool attr[64] = {};  // per device; benign race: idempotent
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
+  if (!attr[dev]) {
+    if (cudaFuncSetAttribute(lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM) != cudaSuccess)
+      return TBA_ERR_CUDA;
+    attr[dev] = true;
+  }
+  int64_t grid = device_sms();
+  if (grid > g.n_items) grid = g.n_items;
+  lmhead_fwd<<<(unsigned)grid, LM_THREADS, LM_SMEM, s>>>(mh, mw, g, x->tokens, x->mask, rs, part, zy);
+  if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  const int64_t blocks = (rows + 255) / 256 < 4096 ? (rows + 255) / 256 : 4096;
+  lmhead_combine<<<(unsigned)blocks, 256, 0, s>>>(part, zy, rows, g.n_groups, x->vocab, x->tokens, x->mask, rs,
+                                                  w.stats, w.lp, dev_status);
+  return launch_status();
+}
+
+}  // namespace tba

@@ -279,6 +279,25 @@ inline int pipe_groups(int64_t group_bytes, int64_t groups) {
   return d;
 }
 
+// tba_lmhead: sizes, strides and alignment the TMA tensor maps need (16-byte strides, int32
+// coordinates), and the row-count limit shared with tba_rows.
+inline int validate_lmhead(const tba_lmhead* x) {
+  if (!x) return TBA_ERR_INVALID_ARG;
+  if (x->n_seq < 0 || x->seq_len < 0 || x->vocab < 1 || x->vocab > (int64_t)INT32_MAX) return TBA_ERR_INVALID_ARG;
+  if (x->d < 8 || x->d % 8 || x->hidden_stride < x->d || x->hidden_stride % 8 || x->weight_stride < x->d ||
+      x->weight_stride % 8 || x->d > (int64_t)1 << 24)
+    return TBA_ERR_INVALID_ARG;
+  if (x->n_seq > 0 && x->seq_len > (int64_t)INT32_MAX / x->n_seq) return TBA_ERR_INVALID_ARG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows > 0) {
+    if (!x->hidden || !x->weight || !x->tokens || !x->mask) return TBA_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(x->hidden) % 16 || reinterpret_cast<uintptr_t>(x->weight) % 16 ||
+        reinterpret_cast<uintptr_t>(x->tokens) % 8)
+      return TBA_ERR_INVALID_ARG;
+  }
+  return TBA_OK;
+}
+
 inline int check_opts(const tba_tb_opts* o) {
   if (!o) return TBA_OK;
   if (!(std::isfinite(o->inv_temp) && o->inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
@@ -320,6 +339,12 @@ int launch_bwd(bool per_row, const tba_rows* x, const float2* stats, const doubl
 
 // fused.cu — the whole VarGrad TB step (a.* filled except nF/nB/RF/RB, set here).
 int launch_fused(FusedArgs& a, int32_t in_dtype, int32_t out_dtype, int tpr_f, int tpr_b, cudaStream_t s);
+
+// lmhead.cu — a1 from hidden states: tcgen05 LM-head GEMM with the online log-softmax in its
+// epilogue + the fixed-order group combine; writes w.stats / w.lp like launch_fwd_rows.
+size_t lmhead_partial_bytes(int64_t rows, int64_t V);
+int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+                       cudaStream_t s);
 
 // deferred.cu — a1 + the unscaled gradient in one pass per row.
 int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,

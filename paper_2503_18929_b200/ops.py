@@ -393,6 +393,91 @@ def vargrad_tb_loss_and_grad(logits, tokens, mask, ref_logp, log_reward, beta: f
     return res
 
 
+# ----------------------------------------------------------------------------- LM-head-fused (NEXT 3)
+def make_lmhead(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor):
+    """Describe [N, T, d] bf16 hidden states and a [V, d] bf16 LM-head weight as tba_lmhead."""
+    if hidden.dim() != 3 or weight.dim() != 2:
+        raise ValueError("hidden must be [N, T, d] and weight [V, d]")
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise ValueError("hidden and weight must be bf16")
+    if not (hidden.is_cuda and weight.is_cuda) or hidden.device != weight.device:
+        raise ValueError("hidden and weight must be CUDA tensors on one device (there is no CPU path)")
+    N, T, d = hidden.shape
+    V, d2 = weight.shape
+    if d2 != d:
+        raise ValueError("hidden and weight disagree on d")
+    if tokens.shape != (N, T) or mask.shape != (N, T) or tokens.dtype != torch.int64 or not tokens.is_contiguous():
+        raise ValueError("tokens must be contiguous int64 [N, T] and mask [N, T]")
+    if mask.dtype == torch.bool:
+        mask = mask.view(torch.uint8)
+    if mask.dtype != torch.uint8 or not mask.is_contiguous():
+        raise ValueError("mask must be contiguous uint8/bool")
+    if hidden.stride(2) != 1 or weight.stride(1) != 1:
+        raise ValueError("hidden and weight need unit stride over d")
+    hs = hidden.stride(1) if T > 1 else (hidden.stride(0) if N > 1 else d)
+    if N > 1 and T > 0 and hidden.stride(0) != T * hs:
+        raise ValueError("hidden rows must be uniformly strided")
+    ws_ = weight.stride(0) if V > 1 else d
+    return _lib.TbaLmhead(hidden.data_ptr(), weight.data_ptr(), N, T, d, V, max(hs, d), max(ws_, d),
+                          tokens.data_ptr(), mask.data_ptr())
+
+
+def lmhead_workspace_bytes(n_seq: int, seq_len: int, vocab: int) -> int:
+    return int(_lib.load().tba_lmhead_workspace_bytes(int(n_seq), int(seq_len), int(vocab)))
+
+
+def _lm_workspace(dev, N, T, V):
+    return torch.empty(max(lmhead_workspace_bytes(N, T, V), 256), dtype=torch.uint8, device=dev)
+
+
+def lmhead_seq_logprob(hidden, weight, tokens, mask, *, inv_temp: float = 1.0, workspace=None,
+                       check_status: bool = _CHECK):
+    """log pi(y_s|x) from hidden states and the LM-head weight, logits never written
+    (tba_lmhead_seq_logprob). Returns (seq_logp fp64 [N], n_tokens int32 [N])."""
+    L = _lib.load()
+    x = make_lmhead(hidden, weight, tokens, mask)
+    N, T = tokens.shape
+    dev = hidden.device
+    out = torch.empty(N, dtype=torch.float64, device=dev)
+    ntok = torch.empty(N, dtype=torch.int32, device=dev)
+    ws = workspace if workspace is not None else _lm_workspace(dev, N, T, weight.shape[0])
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_lmhead_seq_logprob(ctypes.byref(x), float(inv_temp), ws.data_ptr(), out.data_ptr(),
+                                       ntok.data_ptr(), _ptr(st), _stream(dev)), "tba_lmhead_seq_logprob")
+    if st is not None:
+        _raise_dev_status(st, "tba_lmhead_seq_logprob")
+    return out, ntok
+
+
+def lmhead_vargrad_fwd(hidden, weight, tokens, mask, ref_logp, log_reward, beta: float, K: int,
+                       n_seq_global: float, *, inv_temp: float = 1.0, log_z_param=None, workspace=None,
+                       out: _Fwd | None = None, check_status: bool = _CHECK):
+    """VarGrad TB forward (Eqs. 4-5; Eq. 3 with log_z_param) from hidden states
+    (tba_lmhead_tb_loss_fwd). Returns (_Fwd, workspace)."""
+    L = _lib.load()
+    x = make_lmhead(hidden, weight, tokens, mask)
+    N, T = tokens.shape
+    dev = hidden.device
+    for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
+        if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    o = out or _Fwd(N, K, dev)
+    ws = workspace if workspace is not None else _lm_workspace(dev, N, T, weight.shape[0])
+    st = _status(dev) if check_status else None
+    opts = _opts(inv_temp, log_z_param)
+    with torch.cuda.device(dev):
+        check(L.tba_lmhead_tb_loss_fwd(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
+                                       ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K),
+                                       float(n_seq_global), ws.data_ptr(), o.seq_logp.data_ptr(),
+                                       o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None,
+                                       o.resid.data_ptr(), o.partial.data_ptr(), _ptr(st), _stream(dev)),
+              "tba_lmhead_tb_loss_fwd")
+    if st is not None:
+        _raise_dev_status(st, "tba_lmhead_tb_loss_fwd")
+    return o, ws
+
+
 # ----------------------------------------------------------------------------- TBA' (Eq. 16)
 _IS = {"none": 0, "clip": 1, "icepop": 2}
 

@@ -119,6 +119,7 @@ class Workload:
     len_hi: int
     reward: str          # "binary" | "rm" | "redteam" | "unit"
     note: str = ""
+    d: int = 0           # hidden size of the model's LM head (LM-head-fused path, NEXT 3)
 
     @property
     def N(self) -> int:
@@ -141,6 +142,10 @@ WORKLOADS = {
     "qwen": Workload("qwen", 64, 8, 1024, 152064, "bf16", 0.005, 1024, 1024, "binary",
                      "Qwen2.5-7B MATH: V=152064, 1024 tokens, 64x8 (sharded by group over 8 GPUs)"),
 }
+# Hidden sizes of the models named in BASELINE.json (their LM heads: d x V, no bias): Qwen2.5-7B
+# 3584, Pythia-410M 1024, RhoMath-1B (TinyLlama-1.1B architecture) 2048, GPT-2 small 768.
+for _n, _d in (("toy", 64), ("pythia", 1024), ("rhomath", 2048), ("redteam", 768), ("qwen", 3584)):
+    WORKLOADS[_n] = dataclasses.replace(WORKLOADS[_n], d=_d)
 # The per-GPU shard of the Qwen batch at 8xB200 (8 of the 64 groups).
 WORKLOADS["qwen_shard"] = dataclasses.replace(WORKLOADS["qwen"], name="qwen_shard", B=8,
                                               note="Qwen2.5-7B MATH per-GPU shard: 8 groups x K=8, T=1024, V=152064")
@@ -269,6 +274,9 @@ def _load_cuda_twin():
         L.tba_synth_logits.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                        ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                        ctypes.c_int64, ctypes.c_void_p]
+        L.tba_synth_bf16.restype = ctypes.c_int
+        L.tba_synth_bf16.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         _synth_lib = L
     return _synth_lib
 
@@ -324,3 +332,58 @@ def gen_logp(w: Workload, seed: int, seq0: int = 0, n: int | None = None) -> np.
     drift = np.where(out_sel == 0, 3.0, np.where(out_sel == 1, -3.0, drift))
     g = (z.astype(np.float64) - (math.log(w.V) + 2.65) + drift).astype(np.float32).reshape(n, w.T)
     return np.where(mask == 1, g, np.float32(0.0)).astype(np.float32)
+
+
+# ----------------------------------------------------------------------------- LM-head inputs (NEXT 3)
+S_HIDDEN, S_WEIGHT = 10, 11
+
+
+def weight_scale_exp(d: int) -> int:
+    """Power-of-two exponent of the LM-head weight scale: logits z = W h then have a standard
+    deviation of ~2.3 (the logits recipe's Irwin-Hall spread) for hidden states of std ~1.15."""
+    return int(round(math.log2(0.866 / math.sqrt(d)))) - 14
+
+
+def _bf16_matrix(seed: int, stream: int, d: int, rows, scale_exp: int, kind: str) -> np.ndarray:
+    rows = np.asarray(rows, dtype=np.uint64).reshape(-1)
+    idx = rows[:, None] * np.uint64(d) + np.arange(d, dtype=np.uint64)[None, :]
+    h = hash64(seed, stream, idx)
+    if kind == "lattice":  # {-2, -1, 0, 1, 2} / 4: every partial sum of a dot product is exact in fp32
+        x = (mulhi_u64(h, 5).astype(np.int64) - 2).astype(np.float64) * 0.25
+    elif kind == "normal":  # Irwin-Hall(4) of the hash's 16-bit fields, times 2^scale_exp
+        acc = np.zeros(h.shape, dtype=np.int64)
+        for k in range(4):
+            acc += ((h >> np.uint64(16 * k)) & np.uint64(0xFFFF)).astype(np.int64)
+        x = (acc - 131070).astype(np.float64) * (2.0 ** scale_exp)
+    else:
+        raise ValueError(kind)
+    return f32_to_bf16_bits(x.astype(np.float32))
+
+
+def hidden_rows(seed: int, d: int, rows, kind: str = "normal") -> np.ndarray:
+    """Final hidden states h_r (bf16 bits [len(rows), d]) of the given global rows."""
+    return _bf16_matrix(seed, S_HIDDEN, d, rows, -15, kind)
+
+
+def weight_rows(seed: int, d: int, vrows, kind: str = "normal") -> np.ndarray:
+    """LM-head weight rows W_v (bf16 bits [len(vrows), d])."""
+    return _bf16_matrix(seed, S_WEIGHT, d, vrows, weight_scale_exp(d), kind)
+
+
+def fill_bf16_cuda(out, seed: int, which: str, row0: int, kind: str = "normal", stream: int | None = None):
+    """Fill a CUDA bf16 tensor viewed as [nrows, d] (unit stride over d, rows uniformly strided)
+    with hidden_rows / weight_rows of global rows row0..; bit-identical to the NumPy twin."""
+    import torch
+    if out.dtype != torch.bfloat16 or out.stride(-1) != 1:
+        raise ValueError("out must be bf16 with unit stride over d")
+    d = out.shape[-1]
+    nrows = out.numel() // d if out.numel() else 0
+    rs = out.stride(-2) if out.dim() >= 2 and out.shape[-2] > 1 else d
+    stream_id, e = (S_HIDDEN, -15) if which == "hidden" else (S_WEIGHT, weight_scale_exp(d))
+    s = torch.cuda.current_stream(out.device).cuda_stream if stream is None else stream
+    L = _load_cuda_twin()
+    rc = L.tba_synth_bf16(out.data_ptr(), stream_key(seed, stream_id), row0, nrows, d, rs,
+                          1 if kind == "lattice" else 0, e, s)
+    if rc:
+        raise RuntimeError(f"tba_synth_bf16 failed ({rc})")
+    return out

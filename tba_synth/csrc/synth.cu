@@ -51,9 +51,47 @@ __global__ void synth_logits_kernel(void* out, uint64_t key_logits, uint64_t key
   }
 }
 
+// LM-head inputs (hidden states / weight rows): element (r, i) from hash(key, r*d + i).
+// kind 0: Irwin-Hall(4) * 2^scale_exp; kind 1: lattice {-2..2}/4. bf16 by integer RNE.
+__global__ void synth_bf16_kernel(uint16_t* out, uint64_t key, int64_t row0, int64_t nrows, int64_t d,
+                                  int64_t row_stride, int kind, double scale) {
+  for (int64_t r = blockIdx.y; r < nrows; r += gridDim.y) {
+    const uint64_t grow = (uint64_t)(row0 + r);
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < d; c += (int64_t)gridDim.x * blockDim.x) {
+      const uint64_t h = hash_at(key, grow * (uint64_t)d + (uint64_t)c);
+      float x;
+      if (kind == 1) {
+        x = (float)((double)((int64_t)__umul64hi(h, 5ull) - 2) * 0.25);
+      } else {
+        const int64_t acc = (int64_t)(h & 0xFFFF) + (int64_t)((h >> 16) & 0xFFFF) + (int64_t)((h >> 32) & 0xFFFF) +
+                            (int64_t)((h >> 48) & 0xFFFF) - 131070;
+        x = (float)((double)acc * scale);
+      }
+      out[r * row_stride + c] = bf16_rne(x);
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+// Fill a bf16 [nrows, d] matrix (row stride row_stride elements) with global rows row0.. of
+// tba_synth.hidden_rows / weight_rows (key = stream_key(seed, S_HIDDEN / S_WEIGHT)).
+int tba_synth_bf16(void* out, uint64_t key, int64_t row0, int64_t nrows, int64_t d, int64_t row_stride, int kind,
+                   int scale_exp, cudaStream_t stream) {
+  if (!out || nrows < 0 || d <= 0 || row_stride < d || (kind != 0 && kind != 1)) return 1;
+  if (nrows == 0) return 0;
+  int64_t gx = (d + 255) / 256;
+  if (gx > 64) gx = 64;
+  const int64_t gy = nrows < 65535 ? nrows : 65535;
+  double scale = 1.0;
+  for (int i = 0; i < (scale_exp < 0 ? -scale_exp : scale_exp); ++i) scale = scale_exp < 0 ? scale * 0.5 : scale * 2.0;
+  synth_bf16_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, stream>>>(static_cast<uint16_t*>(out), key, row0,
+                                                                          nrows, d, row_stride, kind, scale);
+  return (int)cudaGetLastError();
+}
+
 
 // Fill rows [row0, row0+nrows) (global row ids) of a logits buffer laid out as
 // [nrows, row_stride] elements; columns >= V get NaN. dtype 0 = bf16, 1 = fp32.
