@@ -158,6 +158,192 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- LM-head-fused arm (NEXT 3)
+def tensor_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), \
+            "measured (MEASURED_PEAKS.json bf16_tflops: cuBLAS 8192^3 burst; sustained beside it)"
+    return 2250.0, 2250.0, "nominal dense bf16 (B200_PROFILING.md)"
+
+
+def oracle_lmhead_sample(w: syn.Workload, n_rows: int, seed: int = SEED, chunk: int = 8192):
+    """Bounded oracle sample for the LM-head arm: the first n_rows rows against the full
+    vocabulary. Weight rows are generated chunk by chunk (not timed); the oracle's matmul +
+    log-softmax is. Returns (seconds, rows)."""
+    from oracle import tba_oracle as O
+    tok, _ = syn.tokens_and_mask(w, seed, 0, max(1, -(-n_rows // w.T)))
+    rows = np.arange(n_rows)
+    h = syn.bf16_bits_to_f64(syn.hidden_rows(seed, w.d, rows))
+    secs, zs = 0.0, []
+    for v0 in range(0, w.V, chunk):
+        wv = syn.bf16_bits_to_f64(syn.weight_rows(seed, w.d, np.arange(v0, min(w.V, v0 + chunk))))
+        t0 = time.perf_counter()
+        zs.append(O.lmhead_logits(h, wv))
+        secs += time.perf_counter() - t0
+    t0 = time.perf_counter()
+    z = np.concatenate(zs, axis=1)
+    for r in range(n_rows):
+        O.token_logprob(z[r], int(tok.reshape(-1)[r]))
+    secs += time.perf_counter() - t0
+    return secs, n_rows
+
+
+def lmhead_bench(args, w, tba, torch, dist, dev, world, rank, group):
+    """One step = tba_lmhead_tb_loss_fwd over this rank's groups (z = W h on tcgen05 with the
+    online log-softmax fused; Eq. 4/5 head), + the 24-byte all-reduce when N > 1."""
+    B, K, T, V, d = w.B, w.K, w.T, w.V, w.d
+    N = B * K
+    g0 = rank * B
+    n_global = float(N * world)
+    gi = syn.group_inputs(w, SEED, g0, B)
+    hidden = torch.empty((N, T, d), dtype=torch.bfloat16, device=dev)
+    weight = torch.empty((V, d), dtype=torch.bfloat16, device=dev)
+    syn.fill_bf16_cuda(hidden.view(N * T, d), SEED, "hidden", g0 * K * T)
+    syn.fill_bf16_cuda(weight, SEED, "weight", 0)  # the model's LM head: replicated on every rank
+    tokens = torch.from_numpy(gi["tokens"]).to(dev)
+    mask = torch.from_numpy(gi["mask"]).to(dev)
+    ref = torch.from_numpy(gi["ref_logp"]).to(dev)
+    rew = torch.from_numpy(gi["log_reward"]).to(dev)
+    ws = torch.empty(tba.lmhead_workspace_bytes(N, T, V), dtype=torch.uint8, device=dev)
+    out = tba.ops._Fwd(N, K, dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step():
+        tba.lmhead_vargrad_fwd(hidden, weight, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
+                               check_status=False)
+        if group is not None:
+            dist.all_reduce(out.partial, group=group)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if group is not None:
+        dist.barrier()
+    try:
+        smi_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        smi_id = str(dev.index)
+    t0, t1 = ev(), ev()
+    with Clocks(smi_id) as clk:
+        torch.cuda.synchronize()
+        if group is not None:
+            dist.barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
+    if group is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+    ms = ms.item()
+    loss = out.partial[0].item()
+    rows = N * T
+    valid = int(gi["mask"].sum())
+
+    # unfused comparison on the same inputs: cuBLAS writes the logits, then the logits-path forward
+    variants = {}
+    if rank == 0 and world == 1 and not args.no_variants:
+        logits = torch.empty((N, T, V), dtype=torch.bfloat16, device=dev)
+
+        def unfused(mm_only=False):
+            torch.matmul(hidden.view(rows, d), weight.T, out=logits.view(rows, V))
+            if not mm_only:
+                tba.vargrad_fwd(logits, tokens, mask, ref, rew, w.beta, K, n_global, check_status=False)
+        for _ in range(2):
+            unfused()
+        res = {}
+        for key, mm in (("matmul_ms", True), ("ms_per_step", False)):
+            a, b = ev(), ev()
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(max(3, args.steps // 4)):
+                unfused(mm)
+            b.record(stream)
+            torch.cuda.synchronize()
+            res[key] = a.elapsed_time(b) / max(3, args.steps // 4)
+        variants["unfused_cublas_logits"] = {
+            **res, "value": valid / (res["ms_per_step"] / 1e3), "unit": "tokens/s",
+            "what": "torch.matmul (cuBLAS bf16) writes the [rows, V] logits, then tba_vargrad_tb_loss_fwd reads them",
+            "logits_bytes_written_and_read": rows * V * 2}
+        del logits
+
+    e2e = None
+    if not args.no_e2e:
+        h_hidden = torch.empty(hidden.shape, dtype=torch.bfloat16, pin_memory=True)
+        h_hidden.copy_(hidden)
+        h_tok, h_mask = tokens.cpu().pin_memory(), mask.cpu().pin_memory()
+        h_ref, h_rew = ref.cpu().pin_memory(), rew.cpu().pin_memory()
+        h_loss = torch.empty(1, dtype=torch.float64, pin_memory=True)
+        h2d = sum(t.numel() * t.element_size() for t in (h_hidden, h_tok, h_mask, h_ref, h_rew))
+
+        def e2e_step():
+            hidden.copy_(h_hidden, non_blocking=True)
+            tokens.copy_(h_tok, non_blocking=True)
+            mask.copy_(h_mask, non_blocking=True)
+            ref.copy_(h_ref, non_blocking=True)
+            rew.copy_(h_rew, non_blocking=True)
+            step()
+            h_loss.copy_(out.partial[:1], non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if group is not None:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX, group=group)
+        e_ms = e_ms.item()
+        e2e = {"value": valid * world / (e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 8, "ms_per_step": e_ms, "steps": args.e2e_steps,
+               "path": "pinned host hidden states -> cudaMemcpyAsync -> tba_lmhead_tb_loss_fwd (C ABI) -> loss D2H; "
+                       "the LM-head weight stays resident (a model parameter)"}
+        assert abs(h_loss.item() - loss) <= 1e-12 * max(1.0, abs(loss))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nr = 16
+        secs, nrows = oracle_lmhead_sample(w, nr)
+        cpu = {"value": nrows / secs, "unit": "tokens/s", "cores": int(os.environ.get("OMP_NUM_THREADS", "0")) or
+               len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"first {nr} rows x full vocabulary: oracle z = W h (fp64 NumPy matmul, multithreaded BLAS) "
+                         f"+ log-softmax, {secs:.1f} s (weight-row generation not timed)"}
+
+    if rank == 0:
+        peak, peak_sus, src = tensor_peak()
+        flops = 2.0 * rows * V * d
+        tf = flops / (ms / 1e3) / 1e12
+        line = {
+            "metric": baseline_metric() + " [LM-head-fused forward from hidden states, NEXT 3]",
+            "value": valid * world / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (tba_synth hidden states / LM-head weight, DESIGN.md §6)",
+            "config": {"workload": w.name, "objective": "lmhead", "note": w.note, "B_per_rank": B, "K": K, "T": T,
+                       "V": V, "d": d, "beta": w.beta, "rows_per_rank": rows,
+                       "parallelism": f"group-sharded x{world}",
+                       "l2": "weight 1.09 GB + hidden 0.47 GB per rank >> 126 MB L2; no flush needed"},
+            "roofline": {"bound": "tensor", "kernel": "lmhead_fwd (+ lmhead_combine, seq_head in the same timing)",
+                         "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                         "frac_of_sustained_peak": tf / peak_sus, "peak_source": src,
+                         "traffic": ncu_traffic(w.name, "lmhead_fwd"),
+                         "algorithmic_flops_per_launch": flops, "avg_launch_ms": ms},
+            "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu, "variants": variants,
+            "gpu_launches": args.steps * 3,  # lmhead_fwd, lmhead_combine, seq_head
+            "loss": loss,
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -184,8 +370,9 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
     ap.add_argument("--share-gpu", action="store_true")
-    ap.add_argument("--objective", default="vargrad", choices=["vargrad", "tbap"],
-                    help="vargrad: Eq. 5 (the north-star head); tbap: the TBA' token-level rule (Eq. 16)")
+    ap.add_argument("--objective", default="vargrad", choices=["vargrad", "tbap", "lmhead"],
+                    help="vargrad: Eq. 5 (the north-star head); tbap: the TBA' token-level rule (Eq. 16); "
+                         "lmhead: the Eq. 4/5 forward from hidden states with the LM head fused (NEXT 3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = syn.WORKLOADS[args.workload]
@@ -212,6 +399,8 @@ def main():
             dist.init_process_group(args.dist_backend)
         group = dist.group.WORLD
     tba.load_library()
+    if args.objective == "lmhead":
+        return lmhead_bench(args, w, tba, torch, dist, dev, world, rank, group)
     peer = tba.PeerReducer(group, dev) if (group is not None and args.collective == "peer") else None
 
     # ---- inputs: this rank's whole groups of the global batch, resident in HBM

@@ -22,7 +22,7 @@
 namespace tba {
 namespace {
 
-constexpr int LM_BM = 128, LM_BN = 256, LM_BK = 64, LM_STAGES = 4, LM_G = 4, LM_RB_SWZ = 16;
+constexpr int LM_BM = 128, LM_BN = 256, LM_BK = 64, LM_STAGES = 4, LM_G = 4, LM_RB_SWZ = 32;  // defaults (measured)
 constexpr int LM_A_BYTES = LM_BM * LM_BK * 2;  // 16 KB
 constexpr int LM_B_BYTES = LM_BN * LM_BK * 2;  // 32 KB
 constexpr int LM_STAGE_BYTES = LM_A_BYTES + LM_B_BYTES;
@@ -49,6 +49,27 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// The same load multicast to the CTAs of `mask` (same shared offset in each; each destination's
+// mbarrier at `bar`'s offset receives the complete_tx).
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                               uint16_t mask, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "h"(mask), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -59,6 +80,15 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// Commit arriving on the barrier at `bar`'s offset in every CTA of `mask`.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -83,20 +113,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 struct LmGrid {
   int64_t rows, V;
   int n_rb, n_tiles, n_groups, nkb;
+  int G, swz;  // vocab tiles per item, row blocks per raster super-row
   int64_t n_items;
 };
 
 // item -> (row block, vocab group): super-rows of LM_RB_SWZ row blocks, groups outer.
 __device__ __forceinline__ void lm_item(const LmGrid& g, int64_t item, int& rb, int& grp) {
-  const int64_t per_super = (int64_t)LM_RB_SWZ * g.n_groups;
+  const int64_t per_super = (int64_t)g.swz * g.n_groups;
   const int sup = (int)(item / per_super);
   const int64_t w = item - (int64_t)sup * per_super;
-  const int rb0 = sup * LM_RB_SWZ;
-  const int nrb = (g.n_rb - rb0) < LM_RB_SWZ ? (g.n_rb - rb0) : LM_RB_SWZ;
+  const int rb0 = sup * g.swz;
+  const int nrb = (g.n_rb - rb0) < g.swz ? (g.n_rb - rb0) : g.swz;
   grp = (int)(w / nrb);
   rb = rb0 + (int)(w % nrb);
 }
 
+// MC = 1: one CTA per work item. MC = 2: a cluster of two CTAs takes row blocks 2u and 2u+1 of the
+// same vocabulary tiles; each CTA loads half of every weight tile and multicasts it to both, so
+// the weight is read from L2 once per pair (1/3 less L2 -> SM traffic). Each CTA's MMA frees a
+// stage in both CTAs (multicast commit): a producer refills a stage only when both have used it.
+template <int MC>
 __global__ void __launch_bounds__(LM_THREADS, 1)
     lmhead_fwd(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
                const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
@@ -111,11 +147,13 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = MC > 1 ? cluster_ctarank() : 0u;
+  const int64_t unit0 = blockIdx.x / MC, n_units = gridDim.x / MC;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < LM_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -131,6 +169,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // the partner's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -143,18 +182,24 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_h));
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t it = blockIdx.x; it < g.n_items; it += gridDim.x) {
+      for (int64_t it = unit0; it < g.n_items; it += n_units) {
         int rb, grp;
         lm_item(g, it, rb, grp);
-        const int t0 = grp * LM_G, t1 = min(g.n_tiles, t0 + LM_G);
+        rb = rb * MC + (int)crank;
+        const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
         for (int t = t0; t < t1; ++t) {
           for (int kb = 0; kb < g.nkb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1u);
             mbar_expect_tx(&full[stage], LM_STAGE_BYTES);
             tma_load_2d(smem_u32(sA + stage * LM_A_BYTES), &tmH, kb * LM_BK, rb * LM_BM, smem_u32(&full[stage]),
                         pol_h);
-            tma_load_2d(smem_u32(sB + stage * LM_B_BYTES), &tmW, kb * LM_BK, t * LM_BN, smem_u32(&full[stage]),
-                        pol_w);
+            if (MC == 1)
+              tma_load_2d(smem_u32(sB + stage * LM_B_BYTES), &tmW, kb * LM_BK, t * LM_BN, smem_u32(&full[stage]),
+                          pol_w);
+            else
+              tma_load_2d_mc(smem_u32(sB + stage * LM_B_BYTES + crank * (LM_B_BYTES / MC)), &tmW, kb * LM_BK,
+                             t * LM_BN + (int)crank * (LM_BN / MC), smem_u32(&full[stage]), (uint16_t)((1u << MC) - 1),
+                             pol_w);
             if (++stage == LM_STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -168,10 +213,11 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t j = 0;  // accumulator tile counter
-      for (int64_t it = blockIdx.x; it < g.n_items; it += gridDim.x) {
+      for (int64_t it = unit0; it < g.n_items; it += n_units) {
         int rb, grp;
         lm_item(g, it, rb, grp);
-        const int t0 = grp * LM_G, t1 = min(g.n_tiles, t0 + LM_G);
+        rb = rb * MC + (int)crank;
+        const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
         for (int t = t0; t < t1; ++t, ++j) {
           const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
           mbar_wait(&tempty[acc], aph ^ 1u);
@@ -185,7 +231,8 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < LM_BK / 16; ++k)  // K = 16 per MMA: +32 bytes = +2 in the address field
               umma_bf16(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
-            umma_commit(&empty[stage]);
+            if (MC == 1) umma_commit(&empty[stage]);
+            else umma_commit_mc(&empty[stage], (uint16_t)((1u << MC) - 1));
             if (++stage == LM_STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -201,10 +248,11 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const float sc = rs.sc;
     uint32_t j = 0;
-    for (int64_t it = blockIdx.x; it < g.n_items; it += gridDim.x) {
+    for (int64_t it = unit0; it < g.n_items; it += n_units) {
       int rb, grp;
       lm_item(g, it, rb, grp);
-      const int t0 = grp * LM_G, t1 = min(g.n_tiles, t0 + LM_G);
+      rb = rb * MC + (int)crank;
+      const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
       const int64_t row = (int64_t)rb * LM_BM + row_in;
       const bool in_rows = row < g.rows;
       const int64_t y = in_rows ? tokens[row] : -1;
@@ -259,6 +307,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     }
   }
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // no CTA leaves while its partner may still write into it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -329,42 +378,82 @@ bool make_map(CUtensorMap* m, const void* base, int64_t n_rows, int64_t d, int64
 
 }  // namespace
 
+// A/B knobs (read once): TBA_LM_G vocab tiles per work item (>= LM_G keeps the workspace bound),
+// TBA_LM_SWZ row blocks per raster super-row.
+int lm_g() {
+  static int g = [] { int v = env_int("TBA_LM_G", LM_G); return v >= LM_G ? v : LM_G; }();
+  return g;
+}
+int lm_swz() {
+  static int v = [] { int x = env_int("TBA_LM_SWZ", LM_RB_SWZ); return x >= 1 ? x : LM_RB_SWZ; }();
+  return v;
+}
+
 size_t lmhead_partial_bytes(int64_t rows, int64_t V) {
-  const int64_t groups = ((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G;
+  const int64_t groups = ((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G;  // the most groups any G >= LM_G makes
   return align_up((size_t)groups * (size_t)rows * sizeof(float2), 256) + align_up((size_t)rows * sizeof(float), 256);
+}
+
+int lm_mc() {
+  static int v = [] { int x = env_int("TBA_LM_MC", 1); return x == 2 ? 2 : 1; }();
+  return v;
 }
 
 int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
                        cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
+  const int mc = lm_mc();
+  const int n_rb = (int)((rows + LM_BM - 1) / LM_BM);
   LmGrid g;
   g.rows = rows;
   g.V = x->vocab;
-  g.n_rb = (int)((rows + LM_BM - 1) / LM_BM);
+  g.n_rb = (n_rb + mc - 1) / mc;  // row-block units (pairs when mc = 2)
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
-  g.n_groups = (g.n_tiles + LM_G - 1) / LM_G;
+  g.G = lm_g();
+  g.swz = lm_swz();
+  g.n_groups = (g.n_tiles + g.G - 1) / g.G;
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
   g.n_items = (int64_t)g.n_rb * g.n_groups;
   CUtensorMap mh, mw;
   if (!make_map(&mh, x->hidden, rows, x->d, x->hidden_stride, LM_BM) ||
-      !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN))
+      !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN / mc))
     return TBA_ERR_CUDA;
   float2* part = static_cast<float2*>(part_ws);
   float* zy = reinterpret_cast<float*>(static_cast<char*>(part_ws) +
                                        align_up((size_t)g.n_groups * (size_t)rows * sizeof(float2), 256));
-  static bool attr[64] = {};  // per device; benign race: idempotent
+  static bool attr[2][64] = {};  // per variant and device; benign race: idempotent
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
-  if (!attr[dev]) {
-    if (cudaFuncSetAttribute(lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM) != cudaSuccess)
+  auto kern = mc == 2 ? lmhead_fwd<2> : lmhead_fwd<1>;
+  if (!attr[mc - 1][dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM) != cudaSuccess)
       return TBA_ERR_CUDA;
-    attr[dev] = true;
+    if (mc > 1 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
+      return TBA_ERR_CUDA;
+    attr[mc - 1][dev] = true;
   }
-  int64_t grid = device_sms();
-  if (grid > g.n_items) grid = g.n_items;
-  lmhead_fwd<<<(unsigned)grid, LM_THREADS, LM_SMEM, s>>>(mh, mw, g, x->tokens, x->mask, rs, part, zy);
-  if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.blockDim = dim3(LM_THREADS);
+  cfg.dynamicSmemBytes = LM_SMEM;
+  cfg.stream = s;
+  int64_t units = device_sms() / mc;
+  if (mc > 1) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = mc;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((unsigned)(units * mc));
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0 && ncl < units) units = ncl;
+  }
+  if (units > g.n_items) units = g.n_items;
+  cfg.gridDim = dim3((unsigned)(units * mc));
+  if (cudaLaunchKernelEx(&cfg, kern, mh, mw, g, x->tokens, x->mask, rs, part, zy) != cudaSuccess)
+    return TBA_ERR_CUDA;
   const int64_t blocks = (rows + 255) / 256 < 4096 ? (rows + 255) / 256 : 4096;
   lmhead_combine<<<(unsigned)blocks, 256, 0, s>>>(part, zy, rows, g.n_groups, x->vocab, x->tokens, x->mask, rs,
                                                   w.stats, w.lp, dev_status);
