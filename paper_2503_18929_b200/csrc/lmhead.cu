@@ -128,6 +128,76 @@ __device__ __forceinline__ void lm_item(const LmGrid& g, int64_t item, int& rb, 
   rb = rb0 + (int)(w % nrb);
 }
 
+// One work item of the epilogue (one row per thread): fold the item's vocabulary tiles into an
+// online (reference, sum) state, gather z[y], release each accumulator, write the item partial.
+// tempty_addr: the accumulator-empty barriers (shared::cluster address when `cluster_arrive`,
+// i.e. the leader CTA's barrier in the 2-SM kernel).
+__device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int grp, uint32_t& j, uint32_t tmem_lane,
+                                                 int row_in, int lane, uint64_t* tfull, uint32_t tempty_addr,
+                                                 bool cluster_arrive, const int64_t* __restrict__ tokens,
+                                                 const RowScale& rs, float2* __restrict__ part,
+                                                 float* __restrict__ zy_out) {
+  const float sc = rs.sc;
+  const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
+  const int64_t row = (int64_t)rb * LM_BM + row_in;
+  const bool in_rows = row < g.rows;
+  const int64_t y = in_rows ? tokens[row] : -1;
+  float R = -INFINITY;  // reference in logit units (a running max, moved only by > slack)
+  double S = 0.0;       // sum of 2^((z - R) * sc)
+  float zy = 0.f;
+  bool found = false;
+  for (int t = t0; t < t1; ++t, ++j) {
+    const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+    mbar_wait(&tfull[acc], aph);
+    tc_fence_after();
+    const int64_t nb = (int64_t)t * LM_BN;
+#pragma unroll 1
+    for (int c = 0; c < LM_BN / 32; ++c) {
+      float v[32];
+      tmem_ld32(tmem_lane + acc * LM_BN + c * 32, v);
+      const int64_t n0 = nb + c * 32;
+      const int64_t lim = g.V - n0;  // columns [0, lim) of this chunk are in the vocabulary
+      const int64_t dy = y - n0;
+      float cm = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (dy == i) {
+          zy = v[i];
+          found = true;
+        }
+        v[i] = (i < lim) ? v[i] : -INFINITY;
+        cm = fmaxf(cm, v[i]);
+      }
+      if (cm > R + rs.slack) {  // re-base (rare): exact fp64 rescale of the running sum
+        S = (R == -INFINITY) ? 0.0 : S * exp2(((double)R - (double)cm) * (double)sc);
+        R = cm;
+      }
+      // 2^((z - R) sc): the difference is exact for the terms that matter, so the scale's
+      // rounding never multiplies the row's full log-sum-exp. Pairwise sum (~5 ulp) -> fp64.
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = ex2((v[i] - R) * sc);
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) v[i] += v[i + w];
+      S += (double)v[0];
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t bar = tempty_addr + acc * 8u;
+      if (cluster_arrive)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+      else
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    }
+  }
+  if (in_rows) {
+    part[(int64_t)grp * g.rows + row] = make_float2(R, (float)S);
+    if (found) zy_out[row] = zy;
+  }
+}
+
 // MC = 1: one CTA per work item. MC = 2: a cluster of two CTAs takes row blocks 2u and 2u+1 of the
 // same vocabulary tiles; each CTA loads half of every weight tile and multicasts it to both, so
 // the weight is read from L2 once per pair (1/3 less L2 -> SM traffic). Each CTA's MMA frees a
@@ -246,64 +316,13 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     const int q = warp & 3;
     const int row_in = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const float sc = rs.sc;
     uint32_t j = 0;
     for (int64_t it = unit0; it < g.n_items; it += n_units) {
       int rb, grp;
       lm_item(g, it, rb, grp);
       rb = rb * MC + (int)crank;
-      const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
-      const int64_t row = (int64_t)rb * LM_BM + row_in;
-      const bool in_rows = row < g.rows;
-      const int64_t y = in_rows ? tokens[row] : -1;
-      float R = -INFINITY;  // reference in logit units (a running max, moved only by > slack)
-      double S = 0.0;       // sum of 2^((z - R) * sc)
-      float zy = 0.f;
-      bool found = false;
-      for (int t = t0; t < t1; ++t, ++j) {
-        const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        const int64_t nb = (int64_t)t * LM_BN;
-#pragma unroll 1
-        for (int c = 0; c < LM_BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(tmem + lane_addr + acc * LM_BN + c * 32, v);
-          const int64_t n0 = nb + c * 32;
-          const int64_t lim = g.V - n0;  // columns [0, lim) of this chunk are in the vocabulary
-          const int64_t dy = y - n0;
-          float cm = -INFINITY;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (dy == i) {
-              zy = v[i];
-              found = true;
-            }
-            v[i] = (i < lim) ? v[i] : -INFINITY;
-            cm = fmaxf(cm, v[i]);
-          }
-          if (cm > R + rs.slack) {  // re-base (rare): exact fp64 rescale of the running sum
-            S = (R == -INFINITY) ? 0.0 : S * exp2(((double)R - (double)cm) * (double)sc);
-            R = cm;
-          }
-          // 2^((z - R) sc): the difference is exact for the terms that matter, so the scale's
-          // rounding never multiplies the row's full log-sum-exp. Pairwise sum (~5 ulp) -> fp64.
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = ex2((v[i] - R) * sc);
-#pragma unroll
-          for (int w = 16; w >= 1; w >>= 1)
-#pragma unroll
-            for (int i = 0; i < w; ++i) v[i] += v[i + w];
-          S += (double)v[0];
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-      }
-      if (in_rows) {
-        part[(int64_t)grp * g.rows + row] = make_float2(R, (float)S);
-        if (found) zy_out[row] = zy;
-      }
+      lm_epilogue_item(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, smem_u32(tempty), false, tokens, rs,
+                       part, zy_out);
     }
   }
   __syncthreads();
@@ -311,6 +330,171 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// cta_group::2 variant: an SM pair (cluster of 2) computes a 256 x 256 logit tile per MMA
+// (M = 256 across the pair: each CTA holds its 128 hidden rows and half of the weight tile in
+// shared memory, and its 128 accumulator rows in its own TMEM). Per SM and stage only 32 KB
+// (16 KB hidden + 16 KB weight) are loaded and read by the tensor core, 2/3 of the single-SM
+// kernel's operand traffic. Both CTAs' TMA loads signal the leader's full barrier; the leader's
+// lane issues the MMA and its commits arrive on both CTAs' barriers (multicast); the four
+// epilogue warps of both CTAs release an accumulator on the leader's barrier (count 8).
+constexpr int L2_STAGES = 6;
+constexpr int L2_A_BYTES = LM_BM * LM_BK * 2;        // 16 KB: this CTA's 128 hidden rows
+constexpr int L2_B_BYTES = (LM_BN / 2) * LM_BK * 2;  // 16 KB: this CTA's half of the weight tile
+constexpr int L2_STAGE_BYTES = L2_A_BYTES + L2_B_BYTES;
+constexpr size_t L2_SMEM = 1024 + (size_t)L2_STAGES * L2_STAGE_BYTES + 256;
+constexpr uint32_t L2_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
+                              ((uint32_t)((2 * LM_BM) >> 4) << 24);
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address -> the leader CTA's copy
+
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & kPeerBitMask), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(L2_IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(LM_THREADS, 1)
+    lmhead_fwd_2sm(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
+                   const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
+                   float2* __restrict__ part, float* __restrict__ zy_out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + L2_STAGES * L2_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L2_STAGES * L2_STAGE_BYTES);
+  uint64_t* empty = full + L2_STAGES;
+  uint64_t* tfull = empty + L2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int64_t unit0 = blockIdx.x / 2, n_units = gridDim.x / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L2_STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+      uint64_t pol_w, pol_h;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_w));
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_h));
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t it = unit0; it < g.n_items; it += n_units) {
+        int rb, grp;
+        lm_item(g, it, rb, grp);
+        rb = rb * 2 + (int)crank;
+        const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
+        for (int t = t0; t < t1; ++t) {
+          for (int kb = 0; kb < g.nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            if (leader) mbar_expect_tx(&full[stage], 2 * L2_STAGE_BYTES);
+            tma_load_2d_pair(smem_u32(sA + stage * L2_A_BYTES), &tmH, kb * LM_BK, rb * LM_BM, smem_u32(&full[stage]),
+                             pol_h);
+            tma_load_2d_pair(smem_u32(sB + stage * L2_B_BYTES), &tmW, kb * LM_BK, t * LM_BN + (int)crank * (LM_BN / 2),
+                             smem_u32(&full[stage]), pol_w);
+            if (++stage == L2_STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---- MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t j = 0;
+      for (int64_t it = unit0; it < g.n_items; it += n_units) {
+        int rb, grp;
+        lm_item(g, it, rb, grp);
+        const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
+        for (int t = t0; t < t1; ++t, ++j) {
+          const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+          mbar_wait(&tempty[acc], aph ^ 1u);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + acc * LM_BN;
+          for (int kb = 0; kb < g.nkb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * L2_A_BYTES));
+            const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * L2_B_BYTES));
+#pragma unroll
+            for (int k = 0; k < LM_BK / 16; ++k) umma_bf16_pair(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+            umma_commit_pair(&empty[stage]);
+            if (++stage == L2_STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          umma_commit_pair(&tfull[acc]);
+        }
+      }
+    }
+  } else {  // ---- epilogue (both CTAs): release on the leader's tempty
+    const int q = warp & 3;
+    const int row_in = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    uint32_t tempty_leader;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(tempty_leader) : "r"(smem_u32(tempty)));
+    uint32_t j = 0;
+    for (int64_t it = unit0; it < g.n_items; it += n_units) {
+      int rb, grp;
+      lm_item(g, it, rb, grp);
+      rb = rb * 2 + (int)crank;
+      lm_epilogue_item(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, tempty_leader, true, tokens, rs, part,
+                       zy_out);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -394,8 +578,9 @@ size_t lmhead_partial_bytes(int64_t rows, int64_t V) {
   return align_up((size_t)groups * (size_t)rows * sizeof(float2), 256) + align_up((size_t)rows * sizeof(float), 256);
 }
 
+// TBA_LM_MC: 1 single-SM kernel, 2 cluster pair with weight multicast, 3 cta_group::2 pair.
 int lm_mc() {
-  static int v = [] { int x = env_int("TBA_LM_MC", 1); return x == 2 ? 2 : 1; }();
+  static int v = [] { int x = env_int("TBA_LM_MC", 1); return (x == 2 || x == 3) ? x : 1; }();
   return v;
 }
 
@@ -403,7 +588,8 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
                        cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
-  const int mc = lm_mc();
+  const int mode = lm_mc();
+  const int mc = mode == 1 ? 1 : 2;  // CTAs per cluster
   const int n_rb = (int)((rows + LM_BM - 1) / LM_BM);
   LmGrid g;
   g.rows = rows;
@@ -422,21 +608,20 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   float2* part = static_cast<float2*>(part_ws);
   float* zy = reinterpret_cast<float*>(static_cast<char*>(part_ws) +
                                        align_up((size_t)g.n_groups * (size_t)rows * sizeof(float2), 256));
-  static bool attr[2][64] = {};  // per variant and device; benign race: idempotent
+  static bool attr[3][64] = {};  // per variant and device; benign race: idempotent
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
-  auto kern = mc == 2 ? lmhead_fwd<2> : lmhead_fwd<1>;
-  if (!attr[mc - 1][dev]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM) != cudaSuccess)
+  auto kern = mode == 3 ? lmhead_fwd_2sm : mode == 2 ? lmhead_fwd<2> : lmhead_fwd<1>;
+  const size_t smem = mode == 3 ? L2_SMEM : LM_SMEM;
+  if (!attr[mode - 1][dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return TBA_ERR_CUDA;
-    if (mc > 1 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
-      return TBA_ERR_CUDA;
-    attr[mc - 1][dev] = true;
+    attr[mode - 1][dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.blockDim = dim3(LM_THREADS);
-  cfg.dynamicSmemBytes = LM_SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   int64_t units = device_sms() / mc;
   if (mc > 1) {
