@@ -9,4 +9,6 @@ timeout 600 python bench.py --objective tbap --steps 20 --warmup 5 --no-cpu-base
 tail -c 600 gpurun_out/bench_${TAG}_qwen_shard_tbap.json
 bash scripts/gpu_sanitize.sh
 for w in qwen_shard rhomath pythia redteam; do timeout 600 python bench.py --workload $w --schedule deferred --steps 20 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/bench_${TAG}_${w}_deferred.json 2>/dev/null; done
+bash scripts/gpu_lmhead.sh $TAG > /dev/null 2>&1
+tail -c 300 gpurun_out/bench_${TAG}_qwen_shard_lmhead.json
 timeout 600 python bench.py --workload toy --cuda-graph --steps 50 --warmup 10 --no-e2e --no-cpu-baseline > gpurun_out/bench_${TAG}_toy_graph.json 2>/dev/null

@@ -78,6 +78,7 @@ def main(tag):
         lines.append("")
     dp = os.path.join(G, f"dram_{tag}.csv")
     traffic = {}
+    traffic_lm = None
     if os.path.exists(dp):
         D = read_metric_csv(dp)
         agg = {}
@@ -93,10 +94,30 @@ def main(tag):
             lines.append(f"| {k} | {r / 1e9:.3f} | {w / 1e9:.3f} | {t / 1e3:.1f} | {(r + w) / t:.0f} |")
             traffic[k] = r + w
         lines.append("")
+    lmp = os.path.join(G, f"lmhead_launches_{tag}.csv")
+    if os.path.exists(lmp):
+        M = read_metric_csv(lmp)
+        agg = {}
+        for d in M:
+            agg.setdefault(short(d["Kernel Name"]), {}).setdefault(d["Metric Name"], []).append(float(d["Metric Value"]))
+        tot = sum(statistics.mean(m.get("gpu__time_duration.sum", [0])) for m in agg.values()) or 1
+        lines += ["## LM-head-fused forward (NEXT 3): launch list and DRAM bytes (full Qwen shard, "
+                  "`bench.py --objective lmhead`)", "",
+                  "| kernel | launches | mean µs | share of step | read GB | write GB |", "|---|---|---|---|---|---|"]
+        for k, m in sorted(agg.items(), key=lambda kv: -statistics.mean(kv[1].get("gpu__time_duration.sum", [0]))):
+            t = statistics.mean(m.get("gpu__time_duration.sum", [0]))
+            r = statistics.mean(m.get("dram__bytes_read.sum", [0]))
+            w = statistics.mean(m.get("dram__bytes_write.sum", [0]))
+            lines.append(f"| {k} | {len(m.get('gpu__time_duration.sum', []))} | {t / 1e3:.1f} | {t / tot:.3f} | "
+                         f"{r / 1e9:.3f} | {w / 1e9:.3f} |")
+            if k == "lmhead_fwd":
+                traffic_lm = r + w
+        lines.append("")
     for rep in sorted(f for f in os.listdir(G) if f.startswith("prof_") and f.endswith(f"_{tag}.ncu-rep")):
         det, raw = ncu_details(os.path.join(G, rep))
         kname = rep[len("prof_"):-len(f"_{tag}.ncu-rep")]
-        lines += [f"## `{kname}` — ncu --set full (qwen_group slice)", ""]
+        where = "full Qwen shard, bench --objective lmhead" if kname.startswith("lmhead") else "qwen_group slice"
+        lines += [f"## `{kname}` — ncu --set full ({where})", ""]
         for key in ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "Executed Ipc Active",
                     "Issue Slots Busy", "Registers Per Thread", "Theoretical Occupancy", "Achieved Occupancy",
                     "Warp Cycles Per Issued Instruction", "L2 Hit Rate", "SM Frequency"]:
@@ -106,7 +127,10 @@ def main(tag):
         for key in ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
                     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
                     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
-                    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]:
+                    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+                    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                    "lts__t_sector_hit_rate.pct"]:
             if key in raw:
                 lines.append(f"- {key}: {raw[key]}")
         stalls = []
@@ -124,8 +148,10 @@ def main(tag):
     open(os.path.join(P, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
     tp = os.path.join(P, "ncu_traffic.json")
     cur = json.load(open(tp)) if os.path.exists(tp) else {}
+    if traffic_lm is not None:
+        traffic["lmhead_fwd"] = traffic_lm
     if traffic:
-        cur["qwen_shard"] = {k: v for k, v in traffic.items()}
+        cur["qwen_shard"] = {**cur.get("qwen_shard", {}), **traffic}
         cur["_source"] = f"profiles/{tag}_summary.md (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch)"
         json.dump(cur, open(tp, "w"), indent=1)
     print("\n".join(lines))

@@ -40,9 +40,24 @@ for w in cases:
     tba.tbap_fwd(lg, tok, mask, gen, ref, rew, w.beta, w.K, "clip", 0.0, 8.0, ntok, grad_unscaled=G)
     of, _, df, _ = tba.vargrad_fused(lg, tok, mask, ref, rew, w.beta, w.K, float(w.N), check_status=True)
     od, _, Gd = tba.vargrad_fwd_deferred(lg, tok, mask, ref, rew, w.beta, w.K, float(w.N), check_status=True)
+    op, _, dp, _ = tba.vargrad_pipelined(lg, tok, mask, ref, rew, w.beta, w.K, float(w.N), groups_per_chunk=1,
+                                         check_status=True)
     torch.cuda.synchronize()
+    assert torch.equal(op.partial, o.partial) and torch.equal(dp, d)
     s2 = float(db.float().sum().item() + G.float().sum().item() + df.float().sum().item() + Gd.float().sum().item())
     s = float(d.float().sum().item())  # reads every dlogits element (initcheck)
     print(w.name, w.V, "loss", o.partial[0].item(), "sum dlogits", s, "seq_logprob match",
           torch.equal(sl, o.seq_logp), "other paths", s2, torch.equal(of.partial, o.partial))
+# LM-head-fused forward (tcgen05 + TMA kernel): ragged rows / vocab / d tails
+wl = dataclasses.replace(syn.WORKLOADS["toy"], B=2, K=4, T=37, V=1000, d=200, len_lo=0, len_hi=37)
+gl = syn.group_inputs(wl, 2, 0, wl.B)
+hid = torch.empty((wl.N, wl.T, wl.d), dtype=torch.bfloat16, device="cuda")
+wt = torch.empty((wl.V, wl.d), dtype=torch.bfloat16, device="cuda")
+syn.fill_bf16_cuda(hid.view(wl.N * wl.T, wl.d), 2, "hidden", 0)
+syn.fill_bf16_cuda(wt, 2, "weight", 0)
+ol, _ = tba.lmhead_vargrad_fwd(hid, wt, torch.from_numpy(gl["tokens"]).cuda(), torch.from_numpy(gl["mask"]).cuda(),
+                               torch.from_numpy(gl["ref_logp"]).cuda(), torch.from_numpy(gl["log_reward"]).cuda(),
+                               wl.beta, wl.K, float(wl.N), check_status=True)
+torch.cuda.synchronize()
+print("lmhead loss", ol.partial[0].item())
 print("sanitize cases done")
