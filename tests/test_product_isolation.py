@@ -62,4 +62,5 @@ def test_bench_uses_oracle_only_in_baseline_legs():
             for n in ast.walk(fn):
                 if isinstance(n, ast.ImportFrom) and n.module and n.module.startswith("oracle"):
                     users.add(fn.name)
-    assert users == {"oracle_sample"}
+    # the two bounded-sample timers of the cpu_baseline legs / --impl reference arm
+    assert users == {"oracle_sample", "oracle_lmhead_sample"}
