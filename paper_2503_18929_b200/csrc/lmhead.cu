@@ -114,8 +114,16 @@ struct LmGrid {
   int64_t rows, V;
   int n_rb, n_tiles, n_groups, nkb;
   int G, swz;  // vocab tiles per item, row blocks per raster super-row
+  int pol;     // L2 policy bits: 1 = weight loads evict_last, 2 = hidden loads evict_last
   int64_t n_items;
 };
+
+__device__ __forceinline__ uint64_t l2_policy(int last) {
+  uint64_t p;
+  if (last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 // item -> (row block, vocab group): super-rows of LM_RB_SWZ row blocks, groups outer.
 __device__ __forceinline__ void lm_item(const LmGrid& g, int64_t item, int& rb, int& grp) {
@@ -247,9 +255,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     if (lane == 0) {  // ---- TMA producer
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-      uint64_t pol_w, pol_h;
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_w));
-      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_h));
+      const uint64_t pol_w = l2_policy(g.pol & 1), pol_h = l2_policy(g.pol & 2);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t it = unit0; it < g.n_items; it += n_units) {
@@ -418,9 +424,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     if (lane == 0) {  // ---- TMA producer (both CTAs)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-      uint64_t pol_w, pol_h;
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_w));
-      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_h));
+      const uint64_t pol_w = l2_policy(g.pol & 1), pol_h = l2_policy(g.pol & 2);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t it = unit0; it < g.n_items; it += n_units) {
@@ -598,6 +602,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
   g.G = lm_g();
   g.swz = lm_swz();
+  g.pol = env_int("TBA_LM_POL", 1) & 3;
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
   g.n_items = (int64_t)g.n_rb * g.n_groups;
