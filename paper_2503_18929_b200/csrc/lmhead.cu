@@ -114,7 +114,7 @@ struct LmGrid {
   int64_t rows, V;
   int n_rb, n_tiles, n_groups, nkb;
   int G, swz;  // vocab tiles per item, row blocks per raster super-row
-  int pol;     // L2 policy bits: 1 = weight loads evict_last, 2 = hidden loads evict_last
+  int pol;     // L2 policy bits: 1 = weight loads evict_last, 2 = hidden loads evict_last, 4 = no hint (2-SM)
   int64_t n_items;
 };
 
@@ -356,12 +356,19 @@ constexpr uint32_t L2_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(L
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address -> the leader CTA's copy
 
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
-                                                 uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & kPeerBitMask), "l"(pol)
-      : "memory");
+                                                 uint64_t pol, bool hint) {
+  if (hint)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & kPeerBitMask), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & kPeerBitMask)
+        : "memory");
 }
 
 __device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
@@ -437,9 +444,9 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
             mbar_wait(&empty[stage], phase ^ 1u);
             if (leader) mbar_expect_tx(&full[stage], 2 * L2_STAGE_BYTES);
             tma_load_2d_pair(smem_u32(sA + stage * L2_A_BYTES), &tmH, kb * LM_BK, rb * LM_BM, smem_u32(&full[stage]),
-                             pol_h);
+                             pol_h, (g.pol & 4) == 0);
             tma_load_2d_pair(smem_u32(sB + stage * L2_B_BYTES), &tmW, kb * LM_BK, t * LM_BN + (int)crank * (LM_BN / 2),
-                             smem_u32(&full[stage]), pol_w);
+                             smem_u32(&full[stage]), pol_w, (g.pol & 4) == 0);
             if (++stage == L2_STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -602,7 +609,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
   g.G = lm_g();
   g.swz = lm_swz();
-  g.pol = env_int("TBA_LM_POL", 1) & 3;
+  g.pol = env_int("TBA_LM_POL", 1) & 7;
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
   g.n_items = (int64_t)g.n_rb * g.n_groups;
