@@ -119,3 +119,54 @@ def test_empty_batch_is_ok_without_gpu_work(L):
     x = _rows(n_seq=0, logits=0, tokens=0, mask=0)
     assert L.tba_seq_logprob(ctypes.byref(x), 0, 0, 0, None, None) == _lib.TBA_OK
     assert L.tba_vargrad_tb_loss_bwd(ctypes.byref(x), 0, 0, 1.0, None, 0, 0, 100, None) == _lib.TBA_OK
+
+
+def test_pipelined_validation(L):
+    x = _rows()
+    pipe = lambda xx, beta=1.0, K=4, ng=8.0, gs=0.25, ws=0x100000, out=FAKE + 0x1000, dt=0, ors=100: \
+        L.tba_tb_loss_pipelined(ctypes.byref(xx) if xx is not None else None, None, FAKE, FAKE, beta, K, ng, gs, 0,
+                                ws, FAKE, FAKE, FAKE, FAKE, FAKE, out, dt, ors, None, None, None, None)
+    assert pipe(x, beta=0.0) == _lib.TBA_ERR_INVALID_CONFIG
+    assert pipe(x, K=1) == _lib.TBA_ERR_INVALID_CONFIG
+    assert pipe(_rows(n_seq=6), ng=6.0) == _lib.TBA_ERR_INVALID_ARG
+    assert pipe(x, ng=4.0) == _lib.TBA_ERR_INVALID_ARG
+    assert pipe(x, gs=math.nan) == _lib.TBA_ERR_INVALID_ARG
+    assert pipe(x, dt=2) == _lib.TBA_ERR_INVALID_ARG
+    assert pipe(x, ors=99) == _lib.TBA_ERR_INVALID_ARG
+    assert pipe(x, ws=0x100010) == _lib.TBA_ERR_INVALID_ARG
+    assert pipe(None) == _lib.TBA_ERR_INVALID_ARG
+
+
+def _lm(**kw):
+    d = dict(hidden=FAKE, weight=FAKE, n_seq=8, seq_len=4, d=64, vocab=100, hidden_stride=64, weight_stride=64,
+             tokens=FAKE, mask=FAKE)
+    d.update(kw)
+    return _lib.TbaLmhead(**d)
+
+
+@pytest.mark.parametrize("kw", [dict(d=12), dict(d=4), dict(hidden_stride=60), dict(hidden_stride=68),
+                                dict(weight_stride=72 + 4), dict(hidden=FAKE + 8), dict(weight=FAKE + 2),
+                                dict(hidden=0), dict(tokens=0), dict(mask=0), dict(vocab=0), dict(vocab=2 ** 31),
+                                dict(n_seq=-1), dict(n_seq=2 ** 20, seq_len=2 ** 12), dict(tokens=FAKE + 4)])
+def test_lmhead_validation(L, kw):
+    x = _lm(**kw)
+    assert L.tba_lmhead_seq_logprob(ctypes.byref(x), 1.0, 0x100000, FAKE, FAKE, None, None) == \
+        _lib.TBA_ERR_INVALID_ARG
+    assert L.tba_lmhead_tb_loss_fwd(ctypes.byref(x), None, FAKE, FAKE, 1.0, 4, 8.0, 0x100000, FAKE, FAKE, FAKE, FAKE,
+                                    FAKE, None, None) == _lib.TBA_ERR_INVALID_ARG
+
+
+def test_lmhead_config_and_workspace(L):
+    x = _lm()
+    assert L.tba_lmhead_seq_logprob(ctypes.byref(x), 0.0, 0x100000, FAKE, FAKE, None, None) == \
+        _lib.TBA_ERR_INVALID_CONFIG
+    assert L.tba_lmhead_tb_loss_fwd(ctypes.byref(x), None, FAKE, FAKE, -1.0, 4, 8.0, 0x100000, FAKE, FAKE, FAKE,
+                                    FAKE, FAKE, None, None) == _lib.TBA_ERR_INVALID_CONFIG
+    assert L.tba_lmhead_seq_logprob(ctypes.byref(x), 1.0, 0x100010, FAKE, FAKE, None, None) == \
+        _lib.TBA_ERR_INVALID_ARG  # misaligned workspace
+    base = L.tba_workspace_bytes(64, 1024)
+    lm = L.tba_lmhead_workspace_bytes(64, 1024, 152064)
+    assert lm >= base + 65536 * 149 * 8 + 65536 * 4   # per-(row, group of 1024) partials + gathered logit
+    assert L.tba_lmhead_workspace_bytes(-1, 4, 10) == 0 and L.tba_lmhead_workspace_bytes(1, 4, 0) == 0
+    empty = _lm(n_seq=0, hidden=0, weight=0, tokens=0, mask=0)
+    assert L.tba_lmhead_seq_logprob(ctypes.byref(empty), 1.0, 0, 0, 0, None, None) == _lib.TBA_OK
