@@ -140,6 +140,10 @@ __device__ __forceinline__ void lm_item(const LmGrid& g, int64_t item, int& rb, 
 // online (reference, sum) state, gather z[y], release each accumulator, write the item partial.
 // tempty_addr: the accumulator-empty barriers (shared::cluster address when `cluster_arrive`,
 // i.e. the leader CTA's barrier in the 2-SM kernel).
+// Per element: one FFMA 2^(z sc - Rs) with Rs = fl(R sc) the exponent reference, one MUFU ex2,
+// one FMNMX (chunk max) and the pairwise FADD tree; the vocabulary-tail mask runs only in the
+// last tile and the z[y] gather only in the chunk that holds y. The partial is {R, S} with
+// S = sum 2^(z sc - fl(R sc)); lmhead_combine re-forms fl(R sc) with the same fp32 multiply.
 __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int grp, uint32_t& j, uint32_t tmem_lane,
                                                  int row_in, int lane, uint64_t* tfull, uint32_t tempty_addr,
                                                  bool cluster_arrive, const int64_t* __restrict__ tokens,
@@ -151,7 +155,8 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
   const bool in_rows = row < g.rows;
   const int64_t y = in_rows ? tokens[row] : -1;
   float R = -INFINITY;  // reference in logit units (a running max, moved only by > slack)
-  double S = 0.0;       // sum of 2^((z - R) * sc)
+  float Rs = -INFINITY; // fl(R sc): the exponent reference
+  double S = 0.0;       // sum of 2^(z sc - Rs)
   float zy = 0.f;
   bool found = false;
   for (int t = t0; t < t1; ++t, ++j) {
@@ -159,31 +164,41 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
     mbar_wait(&tfull[acc], aph);
     tc_fence_after();
     const int64_t nb = (int64_t)t * LM_BN;
+    const bool tail = nb + LM_BN > g.V;          // warp-uniform: only the last vocabulary tile
+    const int64_t dyt = y - nb;
+    const int cy = ((uint64_t)dyt < (uint64_t)LM_BN) ? (int)(dyt >> 5) : -1;  // chunk holding y, if any
 #pragma unroll 1
     for (int c = 0; c < LM_BN / 32; ++c) {
       float v[32];
       tmem_ld32(tmem_lane + acc * LM_BN + c * 32, v);
-      const int64_t n0 = nb + c * 32;
-      const int64_t lim = g.V - n0;  // columns [0, lim) of this chunk are in the vocabulary
-      const int64_t dy = y - n0;
-      float cm = -INFINITY;
+      if (tail) {
+        const int64_t lim = g.V - (nb + c * 32);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (dy == i) {
-          zy = v[i];
-          found = true;
-        }
-        v[i] = (i < lim) ? v[i] : -INFINITY;
-        cm = fmaxf(cm, v[i]);
+        for (int i = 0; i < 32; ++i) v[i] = (i < lim) ? v[i] : -INFINITY;
       }
+      if (c == cy) {
+        const int k = (int)(dyt & 31);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i == k) zy = v[i];
+        found = true;
+      }
+      float m[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) m[i] = fmaxf(v[i], v[i + 16]);
+#pragma unroll
+      for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) m[i] = fmaxf(m[i], m[i + w]);
+      const float cm = m[0];
       if (cm > R + rs.slack) {  // re-base (rare): exact fp64 rescale of the running sum
-        S = (R == -INFINITY) ? 0.0 : S * exp2(((double)R - (double)cm) * (double)sc);
+        const float Rs2 = cm * sc;
+        S = (R == -INFINITY) ? 0.0 : S * exp2((double)Rs - (double)Rs2);
         R = cm;
+        Rs = Rs2;
       }
-      // 2^((z - R) sc): the difference is exact for the terms that matter, so the scale's
-      // rounding never multiplies the row's full log-sum-exp. Pairwise sum (~5 ulp) -> fp64.
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = ex2((v[i] - R) * sc);
+      for (int i = 0; i < 32; ++i) v[i] = ex2(fmaf(v[i], sc, -Rs));
 #pragma unroll
       for (int w = 16; w >= 1; w >>= 1)
 #pragma unroll
@@ -519,10 +534,13 @@ __global__ void lmhead_combine(const float2* __restrict__ part, const float* __r
     if (!mask[r]) continue;
     float M = -INFINITY;  // logit units
     for (int k = 0; k < n_groups; ++k) M = fmaxf(M, part[(int64_t)k * rows + r].x);
-    double S = 0.0;  // sum over the vocabulary of 2^((z - M) sc)
+    // sum over the vocabulary of 2^((z - M) sc): group k's sum is relative to fl(R_k sc) (the
+    // kernel's fp32 product, re-formed identically here); M sc is exact in fp64
+    const double Msc = (double)M * (double)rs.sc;
+    double S = 0.0;
     for (int k = 0; k < n_groups; ++k) {
       const float2 p = part[(int64_t)k * rows + r];
-      S += (double)p.y * exp2(((double)p.x - (double)M) * (double)rs.sc);
+      S += (double)p.y * exp2((double)(p.x * rs.sc) - Msc);
     }
     const double l2s = log2(S);
     const int64_t y = tokens[r];
