@@ -329,7 +329,7 @@ def lmhead_bench(args, w, tba, torch, dist, dev, world, rank, group):
 
     if rank == 0:
         peak, peak_sus, src = tensor_peak()
-        flops = 2.0 * rows * V * d
+        flops = 2.0 * valid * V * d  # useful work: masked rows need no logits (whole masked row blocks are skipped)
         tf = flops / (ms / 1e3) / 1e12
         line = {
             "metric": baseline_metric() + " [LM-head-fused forward from hidden states, NEXT 3]",

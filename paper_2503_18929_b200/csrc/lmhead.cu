@@ -112,10 +112,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 struct LmGrid {
   int64_t rows, V;
-  int n_rb, n_tiles, n_groups, nkb;
+  const int* act;    // [units] the row-block units holding a valid row, ascending (lm_compact_units)
+  const int* n_act;  // [1] their number
+  int n_tiles, n_groups, nkb;
   int G, swz;  // vocab tiles per item, row blocks per raster super-row
   int pol;     // L2 policy bits: 1 = weight loads evict_last, 2 = hidden loads evict_last, 4 = no hint (2-SM)
-  int64_t n_items;
 };
 
 __device__ __forceinline__ uint64_t l2_policy(int last) {
@@ -125,15 +126,35 @@ __device__ __forceinline__ uint64_t l2_policy(int last) {
   return p;
 }
 
-// item -> (row block, vocab group): super-rows of LM_RB_SWZ row blocks, groups outer.
-__device__ __forceinline__ void lm_item(const LmGrid& g, int64_t item, int& rb, int& grp) {
+// item -> (active unit index, vocab group): super-rows of g.swz active units, groups outer.
+__device__ __forceinline__ void lm_item(const LmGrid& g, int nact, int64_t item, int& ui, int& grp) {
   const int64_t per_super = (int64_t)g.swz * g.n_groups;
   const int sup = (int)(item / per_super);
   const int64_t w = item - (int64_t)sup * per_super;
-  const int rb0 = sup * g.swz;
-  const int nrb = (g.n_rb - rb0) < g.swz ? (g.n_rb - rb0) : g.swz;
-  grp = (int)(w / nrb);
-  rb = rb0 + (int)(w % nrb);
+  const int u0 = sup * g.swz;
+  const int nu = (nact - u0) < g.swz ? (nact - u0) : g.swz;
+  grp = (int)(w / nu);
+  ui = u0 + (int)(w % nu);
+}
+
+// Does row-block unit `u` (MC row blocks of 128 rows) hold any valid row? Work items of units with
+// no valid row (the tail of short responses in ragged batches) are skipped by every role alike.
+__device__ __forceinline__ bool lm_unit_active(const uint8_t* __restrict__ mask, int u, int MCu, int64_t rows) {
+  const int64_t r0 = (int64_t)u * MCu * LM_BM;
+  const int64_t n = (int64_t)MCu * LM_BM;
+  const int64_t r1 = r0 + n < rows ? r0 + n : rows;
+  if (r1 - r0 == n && (reinterpret_cast<uintptr_t>(mask + r0) & 15) == 0) {
+    const uint4* p = reinterpret_cast<const uint4*>(mask + r0);
+    uint32_t acc = 0;
+    for (int i = 0; i < (int)(n / 16); ++i) {
+      const uint4 v = __ldg(p + i);
+      acc |= v.x | v.y | v.z | v.w;
+    }
+    return acc != 0;
+  }
+  for (int64_t r = r0; r < r1; ++r)
+    if (mask[r]) return true;
+  return false;
 }
 
 // One work item of the epilogue (one row per thread): fold the item's vocabulary tiles into an
@@ -242,6 +263,8 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = MC > 1 ? cluster_ctarank() : 0u;
   const int64_t unit0 = blockIdx.x / MC, n_units = gridDim.x / MC;
+  const int nact = *g.n_act;
+  const int64_t n_items = (int64_t)nact * g.n_groups;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < LM_STAGES; ++s) {
@@ -273,9 +296,10 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       const uint64_t pol_w = l2_policy(g.pol & 1), pol_h = l2_policy(g.pol & 2);
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t it = unit0; it < g.n_items; it += n_units) {
+      for (int64_t it = unit0; it < n_items; it += n_units) {
         int rb, grp;
-        lm_item(g, it, rb, grp);
+        lm_item(g, nact, it, rb, grp);
+        rb = g.act[rb];
         rb = rb * MC + (int)crank;
         const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
         for (int t = t0; t < t1; ++t) {
@@ -304,9 +328,10 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t j = 0;  // accumulator tile counter
-      for (int64_t it = unit0; it < g.n_items; it += n_units) {
+      for (int64_t it = unit0; it < n_items; it += n_units) {
         int rb, grp;
-        lm_item(g, it, rb, grp);
+        lm_item(g, nact, it, rb, grp);
+        rb = g.act[rb];
         rb = rb * MC + (int)crank;
         const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
         for (int t = t0; t < t1; ++t, ++j) {
@@ -338,9 +363,10 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     const int row_in = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint32_t j = 0;
-    for (int64_t it = unit0; it < g.n_items; it += n_units) {
+    for (int64_t it = unit0; it < n_items; it += n_units) {
       int rb, grp;
-      lm_item(g, it, rb, grp);
+      lm_item(g, nact, it, rb, grp);
+      rb = g.act[rb];
       rb = rb * MC + (int)crank;
       lm_epilogue_item(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, smem_u32(tempty), false, tokens, rs,
                        part, zy_out);
@@ -418,6 +444,8 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   const uint32_t crank = cluster_ctarank();
   const bool leader = crank == 0;
   const int64_t unit0 = blockIdx.x / 2, n_units = gridDim.x / 2;
+  const int nact = *g.n_act;
+  const int64_t n_items = (int64_t)nact * g.n_groups;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < L2_STAGES; ++s) {
@@ -449,9 +477,10 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       const uint64_t pol_w = l2_policy(g.pol & 1), pol_h = l2_policy(g.pol & 2);
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t it = unit0; it < g.n_items; it += n_units) {
+      for (int64_t it = unit0; it < n_items; it += n_units) {
         int rb, grp;
-        lm_item(g, it, rb, grp);
+        lm_item(g, nact, it, rb, grp);
+        rb = g.act[rb];
         rb = rb * 2 + (int)crank;
         const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
         for (int t = t0; t < t1; ++t) {
@@ -475,9 +504,10 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t j = 0;
-      for (int64_t it = unit0; it < g.n_items; it += n_units) {
+      for (int64_t it = unit0; it < n_items; it += n_units) {
         int rb, grp;
-        lm_item(g, it, rb, grp);
+        lm_item(g, nact, it, rb, grp);
+        rb = g.act[rb];
         const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
         for (int t = t0; t < t1; ++t, ++j) {
           const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
@@ -508,9 +538,10 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     uint32_t tempty_leader;
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(tempty_leader) : "r"(smem_u32(tempty)));
     uint32_t j = 0;
-    for (int64_t it = unit0; it < g.n_items; it += n_units) {
+    for (int64_t it = unit0; it < n_items; it += n_units) {
       int rb, grp;
-      lm_item(g, it, rb, grp);
+      lm_item(g, nact, it, rb, grp);
+      rb = g.act[rb];
       rb = rb * 2 + (int)crank;
       lm_epilogue_item(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, tempty_leader, true, tokens, rs, part,
                        zy_out);
@@ -522,6 +553,36 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+// Ordered list of the row-block units (MCu row blocks of 128 rows) that hold a valid row: one
+// CTA, chunks of 1024 units, ballot + warp-total scan. Masked tails of short responses then cost
+// no GEMM work and the persistent CTAs stay balanced over the units that remain.
+__global__ void __launch_bounds__(1024) lm_compact_units(const uint8_t* __restrict__ mask, int64_t rows, int MCu,
+                                                          int n_units, int* __restrict__ act, int* __restrict__ n_act) {
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n_units; c0 += 1024) {
+    const int u = c0 + tid;
+    const bool a = u < n_units && lm_unit_active(mask, u, MCu, rows);
+    const unsigned bal = __ballot_sync(0xffffffffu, a);
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < wid; ++w) off += warp_tot[w];
+    if (a) act[base + off + __popc(bal & ((1u << lane) - 1u))] = u;
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < 32; ++w) tot += warp_tot[w];
+      base += tot;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *n_act = base;
 }
 
 // Per valid row: fixed-order fp64 reduction of the group partials, then the same stats / log-prob
@@ -604,7 +665,9 @@ int lm_swz() {
 
 size_t lmhead_partial_bytes(int64_t rows, int64_t V) {
   const int64_t groups = ((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G;  // the most groups any G >= LM_G makes
-  return align_up((size_t)groups * (size_t)rows * sizeof(float2), 256) + align_up((size_t)rows * sizeof(float), 256);
+  const int64_t blocks = (rows + LM_BM - 1) / LM_BM;
+  return align_up((size_t)groups * (size_t)rows * sizeof(float2), 256) + align_up((size_t)rows * sizeof(float), 256) +
+         align_up((size_t)(blocks + 1) * sizeof(int), 256);
 }
 
 // TBA_LM_MC: 1 single-SM kernel, 2 cluster pair with weight multicast, 3 cta_group::2 pair.
@@ -620,24 +683,30 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   const int mode = lm_mc();
   const int mc = mode == 1 ? 1 : 2;  // CTAs per cluster
   const int n_rb = (int)((rows + LM_BM - 1) / LM_BM);
+  const int n_units_total = (n_rb + mc - 1) / mc;  // row-block units (pairs when mc = 2)
   LmGrid g;
   g.rows = rows;
   g.V = x->vocab;
-  g.n_rb = (n_rb + mc - 1) / mc;  // row-block units (pairs when mc = 2)
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
   g.G = lm_g();
   g.swz = lm_swz();
   g.pol = env_int("TBA_LM_POL", 1) & 7;
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
-  g.n_items = (int64_t)g.n_rb * g.n_groups;
   CUtensorMap mh, mw;
   if (!make_map(&mh, x->hidden, rows, x->d, x->hidden_stride, LM_BM) ||
       !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN / mc))
     return TBA_ERR_CUDA;
-  float2* part = static_cast<float2*>(part_ws);
-  float* zy = reinterpret_cast<float*>(static_cast<char*>(part_ws) +
-                                       align_up((size_t)g.n_groups * (size_t)rows * sizeof(float2), 256));
+  char* pw = static_cast<char*>(part_ws);
+  float2* part = reinterpret_cast<float2*>(pw);
+  pw += align_up((size_t)g.n_groups * (size_t)rows * sizeof(float2), 256);
+  float* zy = reinterpret_cast<float*>(pw);
+  pw += align_up((size_t)rows * sizeof(float), 256);
+  int* act = reinterpret_cast<int*>(pw);
+  g.act = act;
+  g.n_act = act + n_rb;
+  lm_compact_units<<<1, 1024, 0, s>>>(x->mask, rows, mc, n_units_total, act, act + n_rb);
+  if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
   static bool attr[3][64] = {};  // per variant and device; benign race: idempotent
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
@@ -665,7 +734,8 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
     int ncl = 0;
     if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0 && ncl < units) units = ncl;
   }
-  if (units > g.n_items) units = g.n_items;
+  const int64_t max_items = (int64_t)n_units_total * g.n_groups;  // the active count is known on the device only
+  if (units > max_items) units = max_items;
   cfg.gridDim = dim3((unsigned)(units * mc));
   if (cudaLaunchKernelEx(&cfg, kern, mh, mw, g, x->tokens, x->mask, rs, part, zy) != cudaSuccess)
     return TBA_ERR_CUDA;

@@ -87,6 +87,8 @@ LATTICE = [
     ("ragged_tails", W("toy", B=3, K=1, T=100, V=1000, d=200, len_lo=0, len_hi=100)),
     ("gpt2_dims", W("redteam", B=2, K=1, T=77, len_lo=1, len_hi=77)),
     ("four_row_blocks", W("pythia", B=2, K=4, T=64, V=5000, d=128)),
+    # responses <= 128 of T = 256: every second row block is fully masked and skipped
+    ("skipped_row_blocks", W("rhomath", B=1, K=4, T=256, V=700, d=64, len_lo=0, len_hi=128)),
 ]
 
 
