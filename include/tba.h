@@ -298,6 +298,17 @@ size_t tba_lmhead_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t vocab)
 int tba_lmhead_seq_logprob(const tba_lmhead* x, double inv_temp, void* workspace, double* seq_logp,
                            int32_t* n_tokens, int32_t* dev_status, tba_stream_t stream);
 
+/* tba_token_logprob from hidden states: tok_logp[s,t] = mask ? log softmax(inv_temp z)[y] : 0. */
+int tba_lmhead_token_logprob(const tba_lmhead* x, double inv_temp, void* workspace, double* tok_logp,
+                             int32_t* dev_status, tba_stream_t stream);
+
+/* tba_tbap_loss_fwd (TBA', Eq. 16) from hidden states: same outputs; gen_logp [N, T] fp32. */
+int tba_lmhead_tbap_loss_fwd(const tba_lmhead* x, const float* gen_logp, const double* ref_logp,
+                             const double* log_reward, double beta, int32_t K, int32_t is_mode, double is_lo,
+                             double is_hi, double n_tok_global, void* workspace, double* seq_logp,
+                             int32_t* n_tokens, double* adv, float* coef, double* partial, int32_t* dev_status,
+                             tba_stream_t stream);
+
 /* tba_tb_loss_fwd from hidden states (Eqs. 4-5 / Eq. 3; opts as there). */
 int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const double* ref_logp,
                            const double* log_reward, double beta, int32_t K, double n_seq_global,

@@ -421,17 +421,23 @@ int tba_vargrad_tb_loss_bwd(const tba_rows* x, const void* workspace, const doub
                          dlogits_row_stride, nullptr, 0, stream);
 }
 
-static int tbap_fwd_impl(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
-                         double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
-                         void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef,
-                         double* partial, int32_t* dev_status, void* grad_unscaled, int32_t g_dtype,
-                         int64_t g_row_stride, tba_stream_t stream) {
+static int check_tbap_config(double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi) {
   if (!(std::isfinite(beta) && beta >= 0.0)) return TBA_ERR_INVALID_CONFIG;  // beta = 0 is Dr. GRPO
   if (K < 2) return TBA_ERR_INVALID_CONFIG;
   if (is_mode != TBA_IS_NONE && is_mode != TBA_IS_CLIP && is_mode != TBA_IS_ICEPOP) return TBA_ERR_INVALID_CONFIG;
   if (is_mode != TBA_IS_NONE && !(is_lo >= 0.0 && is_hi >= is_lo && !std::isnan(is_hi)))
     return TBA_ERR_INVALID_CONFIG;
-  int rc = validate_rows(x);
+  return TBA_OK;
+}
+
+static int tbap_fwd_impl(const tba_rows* x, const float* gen_logp, const double* ref_logp, const double* log_reward,
+                         double beta, int32_t K, int32_t is_mode, double is_lo, double is_hi, double n_tok_global,
+                         void* workspace, double* seq_logp, int32_t* n_tokens, double* adv, float* coef,
+                         double* partial, int32_t* dev_status, void* grad_unscaled, int32_t g_dtype,
+                         int64_t g_row_stride, tba_stream_t stream) {
+  int rc = check_tbap_config(beta, K, is_mode, is_lo, is_hi);
+  if (rc) return rc;
+  rc = validate_rows(x);
   if (rc) return rc;
   if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
   if (!(std::isfinite(n_tok_global) && n_tok_global > 0.0)) return TBA_ERR_INVALID_ARG;
@@ -521,6 +527,52 @@ int tba_lmhead_seq_logprob(const tba_lmhead* x, double inv_temp, void* workspace
   ha.seq_logp = seq_logp;
   ha.n_tokens = n_tokens;
   return launch_seq_head(false, w, x->mask, ha, s);
+}
+
+int tba_lmhead_token_logprob(const tba_lmhead* x, double inv_temp, void* workspace, double* tok_logp,
+                             int32_t* dev_status, tba_stream_t stream) {
+  int rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (!(std::isfinite(inv_temp) && inv_temp > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (rows == 0) return TBA_OK;
+  if (!workspace || !tok_logp || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  rc = launch_lmhead_rows(x, static_cast<char*>(workspace) + ws_bytes(x->n_seq, x->seq_len), w,
+                          make_scale(inv_temp), dev_status, s);
+  if (rc) return rc;
+  return launch_token_lp(w, x->mask, rows, tok_logp, s);
+}
+
+int tba_lmhead_tbap_loss_fwd(const tba_lmhead* x, const float* gen_logp, const double* ref_logp,
+                             const double* log_reward, double beta, int32_t K, int32_t is_mode, double is_lo,
+                             double is_hi, double n_tok_global, void* workspace, double* seq_logp,
+                             int32_t* n_tokens, double* adv, float* coef, double* partial, int32_t* dev_status,
+                             tba_stream_t stream) {
+  int rc = check_tbap_config(beta, K, is_mode, is_lo, is_hi);
+  if (rc) return rc;
+  rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_tok_global) && n_tok_global > 0.0)) return TBA_ERR_INVALID_ARG;
+  if (!partial) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0)
+    return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv || !coef ||
+      (x->seq_len > 0 && !gen_logp))
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(gen_logp) % 4 ||
+      reinterpret_cast<uintptr_t>(coef) % 4)
+    return TBA_ERR_INVALID_ARG;
+  const WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  rc = launch_lmhead_rows(x, static_cast<char*>(workspace) + ws_bytes(x->n_seq, x->seq_len), w, make_scale(1.0),
+                          dev_status, s);
+  if (rc) return rc;
+  return launch_tbap_head(w, x->mask, gen_logp, x->n_seq, x->seq_len, K, ref_logp, log_reward, beta, is_mode, is_lo,
+                          is_hi, -1.0 / n_tok_global, seq_logp, n_tokens, adv, coef, partial, s);
 }
 
 int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const double* ref_logp,

@@ -478,6 +478,25 @@ def lmhead_vargrad_fwd(hidden, weight, tokens, mask, ref_logp, log_reward, beta:
     return o, ws
 
 
+def lmhead_token_logprob(hidden, weight, tokens, mask, *, inv_temp: float = 1.0, workspace=None,
+                         check_status: bool = _CHECK):
+    """Per-token log-probs (fp64 [N, T], 0 where masked) from hidden states
+    (tba_lmhead_token_logprob), logits never written."""
+    L = _lib.load()
+    x = make_lmhead(hidden, weight, tokens, mask)
+    N, T = tokens.shape
+    dev = hidden.device
+    out = torch.empty((N, T), dtype=torch.float64, device=dev)
+    ws = workspace if workspace is not None else _lm_workspace(dev, N, T, weight.shape[0])
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_lmhead_token_logprob(ctypes.byref(x), float(inv_temp), ws.data_ptr(), out.data_ptr(), _ptr(st),
+                                         _stream(dev)), "tba_lmhead_token_logprob")
+    if st is not None:
+        _raise_dev_status(st, "tba_lmhead_token_logprob")
+    return out
+
+
 # ----------------------------------------------------------------------------- TBA' (Eq. 16)
 _IS = {"none": 0, "clip": 1, "icepop": 2}
 
@@ -526,6 +545,35 @@ def tbap_fwd(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, 
                   "tba_tbap_loss_fwd_deferred")
     if st is not None:
         _raise_dev_status(st, "tba_tbap_loss_fwd")
+    return o, ws
+
+
+def lmhead_tbap_fwd(hidden, weight, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, K: int,
+                    is_mode: str = "clip", is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global: float | None = None,
+                    workspace=None, out: _TbapFwd | None = None, check_status: bool = _CHECK):
+    """TBA' forward (Eq. 16) from hidden states (tba_lmhead_tbap_loss_fwd). Returns (_TbapFwd, workspace)."""
+    L = _lib.load()
+    x = make_lmhead(hidden, weight, tokens, mask)
+    N, T = tokens.shape
+    dev = hidden.device
+    if gen_logp.shape != (N, T) or gen_logp.dtype != torch.float32 or not gen_logp.is_contiguous():
+        raise ValueError("gen_logp must be a contiguous fp32 [N, T] tensor")
+    for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
+        if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    if n_tok_global is None:
+        n_tok_global = max(int(mask.sum().item()), 1)
+    o = out or _TbapFwd(N, T, dev)
+    ws = workspace if workspace is not None else _lm_workspace(dev, N, T, weight.shape[0])
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_lmhead_tbap_loss_fwd(ctypes.byref(x), gen_logp.data_ptr(), ref_logp.data_ptr(),
+                                         log_reward.data_ptr(), float(beta), int(K), _IS[is_mode], float(is_lo),
+                                         float(is_hi), float(n_tok_global), ws.data_ptr(), o.seq_logp.data_ptr(),
+                                         o.n_tokens.data_ptr(), o.adv.data_ptr(), o.coef.data_ptr(),
+                                         o.partial.data_ptr(), _ptr(st), _stream(dev)), "tba_lmhead_tbap_loss_fwd")
+    if st is not None:
+        _raise_dev_status(st, "tba_lmhead_tbap_loss_fwd")
     return o, ws
 
 

@@ -184,3 +184,36 @@ def test_synth_cuda_twin_bf16(kind):
         got = buf[:, :128].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
         np.testing.assert_array_equal(got, gen(9, 128, np.arange(1000, 1300), kind))
         assert buf[:, 128:].abs().sum().item() == 0  # the row padding is untouched
+
+
+def test_lmhead_token_logprob_and_tbap_match_oracle():
+    w = W("qwen", B=2, K=4, T=7, V=4001, d=136, len_lo=2, len_hi=7, beta=0.005)
+    inp = lm_inputs(w, 13, "lattice")
+    h = inp["host"]
+    rows = np.arange(w.N * w.T)
+    hid = syn.bf16_bits_to_f64(syn.hidden_rows(13, w.d, rows, "lattice"))
+    wt = syn.bf16_bits_to_f64(syn.weight_rows(13, w.d, np.arange(w.V), "lattice"))
+    logits = O.lmhead_logits(hid, wt).reshape(w.N, w.T, w.V)
+    # per-token log-probs (temperature 0.7)
+    tl = tba.lmhead_token_logprob(inp["hidden"], inp["weight"], inp["tokens"], inp["mask"], inv_temp=1 / 0.7,
+                                  check_status=True).cpu().numpy()
+    for s in range(w.N):
+        for t in range(w.T):
+            if h["mask"][s, t]:
+                ref = O.token_logprob(logits[s, t] / 0.7, int(h["tokens"][s, t]))[0]
+                assert abs(tl[s, t] - ref) <= 1e-6 + 1e-8 * abs(ref), (s, t, tl[s, t], ref)
+            else:
+                assert tl[s, t] == 0.0
+    # TBA' (Eq. 16) from hidden states vs the oracle on the same logits
+    gen = syn.gen_logp(w, 13)
+    ntok = int(h["mask"].sum())
+    o, _ = tba.lmhead_tbap_fwd(inp["hidden"], inp["weight"], inp["tokens"], inp["mask"], torch.from_numpy(gen).cuda(),
+                               inp["ref_logp"], inp["log_reward"], w.beta, w.K, "none", n_tok_global=ntok,
+                               check_status=True)
+    torch.cuda.synchronize()
+    ref = O.tbap_head(logits, h["tokens"], h["mask"], gen, h["ref_logp"], h["log_reward"], w.beta, w.K, "none",
+                      0.0, 0.0, want_grad=False)
+    tol = 1e-6 * (1 + h["mask"].sum(1))
+    assert np.all(np.abs(o.seq_logp.cpu().numpy() - ref["ell"]) <= tol)
+    assert np.all(np.abs(o.adv.cpu().numpy() - ref["adv"]) <= 2 * w.beta * tol.max() + 1e-9)
+    assert abs(o.partial[0].item() - ref["loss"]) <= 1e-5 * max(1.0, abs(ref["loss"]))
