@@ -10,7 +10,7 @@ namespace {
 // the UNSCALED gradient G = inv_temp (1[v=y] - softmax) once. HBM bytes: 2V read + 2V write per
 // valid row (the 4V floor); the per-sequence factor grad_scale * g * eps_s is applied by the
 // consumer (the LM-head backward, as a row scale), SURVEY §8(f) NEXT 2.
-template <class T, class TO, int NT, int CS, int U2 = 4>
+template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false>
 __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                 int64_t stride, const int64_t* __restrict__ tokens,
                                                 const uint8_t* __restrict__ mask, RowScale rs,
@@ -96,18 +96,19 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     sh_L2S = (float)log2(S);
   }
   __syncthreads();
-  bwd_row<T, TO, U2, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
-                           make_policy(false));
+  bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
+                                make_policy(false));
   if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <class T, class TO, int NT, int U2 = 4>
+template <class T, class TO, int NT, int U2 = 4, bool REV = false>
 __global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                   int64_t stride, const int64_t* __restrict__ tokens,
                                                   const uint8_t* __restrict__ mask, RowScale rs,
                                                   float2* __restrict__ stats, double* __restrict__ lp,
                                                   int32_t* dev_status, TO* __restrict__ g_out, int64_t ostride) {
-  row_single_body<T, TO, NT, 1, U2>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out, ostride);
+  row_single_body<T, TO, NT, 1, U2, REV>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out,
+                                         ostride);
 }
 
 template <class T, class TO, int NT, int U2 = 4>
@@ -244,13 +245,15 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
     // Rows in flight x row bytes must stay inside L2 for pass 2 to hit it. Measured:
     // rows <= 128 KB: 256 threads per row (4 CTAs/SM); longer rows: 512 threads (2 CTAs/SM) with 8
     // vectors per thread in pass 2 — it keeps ~70 % of the re-reads in L2 and overlaps the two passes
-    // across the SM's CTAs, which beats the exact-4V 2-CTA cluster variants (cfg 2/3/5/6).
+    // across the SM's CTAs, which beats the exact-4V 2-CTA cluster variants (cfg 2/3/5/6). Pass 2
+    // sweeps the row backwards (cfg 8 / 9 = cfg 4 / 0 reversed): the row's most recently streamed
+    // vectors are re-read first, while still in L2 (Qwen 8.13 -> 7.96 ms, scripts/gpu_ab_rev.sh).
     const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
-    int cfg = rb <= 128 * 1024 ? 0 : 4;
+    int cfg = rb <= 128 * 1024 ? 9 : 8;
     const int ecfg = env_int("TBA_SINGLE_CFG", -1);
-    if (ecfg >= 0 && ecfg <= 7) cfg = ecfg;
-#define TBA_SINGLE1(KERN_, T_, TO_, NT_, CS_, U2_)                                                             \
-  KERN_<T_, TO_, NT_, U2_><<<(unsigned)(rows * CS_), NT_, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab, \
+    if (ecfg >= 0 && ecfg <= 9) cfg = ecfg;
+#define TBA_SINGLE1(KERN_, T_, TO_, NT_, CS_, U2_, ...)                                                        \
+  KERN_<T_, TO_, NT_, U2_, ##__VA_ARGS__><<<(unsigned)(rows * CS_), NT_, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab, \
                                                              x->row_stride, x->tokens, x->mask, rs, w.stats,      \
                                                              w.lp, dev_status, static_cast<TO_*>(grad_unscaled),  \
                                                              g_row_stride)
@@ -263,6 +266,8 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
     else if (cfg == 4) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 8); \
     else if (cfg == 5) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 8); \
     else if (cfg == 6) TBA_SINGLE1(row_single2, T_, TO_, 256, 2, 4); \
+    else if (cfg == 8) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 8, true); \
+    else if (cfg == 9) TBA_SINGLE1(row_single1, T_, TO_, 256, 1, 4, true); \
     else {                                                           \
       const int64_t ncl = (int64_t)device_sms() / 2;                 \
       row_single_pipe<T_, TO_><<<(unsigned)(2 * ncl), 1024, 0, s>>>( \

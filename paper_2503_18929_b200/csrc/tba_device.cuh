@@ -502,7 +502,9 @@ __device__ __forceinline__ void store_vals(TO* o, const float (&d)[N]) {
   }
 }
 
-template <class T, class TO, int U, bool POL = false>
+// REV: walk the row's vectors from the end (the deferred pass re-reads a row it has just streamed:
+// its last vectors are the most recently touched in L2).
+template <class T, class TO, int U, bool POL = false, bool REV = false>
 __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid, int nthr,
                                         bool valid, float sc, float M2, float L2S, float c, int64_t y,
                                         uint64_t pol = 0) {
@@ -539,13 +541,15 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
     uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t k = k0 + (int64_t)u * nthr;
-      if (k < nvec) v[u] = POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k);
+      const int64_t kf = k0 + (int64_t)u * nthr;
+      const int64_t k = REV ? nvec - 1 - kf : kf;
+      if (kf < nvec) v[u] = POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t k = k0 + (int64_t)u * nthr;
-      if (k < nvec) {
+      const int64_t kf = k0 + (int64_t)u * nthr;
+      const int64_t k = REV ? nvec - 1 - kf : kf;
+      if (kf < nvec) {
         float d[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) d[e] = -c * ex2(fmaf(E::get(v[u], e), sc, nM2) - L2S);
