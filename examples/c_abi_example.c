@@ -1,7 +1,8 @@
 /* Plain-C use of libtba.so (no Python, no PyTorch): build the rows of a tiny batch on the
  * host, copy them to the device with the CUDA runtime, run the VarGrad TB head forward and
  * backward through the C ABI, and print the loss, the per-sequence log-probs and a checksum
- * of dlogits. The test suite runs it and compares with the Python path.
+ * of dlogits; then the same sequences' log-probs from hidden states through the LM-head-fused
+ * forward. The test suite runs it and compares with the fp64 oracle.
  *
  *   gcc -O2 -I include -I /usr/local/cuda/include examples/c_abi_example.c \
  *       -L paper_2503_18929_b200 -ltba -L /usr/local/cuda/lib64 -lcudart -o c_abi_example
@@ -115,5 +116,44 @@ int main(void) {
          partial[2]);
   for (int s = 0; s < N; ++s) printf("seq %d logp %.12g ntok %d\n", s, seq[s], ntok[s]);
   printf("dlogits_abs_sum %.9g row0_sum %.3g\n", cs, rowsum);
+
+  /* The LM-head-fused forward: the same sequences' log-probs from bf16 hidden states [N*T, D]
+   * and an LM-head weight [V, D] (entries k/4, k in -2..2: exact in bf16, every logit exact in
+   * fp32), run on the tensor cores without writing the logits. */
+  const int64_t D = 64;
+  uint16_t* h_hid = (uint16_t*)malloc(sizeof(uint16_t) * N * T * D);
+  uint16_t* h_w = (uint16_t*)malloc(sizeof(uint16_t) * V * D);
+  for (int64_t i = 0; i < N * T * D + V * D; ++i) {
+    st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+    float f = (float)((int)(st % 5u) - 2) * 0.25f;
+    uint32_t b;
+    memcpy(&b, &f, sizeof(b));
+    if (i < N * T * D) h_hid[i] = (uint16_t)(b >> 16);
+    else h_w[i - N * T * D] = (uint16_t)(b >> 16);
+  }
+  void *d_hid, *d_w, *d_lws;
+  const size_t lws = tba_lmhead_workspace_bytes(N, T, V);
+  CK(cudaMalloc(&d_hid, sizeof(uint16_t) * N * T * D));
+  CK(cudaMalloc(&d_w, sizeof(uint16_t) * V * D));
+  CK(cudaMalloc(&d_lws, lws));
+  CK(cudaMemcpy(d_hid, h_hid, sizeof(uint16_t) * N * T * D, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_w, h_w, sizeof(uint16_t) * V * D, cudaMemcpyHostToDevice));
+  tba_lmhead lm;
+  memset(&lm, 0, sizeof(lm));
+  lm.hidden = d_hid;
+  lm.weight = d_w;
+  lm.n_seq = N;
+  lm.seq_len = T;
+  lm.d = D;
+  lm.vocab = V;
+  lm.hidden_stride = D;
+  lm.weight_stride = D;
+  lm.tokens = d_tok;
+  lm.mask = d_mask;
+  TB(tba_lmhead_seq_logprob(&lm, 1.0, d_lws, d_seq, d_ntok, d_status, NULL));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(seq, d_seq, sizeof(seq), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&status, d_status, sizeof(status), cudaMemcpyDeviceToHost));
+  for (int s = 0; s < N; ++s) printf("lmhead seq %d logp %.12g\n", s, seq[s]);
   return status != 0;
 }

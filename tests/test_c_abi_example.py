@@ -32,7 +32,15 @@ def _inputs():
         mask[i] = 1 if (i % T) < T - (i // T) % 2 else 0
     ref = np.array([-20.0 + s for s in range(N)])
     rew = np.array([float(s % 2) for s in range(N)])
-    return logits.reshape(N, T, V).astype(np.float64), tok.reshape(N, T), mask.reshape(N, T), ref, rew
+    D = 64
+    vals = np.empty(N * T * D + V * D)
+    for i in range(len(vals)):
+        st = nxt(st)
+        vals[i] = (int(st % 5) - 2) * 0.25
+    hid = vals[:N * T * D].reshape(N * T, D)
+    w = vals[N * T * D:].reshape(V, D)
+    return (logits.reshape(N, T, V).astype(np.float64), tok.reshape(N, T), mask.reshape(N, T), ref, rew,
+            hid, w)
 
 
 def test_c_example_compiles():
@@ -49,7 +57,7 @@ def test_c_example_runs_and_matches_oracle():
     exe = _build.build_c_example()
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
-    logits, tok, mask, ref, rew = _inputs()
+    logits, tok, mask, ref, rew, hid, w = _inputs()
     r = O.vargrad_head(logits, tok, mask, ref, rew, 0.5, 3)
     m = re.search(r"status 0 loss (\S+) n_seq 6 n_groups 2", out.stdout)
     assert m, out.stdout
@@ -58,3 +66,7 @@ def test_c_example_runs_and_matches_oracle():
     np.testing.assert_allclose(got, r["ell"], rtol=1e-6)
     cs = float(re.search(r"dlogits_abs_sum (\S+)", out.stdout).group(1))
     assert abs(cs - np.abs(r["dlogits"]).sum()) <= 1e-5 * np.abs(r["dlogits"]).sum()
+    # the LM-head-fused forward from the lattice hidden states (exact logits)
+    ell, _ = O.lmhead_seq_logprob(hid.reshape(6, 4, 64), w, tok, mask)
+    got = [float(x) for x in re.findall(r"lmhead seq \d+ logp (\S+)", out.stdout)]
+    np.testing.assert_allclose(got, ell, rtol=0, atol=1e-5)
