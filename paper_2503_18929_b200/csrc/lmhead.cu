@@ -689,7 +689,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.V = x->vocab;
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
   g.G = lm_g();
-  g.swz = lm_swz();
+  g.swz = (lm_swz() + mc - 1) / mc;  // the raster counts row blocks: a pair unit holds two
   g.pol = env_int("TBA_LM_POL", 1) & 7;
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
