@@ -29,7 +29,9 @@ TBA' (Eq. 16) pins (tests/test_oracle_tbap.py): Dr. GRPO equality at beta = 0 on
 (0, inf) no-op, per-group shift invariance, finite differences with coefficients held fixed.
 LM-head pins (tests/test_oracle_lmhead.py): brute-force triple loops on tiny inputs, equal
 weight rows (lp = -ln V for any hidden state), one-hot weight rows (closed form), invariance
-to adding a common vector to every weight row, temperature = scaling the weight.
+to adding a common vector to every weight row, temperature = scaling the weight; its
+backward (lmhead_grads): central finite differences of the loss in h and W, the zero
+vocabulary sum of dW (softmax minus one-hot sums to 0), dH = 0 for equal weight rows.
 Every function below is pinned by at least one of them ("parity unpinned": none).
 """
 from __future__ import annotations
@@ -343,3 +345,14 @@ def lmhead_seq_logprob(hidden: np.ndarray, weight: np.ndarray, tokens: np.ndarra
     z = inv_temp * lmhead_logits(np.reshape(hidden, (N * T, d)), weight).reshape(N, T, -1)
     ell, ntok, _ = seq_logprob(z, tokens, mask)
     return ell, ntok
+
+
+def lmhead_grads(hidden: np.ndarray, weight: np.ndarray, dz: np.ndarray):
+    """Backward through z = W h (NEXT 3): the chain rule applied to App. A's dL/dz:
+        dL/dh_r = sum_v dz_{r,v} W_v   and   dL/dW_v = sum_r dz_{r,v} h_r,
+    i.e. dH = dZ W and dW = dZ^T H (library matmuls in fp64). hidden [R, d], weight [V, d],
+    dz [R, V] (e.g. ``vargrad_head(...)["dlogits"]`` reshaped) -> (dH [R, d], dW [V, d])."""
+    H = np.asarray(hidden, np.float64)
+    W = np.asarray(weight, np.float64)
+    Z = np.asarray(dz, np.float64)
+    return Z @ W, Z.T @ H

@@ -100,3 +100,60 @@ def test_generator_lmhead_inputs(kind):
         assert 0.9 < h.std() < 1.4
         # rows are counter-indexed: a sub-range equals the matching rows of a larger call
         assert np.array_equal(syn.weight_rows(0, 64, np.arange(40, 60), kind), syn.weight_rows(0, 64, np.arange(100), kind)[40:60])
+
+
+# ---- backward through the LM head (lmhead_grads): pinned by finite differences of the loss
+def _tiny_lm_case(seed, inv_temp=1.0, learned=False):
+    rng = np.random.default_rng(seed)
+    B, K, T, d, V = 2, 2, 3, 5, 7
+    N = B * K
+    H, W = rng.normal(size=(N, T, d)), rng.normal(size=(V, d))
+    tok = rng.integers(0, V, (N, T))
+    mask = np.array([[1, 1, 1], [1, 1, 0], [1, 0, 0], [1, 1, 1]], np.uint8)
+    ref, rew = rng.normal(size=N) * 2, rng.uniform(0, 1, N)
+    log_z = rng.normal(size=B) if learned else None
+
+    def loss(Hx, Wx):
+        z = O.lmhead_logits(Hx.reshape(N * T, d), Wx).reshape(N, T, V)
+        return O.vargrad_head(z, tok, mask, ref, rew, 0.7, K, want_grad=False, inv_temp=inv_temp,
+                              log_z=log_z)["loss"]
+
+    z = O.lmhead_logits(H.reshape(N * T, d), W).reshape(N, T, V)
+    r = O.vargrad_head(z, tok, mask, ref, rew, 0.7, K, inv_temp=inv_temp, log_z=log_z)
+    dH, dW = O.lmhead_grads(H.reshape(N * T, d), W, r["dlogits"].reshape(N * T, V))
+    return H, W, loss, dH.reshape(N, T, d), dW, mask
+
+
+@pytest.mark.parametrize("inv_temp,learned", [(1.0, False), (1 / 0.7, False), (1.0, True)])
+def test_lmhead_grads_match_central_differences(inv_temp, learned):
+    H, W, loss, dH, dW, mask = _tiny_lm_case(7, inv_temp, learned)
+    h = 1e-6
+    for arr, g in ((H, dH), (W, dW)):
+        fd = np.zeros_like(arr)
+        it = np.nditer(arr, flags=["multi_index"])
+        for _ in it:
+            i = it.multi_index
+            old = arr[i]
+            arr[i] = old + h
+            lp = loss(H, W)
+            arr[i] = old - h
+            lm = loss(H, W)
+            arr[i] = old
+            fd[i] = (lp - lm) / (2 * h)
+        err = np.max(np.abs(fd - g)) / max(np.max(np.abs(g)), 1e-12)
+        assert err < 1e-6, err
+    # masked rows get no gradient
+    assert np.all(dH[mask == 0] == 0.0)
+
+
+def test_lmhead_dw_vocab_sum_is_zero_and_equal_rows_give_zero_dh():
+    # sum_v (onehot - softmax)_v = 0 for every row, so sum_v dW_v = sum_r 0 * h_r = 0
+    H, W, _, dH, dW, _ = _tiny_lm_case(8)
+    np.testing.assert_allclose(dW.sum(axis=0), 0.0, atol=1e-13)
+    # equal weight rows: dH_r = sum_v dz_rv W_0 = 0
+    rng = np.random.default_rng(9)
+    Wc = np.tile(rng.normal(size=(1, 6)), (11, 1))
+    Hc = rng.normal(size=(5, 6))
+    dz = np.stack([O.grad_logprob_row(O.lmhead_logits(Hc[r:r + 1], Wc)[0], r) for r in range(5)])
+    dHc, _ = O.lmhead_grads(Hc, Wc, dz)
+    np.testing.assert_allclose(dHc, 0.0, atol=1e-14)
