@@ -275,8 +275,8 @@ int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coe
  * elements, hidden/weight 16-byte aligned, n_seq*seq_len <= 2^31 - 1, vocab <= 2^31 - 1.
  * tokens / mask as in tba_rows. Numerics: the logits carry the fp32 accumulation error of
  * a d-term dot product; the softmax epilogue is as accurate as the row
- * kernels'. Backward (dL/dhidden, dL/dW) is not provided: use the logits path for training
- * steps that need it. */
+ * kernels'. The backward through the head (dL/dhidden, dL/dW) is tba_lmhead_tb_loss_bwd /
+ * tba_lmhead_tbap_loss_bwd below. */
 typedef struct tba_lmhead {
   const void*    hidden;         /* bf16 */
   const void*    weight;         /* bf16 */
@@ -314,6 +314,40 @@ int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const d
                            const double* log_reward, double beta, int32_t K, double n_seq_global,
                            void* workspace, double* seq_logp, int32_t* n_tokens, double* log_z,
                            double* resid, double* partial, int32_t* dev_status, tba_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * LM-head-fused backward: the gradient of the TB / TBA' loss with
+ * respect to the hidden states and the LM-head weight, by the chain rule through z = W h
+ * applied to App. A:
+ *   dz_{r,v}   = c_r (1[v = y_r] - softmax(inv_temp z_r)_v)       (0 where mask == 0)
+ *   dhidden_r  = sum_v dz_{r,v} W_v          (bf16 or fp32, [n_seq, seq_len] rows of d)
+ *   dweight_v  = sum_r dz_{r,v} hidden_r     (fp32 [vocab] rows of d)
+ * with c_r = grad_scale * g * inv_temp * resid_s (TB: the matching tba_lmhead_tb_loss_fwd's
+ * resid, s = r / seq_len) or grad_scale * g * coef_r (TBA': tba_lmhead_tbap_loss_fwd's coef),
+ * g = *grad_out (NULL = 1). The logits are recomputed on the tensor cores tile by tile from
+ * the forward's row statistics (`workspace` of the matching forward, unmodified since); dz
+ * is formed in bf16 (round-to-nearest-even) for the two gradient GEMMs, which accumulate in
+ * fp32. Valid rows are processed in compacted chunks of chunk_rows (<= 0: 16384; rounded
+ * up to a multiple of 128), so the per-call memory is bwd_workspace, not [rows, V].
+ *   dhidden / dweight: either may be NULL (that gradient is skipped). Row strides in elements
+ *   (>= d). dhidden must not alias hidden. accumulate = 0 overwrites (masked rows of dhidden
+ *   are written with 0), accumulate = 1 adds into the existing contents (micro-batching).
+ *   d_log_z (TB only, nullable): dL/dlog Z_i for a learned log Z, as in tba_tb_loss_bwd.
+ * Deterministic: fixed tile order, no atomics. bwd_workspace: 256-byte aligned, of
+ * tba_lmhead_bwd_workspace_bytes(n_seq, seq_len, d, vocab, chunk_rows) bytes. */
+size_t tba_lmhead_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t d, int64_t vocab,
+                                      int64_t chunk_rows);
+
+int tba_lmhead_tb_loss_bwd(const tba_lmhead* x, const tba_tb_opts* opts, const void* workspace,
+                           const double* resid, double grad_scale, const double* grad_out, void* dhidden,
+                           int32_t dhidden_dtype, int64_t dhidden_row_stride, float* dweight,
+                           int64_t dweight_row_stride, int32_t accumulate, double* d_log_z, int32_t K,
+                           int64_t chunk_rows, void* bwd_workspace, tba_stream_t stream);
+
+int tba_lmhead_tbap_loss_bwd(const tba_lmhead* x, const void* workspace, const float* coef, double grad_scale,
+                             const double* grad_out, void* dhidden, int32_t dhidden_dtype,
+                             int64_t dhidden_row_stride, float* dweight, int64_t dweight_row_stride,
+                             int32_t accumulate, int64_t chunk_rows, void* bwd_workspace, tba_stream_t stream);
 
 #ifdef __cplusplus
 }

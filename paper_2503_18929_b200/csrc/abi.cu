@@ -608,4 +608,75 @@ int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const d
   return launch_seq_head(true, w, x->mask, ha, s);
 }
 
+// ---- LM-head-fused head (NEXT 3), backward
+size_t tba_lmhead_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t d, int64_t vocab,
+                                      int64_t chunk_rows) {
+  if (n_seq < 0 || seq_len < 0 || d < 1 || vocab < 1) return 0;
+  if (n_seq > 0 && seq_len > (int64_t)INT32_MAX / n_seq) return 0;
+  return lmhead_bwd_ws_bytes(n_seq * seq_len, d, vocab, chunk_rows);
+}
+
+static int lmhead_bwd_impl(const tba_lmhead* x, const void* workspace, const double* resid, const float* coef,
+                           double gs, const double* grad_out, float sc, void* dhidden, int32_t dh_dtype,
+                           int64_t dh_stride, float* dweight, int64_t dw_stride, int32_t accumulate,
+                           int64_t chunk_rows, void* bwd_workspace, cudaStream_t s) {
+  int rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (!std::isfinite(gs)) return TBA_ERR_INVALID_ARG;
+  if (dhidden) {
+    if (dh_dtype != TBA_BF16 && dh_dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
+    if (dh_stride < x->d || reinterpret_cast<uintptr_t>(dhidden) % (dh_dtype == TBA_BF16 ? 2 : 4))
+      return TBA_ERR_INVALID_ARG;
+    if (dhidden == x->hidden) return TBA_ERR_INVALID_ARG;  // hidden is re-read chunk by chunk
+  }
+  if (dweight && (dw_stride < x->d || reinterpret_cast<uintptr_t>(dweight) % 4)) return TBA_ERR_INVALID_ARG;
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (!dhidden && !dweight) return TBA_OK;
+  if (rows > 0) {
+    if (!workspace || !bwd_workspace || reinterpret_cast<uintptr_t>(workspace) % 256 ||
+        reinterpret_cast<uintptr_t>(bwd_workspace) % 256)
+      return TBA_ERR_INVALID_ARG;
+    if (!resid && !coef) return TBA_ERR_INVALID_ARG;
+  }
+  const WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
+  return launch_lmhead_bwd(x, rows > 0 ? w.stats : nullptr, resid, coef, gs, grad_out, sc, dhidden, dh_dtype,
+                           dh_stride, dweight, dw_stride, accumulate != 0, chunk_rows, bwd_workspace, s);
+}
+
+int tba_lmhead_tb_loss_bwd(const tba_lmhead* x, const tba_tb_opts* opts, const void* workspace,
+                           const double* resid, double grad_scale, const double* grad_out, void* dhidden,
+                           int32_t dhidden_dtype, int64_t dhidden_row_stride, float* dweight,
+                           int64_t dweight_row_stride, int32_t accumulate, double* d_log_z, int32_t K,
+                           int64_t chunk_rows, void* bwd_workspace, tba_stream_t stream) {
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (d_log_z && (K < 1 || x->n_seq % K)) return TBA_ERR_INVALID_ARG;
+  if (!std::isfinite(grad_scale)) return TBA_ERR_INVALID_ARG;
+  if (x->n_seq > 0 && !resid) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (d_log_z && x->n_seq > 0) {
+    rc = launch_dlogz(resid, x->n_seq / K, K, grad_scale, grad_out, d_log_z, s);
+    if (rc) return rc;
+  }
+  const RowScale rs = make_scale(opt_inv_temp(opts));
+  return lmhead_bwd_impl(x, workspace, resid, nullptr, grad_scale * rs.inv_temp, grad_out, rs.sc, dhidden,
+                         dhidden_dtype, dhidden_row_stride, dweight, dweight_row_stride, accumulate, chunk_rows,
+                         bwd_workspace, s);
+}
+
+int tba_lmhead_tbap_loss_bwd(const tba_lmhead* x, const void* workspace, const float* coef, double grad_scale,
+                             const double* grad_out, void* dhidden, int32_t dhidden_dtype,
+                             int64_t dhidden_row_stride, float* dweight, int64_t dweight_row_stride,
+                             int32_t accumulate, int64_t chunk_rows, void* bwd_workspace, tba_stream_t stream) {
+  int rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (x->n_seq * x->seq_len > 0 && (!coef || reinterpret_cast<uintptr_t>(coef) % 4)) return TBA_ERR_INVALID_ARG;
+  return lmhead_bwd_impl(x, workspace, nullptr, coef, grad_scale, grad_out, make_scale(1.0).sc, dhidden,
+                         dhidden_dtype, dhidden_row_stride, dweight, dweight_row_stride, accumulate, chunk_rows,
+                         bwd_workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"
+

@@ -1,0 +1,579 @@
+// NEXT 3, backward through the LM head: dL/dh and dL/dW for z = W h without
+// materialising the [rows, V] logits or dlogits of the whole batch.
+//
+// App. A gives dL/dz_{r,v} = c_r (1[v = y_r] - softmax(inv_temp z_r)_v) with the
+// per-row coefficient c_r = grad_scale * g * inv_temp * eps_s (TB, Eqs. 3-5) or
+// grad_scale * g * coef_r (TBA', Eq. 16); the chain rule through z = W h gives
+//   dL/dh_r = sum_v dz_{r,v} W_v        (dH = dZ W)
+//   dL/dW_v = sum_r dz_{r,v} h_r        (dW = dZ^T H)
+// The valid rows are processed in chunks of C rows (compacted: masked rows have dz = 0 and are
+// never computed). Per chunk, all on the tcgen05 tensor cores with one persistent kernel shape:
+//   1. lmb_gather_t   H rows of the chunk -> Hc [C, d] and Hc^T [d, C]            (bf16 copy)
+//   2. tc_gemm<DZ>    z = Hc W^T recomputed tile by tile in TMEM; the epilogue forms dz from
+//                     the forward's row statistics and writes it as bf16 to dZ [C, Vp] and
+//                     dZ^T [V, C] (the logits themselves never reach HBM)
+//   3. tc_gemm<STORE> dH rows = dZ (W^T)^T, scattered to the rows' places in dhidden
+//   4. tc_gemm<STORE> dW (+)= dZ^T (Hc^T)^T, fp32, accumulated over the chunks
+// W^T [d, Vp] is formed once per call. Every GEMM is D = A B^T with both operands K-major
+// (TMA SWIZZLE_128B tiles, UMMA M = 128, N = 256, K = 16, fp32 accumulators in TMEM), so the
+// transposed copies are what lets one mainloop serve all three products.
+#include "tc_sm100.cuh"
+
+namespace tba {
+namespace {
+
+constexpr int GB_BM = 128, GB_BN = 256, GB_STAGES = 4, GB_THREADS = 192;
+constexpr int GB_A_BYTES = GB_BM * TC_BK * 2;  // 16 KB
+constexpr int GB_B_BYTES = GB_BN * TC_BK * 2;  // 32 KB
+constexpr int GB_STAGE_BYTES = GB_A_BYTES + GB_B_BYTES;
+constexpr uint32_t GB_IDESC = tc_idesc_bf16(GB_BM, GB_BN);
+constexpr size_t GB_SMEM = 1024 + (size_t)GB_STAGES * GB_STAGE_BYTES + 256;
+constexpr int64_t LMB_DEFAULT_CHUNK = 16384;
+
+enum { EPI_DZ = 0, EPI_STORE = 1 };
+
+// dz epilogue: the chunk's rows i -> batch rows idx[chunk0 + i]
+struct DzArgs {
+  const int* idx;
+  const float2* stats;    // forward row statistics {M2 = M sc, log2 S}
+  const int64_t* tokens;
+  const double* resid;    // per sequence (TB) or nullptr
+  const float* coef;      // per row (TBA') or nullptr
+  int64_t T;
+  double gs;              // grad_scale * inv_temp (TB) or grad_scale (TBA'), times *grad_out
+  const double* grad_out;
+  float sc;               // fl(log2(e) inv_temp)
+  int64_t V, Vp, C;
+  uint16_t* dz;           // [C, Vp]
+  uint16_t* dzt;          // [V, C]
+};
+
+struct StoreArgs {
+  void* D;
+  int64_t ldd;
+  const int* row_map;  // nullable: output row of tile row m = row_map[m]
+  int out_bf16, add, vec;
+};
+
+struct GemmArgs {
+  int64_t M, N, K;     // static extents; dyn = 1: M := the chunk's count, dyn = 2: K := the chunk's count
+  const int* n_valid;  // device count of valid rows (dyn != 0)
+  int64_t chunk0, cap;
+  int dyn, swz, n_inner;
+  int pol;             // bit 0: A loads evict_last, bit 1: B loads evict_last
+  DzArgs dz;
+  StoreArgs st;
+};
+
+__device__ __forceinline__ int64_t chunk_count(const int* n_valid, int64_t chunk0, int64_t cap) {
+  const int64_t n = (int64_t)*n_valid - chunk0;
+  return n < 0 ? 0 : (n > cap ? cap : n);
+}
+
+struct Tiles {
+  int64_t n_mt, n_nt, nkb;
+  int swz, n_inner;
+};
+
+// tile t -> (mb, nb). n_inner: consecutive tiles share the m block (all N tiles of a row block
+// are in flight together; the A slice is fetched once). Otherwise super-rows of swz m blocks,
+// n outer, m inner (consecutive CTAs share the B tile).
+__device__ __forceinline__ void tile_of(const Tiles& g, int64_t t, int64_t& mb, int64_t& nb) {
+  if (g.n_inner) {
+    mb = t / g.n_nt;
+    nb = t - mb * g.n_nt;
+    return;
+  }
+  const int64_t per = (int64_t)g.swz * g.n_nt;
+  const int64_t sup = t / per, w = t - sup * per;
+  const int64_t m0 = sup * g.swz;
+  const int64_t nm = (g.n_mt - m0) < g.swz ? (g.n_mt - m0) : g.swz;
+  nb = w / nm;
+  mb = m0 + (w - nb * nm);
+}
+
+__device__ __forceinline__ void store_bf16x32(uint16_t* p, const float (&d)[32]) {
+  uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    q[u] = make_uint4(pack_bf16x2(d[8 * u + 0], d[8 * u + 1]), pack_bf16x2(d[8 * u + 2], d[8 * u + 3]),
+                      pack_bf16x2(d[8 * u + 4], d[8 * u + 5]), pack_bf16x2(d[8 * u + 6], d[8 * u + 7]));
+}
+
+__device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+
+// D row segment [n0, n0 + 32) of one output row: store or add, fp32 or bf16.
+__device__ __forceinline__ void store_row32(const StoreArgs& st, int64_t orow, int64_t n0, int64_t N, float (&v)[32]) {
+  if (st.out_bf16) {
+    uint16_t* p = static_cast<uint16_t*>(st.D) + orow * st.ldd + n0;
+    if (st.vec && n0 + 32 <= N) {
+      if (st.add) {
+        const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint4 w = q[u];
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v[8 * u + 2 * e] += bf16_to_f((uint16_t)(ws[e] & 0xFFFFu));
+            v[8 * u + 2 * e + 1] += bf16_to_f((uint16_t)(ws[e] >> 16));
+          }
+        }
+      }
+      store_bf16x32(p, v);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (n0 + e < N) p[e] = to_bf16(st.add ? v[e] + bf16_to_f(p[e]) : v[e]);
+    }
+  } else {
+    float* p = static_cast<float*>(st.D) + orow * st.ldd + n0;
+    if (st.vec && n0 + 32 <= N) {
+      float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float4 o = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+        if (st.add) {
+          const float4 w = q[u];
+          o.x += w.x;
+          o.y += w.y;
+          o.z += w.z;
+          o.w += w.w;
+        }
+        q[u] = o;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (n0 + e < N) p[e] = st.add ? v[e] + p[e] : v[e];
+    }
+  }
+}
+
+// Persistent D = A B^T over (M/128) x (N/256) tiles, K in blocks of 64, warp-specialised like
+// lmhead_fwd: warp 0 lane 0 TMA producer (4-stage ring), warp 1 lane 0 MMA issuer (two TMEM
+// accumulators of 256 columns), warps 2-5 epilogue (one TMEM lane = one tile row per thread).
+template <int EPI>
+__global__ void __launch_bounds__(GB_THREADS, 1)
+    tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + GB_STAGES * GB_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GB_STAGES * GB_STAGE_BYTES);
+  uint64_t* empty = full + GB_STAGES;
+  uint64_t* tfull = empty + GB_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  int64_t M = a.M, K = a.K, n_c = 0;
+  if (a.dyn) {
+    n_c = chunk_count(a.n_valid, a.chunk0, a.cap);
+    if (a.dyn == 1) M = n_c;
+    else K = n_c;
+  }
+  Tiles g;
+  g.n_mt = (M + GB_BM - 1) / GB_BM;
+  g.n_nt = (a.N + GB_BN - 1) / GB_BN;
+  g.nkb = (K + TC_BK - 1) / TC_BK;
+  g.swz = a.swz;
+  g.n_inner = a.n_inner;
+  const int64_t n_tiles = g.n_mt * g.n_nt;
+  const bool has_k = g.nkb > 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GB_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && has_k) {  // ---- TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      const uint64_t pol_a = l2_policy(a.pol & 1), pol_b = l2_policy(a.pol & 2);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int64_t mb, nb;
+        tile_of(g, t, mb, nb);
+        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_expect_tx(&full[stage], GB_STAGE_BYTES);
+          tma_load_2d(smem_u32(sA + stage * GB_A_BYTES), &tmA, (int)(kb * TC_BK), (int)(mb * GB_BM),
+                      smem_u32(&full[stage]), pol_a);
+          tma_load_2d(smem_u32(sB + stage * GB_B_BYTES), &tmB, (int)(kb * TC_BK), (int)(nb * GB_BN),
+                      smem_u32(&full[stage]), pol_b);
+          if (++stage == GB_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && has_k) {  // ---- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t j = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+        const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+        mbar_wait(&tempty[acc], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * GB_BN;
+        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * GB_A_BYTES));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * GB_B_BYTES));
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k)  // K = 16 per MMA: +32 bytes = +2 in the address field
+            umma_bf16<GB_IDESC>(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == GB_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4)
+    const int q = warp & 3;
+    const int row_in = q * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
+    uint32_t j = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
+      int64_t mb, nb;
+      tile_of(g, t, mb, nb);
+      const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+      const int64_t m = mb * GB_BM + row_in;
+      if (has_k) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+      }
+      if (EPI == EPI_DZ) {
+        const DzArgs& z = a.dz;
+        const bool valid = m < n_c;
+        float M2 = 0.f, L2S = 0.f, c = 0.f;
+        int64_t y = -1;
+        if (valid) {
+          const int64_t r = z.idx[a.chunk0 + m];
+          const float2 st = z.stats[r];
+          M2 = st.x;
+          L2S = st.y;
+          const double gg = (z.grad_out ? *z.grad_out : 1.0) * z.gs;
+          c = z.coef ? (float)(gg * (double)z.coef[r]) : (float)(gg * z.resid[r / z.T]);
+          y = z.tokens[r];
+        }
+#pragma unroll 1
+        for (int cc = 0; cc < GB_BN / 32; ++cc) {
+          const int64_t v0 = nb * GB_BN + cc * 32;
+          if (v0 >= z.V) break;  // warp-uniform
+          float v[32];
+          tmem_ld32(lane_addr + acc * GB_BN + cc * 32, v);
+          const float nM2 = -M2;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float p = ex2(fmaf(v[e], z.sc, nM2) - L2S);
+            v[e] = valid ? ((v0 + e == y) ? fmaf(-c, p, c) : -c * p) : 0.f;
+          }
+          uint16_t* zr = z.dz + m * z.Vp + v0;
+          if (v0 + 32 <= z.V) {
+            store_bf16x32(zr, v);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) z.dzt[(v0 + e) * z.C + m] = to_bf16(v[e]);
+          } else {
+            for (int e = 0; e < 32; ++e)
+              if (v0 + e < z.V) {
+                const uint16_t b = to_bf16(v[e]);
+                zr[e] = b;
+                z.dzt[(v0 + e) * z.C + m] = b;
+              }
+          }
+        }
+      } else {
+        const StoreArgs& st = a.st;
+        const bool in = m < M;
+        const int64_t orow = in ? (st.row_map ? (int64_t)st.row_map[m] : m) : 0;
+#pragma unroll 1
+        for (int cc = 0; cc < GB_BN / 32; ++cc) {
+          const int64_t n0 = nb * GB_BN + cc * 32;
+          if (n0 >= a.N) break;  // warp-uniform
+          float v[32];
+          if (has_k) {
+            tmem_ld32(lane_addr + acc * GB_BN + cc * 32, v);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0.f;
+          }
+          if (in && (has_k || !st.add)) store_row32(st, orow, n0, a.N, v);
+        }
+      }
+      if (has_k) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// Ascending list of the valid rows (mask != 0): one CTA, chunks of 1024 rows, ballot + warp scan.
+__global__ void __launch_bounds__(1024) lmb_compact_rows(const uint8_t* __restrict__ mask, int64_t rows,
+                                                         int* __restrict__ idx, int* __restrict__ n_out) {
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < rows; c0 += 1024) {
+    const int64_t r = c0 + tid;
+    const bool a = r < rows && mask[r] != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, a);
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < wid; ++w) off += warp_tot[w];
+    if (a) idx[base + off + __popc(bal & ((1u << lane) - 1u))] = (int)r;
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < 32; ++w) tot += warp_tot[w];
+      base += tot;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *n_out = base;
+}
+
+// Row gather + transpose of a bf16 matrix in 64 x 64 tiles: for output rows i in [0, n_pad),
+// src row = idx[chunk0 + i] (idx == nullptr: chunk0 + i), zero for i >= n (the chunk's count):
+//   dst_rm[i, k] = src[row, k]   (nullable; row stride d)
+//   dst_t [k, i] = src[row, k]   (row stride ld_t)
+// n = clamp(*n_valid - chunk0, 0, cap) (n_valid == nullptr: n_static); n_pad = n rounded up to
+// 128 when `pad` (so the GEMM tiles over the chunk read zeros), else n.
+__global__ void __launch_bounds__(256) lmb_gather_t(const uint16_t* __restrict__ src, int64_t sstride, int64_t d,
+                                                    const int* __restrict__ idx, const int* __restrict__ n_valid,
+                                                    int64_t n_static, int64_t chunk0, int64_t cap, int pad,
+                                                    uint16_t* __restrict__ dst_rm, uint16_t* __restrict__ dst_t,
+                                                    int64_t ld_t) {
+  __shared__ uint16_t tile[64][72];
+  const int64_t n = n_valid ? chunk_count(n_valid, chunk0, cap) : n_static;
+  const int64_t n_pad = pad ? (n + 127) / 128 * 128 : n;
+  const int64_t i0 = (int64_t)blockIdx.y * 64, k0 = (int64_t)blockIdx.x * 64;
+  if (i0 >= n_pad) return;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int rl = tid / 8 + 32 * p, kl = (tid % 8) * 8;
+    const int64_t i = i0 + rl, k = k0 + kl;
+    uint4 val = make_uint4(0u, 0u, 0u, 0u);
+    if (i < n && k < d) {
+      const int64_t r = idx ? (int64_t)idx[chunk0 + i] : chunk0 + i;
+      val = *reinterpret_cast<const uint4*>(src + r * sstride + k);
+    }
+    if (dst_rm && i < n_pad && k < d) *reinterpret_cast<uint4*>(dst_rm + i * d + k) = val;
+    uint32_t* tp = reinterpret_cast<uint32_t*>(&tile[rl][kl]);
+    tp[0] = val.x;
+    tp[1] = val.y;
+    tp[2] = val.z;
+    tp[3] = val.w;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int kl = tid / 8 + 32 * p, il = (tid % 8) * 8;
+    const int64_t k = k0 + kl, i = i0 + il;
+    if (k < d && i < n_pad) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = (uint32_t)tile[il + 2 * e][kl] | ((uint32_t)tile[il + 2 * e + 1][kl] << 16);
+      *reinterpret_cast<uint4*>(dst_t + k * ld_t + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+struct LmbWs {
+  int* idx;  // [rows] + the count at idx[rows]
+  uint16_t *wt, *hc, *hct, *dz, *dzt;
+};
+
+inline int64_t lmb_vp(int64_t V) { return (V + 7) / 8 * 8; }
+
+LmbWs lmb_layout(void* base, int64_t rows, int64_t d, int64_t V, int64_t C) {
+  char* p = static_cast<char*>(base);
+  LmbWs w;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* q = p + off;
+    off = align_up(off + bytes, 256);
+    return q;
+  };
+  w.idx = reinterpret_cast<int*>(take((size_t)(rows + 1) * sizeof(int)));
+  w.wt = reinterpret_cast<uint16_t*>(take((size_t)d * (size_t)lmb_vp(V) * 2));
+  w.hc = reinterpret_cast<uint16_t*>(take((size_t)C * (size_t)d * 2));
+  w.hct = reinterpret_cast<uint16_t*>(take((size_t)d * (size_t)C * 2));
+  w.dz = reinterpret_cast<uint16_t*>(take((size_t)C * (size_t)lmb_vp(V) * 2));
+  w.dzt = reinterpret_cast<uint16_t*>(take((size_t)V * (size_t)C * 2));
+  return w;
+}
+
+template <int EPI>
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int64_t max_tiles, cudaStream_t s) {
+  static bool attr[2][64] = {};  // per variant and device; benign race: idempotent
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
+  if (!attr[EPI][dev]) {
+    if (cudaFuncSetAttribute(tc_gemm<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GB_SMEM) != cudaSuccess)
+      return TBA_ERR_CUDA;
+    attr[EPI][dev] = true;
+  }
+  int64_t grid = device_sms();
+  if (grid > max_tiles) grid = max_tiles;
+  if (grid < 1) grid = 1;
+  tc_gemm<EPI><<<(unsigned)grid, GB_THREADS, GB_SMEM, s>>>(ma, mb, a);
+  return launch_status();
+}
+
+}  // namespace
+
+int64_t lmhead_bwd_chunk(int64_t rows, int64_t chunk_rows) {
+  int64_t c = chunk_rows > 0 ? chunk_rows : LMB_DEFAULT_CHUNK;
+  if (c > rows) c = rows;
+  if (c < 1) c = 1;
+  return (c + 127) / 128 * 128;
+}
+
+size_t lmhead_bwd_ws_bytes(int64_t rows, int64_t d, int64_t V, int64_t chunk_rows) {
+  const int64_t C = lmhead_bwd_chunk(rows, chunk_rows);
+  return align_up((size_t)(rows + 1) * sizeof(int), 256) + align_up((size_t)d * (size_t)lmb_vp(V) * 2, 256) +
+         2 * align_up((size_t)C * (size_t)d * 2, 256) + align_up((size_t)C * (size_t)lmb_vp(V) * 2, 256) +
+         align_up((size_t)V * (size_t)C * 2, 256);
+}
+
+// TBA_LMB_SWZ (dz raster), TBA_LMB_NINNER (bit 0: dH, bit 1: dW tiles n-inner), TBA_LMB_POL
+// (bits 0-1 dH, 2-3 dW: A / B loads evict_last): measurement knobs, read once.
+static int lmb_knob(const char* name, int dflt) {
+  return env_int(name, dflt);
+}
+
+int launch_lmhead_bwd(const tba_lmhead* x, const float2* stats, const double* resid, const float* coef, double gs,
+                      const double* grad_out, float sc, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
+                      int64_t dw_stride, bool accumulate, int64_t chunk_rows, void* bws, cudaStream_t s) {
+  const int64_t rows = x->n_seq * x->seq_len, d = x->d, V = x->vocab;
+  static const int swz = [] { int v = lmb_knob("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
+  static const int ninner = lmb_knob("TBA_LMB_NINNER", 3);
+  static const int pol = lmb_knob("TBA_LMB_POL", 0);
+  if (dh && !accumulate) {
+    const size_t esz = dh_dt == TBA_BF16 ? 2 : 4;
+    if (rows > 0 && cudaMemset2DAsync(dh, (size_t)dh_stride * esz, 0, (size_t)d * esz, (size_t)rows, s) != cudaSuccess)
+      return TBA_ERR_CUDA;
+  }
+  if (dw && !accumulate && rows == 0) {
+    return cudaMemset2DAsync(dw, (size_t)dw_stride * 4, 0, (size_t)d * 4, (size_t)V, s) == cudaSuccess ? TBA_OK
+                                                                                                      : TBA_ERR_CUDA;
+  }
+  if (rows == 0 || (!dh && !dw)) return TBA_OK;
+  const int64_t C = lmhead_bwd_chunk(rows, chunk_rows), Vp = lmb_vp(V);
+  const LmbWs w = lmb_layout(bws, rows, d, V, C);
+  int* n_valid = w.idx + rows;
+  lmb_compact_rows<<<1, 1024, 0, s>>>(x->mask, rows, w.idx, n_valid);
+  if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  if (dh) {
+    const dim3 grid((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64));
+    lmb_gather_t<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x->weight), x->weight_stride, d, nullptr,
+                                      nullptr, V, 0, V, 0, nullptr, w.wt, Vp);
+    if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  }
+  CUtensorMap m_hc, m_w, m_dz, m_wt, m_dzt, m_hct;
+  if (!make_map(&m_hc, w.hc, C, d, d, GB_BM) || !make_map(&m_w, x->weight, V, d, x->weight_stride, GB_BN) ||
+      !make_map(&m_dz, w.dz, C, V, Vp, GB_BM) || !make_map(&m_wt, w.wt, d, V, Vp, GB_BN) ||
+      !make_map(&m_dzt, w.dzt, V, C, C, GB_BM) || !make_map(&m_hct, w.hct, d, C, C, GB_BN))
+    return TBA_ERR_CUDA;
+  const int64_t n_chunks = (rows + C - 1) / C;
+  const int64_t nt_v = (V + GB_BN - 1) / GB_BN, nt_d = (d + GB_BN - 1) / GB_BN;
+  for (int64_t ch = 0; ch < n_chunks; ++ch) {
+    const int64_t chunk0 = ch * C;
+    const dim3 ggrid((unsigned)((d + 63) / 64), (unsigned)(C / 64));
+    lmb_gather_t<<<ggrid, 256, 0, s>>>(static_cast<const uint16_t*>(x->hidden), x->hidden_stride, d, w.idx, n_valid,
+                                       0, chunk0, C, 1, w.hc, w.hct, C);
+    if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+    GemmArgs a{};
+    a.n_valid = n_valid;
+    a.chunk0 = chunk0;
+    a.cap = C;
+    // 2. dz tiles: M = the chunk's rows, N = V, K = d
+    a.M = C;
+    a.N = V;
+    a.K = d;
+    a.dyn = 1;
+    a.swz = swz;
+    a.n_inner = 0;
+    a.pol = 2;  // the weight tiles are shared by the row blocks in flight
+    a.dz = DzArgs{w.idx, stats, x->tokens, resid, coef, x->seq_len, gs, grad_out, sc, V, Vp, C, w.dz, w.dzt};
+    int rc = launch_gemm<EPI_DZ>(m_hc, m_w, a, (C / GB_BM) * nt_v, s);
+    if (rc) return rc;
+    if (dh) {  // 3. dH rows = dZ W: M = the chunk's rows, N = d, K = V
+      GemmArgs b{};
+      b.n_valid = n_valid;
+      b.chunk0 = chunk0;
+      b.cap = C;
+      b.M = C;
+      b.N = d;
+      b.K = V;
+      b.dyn = 1;
+      b.swz = swz;
+      b.n_inner = ninner & 1;
+      b.pol = pol & 3;
+      const int64_t esz = dh_dt == TBA_BF16 ? 2 : 4;
+      b.st = StoreArgs{dh, dh_stride, w.idx + chunk0, dh_dt == TBA_BF16, accumulate ? 1 : 0,
+                       ((reinterpret_cast<uintptr_t>(dh) | (uintptr_t)(dh_stride * esz)) & 15) == 0};
+      rc = launch_gemm<EPI_STORE>(m_dz, m_wt, b, (C / GB_BM) * nt_d, s);
+      if (rc) return rc;
+    }
+    if (dw) {  // 4. dW (+)= dZ^T H: M = V, N = d, K = the chunk's rows
+      GemmArgs b{};
+      b.n_valid = n_valid;
+      b.chunk0 = chunk0;
+      b.cap = C;
+      b.M = V;
+      b.N = d;
+      b.K = C;
+      b.dyn = 2;
+      b.swz = swz;
+      b.n_inner = (ninner >> 1) & 1;
+      b.pol = (pol >> 2) & 3;
+      b.st = StoreArgs{dw, dw_stride, nullptr, 0, (accumulate || ch > 0) ? 1 : 0,
+                       ((reinterpret_cast<uintptr_t>(dw) | (uintptr_t)(dw_stride * 4)) & 15) == 0};
+      rc = launch_gemm<EPI_STORE>(m_dzt, m_hct, b, nt_v * nt_d, s);
+      if (rc) return rc;
+    }
+  }
+  return TBA_OK;
+}
+
+}  // namespace tba

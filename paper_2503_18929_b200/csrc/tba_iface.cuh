@@ -346,6 +346,15 @@ size_t lmhead_partial_bytes(int64_t rows, int64_t V);
 int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
                        cudaStream_t s);
 
+// lmhead_bwd.cu — backward through the LM head (dz recomputed on the tensor cores, dH = dZ W,
+// dW (+)= dZ^T H) over compacted chunks of valid rows. Per-row coefficient c_r = gs * g *
+// (coef ? coef[r] : resid[r / T]); sc = fl(log2(e) inv_temp).
+int64_t lmhead_bwd_chunk(int64_t rows, int64_t chunk_rows);
+size_t lmhead_bwd_ws_bytes(int64_t rows, int64_t d, int64_t V, int64_t chunk_rows);
+int launch_lmhead_bwd(const tba_lmhead* x, const float2* stats, const double* resid, const float* coef, double gs,
+                      const double* grad_out, float sc, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
+                      int64_t dw_stride, bool accumulate, int64_t chunk_rows, void* bws, cudaStream_t s);
+
 // deferred.cu — a1 + the unscaled gradient in one pass per row.
 int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
                   void* grad_unscaled, int32_t g_dtype, int64_t g_row_stride, cudaStream_t s);

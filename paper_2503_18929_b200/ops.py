@@ -497,6 +497,139 @@ def lmhead_token_logprob(hidden, weight, tokens, mask, *, inv_temp: float = 1.0,
     return out
 
 
+# ----------------------------------------------------------------------------- LM-head backward
+def lmhead_bwd_workspace_bytes(n_seq: int, seq_len: int, d: int, vocab: int, chunk_rows: int = 0) -> int:
+    return int(_lib.load().tba_lmhead_bwd_workspace_bytes(int(n_seq), int(seq_len), int(d), int(vocab),
+                                                          int(chunk_rows)))
+
+
+def _lm_grad_bufs(hidden, weight, dhidden, dweight, dhidden_dtype, want_dh, want_dw):
+    dev = hidden.device
+    if want_dh and dhidden is None:
+        dhidden = torch.empty(hidden.shape, dtype=dhidden_dtype or torch.float32, device=dev)
+    if want_dw and dweight is None:
+        dweight = torch.empty(weight.shape, dtype=torch.float32, device=dev)
+    dh_args = (None, 0, 0)
+    if dhidden is not None:
+        if dhidden.shape != hidden.shape or dhidden.dtype not in _DT or dhidden.stride(2) != 1 or \
+                not dhidden.is_contiguous():
+            raise ValueError("dhidden must be a contiguous bf16/fp32 tensor shaped like hidden")
+        dh_args = (dhidden.data_ptr(), _DT[dhidden.dtype], hidden.shape[2])
+    dw_args = (None, 0)
+    if dweight is not None:
+        if dweight.shape != weight.shape or dweight.dtype != torch.float32 or not dweight.is_contiguous():
+            raise ValueError("dweight must be a contiguous fp32 tensor shaped like weight")
+        dw_args = (dweight.data_ptr(), weight.shape[1])
+    return dhidden, dweight, dh_args, dw_args
+
+
+def _lm_bwd_ws(dev, N, T, d, V, chunk_rows):
+    return torch.empty(max(lmhead_bwd_workspace_bytes(N, T, d, V, chunk_rows), 256), dtype=torch.uint8, device=dev)
+
+
+def lmhead_vargrad_bwd(hidden, weight, tokens, mask, workspace, resid, grad_scale: float, *, grad_out=None,
+                       inv_temp: float = 1.0, log_z_param=None, K: int = 0, dhidden=None, dweight=None,
+                       dhidden_dtype=None, want_dhidden: bool = True, want_dweight: bool = True,
+                       accumulate: bool = False, chunk_rows: int = 0, bwd_workspace=None):
+    """Backward of the TB loss through the LM head (tba_lmhead_tb_loss_bwd): dL/dhidden ([N, T, d],
+    fp32 unless dhidden_dtype=bf16) and dL/dW (fp32 [V, d]); the logits are recomputed on the tensor
+    cores from the forward's `workspace`. Returns (dhidden, dweight[, d_log_z])."""
+    L = _lib.load()
+    x = make_lmhead(hidden, weight, tokens, mask)
+    N, T, d = hidden.shape
+    dev = hidden.device
+    dhidden, dweight, (dhp, dht, dhs), (dwp, dws) = _lm_grad_bufs(hidden, weight, dhidden, dweight, dhidden_dtype,
+                                                                  want_dhidden, want_dweight)
+    if grad_out is not None:
+        grad_out = grad_out.to(device=dev, dtype=torch.float64).contiguous()
+    opts = _opts(inv_temp, log_z_param)
+    d_log_z = None
+    if log_z_param is not None:
+        if K < 2:
+            raise ValueError("K is required with a learned log_z_param")
+        d_log_z = torch.empty(N // K, dtype=torch.float64, device=dev)
+    bws = bwd_workspace if bwd_workspace is not None else _lm_bwd_ws(dev, N, T, d, weight.shape[0], chunk_rows)
+    with torch.cuda.device(dev):
+        check(L.tba_lmhead_tb_loss_bwd(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
+                                       workspace.data_ptr(), resid.data_ptr(), float(grad_scale), _ptr(grad_out),
+                                       dhp, dht, dhs, dwp, dws, int(bool(accumulate)), _ptr(d_log_z), int(K),
+                                       int(chunk_rows), bws.data_ptr(), _stream(dev)), "tba_lmhead_tb_loss_bwd")
+    return (dhidden, dweight) if d_log_z is None else (dhidden, dweight, d_log_z)
+
+
+def lmhead_tbap_bwd(hidden, weight, tokens, mask, workspace, coef, n_tok_global: float, *, grad_out=None,
+                    dhidden=None, dweight=None, dhidden_dtype=None, want_dhidden: bool = True,
+                    want_dweight: bool = True, accumulate: bool = False, chunk_rows: int = 0, bwd_workspace=None):
+    """Backward of the TBA' surrogate (Eq. 16) through the LM head (tba_lmhead_tbap_loss_bwd);
+    grad_scale = -1 / n_tok_global. Returns (dhidden, dweight)."""
+    L = _lib.load()
+    x = make_lmhead(hidden, weight, tokens, mask)
+    N, T, d = hidden.shape
+    dev = hidden.device
+    dhidden, dweight, (dhp, dht, dhs), (dwp, dws) = _lm_grad_bufs(hidden, weight, dhidden, dweight, dhidden_dtype,
+                                                                  want_dhidden, want_dweight)
+    if grad_out is not None:
+        grad_out = grad_out.to(device=dev, dtype=torch.float64).contiguous()
+    bws = bwd_workspace if bwd_workspace is not None else _lm_bwd_ws(dev, N, T, d, weight.shape[0], chunk_rows)
+    with torch.cuda.device(dev):
+        check(L.tba_lmhead_tbap_loss_bwd(ctypes.byref(x), workspace.data_ptr(), coef.data_ptr(),
+                                         -1.0 / float(n_tok_global), _ptr(grad_out), dhp, dht, dhs, dwp, dws,
+                                         int(bool(accumulate)), int(chunk_rows), bws.data_ptr(), _stream(dev)),
+              "tba_lmhead_tbap_loss_bwd")
+    return dhidden, dweight
+
+
+class LmHeadTBLoss(torch.autograd.Function):
+    """Eq. 5 (or Eq. 3 with a learned log Z) from hidden states through the LM head, logits never
+    materialised: forward tba_lmhead_tb_loss_fwd, backward tba_lmhead_tb_loss_bwd (dhidden, dW)."""
+
+    @staticmethod
+    def forward(ctx, hidden, weight, log_z_param, tokens, mask, ref_logp, log_reward, beta, K, n_global, group,
+                inv_temp, chunk_rows, aux):
+        lzp = None if log_z_param is None else log_z_param.detach().contiguous()
+        o, ws = lmhead_vargrad_fwd(hidden, weight, tokens, mask, ref_logp, log_reward, beta, K, n_global,
+                                   inv_temp=inv_temp, log_z_param=lzp)
+        if group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
+        ctx.save_for_backward(hidden, weight, tokens, mask, ws, o.resid)
+        ctx.n_global, ctx.K, ctx.inv_temp, ctx.lzp, ctx.chunk_rows = n_global, K, inv_temp, lzp, chunk_rows
+        if aux is not None:
+            aux.update(seq_logp=o.seq_logp, n_tokens=o.n_tokens, log_z=o.log_z, resid=o.resid, partial=o.partial)
+        return o.partial[0]
+
+    @staticmethod
+    def backward(ctx, grad):
+        hidden, weight, tokens, mask, ws, resid = ctx.saved_tensors
+        r = lmhead_vargrad_bwd(hidden, weight, tokens, mask, ws, resid, 2.0 / ctx.n_global, grad_out=grad,
+                               inv_temp=ctx.inv_temp, log_z_param=ctx.lzp, K=ctx.K,
+                               dhidden_dtype=hidden.dtype if hidden.dtype == torch.float32 else torch.float32,
+                               want_dhidden=ctx.needs_input_grad[0], want_dweight=ctx.needs_input_grad[1],
+                               chunk_rows=ctx.chunk_rows)
+        dh, dw = r[0], r[1]
+        dz = r[2] if ctx.lzp is not None else None
+        return (dh.to(hidden.dtype) if dh is not None else None, dw.to(weight.dtype) if dw is not None else None,
+                dz) + (None,) * 11
+
+
+def lmhead_tb_loss(hidden, weight, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
+                   group=None, log_z=None, inv_temp: float = 1.0, chunk_rows: int = 0, return_aux: bool = False):
+    """The trajectory-balance loss from final hidden states [N, T, d] (bf16) and the LM-head weight
+    [V, d] (bf16), autograd-enabled for hidden, weight and a learned log_z; z = W h is never written
+    to memory in either direction. Arguments otherwise as vargrad_tb_loss."""
+    N = tokens.shape[0]
+    if n_seq_global is None:
+        if group is not None:
+            import torch.distributed as dist
+            n_seq_global = N * dist.get_world_size(group)
+        else:
+            n_seq_global = N
+    aux = {} if return_aux else None
+    loss = LmHeadTBLoss.apply(hidden, weight, log_z, tokens, mask, ref_logp, log_reward, float(beta), int(K),
+                              float(n_seq_global), group, float(inv_temp), int(chunk_rows), aux)
+    return (loss, aux) if return_aux else loss
+
+
 # ----------------------------------------------------------------------------- TBA' (Eq. 16)
 _IS = {"none": 0, "clip": 1, "icepop": 2}
 

@@ -170,3 +170,46 @@ def test_lmhead_config_and_workspace(L):
     assert L.tba_lmhead_workspace_bytes(-1, 4, 10) == 0 and L.tba_lmhead_workspace_bytes(1, 4, 0) == 0
     empty = _lm(n_seq=0, hidden=0, weight=0, tokens=0, mask=0)
     assert L.tba_lmhead_seq_logprob(ctypes.byref(empty), 1.0, 0, 0, 0, None, None) == _lib.TBA_OK
+
+
+def _lmb(L, x, opts=None, ws=0x100000, resid=FAKE, gs=0.25, dh=FAKE + 0x10000, dht=_lib.TBA_FP32, dhs=64,
+         dw=FAKE + 0x20000, dws=64, acc=0, dlz=None, K=4, chunk=0, bws=0x200000):
+    return L.tba_lmhead_tb_loss_bwd(ctypes.byref(x), opts, ws, resid, gs, None, dh, dht, dhs, dw, dws, acc, dlz, K,
+                                    chunk, bws, None)
+
+
+def test_lmhead_bwd_validation(L):
+    x = _lm()
+    bad = _lib.TBA_ERR_INVALID_ARG
+    assert _lmb(L, _lm(d=12)) == bad
+    assert _lmb(L, x, dht=7) == bad                       # unknown dhidden dtype
+    assert _lmb(L, x, dhs=32) == bad                      # dhidden row stride < d
+    assert _lmb(L, x, dh=FAKE + 2) == bad                 # misaligned fp32 dhidden
+    assert _lmb(L, x, dh=FAKE) == bad                     # dhidden aliases hidden
+    assert _lmb(L, x, dws=63) == bad                      # dweight row stride < d
+    assert _lmb(L, x, dw=FAKE + 0x20002) == bad           # misaligned dweight
+    assert _lmb(L, x, bws=0x200010) == bad                # misaligned bwd workspace
+    assert _lmb(L, x, bws=0) == bad                       # missing bwd workspace
+    assert _lmb(L, x, ws=0x100008) == bad                 # misaligned forward workspace
+    assert _lmb(L, x, resid=None) == bad
+    assert _lmb(L, x, gs=math.inf) == bad
+    assert _lmb(L, x, dlz=FAKE, K=3) == bad               # 8 sequences are not groups of 3
+    opts = _lib.TbaTbOpts(0.0, None)
+    assert _lmb(L, x, opts=ctypes.byref(opts)) == _lib.TBA_ERR_INVALID_CONFIG
+    # nothing requested: OK without touching CUDA
+    assert _lmb(L, x, dh=None, dw=None) == _lib.TBA_OK
+    assert L.tba_lmhead_tbap_loss_bwd(ctypes.byref(x), 0x100000, None, -0.1, None, FAKE + 0x10000, _lib.TBA_FP32,
+                                      64, None, 0, 0, 0, 0x200000, None) == bad  # no coef
+    assert L.tba_lmhead_tbap_loss_bwd(ctypes.byref(x), 0x100000, FAKE + 2, -0.1, None, FAKE + 0x10000,
+                                      _lib.TBA_FP32, 64, None, 0, 0, 0, 0x200000, None) == bad  # misaligned coef
+
+
+def test_lmhead_bwd_workspace_bytes(L):
+    rows, d, V, C = 65536, 3584, 152064, 16384
+    b = L.tba_lmhead_bwd_workspace_bytes(64, 1024, d, V, C)
+    assert b >= d * V * 2 + 2 * C * d * 2 + 2 * C * V * 2 + rows * 4   # W^T, Hc, Hc^T, dZ, dZ^T, row list
+    assert b < d * V * 2 + 2 * C * d * 2 + 2 * C * V * 2 + rows * 4 + 16 * 256
+    # the chunk is rounded up to 128 rows and capped at the batch
+    assert L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 0) == L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 128)
+    assert L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 1) == L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 100)
+    assert L.tba_lmhead_bwd_workspace_bytes(-1, 4, 64, 10, 0) == 0 and L.tba_lmhead_bwd_workspace_bytes(1, 4, 64, 0, 0) == 0
