@@ -356,6 +356,155 @@ def lmhead_bench(args, w, tba, torch, dist, dev, world, rank, group):
         dist.destroy_process_group()
 
 
+def lmhead_train_bench(args, w, tba, torch, dist, dev, world, rank, group):
+    """One step = the LM-head-fused forward AND backward over this rank's groups: tba_lmhead_tb_loss_fwd
+    (z = W h on tcgen05, online log-softmax, Eq. 4/5 head) + the 24-byte all-reduce when N > 1 +
+    tba_lmhead_tb_loss_bwd (dz recomputed tile by tile on tcgen05, dhidden = dZ W in bf16, dW = dZ^T H
+    in fp32). The logits and dlogits never exist as [rows, V] tensors."""
+    B, K, T, V, d = w.B, w.K, w.T, w.V, w.d
+    N = B * K
+    g0 = rank * B
+    n_global = float(N * world)
+    gi = syn.group_inputs(w, SEED, g0, B)
+    hidden = torch.empty((N, T, d), dtype=torch.bfloat16, device=dev)
+    weight = torch.empty((V, d), dtype=torch.bfloat16, device=dev)
+    syn.fill_bf16_cuda(hidden.view(N * T, d), SEED, "hidden", g0 * K * T)
+    syn.fill_bf16_cuda(weight, SEED, "weight", 0)
+    tokens = torch.from_numpy(gi["tokens"]).to(dev)
+    mask = torch.from_numpy(gi["mask"]).to(dev)
+    ref = torch.from_numpy(gi["ref_logp"]).to(dev)
+    rew = torch.from_numpy(gi["log_reward"]).to(dev)
+    ws = torch.empty(tba.lmhead_workspace_bytes(N, T, V), dtype=torch.uint8, device=dev)
+    bws = torch.empty(tba.lmhead_bwd_workspace_bytes(N, T, d, V, args.lm_chunk), dtype=torch.uint8, device=dev)
+    out = tba.ops._Fwd(N, K, dev)
+    dh = torch.empty((N, T, d), dtype=torch.bfloat16, device=dev)
+    dw = torch.empty((V, d), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    marks = {}
+
+    def step(rec=False):
+        if rec:
+            marks["a"].record(stream)
+        tba.lmhead_vargrad_fwd(hidden, weight, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
+                               check_status=False)
+        if group is not None:
+            dist.all_reduce(out.partial, group=group)
+        if rec:
+            marks["b"].record(stream)
+        tba.lmhead_vargrad_bwd(hidden, weight, tokens, mask, ws, out.resid, 2.0 / n_global, dhidden=dh, dweight=dw,
+                               chunk_rows=args.lm_chunk, bwd_workspace=bws)
+        if rec:
+            marks["c"].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if group is not None:
+        dist.barrier()
+    try:
+        smi_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        smi_id = str(dev.index)
+    t0, t1 = ev(), ev()
+    with Clocks(smi_id) as clk:
+        torch.cuda.synchronize()
+        if group is not None:
+            dist.barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
+    if group is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+    ms = ms.item()
+    # phase split (one extra step with events between the calls)
+    marks.update(a=ev(), b=ev(), c=ev())
+    step(rec=True)
+    torch.cuda.synchronize()
+    fwd_ms, bwd_ms = marks["a"].elapsed_time(marks["b"]), marks["b"].elapsed_time(marks["c"])
+    loss = out.partial[0].item()
+    rows = N * T
+    valid = int(gi["mask"].sum())
+
+    variants = {}
+    if rank == 0 and world == 1 and not args.no_variants:
+        # unfused on the same inputs: cuBLAS logits -> logits-path fwd + bwd (dlogits in place) -> cuBLAS dH, dW
+        logits = torch.empty((N, T, V), dtype=torch.bfloat16, device=dev)
+        lws = torch.empty(tba.workspace_bytes(N, T), dtype=torch.uint8, device=dev)
+        dh_u = torch.empty((rows, d), dtype=torch.bfloat16, device=dev)
+        dw_u = torch.empty((V, d), dtype=torch.bfloat16, device=dev)
+
+        def unfused():
+            lg = logits.view(rows, V)
+            torch.matmul(hidden.view(rows, d), weight.T, out=lg)
+            o, _ = tba.vargrad_fwd(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=lws,
+                                   check_status=False)
+            tba.vargrad_bwd(logits, tokens, mask, lws, o.resid, 2.0 / n_global, dlogits=logits)
+            torch.matmul(lg, weight, out=dh_u)
+            torch.matmul(lg.T, hidden.view(rows, d), out=dw_u)
+
+        def timed(fn, n):
+            a, b = ev(), ev()
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(n):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / n
+        unfused()
+        n = max(2, args.steps // 4)
+        fz, uf = [], []
+        for _ in range(3):
+            fz.append(timed(step, n))
+            uf.append(timed(unfused, n))
+        med = statistics.median
+        variants["unfused_cublas"] = {
+            "ms_per_step": med(uf), "fused_ms_paired": med(fz), "fused_over_unfused": med(fz) / med(uf),
+            "value": valid / (med(uf) / 1e3), "unit": "tokens/s", "pairs": 3, "steps_per_run": n,
+            "what": "torch.matmul (cuBLAS bf16) writes the [rows, V] logits; tba_vargrad_tb_loss_fwd/_bwd (dlogits "
+                    "in place, bf16); torch.matmul dH = dZ W and dW = dZ^T H (bf16 outputs); interleaved medians",
+            "extra_hbm_bytes": rows * V * 2 * 2}
+        del logits, lws, dh_u, dw_u
+
+    if rank == 0:
+        peak, peak_sus, src = tensor_peak()
+        gemm = 2.0 * valid * V * d
+        flops = 3 * gemm       # algorithmic: z = W h, dH = dZ W, dW = dZ^T H
+        tf = flops / (ms / 1e3) / 1e12
+        line = {
+            "metric": baseline_metric() + " [LM-head-fused forward + backward from hidden states, NEXT 3]",
+            "value": valid * world / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (tba_synth hidden states / LM-head weight, DESIGN.md §6)",
+            "config": {"workload": w.name, "objective": "lmhead_train", "note": w.note, "B_per_rank": B, "K": K,
+                       "T": T, "V": V, "d": d, "beta": w.beta, "rows_per_rank": rows, "chunk_rows": args.lm_chunk,
+                       "dhidden_dtype": "bf16", "dweight_dtype": "fp32", "parallelism": f"group-sharded x{world}",
+                       "l2": "weight 1.09 GB + hidden 0.47 GB + dz chunks per rank >> 126 MB L2; no flush needed"},
+            "roofline": {"bound": "tensor", "kernel": "whole step (lmhead_fwd, tc_gemm<DZ>, 2x tc_gemm<STORE>, "
+                                                      "gathers, combine, head)",
+                         "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                         "frac_of_sustained_peak": tf / peak_sus, "peak_source": src,
+                         "traffic": None, "algorithmic_flops_per_launch": flops, "avg_launch_ms": ms,
+                         "executed_flops": 4 * gemm,
+                         "note": "algorithmic = 3 GEMMs; the backward recomputes z (a 4th) instead of storing it"},
+            "kernels": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms},
+            "clocks": clk.summary(), "e2e": None, "cpu_baseline": None, "variants": variants,
+            # per step: lm_compact_units, lmhead_fwd, lmhead_combine, seq_head; lmb_compact_rows, W^T gather;
+            # per chunk: H gather, tc_gemm<DZ>, tc_gemm<STORE> x2 (cudaMemset launches not counted)
+            "gpu_launches": args.steps * (6 + 4 * -(-rows // (args.lm_chunk if args.lm_chunk > 0 else 16384))),
+            "loss": loss,
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -382,9 +531,11 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
     ap.add_argument("--share-gpu", action="store_true")
-    ap.add_argument("--objective", default="vargrad", choices=["vargrad", "tbap", "lmhead"],
+    ap.add_argument("--lm-chunk", type=int, default=0, help="rows per chunk of the LM-head backward (0 = 16384)")
+    ap.add_argument("--objective", default="vargrad", choices=["vargrad", "tbap", "lmhead", "lmhead_train"],
                     help="vargrad: Eq. 5 (the north-star head); tbap: the TBA' token-level rule (Eq. 16); "
-                         "lmhead: the Eq. 4/5 forward from hidden states with the LM head fused (NEXT 3)")
+                         "lmhead: the Eq. 4/5 forward from hidden states with the LM head fused (NEXT 3); "
+                         "lmhead_train: that forward + the backward through the head (dhidden, dW)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = syn.WORKLOADS[args.workload]
@@ -413,6 +564,8 @@ def main():
     tba.load_library()
     if args.objective == "lmhead":
         return lmhead_bench(args, w, tba, torch, dist, dev, world, rank, group)
+    if args.objective == "lmhead_train":
+        return lmhead_train_bench(args, w, tba, torch, dist, dev, world, rank, group)
     peer = tba.PeerReducer(group, dev) if (group is not None and args.collective == "peer") else None
 
     # ---- inputs: this rank's whole groups of the global batch, resident in HBM

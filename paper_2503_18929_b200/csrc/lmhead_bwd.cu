@@ -487,7 +487,7 @@ int launch_lmhead_bwd(const tba_lmhead* x, const float2* stats, const double* re
   const int64_t rows = x->n_seq * x->seq_len, d = x->d, V = x->vocab;
   static const int swz = [] { int v = lmb_knob("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
   static const int ninner = lmb_knob("TBA_LMB_NINNER", 3);
-  static const int pol = lmb_knob("TBA_LMB_POL", 0);
+  static const int pol = lmb_knob("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
   if (dh && !accumulate) {
     const size_t esz = dh_dt == TBA_BF16 ? 2 : 4;
     if (rows > 0 && cudaMemset2DAsync(dh, (size_t)dh_stride * esz, 0, (size_t)d * esz, (size_t)rows, s) != cudaSuccess)
