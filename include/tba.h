@@ -349,6 +349,27 @@ int tba_lmhead_tbap_loss_bwd(const tba_lmhead* x, const void* workspace, const f
                              int64_t dhidden_row_stride, float* dweight, int64_t dweight_row_stride,
                              int32_t accumulate, int64_t chunk_rows, void* bwd_workspace, tba_stream_t stream);
 
+/* One-call forward + backward from hidden states: the outputs of
+ * tba_lmhead_tb_loss_fwd followed by tba_lmhead_tb_loss_bwd with grad_scale = 2 g / n_seq_global
+ * fixed at call time, scheduled over chunks of groups_per_chunk WHOLE groups (<= 0: as many as
+ * fit in 16384 rows, at least 1). Eq. 4 couples only the K samples of one prompt, so once a
+ * chunk's forward and head are done its gradient is final: the forward's epilogue also stores
+ * the chunk's logits in fp32 (bwd_workspace), and the gradient pass forms dz from them instead
+ * of recomputing z = W h (one GEMM of three fewer than the two calls). Same results as the two
+ * calls (seq_logp, resid, log_z, loss bitwise; the logits the gradient uses are the same fp32
+ * tensor-core values). bwd_workspace: tba_lmhead_fwd_bwd_workspace_bytes(...) bytes (256-B
+ * aligned); workspace: tba_lmhead_workspace_bytes(...) as for the forward. */
+size_t tba_lmhead_fwd_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t d, int64_t vocab, int32_t K,
+                                          int32_t groups_per_chunk);
+
+int tba_lmhead_tb_loss_fwd_bwd(const tba_lmhead* x, const tba_tb_opts* opts, const double* ref_logp,
+                               const double* log_reward, double beta, int32_t K, double n_seq_global,
+                               double grad_scale, int32_t groups_per_chunk, void* workspace, double* seq_logp,
+                               int32_t* n_tokens, double* log_z, double* resid, double* partial, void* dhidden,
+                               int32_t dhidden_dtype, int64_t dhidden_row_stride, float* dweight,
+                               int64_t dweight_row_stride, int32_t accumulate, double* d_log_z,
+                               void* bwd_workspace, int32_t* dev_status, tba_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

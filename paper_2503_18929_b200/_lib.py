@@ -24,7 +24,8 @@ EXPORTS = ("tba_abi_version", "tba_status_string", "tba_workspace_bytes", "tba_s
            "tba_ipc_alloc", "tba_ipc_open", "tba_ipc_close", "tba_ipc_free",
            "tba_lmhead_workspace_bytes", "tba_lmhead_seq_logprob", "tba_lmhead_tb_loss_fwd",
            "tba_lmhead_token_logprob", "tba_lmhead_tbap_loss_fwd", "tba_lmhead_bwd_workspace_bytes",
-           "tba_lmhead_tb_loss_bwd", "tba_lmhead_tbap_loss_bwd")
+           "tba_lmhead_tb_loss_bwd", "tba_lmhead_tbap_loss_bwd", "tba_lmhead_fwd_bwd_workspace_bytes",
+           "tba_lmhead_tb_loss_fwd_bwd")
 TBA_DEV_PEER_TIMEOUT = 4
 TBA_IS_NONE, TBA_IS_CLIP, TBA_IS_ICEPOP = 0, 1, 2
 
@@ -118,6 +119,11 @@ def load(path: str | None = None) -> ctypes.CDLL:
         L.tba_lmhead_tb_loss_bwd.argtypes = [LP, OP, P, P, D, P, P, I32, I64, P, I64, I32, P, I32, I64, P, P]
         L.tba_lmhead_tbap_loss_bwd.restype = ctypes.c_int
         L.tba_lmhead_tbap_loss_bwd.argtypes = [LP, P, P, D, P, P, I32, I64, P, I64, I32, I64, P, P]
+        L.tba_lmhead_fwd_bwd_workspace_bytes.restype = SZ
+        L.tba_lmhead_fwd_bwd_workspace_bytes.argtypes = [I64, I64, I64, I64, I32, I32]
+        L.tba_lmhead_tb_loss_fwd_bwd.restype = ctypes.c_int
+        L.tba_lmhead_tb_loss_fwd_bwd.argtypes = [LP, OP, P, P, D, I32, D, D, I32, P, P, P, P, P, P, P, I32, I64, P,
+                                                 I64, I32, P, P, P, P]
         L.tba_ipc_alloc.restype = ctypes.c_int
         L.tba_ipc_alloc.argtypes = [SZ, ctypes.POINTER(ctypes.c_void_p), P]
         L.tba_ipc_open.restype = ctypes.c_int

@@ -678,5 +678,66 @@ int tba_lmhead_tbap_loss_bwd(const tba_lmhead* x, const void* workspace, const f
                          bwd_workspace, reinterpret_cast<cudaStream_t>(stream));
 }
 
+size_t tba_lmhead_fwd_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t d, int64_t vocab, int32_t K,
+                                          int32_t groups_per_chunk) {
+  if (n_seq < 0 || seq_len < 0 || d < 1 || vocab < 1 || K < 1 || n_seq % K) return 0;
+  if (n_seq > 0 && seq_len > (int64_t)INT32_MAX / n_seq) return 0;
+  if (n_seq == 0 || seq_len == 0) return 256;
+  return lmhead_fb_ws_bytes(n_seq, seq_len, d, vocab, K, groups_per_chunk);
+}
+
+int tba_lmhead_tb_loss_fwd_bwd(const tba_lmhead* x, const tba_tb_opts* opts, const double* ref_logp,
+                               const double* log_reward, double beta, int32_t K, double n_seq_global,
+                               double grad_scale, int32_t groups_per_chunk, void* workspace, double* seq_logp,
+                               int32_t* n_tokens, double* log_z, double* resid, double* partial, void* dhidden,
+                               int32_t dhidden_dtype, int64_t dhidden_row_stride, float* dweight,
+                               int64_t dweight_row_stride, int32_t accumulate, double* d_log_z,
+                               void* bwd_workspace, int32_t* dev_status, tba_stream_t stream) {
+  if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
+  if (K < 2) return TBA_ERR_INVALID_CONFIG;
+  int rc = check_opts(opts);
+  if (rc) return rc;
+  rc = validate_lmhead(x);
+  if (rc) return rc;
+  if (x->n_seq % K) return TBA_ERR_INVALID_ARG;
+  if (!(std::isfinite(n_seq_global) && n_seq_global >= (double)x->n_seq && n_seq_global > 0.0))
+    return TBA_ERR_INVALID_ARG;
+  if (!std::isfinite(grad_scale) || !partial) return TBA_ERR_INVALID_ARG;
+  if (dhidden) {
+    if (dhidden_dtype != TBA_BF16 && dhidden_dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
+    if (dhidden_row_stride < x->d || reinterpret_cast<uintptr_t>(dhidden) % (dhidden_dtype == TBA_BF16 ? 2 : 4) ||
+        dhidden == x->hidden)
+      return TBA_ERR_INVALID_ARG;
+  }
+  if (dweight && (dweight_row_stride < x->d || reinterpret_cast<uintptr_t>(dweight) % 4)) return TBA_ERR_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (x->n_seq == 0 || x->seq_len == 0) {  // no rows: the two calls handle these shapes
+    rc = tba_lmhead_tb_loss_fwd(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens,
+                                log_z, resid, partial, dev_status, stream);
+    if (rc) return rc;
+    return lmhead_bwd_impl(x, workspace, resid, nullptr, grad_scale * opt_inv_temp(opts), nullptr,
+                           make_scale(opt_inv_temp(opts)).sc, dhidden, dhidden_dtype, dhidden_row_stride, dweight,
+                           dweight_row_stride, accumulate, 0, bwd_workspace, s);
+  }
+  if (!workspace || !bwd_workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !log_z || !resid)
+    return TBA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(bwd_workspace) % 256)
+    return TBA_ERR_INVALID_ARG;
+  const WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
+  const RowScale rs = make_scale(opt_inv_temp(opts));
+  tba_rows xr{};
+  xr.n_seq = x->n_seq;
+  xr.seq_len = x->seq_len;
+  const HeadArgs ha = tb_head_args(&xr, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
+                                   log_z, resid, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+  rc = launch_lmhead_fwd_bwd(x, rs, w, ha, K, grad_scale, 1.0 / n_seq_global, dhidden, dhidden_dtype,
+                             dhidden_row_stride, dweight, dweight_row_stride, accumulate != 0, groups_per_chunk,
+                             bwd_workspace, dev_status, s);
+  if (!rc && d_log_z && opts && opts->log_z_param)
+    rc = launch_dlogz(resid, x->n_seq / K, K, grad_scale, nullptr, d_log_z, s);
+  return rc;
+}
+
 }  // extern "C"
+
 

@@ -66,6 +66,8 @@ struct LmGrid {
   int n_tiles, n_groups, nkb;
   int G, swz;  // vocab tiles per item, row blocks per raster super-row
   int pol;     // L2 policy bits: 1 = weight loads evict_last, 2 = hidden loads evict_last, 4 = no hint (2-SM)
+  float* zst;  // nullable: the fp32 logits are also stored here, row r at zst + r * zst_ld (the one-call
+  int64_t zst_ld;  // forward + backward keeps them for its gradient pass instead of recomputing them)
 };
 
 // item -> (active unit index, vocab group): super-rows of g.swz active units, groups outer.
@@ -134,6 +136,17 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
     for (int c = 0; c < LM_BN / 32; ++c) {
       float v[32];
       tmem_ld32(tmem_lane + acc * LM_BN + c * 32, v);
+      if (g.zst && in_rows) {
+        float* zp = g.zst + row * g.zst_ld + nb + c * 32;
+        if (nb + c * 32 + 32 <= g.V) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            reinterpret_cast<float4*>(zp)[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+        } else {
+          for (int i = 0; i < 32; ++i)
+            if (nb + c * 32 + i < g.V) zp[i] = v[i];
+        }
+      }
       if (tail) {
         const int64_t lim = g.V - (nb + c * 32);
 #pragma unroll
@@ -592,7 +605,7 @@ int lm_mc() {
 }
 
 int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
-                       cudaStream_t s) {
+                       cudaStream_t s, float* zst, int64_t zst_ld) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
   const int mode = lm_mc();
@@ -608,6 +621,9 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.pol = env_int("TBA_LM_POL", 1) & 7;
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
+  g.zst = zst;
+  g.zst_ld = zst_ld;
+  if (zst && mode != 1) return TBA_ERR_INVALID_ARG;  // the stash is written by the single-SM kernel only
   CUtensorMap mh, mw;
   if (!make_map(&mh, x->hidden, rows, x->d, x->hidden_stride, LM_BM) ||
       !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN / mc))

@@ -341,8 +341,9 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
   }
 }
 
-// Ascending list of the valid rows (mask != 0): one CTA, chunks of 1024 rows, ballot + warp scan.
-__global__ void __launch_bounds__(1024) lmb_compact_rows(const uint8_t* __restrict__ mask, int64_t rows,
+// Ascending list of the valid rows (mask != 0), stored as r0 + row: one CTA, chunks of 1024 rows,
+// ballot + warp scan.
+__global__ void __launch_bounds__(1024) lmb_compact_rows(const uint8_t* __restrict__ mask, int64_t rows, int64_t r0,
                                                          int* __restrict__ idx, int* __restrict__ n_out) {
   __shared__ int warp_tot[32];
   __shared__ int base;
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(1024) lmb_compact_rows(const uint8_t* __restri
     __syncthreads();
     int off = 0;
     for (int w = 0; w < wid; ++w) off += warp_tot[w];
-    if (a) idx[base + off + __popc(bal & ((1u << lane) - 1u))] = (int)r;
+    if (a) idx[base + off + __popc(bal & ((1u << lane) - 1u))] = (int)(r0 + r);
     __syncthreads();
     if (tid == 0) {
       int tot = 0;
@@ -413,6 +414,80 @@ __global__ void __launch_bounds__(256) lmb_gather_t(const uint16_t* __restrict__
       for (int e = 0; e < 4; ++e)
         w[e] = (uint32_t)tile[il + 2 * e][kl] | ((uint32_t)tile[il + 2 * e + 1][kl] << 16);
       *reinterpret_cast<uint4*>(dst_t + k * ld_t + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+// dz from stored fp32 logits (the one-call forward + backward): tiles of 64 compacted rows x 128
+// vocabulary columns; row i of the chunk is batch row r = idx[i], its logits at zst + (r - zrow0) * zst_ld.
+//   dz [i, v] = c_r (1[v = y_r] - 2^(z sc - M2 - log2 S))  (bf16)  and  dz^T [v, i] the same
+// (rows i in [n, n rounded up to 128) are written as 0 so the GEMM tiles over them read zeros).
+__global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __restrict__ n_valid, int64_t cap,
+                                                     const float* __restrict__ zst, int64_t zst_ld, int64_t zrow0) {
+  __shared__ uint16_t tile[64][136];
+  __shared__ float s_c[64], s_m2[64], s_l2s[64];
+  __shared__ long long s_y[64], s_off[64];
+  const int64_t n = chunk_count(n_valid, 0, cap);
+  const int64_t n_pad = (n + 127) / 128 * 128;
+  const int64_t i0 = (int64_t)blockIdx.y * 64, v0 = (int64_t)blockIdx.x * 128;
+  if (i0 >= n_pad) return;
+  const int tid = threadIdx.x;
+  if (tid < 64) {
+    const int64_t i = i0 + tid;
+    float c = 0.f, M2 = 0.f, L2S = 0.f;
+    long long y = -1, off = -1;
+    if (i < n) {
+      const int64_t r = z.idx[i];
+      const float2 st = z.stats[r];
+      M2 = st.x;
+      L2S = st.y;
+      const double gg = (z.grad_out ? *z.grad_out : 1.0) * z.gs;
+      c = z.coef ? (float)(gg * (double)z.coef[r]) : (float)(gg * z.resid[r / z.T]);
+      y = z.tokens[r];
+      off = (r - zrow0) * zst_ld;
+    }
+    s_c[tid] = c;
+    s_m2[tid] = M2;
+    s_l2s[tid] = L2S;
+    s_y[tid] = y;
+    s_off[tid] = off;
+  }
+  __syncthreads();
+  // 64 rows x 128 columns: each thread 4 consecutive columns of 8 rows (float4 loads, 32 threads per row)
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int rl = tid / 32 + 8 * p, cl = (tid % 32) * 4;
+    const int64_t i = i0 + rl, v = v0 + cl;
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+    if (i < n && v < z.V) {
+      const float* zp = zst + s_off[rl] + v;
+      float4 q;
+      if (v + 4 <= z.V) q = __ldcs(reinterpret_cast<const float4*>(zp));
+      else q = make_float4(zp[0], v + 1 < z.V ? zp[1] : 0.f, v + 2 < z.V ? zp[2] : 0.f, 0.f);
+      const float zz[4] = {q.x, q.y, q.z, q.w};
+      const float c = s_c[rl], nM2 = -s_m2[rl], L2S = s_l2s[rl];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float pr = ex2(fmaf(zz[e], z.sc, nM2) - L2S);
+        d[e] = (v + e == s_y[rl]) ? fmaf(-c, pr, c) : -c * pr;
+      }
+    }
+    const uint32_t lo = pack_bf16x2(d[0], d[1]), hi = pack_bf16x2(d[2], d[3]);
+    if (v + 4 <= z.Vp && i < cap) *reinterpret_cast<uint2*>(z.dz + i * z.Vp + v) = make_uint2(lo, hi);
+    *reinterpret_cast<uint2*>(&tile[rl][cl]) = make_uint2(lo, hi);
+  }
+  __syncthreads();
+  // dz^T: 128 vocabulary rows of 64 chunk rows (128 B each): 8 threads x 16 B per row
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int vl = tid / 8 + 32 * p, il = (tid % 8) * 8;
+    const int64_t v = v0 + vl;
+    if (v < z.V) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = (uint32_t)tile[il + 2 * e][vl] | ((uint32_t)tile[il + 2 * e + 1][vl] << 16);
+      *reinterpret_cast<uint4*>(z.dzt + v * z.C + i0 + il) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
 }
@@ -475,105 +550,239 @@ size_t lmhead_bwd_ws_bytes(int64_t rows, int64_t d, int64_t V, int64_t chunk_row
          align_up((size_t)V * (size_t)C * 2, 256);
 }
 
-// TBA_LMB_SWZ (dz raster), TBA_LMB_NINNER (bit 0: dH, bit 1: dW tiles n-inner), TBA_LMB_POL
-// (bits 0-1 dH, 2-3 dW: A / B loads evict_last): measurement knobs, read once.
-static int lmb_knob(const char* name, int dflt) {
-  return env_int(name, dflt);
-}
+namespace {
 
-int launch_lmhead_bwd(const tba_lmhead* x, const float2* stats, const double* resid, const float* coef, double gs,
-                      const double* grad_out, float sc, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
-                      int64_t dw_stride, bool accumulate, int64_t chunk_rows, void* bws, cudaStream_t s) {
-  const int64_t rows = x->n_seq * x->seq_len, d = x->d, V = x->vocab;
-  static const int swz = [] { int v = lmb_knob("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
-  static const int ninner = lmb_knob("TBA_LMB_NINNER", 3);
-  static const int pol = lmb_knob("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
-  if (dh && !accumulate) {
-    const size_t esz = dh_dt == TBA_BF16 ? 2 : 4;
-    if (rows > 0 && cudaMemset2DAsync(dh, (size_t)dh_stride * esz, 0, (size_t)d * esz, (size_t)rows, s) != cudaSuccess)
-      return TBA_ERR_CUDA;
-  }
-  if (dw && !accumulate && rows == 0) {
-    return cudaMemset2DAsync(dw, (size_t)dw_stride * 4, 0, (size_t)d * 4, (size_t)V, s) == cudaSuccess ? TBA_OK
-                                                                                                      : TBA_ERR_CUDA;
-  }
-  if (rows == 0 || (!dh && !dw)) return TBA_OK;
-  const int64_t C = lmhead_bwd_chunk(rows, chunk_rows), Vp = lmb_vp(V);
-  const LmbWs w = lmb_layout(bws, rows, d, V, C);
-  int* n_valid = w.idx + rows;
-  lmb_compact_rows<<<1, 1024, 0, s>>>(x->mask, rows, w.idx, n_valid);
-  if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
-  if (dh) {
+// Per-call state of the backward: workspace layout, tensor maps, knobs (TBA_LMB_SWZ dz raster,
+// TBA_LMB_NINNER bit 0: dH / bit 1: dW tiles n-inner, TBA_LMB_POL bits 0-1 dH / 2-3 dW A / B loads
+// evict_last: measurement knobs, read once).
+struct LmbCtx {
+  const tba_lmhead* x;
+  int64_t C, Vp;
+  LmbWs w;
+  CUtensorMap m_hc, m_w, m_dz, m_wt, m_dzt, m_hct;
+  int swz, ninner, pol;
+};
+
+int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, void* bws, bool need_wt, cudaStream_t s) {
+  static const int swz = [] { int v = env_int("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
+  static const int ninner = env_int("TBA_LMB_NINNER", 3);
+  static const int pol = env_int("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
+  const int64_t d = x->d, V = x->vocab;
+  k.x = x;
+  k.C = C;
+  k.Vp = lmb_vp(V);
+  k.w = lmb_layout(bws, idx_rows, d, V, C);
+  k.swz = swz;
+  k.ninner = ninner;
+  k.pol = pol;
+  if (need_wt) {
     const dim3 grid((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64));
     lmb_gather_t<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x->weight), x->weight_stride, d, nullptr,
-                                      nullptr, V, 0, V, 0, nullptr, w.wt, Vp);
+                                      nullptr, V, 0, V, 0, nullptr, k.w.wt, k.Vp);
     if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
   }
-  CUtensorMap m_hc, m_w, m_dz, m_wt, m_dzt, m_hct;
-  if (!make_map(&m_hc, w.hc, C, d, d, GB_BM) || !make_map(&m_w, x->weight, V, d, x->weight_stride, GB_BN) ||
-      !make_map(&m_dz, w.dz, C, V, Vp, GB_BM) || !make_map(&m_wt, w.wt, d, V, Vp, GB_BN) ||
-      !make_map(&m_dzt, w.dzt, V, C, C, GB_BM) || !make_map(&m_hct, w.hct, d, C, C, GB_BN))
+  if (!make_map(&k.m_hc, k.w.hc, C, d, d, GB_BM) || !make_map(&k.m_w, x->weight, V, d, x->weight_stride, GB_BN) ||
+      !make_map(&k.m_dz, k.w.dz, C, V, k.Vp, GB_BM) || !make_map(&k.m_wt, k.w.wt, d, V, k.Vp, GB_BN) ||
+      !make_map(&k.m_dzt, k.w.dzt, V, C, C, GB_BM) || !make_map(&k.m_hct, k.w.hct, d, C, C, GB_BN))
     return TBA_ERR_CUDA;
-  const int64_t n_chunks = (rows + C - 1) / C;
+  return TBA_OK;
+}
+
+// One chunk: rows idx[chunk0 + i], i < clamp(*n_valid - chunk0, 0, C). dz from a GEMM recompute
+// (zst == nullptr) or from the stored fp32 logits (zst, row r at zst + (r - zrow0) * zst_ld; chunk0 = 0).
+int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, const float* zst, int64_t zst_ld,
+              int64_t zrow0, void* dh, int32_t dh_dt, int64_t dh_stride, bool dh_add, float* dw, int64_t dw_stride,
+              bool dw_add, cudaStream_t s) {
+  const tba_lmhead* x = k.x;
+  const int64_t d = x->d, V = x->vocab, C = k.C;
   const int64_t nt_v = (V + GB_BN - 1) / GB_BN, nt_d = (d + GB_BN - 1) / GB_BN;
-  for (int64_t ch = 0; ch < n_chunks; ++ch) {
-    const int64_t chunk0 = ch * C;
-    const dim3 ggrid((unsigned)((d + 63) / 64), (unsigned)(C / 64));
-    lmb_gather_t<<<ggrid, 256, 0, s>>>(static_cast<const uint16_t*>(x->hidden), x->hidden_stride, d, w.idx, n_valid,
-                                       0, chunk0, C, 1, w.hc, w.hct, C);
-    if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  const dim3 ggrid((unsigned)((d + 63) / 64), (unsigned)(C / 64));
+  lmb_gather_t<<<ggrid, 256, 0, s>>>(static_cast<const uint16_t*>(x->hidden), x->hidden_stride, d, k.w.idx, n_valid, 0,
+                                     chunk0, C, 1, k.w.hc, k.w.hct, C);
+  if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  dz.V = V;
+  dz.Vp = k.Vp;
+  dz.C = C;
+  dz.dz = k.w.dz;
+  dz.dzt = k.w.dzt;
+  int rc;
+  if (zst) {  // 2'. dz from the stored logits (chunk0 == 0: the chunk's own row list)
+    dz.idx = k.w.idx;
+    const dim3 grid((unsigned)((V + 127) / 128), (unsigned)(C / 64));
+    lmb_dz_from_z<<<grid, 256, 0, s>>>(dz, n_valid, C, zst, zst_ld, zrow0);
+    rc = launch_status();
+  } else {  // 2. dz tiles recomputed: M = the chunk's rows, N = V, K = d
     GemmArgs a{};
     a.n_valid = n_valid;
     a.chunk0 = chunk0;
     a.cap = C;
-    // 2. dz tiles: M = the chunk's rows, N = V, K = d
     a.M = C;
     a.N = V;
     a.K = d;
     a.dyn = 1;
-    a.swz = swz;
+    a.swz = k.swz;
     a.n_inner = 0;
     a.pol = 2;  // the weight tiles are shared by the row blocks in flight
-    a.dz = DzArgs{w.idx, stats, x->tokens, resid, coef, x->seq_len, gs, grad_out, sc, V, Vp, C, w.dz, w.dzt};
-    int rc = launch_gemm<EPI_DZ>(m_hc, m_w, a, (C / GB_BM) * nt_v, s);
-    if (rc) return rc;
-    if (dh) {  // 3. dH rows = dZ W: M = the chunk's rows, N = d, K = V
-      GemmArgs b{};
-      b.n_valid = n_valid;
-      b.chunk0 = chunk0;
-      b.cap = C;
-      b.M = C;
-      b.N = d;
-      b.K = V;
-      b.dyn = 1;
-      b.swz = swz;
-      b.n_inner = ninner & 1;
-      b.pol = pol & 3;
-      const int64_t esz = dh_dt == TBA_BF16 ? 2 : 4;
-      b.st = StoreArgs{dh, dh_stride, w.idx + chunk0, dh_dt == TBA_BF16, accumulate ? 1 : 0,
-                       ((reinterpret_cast<uintptr_t>(dh) | (uintptr_t)(dh_stride * esz)) & 15) == 0};
-      rc = launch_gemm<EPI_STORE>(m_dz, m_wt, b, (C / GB_BM) * nt_d, s);
-      if (rc) return rc;
-    }
-    if (dw) {  // 4. dW (+)= dZ^T H: M = V, N = d, K = the chunk's rows
-      GemmArgs b{};
-      b.n_valid = n_valid;
-      b.chunk0 = chunk0;
-      b.cap = C;
-      b.M = V;
-      b.N = d;
-      b.K = C;
-      b.dyn = 2;
-      b.swz = swz;
-      b.n_inner = (ninner >> 1) & 1;
-      b.pol = (pol >> 2) & 3;
-      b.st = StoreArgs{dw, dw_stride, nullptr, 0, (accumulate || ch > 0) ? 1 : 0,
-                       ((reinterpret_cast<uintptr_t>(dw) | (uintptr_t)(dw_stride * 4)) & 15) == 0};
-      rc = launch_gemm<EPI_STORE>(m_dzt, m_hct, b, nt_v * nt_d, s);
-      if (rc) return rc;
-    }
+    dz.idx = k.w.idx;
+    a.dz = dz;
+    rc = launch_gemm<EPI_DZ>(k.m_hc, k.m_w, a, (C / GB_BM) * nt_v, s);
   }
+  if (rc) return rc;
+  if (dh) {  // 3. dH rows = dZ W: M = the chunk's rows, N = d, K = V
+    GemmArgs b{};
+    b.n_valid = n_valid;
+    b.chunk0 = chunk0;
+    b.cap = C;
+    b.M = C;
+    b.N = d;
+    b.K = V;
+    b.dyn = 1;
+    b.swz = k.swz;
+    b.n_inner = k.ninner & 1;
+    b.pol = k.pol & 3;
+    const int64_t esz = dh_dt == TBA_BF16 ? 2 : 4;
+    b.st = StoreArgs{dh, dh_stride, k.w.idx + chunk0, dh_dt == TBA_BF16, dh_add ? 1 : 0,
+                     ((reinterpret_cast<uintptr_t>(dh) | (uintptr_t)(dh_stride * esz)) & 15) == 0};
+    rc = launch_gemm<EPI_STORE>(k.m_dz, k.m_wt, b, (C / GB_BM) * nt_d, s);
+    if (rc) return rc;
+  }
+  if (dw) {  // 4. dW (+)= dZ^T H: M = V, N = d, K = the chunk's rows
+    GemmArgs b{};
+    b.n_valid = n_valid;
+    b.chunk0 = chunk0;
+    b.cap = C;
+    b.M = V;
+    b.N = d;
+    b.K = C;
+    b.dyn = 2;
+    b.swz = k.swz;
+    b.n_inner = (k.ninner >> 1) & 1;
+    b.pol = (k.pol >> 2) & 3;
+    b.st = StoreArgs{dw, dw_stride, nullptr, 0, dw_add ? 1 : 0,
+                     ((reinterpret_cast<uintptr_t>(dw) | (uintptr_t)(dw_stride * 4)) & 15) == 0};
+    rc = launch_gemm<EPI_STORE>(k.m_dzt, k.m_hct, b, nt_v * nt_d, s);
+  }
+  return rc;
+}
+
+int lmb_zero_outputs(const tba_lmhead* x, int64_t rows, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
+                     int64_t dw_stride, bool zero_dw, cudaStream_t s) {
+  const size_t esz = dh_dt == TBA_BF16 ? 2 : 4;
+  if (dh && rows > 0 &&
+      cudaMemset2DAsync(dh, (size_t)dh_stride * esz, 0, (size_t)x->d * esz, (size_t)rows, s) != cudaSuccess)
+    return TBA_ERR_CUDA;
+  if (dw && zero_dw &&
+      cudaMemset2DAsync(dw, (size_t)dw_stride * 4, 0, (size_t)x->d * 4, (size_t)x->vocab, s) != cudaSuccess)
+    return TBA_ERR_CUDA;
   return TBA_OK;
+}
+
+DzArgs dz_args(const tba_lmhead* x, const float2* stats, const double* resid, const float* coef, double gs,
+               const double* grad_out, float sc) {
+  DzArgs z{};
+  z.stats = stats;
+  z.tokens = x->tokens;
+  z.resid = resid;
+  z.coef = coef;
+  z.T = x->seq_len;
+  z.gs = gs;
+  z.grad_out = grad_out;
+  z.sc = sc;
+  return z;
+}
+
+}  // namespace
+
+int launch_lmhead_bwd(const tba_lmhead* x, const float2* stats, const double* resid, const float* coef, double gs,
+                      const double* grad_out, float sc, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
+                      int64_t dw_stride, bool accumulate, int64_t chunk_rows, void* bws, cudaStream_t s) {
+  const int64_t rows = x->n_seq * x->seq_len;
+  if (!accumulate) {
+    const int rc = lmb_zero_outputs(x, rows, dh, dh_dt, dh_stride, dw, dw_stride, rows == 0, s);
+    if (rc) return rc;
+  }
+  if (rows == 0 || (!dh && !dw)) return TBA_OK;
+  LmbCtx k;
+  int rc = lmb_prepare(k, x, rows, lmhead_bwd_chunk(rows, chunk_rows), bws, dh != nullptr, s);
+  if (rc) return rc;
+  int* n_valid = k.w.idx + rows;
+  lmb_compact_rows<<<1, 1024, 0, s>>>(x->mask, rows, 0, k.w.idx, n_valid);
+  if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
+  const DzArgs dz = dz_args(x, stats, resid, coef, gs, grad_out, sc);
+  const int64_t n_chunks = (rows + k.C - 1) / k.C;
+  for (int64_t ch = 0; ch < n_chunks && !rc; ++ch)
+    rc = lmb_chunk(k, n_valid, ch * k.C, dz, nullptr, 0, 0, dh, dh_dt, dh_stride, accumulate, dw, dw_stride,
+                   accumulate || ch > 0, s);
+  return rc;
+}
+
+// ---- one-call forward + backward: chunks of whole groups, logits stored once (fp32) per chunk
+int64_t lmhead_fb_groups(int64_t groups, int64_t rows_per_group, int32_t groups_per_chunk) {
+  int64_t g = groups_per_chunk > 0 ? groups_per_chunk : LMB_DEFAULT_CHUNK / (rows_per_group > 0 ? rows_per_group : 1);
+  if (g < 1) g = 1;
+  if (g > groups) g = groups;
+  return g < 1 ? 1 : g;
+}
+
+size_t lmhead_fb_ws_bytes(int64_t n_seq, int64_t T, int64_t d, int64_t V, int32_t K, int32_t groups_per_chunk) {
+  const int64_t gpc = lmhead_fb_groups(n_seq / K, (int64_t)K * T, groups_per_chunk);
+  const int64_t R = gpc * K * T;  // rows per chunk
+  const int64_t C = lmhead_bwd_chunk(R, R);
+  return lmhead_bwd_ws_bytes(R, d, V, C) + align_up((size_t)R * (size_t)lmb_vp(V) * 4, 256) +
+         lmhead_partial_bytes(R, V);
+}
+
+int launch_lmhead_fwd_bwd(const tba_lmhead* x, const RowScale& rs, const WsLayout& w, const HeadArgs& ha0, int32_t K,
+                          double grad_scale, double inv_n_global, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
+                          int64_t dw_stride, bool accumulate, int32_t groups_per_chunk, void* bws,
+                          int32_t* dev_status, cudaStream_t s) {
+  const int64_t T = x->seq_len, groups = x->n_seq / K, rows = x->n_seq * T;
+  const int64_t gpc = lmhead_fb_groups(groups, (int64_t)K * T, groups_per_chunk);
+  const int64_t R = gpc * K * T, C = lmhead_bwd_chunk(R, R);
+  int rc = TBA_OK;
+  if (!accumulate) rc = lmb_zero_outputs(x, rows, dh, dh_dt, dh_stride, dw, dw_stride, false, s);
+  if (rc) return rc;
+  LmbCtx k;
+  rc = lmb_prepare(k, x, R, C, bws, dh != nullptr, s);
+  if (rc) return rc;
+  char* tail = static_cast<char*>(bws) + lmhead_bwd_ws_bytes(R, x->d, x->vocab, C);
+  float* zst = reinterpret_cast<float*>(tail);
+  void* part_ws = tail + align_up((size_t)R * (size_t)k.Vp * 4, 256);
+  int* n_valid = k.w.idx + R;
+  const DzArgs dz0 = dz_args(x, w.stats, ha0.resid, nullptr, grad_scale * rs.inv_temp, nullptr, rs.sc);
+  const int64_t n_chunks = (groups + gpc - 1) / gpc;
+  for (int64_t c = 0; c < n_chunks && !rc; ++c) {
+    const int64_t g0 = c * gpc, gc = (g0 + gpc <= groups) ? gpc : groups - g0;
+    const int64_t s0 = g0 * K, r0 = s0 * T, rc_rows = gc * K * T;
+    tba_lmhead xc = *x;
+    xc.hidden = static_cast<const uint16_t*>(x->hidden) + r0 * x->hidden_stride;
+    xc.tokens = x->tokens + r0;
+    xc.mask = x->mask + r0;
+    xc.n_seq = gc * K;
+    const WsLayout wc{w.stats + r0, w.lp + r0, w.group_sq + g0, nullptr, nullptr};
+    // forward of the chunk, logits kept (row r0 + i at zst + i * Vp)
+    rc = launch_lmhead_rows(&xc, part_ws, wc, rs, dev_status, s, zst, k.Vp);
+    if (rc) break;
+    HeadArgs ha = ha0;
+    ha.n_seq = xc.n_seq;
+    ha.ref_logp += s0;
+    ha.log_reward += s0;
+    ha.seq_logp += s0;
+    ha.n_tokens += s0;
+    ha.log_z += g0;
+    ha.resid += s0;
+    ha.group_sq = wc.group_sq;
+    if (ha.log_z_param) ha.log_z_param += g0;
+    rc = launch_seq_head(true, wc, xc.mask, ha, s);  // wc.counter == NULL: no per-chunk reduction
+    if (rc) break;
+    // backward of the chunk from the stored logits
+    lmb_compact_rows<<<1, 1024, 0, s>>>(xc.mask, rc_rows, r0, k.w.idx, n_valid);
+    if ((rc = launch_status())) break;
+    rc = lmb_chunk(k, n_valid, 0, dz0, zst, k.Vp, r0, dh, dh_dt, dh_stride, accumulate, dw, dw_stride,
+                   accumulate || c > 0, s);
+  }
+  if (!rc) rc = launch_tb_finish(w.group_sq, groups, x->n_seq, inv_n_global, ha0.partial, s);
+  return rc;
 }
 
 }  // namespace tba

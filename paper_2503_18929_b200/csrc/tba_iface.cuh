@@ -343,8 +343,9 @@ int launch_fused(FusedArgs& a, int32_t in_dtype, int32_t out_dtype, int tpr_f, i
 // lmhead.cu — a1 from hidden states: tcgen05 LM-head GEMM with the online log-softmax in its
 // epilogue + the fixed-order group combine; writes w.stats / w.lp like launch_fwd_rows.
 size_t lmhead_partial_bytes(int64_t rows, int64_t V);
+// zst (nullable): also store the fp32 logits, row r at zst + r * zst_ld (16-byte aligned rows).
 int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
-                       cudaStream_t s);
+                       cudaStream_t s, float* zst = nullptr, int64_t zst_ld = 0);
 
 // lmhead_bwd.cu — backward through the LM head (dz recomputed on the tensor cores, dH = dZ W,
 // dW (+)= dZ^T H) over compacted chunks of valid rows. Per-row coefficient c_r = gs * g *
@@ -354,6 +355,14 @@ size_t lmhead_bwd_ws_bytes(int64_t rows, int64_t d, int64_t V, int64_t chunk_row
 int launch_lmhead_bwd(const tba_lmhead* x, const float2* stats, const double* resid, const float* coef, double gs,
                       const double* grad_out, float sc, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
                       int64_t dw_stride, bool accumulate, int64_t chunk_rows, void* bws, cudaStream_t s);
+// One-call forward + backward from hidden states over chunks of whole groups: per chunk the forward
+// (logits also stored in fp32), the Eq. 4/5 head, dz from the stored logits, dH and dW; then the
+// fixed-order loss reduction into ha0.partial. ha0 = tb_head_args of the whole call.
+size_t lmhead_fb_ws_bytes(int64_t n_seq, int64_t T, int64_t d, int64_t V, int32_t K, int32_t groups_per_chunk);
+int launch_lmhead_fwd_bwd(const tba_lmhead* x, const RowScale& rs, const WsLayout& w, const HeadArgs& ha0, int32_t K,
+                          double grad_scale, double inv_n_global, void* dh, int32_t dh_dt, int64_t dh_stride, float* dw,
+                          int64_t dw_stride, bool accumulate, int32_t groups_per_chunk, void* bws,
+                          int32_t* dev_status, cudaStream_t s);
 
 // deferred.cu — a1 + the unscaled gradient in one pass per row.
 int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,

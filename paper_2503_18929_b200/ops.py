@@ -579,6 +579,54 @@ def lmhead_tbap_bwd(hidden, weight, tokens, mask, workspace, coef, n_tok_global:
     return dhidden, dweight
 
 
+def lmhead_fwd_bwd_workspace_bytes(n_seq: int, seq_len: int, d: int, vocab: int, K: int,
+                                   groups_per_chunk: int = 0) -> int:
+    return int(_lib.load().tba_lmhead_fwd_bwd_workspace_bytes(int(n_seq), int(seq_len), int(d), int(vocab), int(K),
+                                                              int(groups_per_chunk)))
+
+
+def lmhead_vargrad_fwd_bwd(hidden, weight, tokens, mask, ref_logp, log_reward, beta: float, K: int,
+                           n_seq_global: float, *, grad_out: float = 1.0, inv_temp: float = 1.0, log_z_param=None,
+                           dhidden=None, dweight=None, dhidden_dtype=None, want_dhidden: bool = True,
+                           want_dweight: bool = True, accumulate: bool = False, groups_per_chunk: int = 0,
+                           workspace=None, bwd_workspace=None, out: _Fwd | None = None,
+                           check_status: bool = _CHECK):
+    """TB loss and its gradient through the LM head in one call (tba_lmhead_tb_loss_fwd_bwd): chunks of
+    whole groups, the chunk's logits stored once in fp32 and reused by the gradient pass.
+    grad_out (host float) scales the gradient: grad_scale = 2 grad_out / n_seq_global.
+    Returns (_Fwd, dhidden, dweight[, d_log_z])."""
+    L = _lib.load()
+    x = make_lmhead(hidden, weight, tokens, mask)
+    N, T, d = hidden.shape
+    V = weight.shape[0]
+    dev = hidden.device
+    for name, t in (("ref_logp", ref_logp), ("log_reward", log_reward)):
+        if t.shape != (N,) or t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous fp64 [N] tensor on {dev}")
+    dhidden, dweight, (dhp, dht, dhs), (dwp, dws) = _lm_grad_bufs(hidden, weight, dhidden, dweight, dhidden_dtype,
+                                                                  want_dhidden, want_dweight)
+    o = out or _Fwd(N, K, dev)
+    ws = workspace if workspace is not None else _lm_workspace(dev, N, T, V)
+    if bwd_workspace is None:
+        bwd_workspace = torch.empty(max(lmhead_fwd_bwd_workspace_bytes(N, T, d, V, K, groups_per_chunk), 256),
+                                    dtype=torch.uint8, device=dev)
+    opts = _opts(inv_temp, log_z_param)
+    d_log_z = torch.empty(N // K, dtype=torch.float64, device=dev) if log_z_param is not None else None
+    st = _status(dev) if check_status else None
+    with torch.cuda.device(dev):
+        check(L.tba_lmhead_tb_loss_fwd_bwd(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
+                                           ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K),
+                                           float(n_seq_global), 2.0 * float(grad_out) / float(n_seq_global),
+                                           int(groups_per_chunk), ws.data_ptr(), o.seq_logp.data_ptr(),
+                                           o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None,
+                                           o.resid.data_ptr(), o.partial.data_ptr(), dhp, dht, dhs, dwp, dws,
+                                           int(bool(accumulate)), _ptr(d_log_z), bwd_workspace.data_ptr(), _ptr(st),
+                                           _stream(dev)), "tba_lmhead_tb_loss_fwd_bwd")
+    if st is not None:
+        _raise_dev_status(st, "tba_lmhead_tb_loss_fwd_bwd")
+    return (o, dhidden, dweight) if d_log_z is None else (o, dhidden, dweight, d_log_z)
+
+
 class LmHeadTBLoss(torch.autograd.Function):
     """Eq. 5 (or Eq. 3 with a learned log Z) from hidden states through the LM head, logits never
     materialised: forward tba_lmhead_tb_loss_fwd, backward tba_lmhead_tb_loss_bwd (dhidden, dW)."""

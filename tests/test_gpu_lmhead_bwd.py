@@ -204,3 +204,42 @@ def test_lmhead_bwd_qwen_dims_sampled():
     dW = dz[:, vs].T @ H
     AW = np.abs(dz[:, vs]).T @ np.abs(H)
     check_grad(dw[torch.from_numpy(vs).cuda()].double().cpu().numpy(), dW, AW, N * T, "dweight")
+
+
+FB_CASES = [
+    ("pythia_chunks_of_1", W("pythia", B=3, K=4, T=53, V=5000, d=128), "normal", 1, 1.0, False),
+    ("ragged_temp_learned_z", W("rhomath", B=2, K=4, T=96, V=3000, d=64, len_lo=0, len_hi=96), "lattice", 1,
+     1 / 0.7, True),
+    ("gpt2_one_chunk", W("redteam", B=4, K=2, T=20, d=96), "normal", 0, 1.0, False),
+]
+
+
+@pytest.mark.parametrize("name,w,kind,gpc,inv_temp,learned", FB_CASES, ids=[c[0] for c in FB_CASES])
+def test_lmhead_fwd_bwd_one_call(name, w, kind, gpc, inv_temp, learned):
+    """tba_lmhead_tb_loss_fwd_bwd: forward outputs and dhidden bitwise equal to the two calls (same
+    tensor-core logits, same fixed-order reductions); dweight (summed over different row chunks)
+    within the oracle bound."""
+    dev, gi, H, Wh = inputs(w, 16, kind)
+    N, T, V = w.N, w.T, w.V
+    lz = torch.linspace(-1, 1, w.B, dtype=torch.float64, device="cuda") if learned else None
+    args = (dev["hidden"], dev["weight"], dev["tokens"], dev["mask"], dev["ref_logp"], dev["log_reward"], w.beta, w.K,
+            N)
+    r1 = tba.lmhead_vargrad_fwd_bwd(*args, inv_temp=inv_temp, log_z_param=lz, groups_per_chunk=gpc,
+                                    check_status=True)
+    o2, ws = tba.lmhead_vargrad_fwd(*args, inv_temp=inv_temp, log_z_param=lz, check_status=True)
+    r2 = tba.lmhead_vargrad_bwd(dev["hidden"], dev["weight"], dev["tokens"], dev["mask"], ws, o2.resid, 2.0 / N,
+                                inv_temp=inv_temp, log_z_param=lz, K=w.K)
+    torch.cuda.synchronize()
+    o1, dh1, dw1 = r1[:3]
+    for f in ("seq_logp", "n_tokens", "log_z", "resid", "partial"):
+        assert torch.equal(getattr(o1, f), getattr(o2, f)), f
+    assert torch.equal(dh1, r2[0])
+    if learned:
+        assert torch.equal(r1[3], r2[2])
+    z = O.lmhead_logits(H, Wh).reshape(N, T, V)
+    r = O.vargrad_head(z, gi["tokens"], gi["mask"], gi["ref_logp"], gi["log_reward"], w.beta, w.K,
+                       inv_temp=inv_temp, log_z=None if lz is None else lz.cpu().numpy())
+    assert abs(o1.partial[0].item() - r["loss"]) <= max(1e-4 * abs(r["loss"]), 1e-5)
+    dH, dW, AH, AW = oracle_grads(H, Wh, r["dlogits"].reshape(N * T, V))
+    check_grad(dh1.double().cpu().numpy().reshape(N * T, -1), dH, AH, V, "dhidden")
+    check_grad(dw1.double().cpu().numpy(), dW, AW, N * T, "dweight")
