@@ -379,11 +379,21 @@ def lmhead_train_bench(args, w, tba, torch, dist, dev, world, rank, group):
     out = tba.ops._Fwd(N, K, dev)
     dh = torch.empty((N, T, d), dtype=torch.bfloat16, device=dev)
     dw = torch.empty((V, d), dtype=torch.float32, device=dev)
+    fb_ws = torch.empty(tba.lmhead_fwd_bwd_workspace_bytes(N, T, d, V, K, args.lm_groups), dtype=torch.uint8,
+                        device=dev)
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     marks = {}
+    one_call = args.lm_schedule == "one-call"
 
-    def step(rec=False):
+    def step_one(rec=False):
+        tba.lmhead_vargrad_fwd_bwd(hidden, weight, tokens, mask, ref, rew, w.beta, K, n_global, dhidden=dh,
+                                   dweight=dw, groups_per_chunk=args.lm_groups, workspace=ws, bwd_workspace=fb_ws,
+                                   out=out, check_status=False)
+        if group is not None:
+            dist.all_reduce(out.partial, group=group)
+
+    def step_two(rec=False):
         if rec:
             marks["a"].record(stream)
         tba.lmhead_vargrad_fwd(hidden, weight, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
@@ -397,6 +407,7 @@ def lmhead_train_bench(args, w, tba, torch, dist, dev, world, rank, group):
         if rec:
             marks["c"].record(stream)
 
+    step = step_one if one_call else step_two
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -420,9 +431,9 @@ def lmhead_train_bench(args, w, tba, torch, dist, dev, world, rank, group):
     if group is not None:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
     ms = ms.item()
-    # phase split (one extra step with events between the calls)
+    # phase split of the two-call schedule (one extra step with events between the calls)
     marks.update(a=ev(), b=ev(), c=ev())
-    step(rec=True)
+    step_two(rec=True)
     torch.cuda.synchronize()
     fwd_ms, bwd_ms = marks["a"].elapsed_time(marks["b"]), marks["b"].elapsed_time(marks["c"])
     loss = out.partial[0].item()
@@ -456,12 +467,19 @@ def lmhead_train_bench(args, w, tba, torch, dist, dev, world, rank, group):
             torch.cuda.synchronize()
             return a.elapsed_time(b) / n
         unfused()
+        other = step_two if one_call else step_one
         n = max(2, args.steps // 4)
-        fz, uf = [], []
+        fz, uf, ot = [], [], []
         for _ in range(3):
             fz.append(timed(step, n))
             uf.append(timed(unfused, n))
+            ot.append(timed(other, n))
         med = statistics.median
+        variants["two_call" if one_call else "one_call"] = {
+            "ms_per_step": med(ot), "ms_paired_this_schedule": med(fz), "value": valid / (med(ot) / 1e3),
+            "unit": "tokens/s",
+            "what": ("tba_lmhead_tb_loss_fwd + tba_lmhead_tb_loss_bwd (z recomputed by a 4th GEMM)" if one_call else
+                     "tba_lmhead_tb_loss_fwd_bwd (chunks of whole groups, logits stored in fp32 once)")}
         variants["unfused_cublas"] = {
             "ms_per_step": med(uf), "fused_ms_paired": med(fz), "fused_over_unfused": med(fz) / med(uf),
             "value": valid / (med(uf) / 1e3), "unit": "tokens/s", "pairs": 3, "steps_per_run": n,
@@ -482,21 +500,27 @@ def lmhead_train_bench(args, w, tba, torch, dist, dev, world, rank, group):
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (tba_synth hidden states / LM-head weight, DESIGN.md §6)",
             "config": {"workload": w.name, "objective": "lmhead_train", "note": w.note, "B_per_rank": B, "K": K,
-                       "T": T, "V": V, "d": d, "beta": w.beta, "rows_per_rank": rows, "chunk_rows": args.lm_chunk,
+                       "T": T, "V": V, "d": d, "beta": w.beta, "rows_per_rank": rows, "schedule": args.lm_schedule,
+                       "groups_per_chunk": args.lm_groups, "chunk_rows": args.lm_chunk,
                        "dhidden_dtype": "bf16", "dweight_dtype": "fp32", "parallelism": f"group-sharded x{world}",
                        "l2": "weight 1.09 GB + hidden 0.47 GB + dz chunks per rank >> 126 MB L2; no flush needed"},
-            "roofline": {"bound": "tensor", "kernel": "whole step (lmhead_fwd, tc_gemm<DZ>, 2x tc_gemm<STORE>, "
-                                                      "gathers, combine, head)",
+            "roofline": {"bound": "tensor", "kernel": "whole step (lmhead_fwd, 2x tc_gemm<STORE>, dz pass / "
+                                                      "tc_gemm<DZ>, gathers, combine, head)",
                          "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
                          "frac_of_sustained_peak": tf / peak_sus, "peak_source": src,
                          "traffic": None, "algorithmic_flops_per_launch": flops, "avg_launch_ms": ms,
-                         "executed_flops": 4 * gemm,
-                         "note": "algorithmic = 3 GEMMs; the backward recomputes z (a 4th) instead of storing it"},
-            "kernels": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms},
+                         "executed_flops": (3 if one_call else 4) * gemm,
+                         "note": "algorithmic = 3 GEMMs; the one-call schedule stores z (fp32, per chunk of whole "
+                                 "groups), the two-call backward recomputes it (a 4th GEMM)"},
+            "kernels": {"two_call_fwd_ms": fwd_ms, "two_call_bwd_ms": bwd_ms},
             "clocks": clk.summary(), "e2e": None, "cpu_baseline": None, "variants": variants,
-            # per step: lm_compact_units, lmhead_fwd, lmhead_combine, seq_head; lmb_compact_rows, W^T gather;
-            # per chunk: H gather, tc_gemm<DZ>, tc_gemm<STORE> x2 (cudaMemset launches not counted)
-            "gpu_launches": args.steps * (6 + 4 * -(-rows // (args.lm_chunk if args.lm_chunk > 0 else 16384))),
+            # one-call: per step W^T gather, tb_finish; per chunk lm_compact_units, lmhead_fwd, lmhead_combine,
+            # seq_head, lmb_compact_rows, H gather, lmb_dz_from_z, tc_gemm<STORE> x2. Two-call: per step
+            # lm_compact_units, lmhead_fwd, lmhead_combine, seq_head, lmb_compact_rows, W^T gather; per chunk
+            # H gather, tc_gemm<DZ>, tc_gemm<STORE> x2 (cudaMemset launches not counted)
+            "gpu_launches": args.steps * (
+                (2 + 9 * -(-B // (args.lm_groups if args.lm_groups > 0 else max(1, 16384 // (K * T))))) if one_call
+                else (6 + 4 * -(-rows // (args.lm_chunk if args.lm_chunk > 0 else 16384)))),
             "loss": loss,
         }
         print(json.dumps(line), flush=True)
@@ -532,6 +556,10 @@ def main():
                     help="process-group backend for N > 1 (gloo + --share-gpu only to test the multi-rank flow on 1 GPU)")
     ap.add_argument("--share-gpu", action="store_true")
     ap.add_argument("--lm-chunk", type=int, default=0, help="rows per chunk of the LM-head backward (0 = 16384)")
+    ap.add_argument("--lm-groups", type=int, default=0,
+                    help="groups per chunk of the one-call LM-head fwd+bwd (0 = as many as fit 16384 rows)")
+    ap.add_argument("--lm-schedule", default="one-call", choices=["one-call", "two-call"],
+                    help="lmhead_train: tba_lmhead_tb_loss_fwd_bwd, or tba_lmhead_tb_loss_fwd + _bwd")
     ap.add_argument("--objective", default="vargrad", choices=["vargrad", "tbap", "lmhead", "lmhead_train"],
                     help="vargrad: Eq. 5 (the north-star head); tbap: the TBA' token-level rule (Eq. 16); "
                          "lmhead: the Eq. 4/5 forward from hidden states with the LM head fused (NEXT 3); "

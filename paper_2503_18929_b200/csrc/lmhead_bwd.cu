@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256) lmb_gather_t(const uint16_t* __restrict__
                                                     int64_t n_static, int64_t chunk0, int64_t cap, int pad,
                                                     uint16_t* __restrict__ dst_rm, uint16_t* __restrict__ dst_t,
                                                     int64_t ld_t) {
-  __shared__ uint16_t tile[64][72];
+  __shared__ uint16_t tile[64][66];  // 33-word rows: the column reads below are conflict-free
   const int64_t n = n_valid ? chunk_count(n_valid, chunk0, cap) : n_static;
   const int64_t n_pad = pad ? (n + 127) / 128 * 128 : n;
   const int64_t i0 = (int64_t)blockIdx.y * 64, k0 = (int64_t)blockIdx.x * 64;
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256) lmb_gather_t(const uint16_t* __restrict__
 // (rows i in [n, n rounded up to 128) are written as 0 so the GEMM tiles over them read zeros).
 __global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __restrict__ n_valid, int64_t cap,
                                                      const float* __restrict__ zst, int64_t zst_ld, int64_t zrow0) {
-  __shared__ uint16_t tile[64][136];
+  __shared__ uint16_t tile[64][130];  // 65-word rows: the column reads below hit distinct banks
   __shared__ float s_c[64], s_m2[64], s_l2s[64];
   __shared__ long long s_y[64], s_off[64];
   const int64_t n = chunk_count(n_valid, 0, cap);
@@ -474,7 +474,9 @@ __global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __rest
     }
     const uint32_t lo = pack_bf16x2(d[0], d[1]), hi = pack_bf16x2(d[2], d[3]);
     if (v + 4 <= z.Vp && i < cap) *reinterpret_cast<uint2*>(z.dz + i * z.Vp + v) = make_uint2(lo, hi);
-    *reinterpret_cast<uint2*>(&tile[rl][cl]) = make_uint2(lo, hi);
+    uint32_t* tp = reinterpret_cast<uint32_t*>(&tile[rl][cl]);
+    tp[0] = lo;
+    tp[1] = hi;
   }
   __syncthreads();
   // dz^T: 128 vocabulary rows of 64 chunk rows (128 B each): 8 threads x 16 B per row

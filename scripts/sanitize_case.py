@@ -55,9 +55,17 @@ hid = torch.empty((wl.N, wl.T, wl.d), dtype=torch.bfloat16, device="cuda")
 wt = torch.empty((wl.V, wl.d), dtype=torch.bfloat16, device="cuda")
 syn.fill_bf16_cuda(hid.view(wl.N * wl.T, wl.d), 2, "hidden", 0)
 syn.fill_bf16_cuda(wt, 2, "weight", 0)
-ol, _ = tba.lmhead_vargrad_fwd(hid, wt, torch.from_numpy(gl["tokens"]).cuda(), torch.from_numpy(gl["mask"]).cuda(),
+ol, lws = tba.lmhead_vargrad_fwd(hid, wt, torch.from_numpy(gl["tokens"]).cuda(), torch.from_numpy(gl["mask"]).cuda(),
                                torch.from_numpy(gl["ref_logp"]).cuda(), torch.from_numpy(gl["log_reward"]).cuda(),
                                wl.beta, wl.K, float(wl.N), check_status=True)
+# LM-head backward: two-call (GEMM recompute of dz, chunks of 128 rows) and one-call (stored logits)
+dh, dw = tba.lmhead_vargrad_bwd(hid, wt, torch.from_numpy(gl["tokens"]).cuda(), torch.from_numpy(gl["mask"]).cuda(),
+                                lws, ol.resid, 2.0 / wl.N, chunk_rows=128)
+o1, dh1, dw1 = tba.lmhead_vargrad_fwd_bwd(hid, wt, torch.from_numpy(gl["tokens"]).cuda(),
+                                          torch.from_numpy(gl["mask"]).cuda(), torch.from_numpy(gl["ref_logp"]).cuda(),
+                                          torch.from_numpy(gl["log_reward"]).cuda(), wl.beta, wl.K, float(wl.N),
+                                          groups_per_chunk=1, check_status=True)
 torch.cuda.synchronize()
-print("lmhead loss", ol.partial[0].item())
+assert torch.equal(dh, dh1)
+print("lmhead loss", ol.partial[0].item(), "dW sum", float(dw.sum().item()), float(dw1.sum().item()))
 print("sanitize cases done")
