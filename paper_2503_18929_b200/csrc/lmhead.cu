@@ -40,16 +40,6 @@ __device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* 
       : "memory");
 }
 
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
 // Commit arriving on the barrier at `bar`'s offset in every CTA of `mask`.
 __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -349,38 +339,6 @@ constexpr int L2_STAGE_BYTES = L2_A_BYTES + L2_B_BYTES;
 constexpr size_t L2_SMEM = 1024 + (size_t)L2_STAGES * L2_STAGE_BYTES + 256;
 constexpr uint32_t L2_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
                               ((uint32_t)((2 * LM_BM) >> 4) << 24);
-constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address -> the leader CTA's copy
-
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
-                                                 uint64_t pol, bool hint) {
-  if (hint)
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & kPeerBitMask), "l"(pol)
-        : "memory");
-  else
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar & kPeerBitMask)
-        : "memory");
-}
-
-__device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(L2_IDESC), "r"(accumulate));
-}
-
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
 
 __global__ void __launch_bounds__(LM_THREADS, 1)
     lmhead_fwd_2sm(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
@@ -475,7 +433,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
             const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * L2_A_BYTES));
             const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * L2_B_BYTES));
 #pragma unroll
-            for (int k = 0; k < LM_BK / 16; ++k) umma_bf16_pair(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+            for (int k = 0; k < LM_BK / 16; ++k) umma_bf16_pair<L2_IDESC>(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
             umma_commit_pair(&empty[stage]);
             if (++stage == L2_STAGES) {
               stage = 0;

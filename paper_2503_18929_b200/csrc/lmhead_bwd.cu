@@ -341,6 +341,173 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
   }
 }
 
+// cta_group::2 form of tc_gemm<EPI_STORE>: an SM pair (cluster of 2) computes a 256 x 256 tile per
+// MMA (M = 256 across the pair). Each CTA loads its 128 rows of A and its half (128 rows) of the
+// B tile per stage, so per SM only 32 KB (2/3 of the single-SM kernel's 48 KB) move from L2 per
+// 128 x 256 x 64 of MMA work. Both CTAs' TMA loads signal the leader's full barrier; the leader's
+// lane issues the MMA, whose commits arrive on both CTAs' barriers; the epilogue warps of both CTAs
+// release an accumulator on the leader's barrier (count 8). Same arithmetic per output element
+// as tc_gemm (one K-ordered fp32 accumulation), so results are bitwise equal.
+constexpr int G2_STAGES = 6;
+constexpr int G2_A_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's 128 rows of A
+constexpr int G2_B_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's half of the 256-row B tile
+constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
+constexpr size_t G2_SMEM = 1024 + (size_t)G2_STAGES * G2_STAGE_BYTES + 256;
+constexpr uint32_t G2_IDESC = tc_idesc_bf16(256, GB_BN);
+
+__global__ void __launch_bounds__(GB_THREADS, 1)
+    tc_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + G2_STAGES * G2_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_STAGES * G2_STAGE_BYTES);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int64_t pair0 = blockIdx.x / 2, n_pairs = gridDim.x / 2;
+
+  int64_t M = a.M, K = a.K;
+  if (a.dyn) {
+    const int64_t n_c = chunk_count(a.n_valid, a.chunk0, a.cap);
+    if (a.dyn == 1) M = n_c;
+    else K = n_c;
+  }
+  Tiles g;
+  g.n_mt = (M + 255) / 256;
+  g.n_nt = (a.N + GB_BN - 1) / GB_BN;
+  g.nkb = (K + TC_BK - 1) / TC_BK;
+  g.swz = (a.swz + 1) / 2;
+  g.n_inner = a.n_inner;
+  const int64_t n_tiles = g.n_mt * g.n_nt;
+  const bool has_k = g.nkb > 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < G2_STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&tfull[q], 1);
+      mbar_init(&tempty[q], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && has_k) {  // ---- TMA producer (both CTAs)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      const uint64_t pol_a = l2_policy(a.pol & 1), pol_b = l2_policy(a.pol & 2);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = pair0; t < n_tiles; t += n_pairs) {
+        int64_t mb, nb;
+        tile_of(g, t, mb, nb);
+        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (leader) mbar_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
+          tma_load_2d_pair(smem_u32(sA + stage * G2_A_BYTES), &tmA, (int)(kb * TC_BK), (int)(mb * 256 + crank * 128),
+                           smem_u32(&full[stage]), pol_a, true);
+          tma_load_2d_pair(smem_u32(sB + stage * G2_B_BYTES), &tmB, (int)(kb * TC_BK),
+                           (int)(nb * GB_BN + crank * 128), smem_u32(&full[stage]), pol_b, true);
+          if (++stage == G2_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader && has_k) {  // ---- MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t j = 0;
+      for (int64_t t = pair0; t < n_tiles; t += n_pairs, ++j) {
+        const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+        mbar_wait(&tempty[acc], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * GB_BN;
+        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * G2_A_BYTES));
+          const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * G2_B_BYTES));
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) umma_bf16_pair<G2_IDESC>(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == G2_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {  // ---- epilogue (both CTAs): release on the leader's tempty
+    const int q = warp & 3;
+    const int row_in = q * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
+    uint32_t tempty_leader;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(tempty_leader) : "r"(smem_u32(tempty)));
+    const StoreArgs& st = a.st;
+    uint32_t j = 0;
+    for (int64_t t = pair0; t < n_tiles; t += n_pairs, ++j) {
+      int64_t mb, nb;
+      tile_of(g, t, mb, nb);
+      const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+      const int64_t m = mb * 256 + (int64_t)crank * 128 + row_in;
+      if (has_k) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+      }
+      const bool in = m < M;
+      const int64_t orow = in ? (st.row_map ? (int64_t)st.row_map[m] : m) : 0;
+#pragma unroll 1
+      for (int cc = 0; cc < GB_BN / 32; ++cc) {
+        const int64_t n0 = nb * GB_BN + cc * 32;
+        if (n0 >= a.N) break;  // warp-uniform
+        float v[32];
+        if (has_k) {
+          tmem_ld32(lane_addr + acc * GB_BN + cc * 32, v);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0.f;
+        }
+        if (in && (has_k || !st.add)) store_row32(st, orow, n0, a.N, v);
+      }
+      if (has_k) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader + acc * 8u)
+                       : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 // Ascending list of the valid rows (mask != 0), stored as r0 + row: one CTA, chunks of 1024 rows,
 // ballot + warp scan.
 __global__ void __launch_bounds__(1024) lmb_compact_rows(const uint8_t* __restrict__ mask, int64_t rows, int64_t r0,
@@ -536,6 +703,38 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
   return launch_status();
 }
 
+int launch_gemm2(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int64_t max_pair_tiles,
+                 cudaStream_t s) {
+  static bool attr[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
+  if (!attr[dev]) {
+    if (cudaFuncSetAttribute(tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2_SMEM) != cudaSuccess)
+      return TBA_ERR_CUDA;
+    attr[dev] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(GB_THREADS);
+  cfg.dynamicSmemBytes = G2_SMEM;
+  cfg.stream = s;
+  int64_t pairs = device_sms() / 2;
+  cfg.gridDim = dim3((unsigned)(pairs * 2));
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, tc_gemm2, &cfg) == cudaSuccess && ncl > 0 && ncl < pairs) pairs = ncl;
+  if (pairs > max_pair_tiles) pairs = max_pair_tiles;
+  if (pairs < 1) pairs = 1;
+  cfg.gridDim = dim3((unsigned)(pairs * 2));
+  if (cudaLaunchKernelEx(&cfg, tc_gemm2, ma, mb, a) != cudaSuccess) return TBA_ERR_CUDA;
+  return TBA_OK;
+}
+
 }  // namespace
 
 int64_t lmhead_bwd_chunk(int64_t rows, int64_t chunk_rows) {
@@ -562,13 +761,15 @@ struct LmbCtx {
   int64_t C, Vp;
   LmbWs w;
   CUtensorMap m_hc, m_w, m_dz, m_wt, m_dzt, m_hct;
-  int swz, ninner, pol;
+  int swz, ninner, pol, pair;  // pair: bit 0 dH, bit 1 dW on the cta_group::2 kernel
+  CUtensorMap m_wt2, m_hct2;   // B operands with 128-row boxes for the pair kernel (A boxes are 128 rows already)
 };
 
 int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, void* bws, bool need_wt, cudaStream_t s) {
   static const int swz = [] { int v = env_int("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
   static const int ninner = env_int("TBA_LMB_NINNER", 3);
   static const int pol = env_int("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
+  static const int pair = env_int("TBA_LMB_2SM", 0);
   const int64_t d = x->d, V = x->vocab;
   k.x = x;
   k.C = C;
@@ -577,6 +778,7 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   k.swz = swz;
   k.ninner = ninner;
   k.pol = pol;
+  k.pair = pair;
   if (need_wt) {
     const dim3 grid((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64));
     lmb_gather_t<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x->weight), x->weight_stride, d, nullptr,
@@ -586,6 +788,8 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   if (!make_map(&k.m_hc, k.w.hc, C, d, d, GB_BM) || !make_map(&k.m_w, x->weight, V, d, x->weight_stride, GB_BN) ||
       !make_map(&k.m_dz, k.w.dz, C, V, k.Vp, GB_BM) || !make_map(&k.m_wt, k.w.wt, d, V, k.Vp, GB_BN) ||
       !make_map(&k.m_dzt, k.w.dzt, V, C, C, GB_BM) || !make_map(&k.m_hct, k.w.hct, d, C, C, GB_BN))
+    return TBA_ERR_CUDA;
+  if (pair && (!make_map(&k.m_wt2, k.w.wt, d, V, k.Vp, 128) || !make_map(&k.m_hct2, k.w.hct, d, C, C, 128)))
     return TBA_ERR_CUDA;
   return TBA_OK;
 }
@@ -645,7 +849,8 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
     const int64_t esz = dh_dt == TBA_BF16 ? 2 : 4;
     b.st = StoreArgs{dh, dh_stride, k.w.idx + chunk0, dh_dt == TBA_BF16, dh_add ? 1 : 0,
                      ((reinterpret_cast<uintptr_t>(dh) | (uintptr_t)(dh_stride * esz)) & 15) == 0};
-    rc = launch_gemm<EPI_STORE>(k.m_dz, k.m_wt, b, (C / GB_BM) * nt_d, s);
+    rc = (k.pair & 1) ? launch_gemm2(k.m_dz, k.m_wt2, b, (C / 256 + 1) * nt_d, s)
+                      : launch_gemm<EPI_STORE>(k.m_dz, k.m_wt, b, (C / GB_BM) * nt_d, s);
     if (rc) return rc;
   }
   if (dw) {  // 4. dW (+)= dZ^T H: M = V, N = d, K = the chunk's rows
@@ -662,7 +867,8 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
     b.pol = (k.pol >> 2) & 3;
     b.st = StoreArgs{dw, dw_stride, nullptr, 0, dw_add ? 1 : 0,
                      ((reinterpret_cast<uintptr_t>(dw) | (uintptr_t)(dw_stride * 4)) & 15) == 0};
-    rc = launch_gemm<EPI_STORE>(k.m_dzt, k.m_hct, b, nt_v * nt_d, s);
+    rc = (k.pair & 2) ? launch_gemm2(k.m_dzt, k.m_hct2, b, ((V + 255) / 256) * nt_d, s)
+                      : launch_gemm<EPI_STORE>(k.m_dzt, k.m_hct, b, ((V + GB_BM - 1) / GB_BM) * nt_d, s);
   }
   return rc;
 }

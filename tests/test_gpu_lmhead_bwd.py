@@ -243,3 +243,35 @@ def test_lmhead_fwd_bwd_one_call(name, w, kind, gpc, inv_temp, learned):
     dH, dW, AH, AW = oracle_grads(H, Wh, r["dlogits"].reshape(N * T, V))
     check_grad(dh1.double().cpu().numpy().reshape(N * T, -1), dH, AH, V, "dhidden")
     check_grad(dw1.double().cpu().numpy(), dW, AW, N * T, "dweight")
+
+
+_PAIR_SCRIPT = r"""
+import sys, torch, dataclasses
+sys.path.insert(0, sys.argv[1])
+import paper_2503_18929_b200 as tba, tba_synth as syn
+w = dataclasses.replace(syn.WORKLOADS["pythia"], B=2, K=4, T=50, V=3000, d=320, len_lo=5, len_hi=50)
+gi = syn.group_inputs(w, 17, 0, w.B)
+h = torch.empty((w.N, w.T, w.d), dtype=torch.bfloat16, device="cuda")
+wt = torch.empty((w.V, w.d), dtype=torch.bfloat16, device="cuda")
+syn.fill_bf16_cuda(h.view(-1, w.d), 17, "hidden", 0)
+syn.fill_bf16_cuda(wt, 17, "weight", 0)
+dev = [torch.from_numpy(gi[k]).cuda() for k in ("tokens", "mask", "ref_logp", "log_reward")]
+o, dh, dw = tba.lmhead_vargrad_fwd_bwd(h, wt, *dev, w.beta, w.K, w.N, groups_per_chunk=1)
+torch.save({"dh": dh.cpu(), "dw": dw.cpu()}, sys.argv[2])
+"""
+
+
+def test_lmhead_bwd_pair_kernel_bitwise(tmp_path):
+    """TBA_LMB_2SM=3 (dH and dW on the cta_group::2 kernel) gives bitwise the single-SM results:
+    each output element is one K-ordered fp32 accumulation either way."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("0", "3"):
+        f = tmp_path / f"r{mode}.pt"
+        env = dict(os.environ, TBA_LMB_2SM=mode)
+        subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
+        out[mode] = torch.load(f)
+    assert torch.equal(out["0"]["dh"], out["3"]["dh"]) and torch.equal(out["0"]["dw"], out["3"]["dw"])
