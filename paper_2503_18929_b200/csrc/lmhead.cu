@@ -566,7 +566,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
                        cudaStream_t s, float* zst, int64_t zst_ld) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
-  const int mode = lm_mc();
+  const int mode = zst ? 1 : lm_mc();  // the logits store is written by the single-SM kernel only
   const int mc = mode == 1 ? 1 : 2;  // CTAs per cluster
   const int n_rb = (int)((rows + LM_BM - 1) / LM_BM);
   const int n_units_total = (n_rb + mc - 1) / mc;  // row-block units (pairs when mc = 2)
@@ -581,7 +581,6 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
   g.zst = zst;
   g.zst_ld = zst_ld;
-  if (zst && mode != 1) return TBA_ERR_INVALID_ARG;  // the stash is written by the single-SM kernel only
   CUtensorMap mh, mw;
   if (!make_map(&mh, x->hidden, rows, x->d, x->hidden_stride, LM_BM) ||
       !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN / mc))

@@ -348,15 +348,26 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
 // lane issues the MMA, whose commits arrive on both CTAs' barriers; the epilogue warps of both CTAs
 // release an accumulator on the leader's barrier (count 8). Same arithmetic per output element
 // as tc_gemm (one K-ordered fp32 accumulation), so results are bitwise equal.
-constexpr int G2_STAGES = 6;
-constexpr int G2_A_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's 128 rows of A
-constexpr int G2_B_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's half of the 256-row B tile
-constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
-constexpr size_t G2_SMEM = 1024 + (size_t)G2_STAGES * G2_STAGE_BYTES + 256;
+// NT = 2: each pair tile is 256 x 512 (two N = 256 MMAs per K step sharing the A stage; the two
+// accumulators hold one tile, so the epilogue is not overlapped with the next tile's MMAs — fine
+// when K is long): per SM 48 KB move from L2 per 128 x 512 x 64, half the single-SM kernel's rate.
+template <int NT>
+struct G2 {
+  static constexpr int STAGES = NT == 1 ? 6 : 4;
+  static constexpr int A_BYTES = 128 * TC_BK * 2;       // 16 KB: this CTA's 128 rows of A
+  static constexpr int B_BYTES = NT * 128 * TC_BK * 2;  // this CTA's halves of the NT 256-row B tiles
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static constexpr int NACC = 2 / NT;                   // accumulator buffers of NT x 256 columns
+};
 constexpr uint32_t G2_IDESC = tc_idesc_bf16(256, GB_BN);
 
+template <int NT>
 __global__ void __launch_bounds__(GB_THREADS, 1)
     tc_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs a) {
+  using C = G2<NT>;
+  constexpr int G2_STAGES = C::STAGES, G2_A_BYTES = C::A_BYTES, G2_B_BYTES = C::B_BYTES,
+                G2_STAGE_BYTES = C::STAGE_BYTES, NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
   }
   Tiles g;
   g.n_mt = (M + 255) / 256;
-  g.n_nt = (a.N + GB_BN - 1) / GB_BN;
+  g.n_nt = (a.N + NT * GB_BN - 1) / (NT * GB_BN);
   g.nkb = (K + TC_BK - 1) / TC_BK;
   g.swz = (a.swz + 1) / 2;
   g.n_inner = a.n_inner;
@@ -424,8 +435,10 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
           if (leader) mbar_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
           tma_load_2d_pair(smem_u32(sA + stage * G2_A_BYTES), &tmA, (int)(kb * TC_BK), (int)(mb * 256 + crank * 128),
                            smem_u32(&full[stage]), pol_a, true);
-          tma_load_2d_pair(smem_u32(sB + stage * G2_B_BYTES), &tmB, (int)(kb * TC_BK),
-                           (int)(nb * GB_BN + crank * 128), smem_u32(&full[stage]), pol_b, true);
+#pragma unroll
+          for (int u = 0; u < NT; ++u)
+            tma_load_2d_pair(smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2)), &tmB, (int)(kb * TC_BK),
+                             (int)((nb * NT + u) * GB_BN + crank * 128), smem_u32(&full[stage]), pol_b, true);
           if (++stage == G2_STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -439,17 +452,21 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
       uint32_t phase = 0;
       uint32_t j = 0;
       for (int64_t t = pair0; t < n_tiles; t += n_pairs, ++j) {
-        const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+        const uint32_t acc = j % NACC, aph = (j / NACC) & 1u;
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + acc * GB_BN;
+        const uint32_t d_tmem = tmem + acc * NT * GB_BN;
         for (int64_t kb = 0; kb < g.nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * G2_A_BYTES));
-          const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * G2_B_BYTES));
 #pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) umma_bf16_pair<G2_IDESC>(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+          for (int k = 0; k < TC_BK / 16; ++k)
+#pragma unroll
+            for (int u = 0; u < NT; ++u) {
+              const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2)));
+              umma_bf16_pair<G2_IDESC>(d_tmem + u * GB_BN, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+            }
           umma_commit_pair(&empty[stage]);
           if (++stage == G2_STAGES) {
             stage = 0;
@@ -470,7 +487,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
     for (int64_t t = pair0; t < n_tiles; t += n_pairs, ++j) {
       int64_t mb, nb;
       tile_of(g, t, mb, nb);
-      const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+      const uint32_t acc = j % NACC, aph = (j / NACC) & 1u;
       const int64_t m = mb * 256 + (int64_t)crank * 128 + row_in;
       if (has_k) {
         mbar_wait(&tfull[acc], aph);
@@ -479,12 +496,12 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
       const bool in = m < M;
       const int64_t orow = in ? (st.row_map ? (int64_t)st.row_map[m] : m) : 0;
 #pragma unroll 1
-      for (int cc = 0; cc < GB_BN / 32; ++cc) {
-        const int64_t n0 = nb * GB_BN + cc * 32;
+      for (int cc = 0; cc < NT * GB_BN / 32; ++cc) {
+        const int64_t n0 = nb * NT * GB_BN + cc * 32;
         if (n0 >= a.N) break;  // warp-uniform
         float v[32];
         if (has_k) {
-          tmem_ld32(lane_addr + acc * GB_BN + cc * 32, v);
+          tmem_ld32(lane_addr + acc * NT * GB_BN + cc * 32, v);
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0.f;
@@ -703,13 +720,15 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
   return launch_status();
 }
 
+template <int NT>
 int launch_gemm2(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int64_t max_pair_tiles,
                  cudaStream_t s) {
   static bool attr[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
   if (!attr[dev]) {
-    if (cudaFuncSetAttribute(tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2_SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(tc_gemm2<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2<NT>::SMEM) !=
+        cudaSuccess)
       return TBA_ERR_CUDA;
     attr[dev] = true;
   }
@@ -722,16 +741,16 @@ int launch_gemm2(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cfg.blockDim = dim3(GB_THREADS);
-  cfg.dynamicSmemBytes = G2_SMEM;
+  cfg.dynamicSmemBytes = G2<NT>::SMEM;
   cfg.stream = s;
   int64_t pairs = device_sms() / 2;
   cfg.gridDim = dim3((unsigned)(pairs * 2));
   int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, tc_gemm2, &cfg) == cudaSuccess && ncl > 0 && ncl < pairs) pairs = ncl;
+  if (cudaOccupancyMaxActiveClusters(&ncl, tc_gemm2<NT>, &cfg) == cudaSuccess && ncl > 0 && ncl < pairs) pairs = ncl;
   if (pairs > max_pair_tiles) pairs = max_pair_tiles;
   if (pairs < 1) pairs = 1;
   cfg.gridDim = dim3((unsigned)(pairs * 2));
-  if (cudaLaunchKernelEx(&cfg, tc_gemm2, ma, mb, a) != cudaSuccess) return TBA_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, tc_gemm2<NT>, ma, mb, a) != cudaSuccess) return TBA_ERR_CUDA;
   return TBA_OK;
 }
 
@@ -761,7 +780,7 @@ struct LmbCtx {
   int64_t C, Vp;
   LmbWs w;
   CUtensorMap m_hc, m_w, m_dz, m_wt, m_dzt, m_hct;
-  int swz, ninner, pol, pair;  // pair: bit 0 dH, bit 1 dW on the cta_group::2 kernel
+  int swz, ninner, pol, pair, wide;  // pair: bit 0 dH, bit 1 dW on the cta_group::2 kernel; wide: NT = 2
   CUtensorMap m_wt2, m_hct2;   // B operands with 128-row boxes for the pair kernel (A boxes are 128 rows already)
 };
 
@@ -769,7 +788,8 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   static const int swz = [] { int v = env_int("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
   static const int ninner = env_int("TBA_LMB_NINNER", 3);
   static const int pol = env_int("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
-  static const int pair = env_int("TBA_LMB_2SM", 0);
+  static const int pair = env_int("TBA_LMB_2SM", 3);  // measured: 196-203 ms vs 218-223 (one-call Qwen step)
+  static const int wide = env_int("TBA_LMB_NT2", 3);  // bit 0 dH, bit 1 dW: 256 x 512 pair tiles
   const int64_t d = x->d, V = x->vocab;
   k.x = x;
   k.C = C;
@@ -779,6 +799,7 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   k.ninner = ninner;
   k.pol = pol;
   k.pair = pair;
+  k.wide = wide;
   if (need_wt) {
     const dim3 grid((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64));
     lmb_gather_t<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x->weight), x->weight_stride, d, nullptr,
@@ -849,7 +870,8 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
     const int64_t esz = dh_dt == TBA_BF16 ? 2 : 4;
     b.st = StoreArgs{dh, dh_stride, k.w.idx + chunk0, dh_dt == TBA_BF16, dh_add ? 1 : 0,
                      ((reinterpret_cast<uintptr_t>(dh) | (uintptr_t)(dh_stride * esz)) & 15) == 0};
-    rc = (k.pair & 1) ? launch_gemm2(k.m_dz, k.m_wt2, b, (C / 256 + 1) * nt_d, s)
+    rc = (k.pair & 1) ? ((k.wide & 1) ? launch_gemm2<2>(k.m_dz, k.m_wt2, b, (C / 256 + 1) * nt_d, s)
+                                      : launch_gemm2<1>(k.m_dz, k.m_wt2, b, (C / 256 + 1) * nt_d, s))
                       : launch_gemm<EPI_STORE>(k.m_dz, k.m_wt, b, (C / GB_BM) * nt_d, s);
     if (rc) return rc;
   }
@@ -867,7 +889,8 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
     b.pol = (k.pol >> 2) & 3;
     b.st = StoreArgs{dw, dw_stride, nullptr, 0, dw_add ? 1 : 0,
                      ((reinterpret_cast<uintptr_t>(dw) | (uintptr_t)(dw_stride * 4)) & 15) == 0};
-    rc = (k.pair & 2) ? launch_gemm2(k.m_dzt, k.m_hct2, b, ((V + 255) / 256) * nt_d, s)
+    rc = (k.pair & 2) ? ((k.wide & 2) ? launch_gemm2<2>(k.m_dzt, k.m_hct2, b, ((V + 255) / 256) * nt_d, s)
+                                      : launch_gemm2<1>(k.m_dzt, k.m_hct2, b, ((V + 255) / 256) * nt_d, s))
                       : launch_gemm<EPI_STORE>(k.m_dzt, k.m_hct, b, ((V + GB_BM - 1) / GB_BM) * nt_d, s);
   }
   return rc;

@@ -262,16 +262,18 @@ torch.save({"dh": dh.cpu(), "dw": dw.cpu()}, sys.argv[2])
 
 
 def test_lmhead_bwd_pair_kernel_bitwise(tmp_path):
-    """TBA_LMB_2SM=3 (dH and dW on the cta_group::2 kernel) gives bitwise the single-SM results:
-    each output element is one K-ordered fp32 accumulation either way."""
+    """TBA_LMB_2SM=3 (dH and dW on the cta_group::2 kernel, with TBA_LMB_NT2=3 on 256 x 512 pair
+    tiles) gives bitwise the single-SM results: each output element is one K-ordered fp32
+    accumulation either way."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    for mode in ("0", "3"):
-        f = tmp_path / f"r{mode}.pt"
-        env = dict(os.environ, TBA_LMB_2SM=mode)
+    for mode, nt2 in (("0", "0"), ("3", "0"), ("3", "3")):
+        f = tmp_path / f"r{mode}{nt2}.pt"
+        env = dict(os.environ, TBA_LMB_2SM=mode, TBA_LMB_NT2=nt2)
         subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
-        out[mode] = torch.load(f)
-    assert torch.equal(out["0"]["dh"], out["3"]["dh"]) and torch.equal(out["0"]["dw"], out["3"]["dw"])
+        out[mode + nt2] = torch.load(f)
+    for k in ("30", "33"):  # 256 x 256 and 256 x 512 pair tiles
+        assert torch.equal(out["00"]["dh"], out[k]["dh"]) and torch.equal(out["00"]["dw"], out[k]["dw"]), k
