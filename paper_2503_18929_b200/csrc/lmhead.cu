@@ -99,6 +99,9 @@ __device__ __forceinline__ bool lm_unit_active(const uint8_t* __restrict__ mask,
 // one FMNMX (chunk max) and the pairwise FADD tree; the vocabulary-tail mask runs only in the
 // last tile and the z[y] gather only in the chunk that holds y. The partial is {R, S} with
 // S = sum 2^(z sc - fl(R sc)); lmhead_combine re-forms fl(R sc) with the same fp32 multiply.
+// NT = 2 (wide pair tiles): one accumulator of 2 x 256 columns holds vocabulary tiles t and t+1;
+// it is waited for before the first and released after the second (or after the group's last).
+template <int NT = 1>
 __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int grp, uint32_t& j, uint32_t tmem_lane,
                                                  int row_in, int lane, uint64_t* tfull, uint32_t tempty_addr,
                                                  bool cluster_arrive, const int64_t* __restrict__ tokens,
@@ -114,10 +117,15 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
   double S = 0.0;       // sum of 2^(z sc - Rs)
   float zy = 0.f;
   bool found = false;
-  for (int t = t0; t < t1; ++t, ++j) {
-    const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
-    mbar_wait(&tfull[acc], aph);
-    tc_fence_after();
+  constexpr int NACC = 2 / NT;
+  for (int t = t0; t < t1; ++t) {
+    const int u = (t - t0) % NT;  // sub-tile of the accumulator (t0 is a multiple of NT)
+    const uint32_t acc = j % NACC, aph = (j / NACC) & 1u;
+    if (u == 0) {
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+    }
+    const uint32_t col0 = (acc * NT + u) * LM_BN;
     const int64_t nb = (int64_t)t * LM_BN;
     const bool tail = nb + LM_BN > g.V;          // warp-uniform: only the last vocabulary tile
     const int64_t dyt = y - nb;
@@ -125,7 +133,7 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
 #pragma unroll 1
     for (int c = 0; c < LM_BN / 32; ++c) {
       float v[32];
-      tmem_ld32(tmem_lane + acc * LM_BN + c * 32, v);
+      tmem_ld32(tmem_lane + col0 + c * 32, v);
       if (g.zst && in_rows) {
         float* zp = g.zst + row * g.zst_ld + nb + c * 32;
         if (nb + c * 32 + 32 <= g.V) {
@@ -171,14 +179,17 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
         for (int i = 0; i < w; ++i) v[i] += v[i + w];
       S += (double)v[0];
     }
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t bar = tempty_addr + acc * 8u;
-      if (cluster_arrive)
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
-      else
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    if (u == NT - 1 || t + 1 == t1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bar = tempty_addr + acc * 8u;
+        if (cluster_arrive)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+        else
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+      }
+      ++j;
     }
   }
   if (in_rows) {
@@ -332,18 +343,26 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
 // kernel's operand traffic. Both CTAs' TMA loads signal the leader's full barrier; the leader's
 // lane issues the MMA and its commits arrive on both CTAs' barriers (multicast); the four
 // epilogue warps of both CTAs release an accumulator on the leader's barrier (count 8).
-constexpr int L2_STAGES = 6;
-constexpr int L2_A_BYTES = LM_BM * LM_BK * 2;        // 16 KB: this CTA's 128 hidden rows
-constexpr int L2_B_BYTES = (LM_BN / 2) * LM_BK * 2;  // 16 KB: this CTA's half of the weight tile
-constexpr int L2_STAGE_BYTES = L2_A_BYTES + L2_B_BYTES;
-constexpr size_t L2_SMEM = 1024 + (size_t)L2_STAGES * L2_STAGE_BYTES + 256;
-constexpr uint32_t L2_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LM_BN >> 3) << 17) |
-                              ((uint32_t)((2 * LM_BM) >> 4) << 24);
+// NT = 2: 256 x 512 pair tiles (two N = 256 MMAs per K step share the hidden stage; one
+// accumulator of 512 columns, so the softmax epilogue of a tile is not overlapped with the next
+// tile's MMAs): per SM 48 KB per 128 x 512 x 64 of work, half the single-SM kernel's L2 feed.
+template <int NT>
+struct L2Cfg {
+  static constexpr int STAGES = NT == 1 ? 6 : 4;
+  static constexpr int A_BYTES = LM_BM * LM_BK * 2;              // 16 KB: this CTA's 128 hidden rows
+  static constexpr int B_BYTES = NT * (LM_BN / 2) * LM_BK * 2;   // this CTA's halves of the NT weight tiles
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+};
+constexpr uint32_t L2_IDESC = tc_idesc_bf16(2 * LM_BM, LM_BN);
 
+template <int NT>
 __global__ void __launch_bounds__(LM_THREADS, 1)
     lmhead_fwd_2sm(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
                    const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
                    float2* __restrict__ part, float* __restrict__ zy_out) {
+  constexpr int L2_STAGES = L2Cfg<NT>::STAGES, L2_A_BYTES = L2Cfg<NT>::A_BYTES, L2_B_BYTES = L2Cfg<NT>::B_BYTES,
+                L2_STAGE_BYTES = L2Cfg<NT>::STAGE_BYTES, NACC = 2 / NT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -396,14 +415,17 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
         rb = g.act[rb];
         rb = rb * 2 + (int)crank;
         const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
-        for (int t = t0; t < t1; ++t) {
+        for (int t = t0; t < t1; t += NT) {
           for (int kb = 0; kb < g.nkb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1u);
             if (leader) mbar_expect_tx(&full[stage], 2 * L2_STAGE_BYTES);
             tma_load_2d_pair(smem_u32(sA + stage * L2_A_BYTES), &tmH, kb * LM_BK, rb * LM_BM, smem_u32(&full[stage]),
                              pol_h, (g.pol & 4) == 0);
-            tma_load_2d_pair(smem_u32(sB + stage * L2_B_BYTES), &tmW, kb * LM_BK, t * LM_BN + (int)crank * (LM_BN / 2),
-                             smem_u32(&full[stage]), pol_w, (g.pol & 4) == 0);
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+              tma_load_2d_pair(smem_u32(sB + stage * L2_B_BYTES + u * (L2_B_BYTES / NT)), &tmW, kb * LM_BK,
+                               (t + u) * LM_BN + (int)crank * (LM_BN / 2), smem_u32(&full[stage]), pol_w,
+                               (g.pol & 4) == 0);
             if (++stage == L2_STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -422,18 +444,22 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
         lm_item(g, nact, it, rb, grp);
         rb = g.act[rb];
         const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
-        for (int t = t0; t < t1; ++t, ++j) {
-          const uint32_t acc = j & 1u, aph = (j >> 1) & 1u;
+        for (int t = t0; t < t1; t += NT, ++j) {
+          const uint32_t acc = j % NACC, aph = (j / NACC) & 1u;
           mbar_wait(&tempty[acc], aph ^ 1u);
           tc_fence_after();
-          const uint32_t d_tmem = tmem + acc * LM_BN;
+          const uint32_t d_tmem = tmem + acc * NT * LM_BN;
           for (int kb = 0; kb < g.nkb; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * L2_A_BYTES));
-            const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * L2_B_BYTES));
 #pragma unroll
-            for (int k = 0; k < LM_BK / 16; ++k) umma_bf16_pair<L2_IDESC>(d_tmem, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+            for (int k = 0; k < LM_BK / 16; ++k)
+#pragma unroll
+              for (int u = 0; u < NT; ++u) {
+                const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * L2_B_BYTES + u * (L2_B_BYTES / NT)));
+                umma_bf16_pair<L2_IDESC>(d_tmem + u * LM_BN, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+              }
             umma_commit_pair(&empty[stage]);
             if (++stage == L2_STAGES) {
               stage = 0;
@@ -456,8 +482,8 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       lm_item(g, nact, it, rb, grp);
       rb = g.act[rb];
       rb = rb * 2 + (int)crank;
-      lm_epilogue_item(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, tempty_leader, true, tokens, rs, part,
-                       zy_out);
+      lm_epilogue_item<NT>(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, tempty_leader, true, tokens, rs,
+                           part, zy_out);
     }
   }
   __syncthreads();
@@ -556,9 +582,10 @@ size_t lmhead_partial_bytes(int64_t rows, int64_t V) {
          align_up((size_t)(blocks + 1) * sizeof(int), 256);
 }
 
-// TBA_LM_MC: 1 single-SM kernel, 2 cluster pair with weight multicast, 3 cta_group::2 pair.
+// TBA_LM_MC: 1 single-SM kernel, 2 cluster pair with weight multicast, 3 cta_group::2 pair (256 x 256
+// tiles), 4 cta_group::2 pair with 256 x 512 tiles.
 int lm_mc() {
-  static int v = [] { int x = env_int("TBA_LM_MC", 1); return (x == 2 || x == 3) ? x : 1; }();
+  static int v = [] { int x = env_int("TBA_LM_MC", 1); return (x >= 2 && x <= 4) ? x : 1; }();
   return v;
 }
 
@@ -566,7 +593,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
                        cudaStream_t s, float* zst, int64_t zst_ld) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
-  const int mode = zst ? 1 : lm_mc();  // the logits store is written by the single-SM kernel only
+  const int mode = lm_mc();
   const int mc = mode == 1 ? 1 : 2;  // CTAs per cluster
   const int n_rb = (int)((rows + LM_BM - 1) / LM_BM);
   const int n_units_total = (n_rb + mc - 1) / mc;  // row-block units (pairs when mc = 2)
@@ -575,6 +602,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.V = x->vocab;
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
   g.G = lm_g();
+  if (mode == 4 && (g.G & 1)) ++g.G;  // a wide tile holds two vocabulary tiles of one group
   g.swz = (lm_swz() + mc - 1) / mc;  // the raster counts row blocks: a pair unit holds two
   g.pol = env_int("TBA_LM_POL", 1) & 7;
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
@@ -595,11 +623,11 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.n_act = act + n_rb;
   lm_compact_units<<<1, 1024, 0, s>>>(x->mask, rows, mc, n_units_total, act, act + n_rb);
   if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
-  static bool attr[3][64] = {};  // per variant and device; benign race: idempotent
+  static bool attr[4][64] = {};  // per variant and device; benign race: idempotent
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
-  auto kern = mode == 3 ? lmhead_fwd_2sm : mode == 2 ? lmhead_fwd<2> : lmhead_fwd<1>;
-  const size_t smem = mode == 3 ? L2_SMEM : LM_SMEM;
+  auto kern = mode == 4 ? lmhead_fwd_2sm<2> : mode == 3 ? lmhead_fwd_2sm<1> : mode == 2 ? lmhead_fwd<2> : lmhead_fwd<1>;
+  const size_t smem = mode == 4 ? L2Cfg<2>::SMEM : mode == 3 ? L2Cfg<1>::SMEM : LM_SMEM;
   if (!attr[mode - 1][dev]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return TBA_ERR_CUDA;

@@ -257,23 +257,29 @@ syn.fill_bf16_cuda(h.view(-1, w.d), 17, "hidden", 0)
 syn.fill_bf16_cuda(wt, 17, "weight", 0)
 dev = [torch.from_numpy(gi[k]).cuda() for k in ("tokens", "mask", "ref_logp", "log_reward")]
 o, dh, dw = tba.lmhead_vargrad_fwd_bwd(h, wt, *dev, w.beta, w.K, w.N, groups_per_chunk=1)
-torch.save({"dh": dh.cpu(), "dw": dw.cpu()}, sys.argv[2])
+f, _ = tba.lmhead_vargrad_fwd(h, wt, *dev, w.beta, w.K, w.N)
+torch.save({"dh": dh.cpu(), "dw": dw.cpu(), "ell": f.seq_logp.cpu(), "resid": o.resid.cpu(),
+            "loss": o.partial.cpu()}, sys.argv[2])
 """
 
 
 def test_lmhead_bwd_pair_kernel_bitwise(tmp_path):
-    """TBA_LMB_2SM=3 (dH and dW on the cta_group::2 kernel, with TBA_LMB_NT2=3 on 256 x 512 pair
-    tiles) gives bitwise the single-SM results: each output element is one K-ordered fp32
-    accumulation either way."""
+    """Every kernel variant gives bitwise the single-SM results (each logit / gradient element is
+    one K-ordered fp32 accumulation whatever the tile shape): the forward on the multicast pair
+    (TBA_LM_MC=2) and the cta_group::2 pair with 256 x 256 (3) or 256 x 512 tiles (4), the backward
+    GEMMs on the pair kernel (TBA_LMB_2SM=3) with 256 x 256 or 256 x 512 tiles (TBA_LMB_NT2=3)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    for mode, nt2 in (("0", "0"), ("3", "0"), ("3", "3")):
-        f = tmp_path / f"r{mode}{nt2}.pt"
-        env = dict(os.environ, TBA_LMB_2SM=mode, TBA_LMB_NT2=nt2)
+    # (forward kernel TBA_LM_MC, backward TBA_LMB_2SM, TBA_LMB_NT2): single-SM everywhere first
+    for cfg in (("1", "0", "0"), ("1", "3", "0"), ("1", "3", "3"), ("3", "3", "3"), ("4", "3", "3"), ("2", "0", "0")):
+        f = tmp_path / f"r{''.join(cfg)}.pt"
+        env = dict(os.environ, TBA_LM_MC=cfg[0], TBA_LMB_2SM=cfg[1], TBA_LMB_NT2=cfg[2])
         subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
-        out[mode + nt2] = torch.load(f)
-    for k in ("30", "33"):  # 256 x 256 and 256 x 512 pair tiles
-        assert torch.equal(out["00"]["dh"], out[k]["dh"]) and torch.equal(out["00"]["dw"], out[k]["dw"]), k
+        out[cfg] = torch.load(f)
+    base = out[("1", "0", "0")]
+    for cfg, r in out.items():
+        for k in base:
+            assert torch.equal(base[k], r[k]), (cfg, k)
