@@ -101,12 +101,15 @@ __device__ __forceinline__ bool lm_unit_active(const uint8_t* __restrict__ mask,
 // S = sum 2^(z sc - fl(R sc)); lmhead_combine re-forms fl(R sc) with the same fp32 multiply.
 // NT = 2 (wide pair tiles): one accumulator of 2 x 256 columns holds vocabulary tiles t and t+1;
 // it is waited for before the first and released after the second (or after the group's last).
-template <int NT = 1>
+// H = 2 (with NT = 2): two epilogue warps per TMEM lane quarter; warp-half h folds only the tiles
+// t0 + h, t0 + h + 2, ... and writes its own partial (group slot grp * 2 + h), so the softmax of
+// the two halves of a wide tile runs in parallel; lmhead_combine reduces 2 x n_groups partials.
+template <int NT = 1, int H = 1>
 __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int grp, uint32_t& j, uint32_t tmem_lane,
                                                  int row_in, int lane, uint64_t* tfull, uint32_t tempty_addr,
                                                  bool cluster_arrive, const int64_t* __restrict__ tokens,
                                                  const RowScale& rs, float2* __restrict__ part,
-                                                 float* __restrict__ zy_out) {
+                                                 float* __restrict__ zy_out, int h = 0) {
   const float sc = rs.sc;
   const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
   const int64_t row = (int64_t)rb * LM_BM + row_in;
@@ -131,7 +134,7 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
     const int64_t dyt = y - nb;
     const int cy = ((uint64_t)dyt < (uint64_t)LM_BN) ? (int)(dyt >> 5) : -1;  // chunk holding y, if any
 #pragma unroll 1
-    for (int c = 0; c < LM_BN / 32; ++c) {
+    for (int c = 0; c < ((H == 1 || u == h) ? LM_BN / 32 : 0); ++c) {
       float v[32];
       tmem_ld32(tmem_lane + col0 + c * 32, v);
       if (g.zst && in_rows) {
@@ -193,7 +196,7 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
     }
   }
   if (in_rows) {
-    part[(int64_t)grp * g.rows + row] = make_float2(R, (float)S);
+    part[((int64_t)grp * H + h) * g.rows + row] = make_float2(R, (float)S);
     if (found) zy_out[row] = zy;
   }
 }
@@ -356,8 +359,8 @@ struct L2Cfg {
 };
 constexpr uint32_t L2_IDESC = tc_idesc_bf16(2 * LM_BM, LM_BN);
 
-template <int NT>
-__global__ void __launch_bounds__(LM_THREADS, 1)
+template <int NT, int H = 1>
+__global__ void __launch_bounds__(64 + 128 * H, 1)
     lmhead_fwd_2sm(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
                    const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
                    float2* __restrict__ part, float* __restrict__ zy_out) {
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // leader: 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[a], 8 * H);  // leader: 4 H epilogue warps x 2 CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -472,6 +475,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     }
   } else {  // ---- epilogue (both CTAs): release on the leader's tempty
     const int q = warp & 3;
+    const int h = (warp - 2) / 4;  // warp-half (H = 2)
     const int row_in = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint32_t tempty_leader;
@@ -482,8 +486,8 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       lm_item(g, nact, it, rb, grp);
       rb = g.act[rb];
       rb = rb * 2 + (int)crank;
-      lm_epilogue_item<NT>(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, tempty_leader, true, tokens, rs,
-                           part, zy_out);
+      lm_epilogue_item<NT, H>(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, tempty_leader, true, tokens, rs,
+                              part, zy_out, h);
     }
   }
   __syncthreads();
@@ -576,16 +580,17 @@ int lm_swz() {
 }
 
 size_t lmhead_partial_bytes(int64_t rows, int64_t V) {
-  const int64_t groups = ((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G;  // the most groups any G >= LM_G makes
+  // the most partials any G >= LM_G makes: two per group with the split epilogue (TBA_LM_MC=5)
+  const int64_t groups = 2 * (((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G);
   const int64_t blocks = (rows + LM_BM - 1) / LM_BM;
   return align_up((size_t)groups * (size_t)rows * sizeof(float2), 256) + align_up((size_t)rows * sizeof(float), 256) +
          align_up((size_t)(blocks + 1) * sizeof(int), 256);
 }
 
 // TBA_LM_MC: 1 single-SM kernel, 2 cluster pair with weight multicast, 3 cta_group::2 pair (256 x 256
-// tiles), 4 cta_group::2 pair with 256 x 512 tiles.
+// tiles), 4 cta_group::2 pair with 256 x 512 tiles, 5 the same with eight epilogue warps.
 int lm_mc() {
-  static int v = [] { int x = env_int("TBA_LM_MC", 1); return (x >= 2 && x <= 4) ? x : 1; }();
+  static int v = [] { int x = env_int("TBA_LM_MC", 1); return (x >= 2 && x <= 5) ? x : 1; }();
   return v;
 }
 
@@ -602,7 +607,8 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.V = x->vocab;
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
   g.G = lm_g();
-  if (mode == 4 && (g.G & 1)) ++g.G;  // a wide tile holds two vocabulary tiles of one group
+  if (mode >= 4 && (g.G & 1)) ++g.G;  // a wide tile holds two vocabulary tiles of one group
+  const int H = mode == 5 ? 2 : 1;      // partials per group
   g.swz = (lm_swz() + mc - 1) / mc;  // the raster counts row blocks: a pair unit holds two
   g.pol = env_int("TBA_LM_POL", 1) & 7;
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
@@ -615,7 +621,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
     return TBA_ERR_CUDA;
   char* pw = static_cast<char*>(part_ws);
   float2* part = reinterpret_cast<float2*>(pw);
-  pw += align_up((size_t)g.n_groups * (size_t)rows * sizeof(float2), 256);
+  pw += align_up((size_t)g.n_groups * H * (size_t)rows * sizeof(float2), 256);
   float* zy = reinterpret_cast<float*>(pw);
   pw += align_up((size_t)rows * sizeof(float), 256);
   int* act = reinterpret_cast<int*>(pw);
@@ -623,11 +629,15 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.n_act = act + n_rb;
   lm_compact_units<<<1, 1024, 0, s>>>(x->mask, rows, mc, n_units_total, act, act + n_rb);
   if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
-  static bool attr[4][64] = {};  // per variant and device; benign race: idempotent
+  static bool attr[5][64] = {};  // per variant and device; benign race: idempotent
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
-  auto kern = mode == 4 ? lmhead_fwd_2sm<2> : mode == 3 ? lmhead_fwd_2sm<1> : mode == 2 ? lmhead_fwd<2> : lmhead_fwd<1>;
-  const size_t smem = mode == 4 ? L2Cfg<2>::SMEM : mode == 3 ? L2Cfg<1>::SMEM : LM_SMEM;
+  auto kern = mode == 5   ? lmhead_fwd_2sm<2, 2>
+              : mode == 4 ? lmhead_fwd_2sm<2, 1>
+              : mode == 3 ? lmhead_fwd_2sm<1, 1>
+              : mode == 2 ? lmhead_fwd<2>
+                          : lmhead_fwd<1>;
+  const size_t smem = mode >= 4 ? L2Cfg<2>::SMEM : mode == 3 ? L2Cfg<1>::SMEM : LM_SMEM;
   if (!attr[mode - 1][dev]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return TBA_ERR_CUDA;
@@ -635,7 +645,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
-  cfg.blockDim = dim3(LM_THREADS);
+  cfg.blockDim = dim3(mode == 5 ? 64 + 256 : LM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   int64_t units = device_sms() / mc;
@@ -656,7 +666,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   if (cudaLaunchKernelEx(&cfg, kern, mh, mw, g, x->tokens, x->mask, rs, part, zy) != cudaSuccess)
     return TBA_ERR_CUDA;
   const int64_t blocks = (rows + 255) / 256 < 4096 ? (rows + 255) / 256 : 4096;
-  lmhead_combine<<<(unsigned)blocks, 256, 0, s>>>(part, zy, rows, g.n_groups, x->vocab, x->tokens, x->mask, rs,
+  lmhead_combine<<<(unsigned)blocks, 256, 0, s>>>(part, zy, rows, g.n_groups * H, x->vocab, x->tokens, x->mask, rs,
                                                   w.stats, w.lp, dev_status);
   return launch_status();
 }
