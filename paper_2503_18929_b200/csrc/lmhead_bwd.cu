@@ -15,8 +15,11 @@
 //   3. tc_gemm<STORE> dH rows = dZ (W^T)^T, scattered to the rows' places in dhidden
 //   4. tc_gemm<STORE> dW (+)= dZ^T (Hc^T)^T, fp32, accumulated over the chunks
 // W^T [d, Vp] is formed once per call. Every GEMM is D = A B^T with both operands K-major
-// (TMA SWIZZLE_128B tiles, UMMA M = 128, N = 256, K = 16, fp32 accumulators in TMEM), so the
-// transposed copies are what lets one mainloop serve all three products.
+// (TMA SWIZZLE_128B tiles, UMMA K = 16, fp32 accumulators in TMEM), so the transposed copies are
+// what lets one mainloop serve all three products. dH and dW run by default on tc_gemm2<2>, the
+// cta_group::2 form with 256 x 512 tiles per SM pair (half the single-SM kernel's L2 -> SM feed).
+// The one-call schedule (launch_lmhead_fwd_bwd) takes chunks of whole groups: the forward stores
+// the chunk's fp32 logits and lmb_dz_from_z replaces step 2's recompute GEMM.
 #include "tc_sm100.cuh"
 
 namespace tba {

@@ -12,3 +12,6 @@ for w in qwen_shard rhomath pythia redteam; do timeout 600 python bench.py --wor
 bash scripts/gpu_lmhead.sh $TAG > /dev/null 2>&1
 tail -c 300 gpurun_out/bench_${TAG}_qwen_shard_lmhead.json
 timeout 600 python bench.py --workload toy --cuda-graph --steps 50 --warmup 10 --no-e2e --no-cpu-baseline > gpurun_out/bench_${TAG}_toy_graph.json 2>/dev/null
+# LM-head forward + backward (NEXT 3): bench lines (one-call vs two-call vs cuBLAS) and the launch list
+bash scripts/gpu_lmtrain.sh $TAG
+timeout 600 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum,sm__cycles_elapsed.avg.per_second,lts__t_sector_hit_rate.pct,lts__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none --csv --log-file gpurun_out/lmtrain_launches_${TAG}.csv python scripts/lm_bwd_probe.py --one-call > /dev/null 2>&1

@@ -213,3 +213,31 @@ def test_lmhead_bwd_workspace_bytes(L):
     assert L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 0) == L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 128)
     assert L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 1) == L.tba_lmhead_bwd_workspace_bytes(1, 100, 64, 1000, 100)
     assert L.tba_lmhead_bwd_workspace_bytes(-1, 4, 64, 10, 0) == 0 and L.tba_lmhead_bwd_workspace_bytes(1, 4, 64, 0, 0) == 0
+
+
+def test_lmhead_fwd_bwd_validation_and_workspace(L):
+    x = _lm()
+
+    def fb(x=x, beta=1.0, K=4, ng=8.0, gs=0.25, ws=0x100000, bws=0x200000, dh=FAKE + 0x10000, dht=_lib.TBA_FP32,
+           dhs=64, partial=FAKE):
+        return L.tba_lmhead_tb_loss_fwd_bwd(ctypes.byref(x), None, FAKE, FAKE, beta, K, ng, gs, 0, ws, FAKE, FAKE,
+                                            FAKE, FAKE, partial, dh, dht, dhs, FAKE + 0x20000, 64, 0, None, bws,
+                                            None, None)
+    assert fb(beta=0.0) == _lib.TBA_ERR_INVALID_CONFIG
+    assert fb(K=1) == _lib.TBA_ERR_INVALID_CONFIG
+    assert fb(K=3) == _lib.TBA_ERR_INVALID_ARG          # 8 sequences are not groups of 3
+    assert fb(ng=4.0) == _lib.TBA_ERR_INVALID_ARG       # n_seq_global < n_seq
+    assert fb(gs=math.nan) == _lib.TBA_ERR_INVALID_ARG
+    assert fb(partial=None) == _lib.TBA_ERR_INVALID_ARG
+    assert fb(dh=FAKE) == _lib.TBA_ERR_INVALID_ARG      # dhidden aliases hidden
+    assert fb(dht=5) == _lib.TBA_ERR_INVALID_ARG
+    assert fb(dhs=8) == _lib.TBA_ERR_INVALID_ARG
+    assert fb(ws=0x100004) == _lib.TBA_ERR_INVALID_ARG
+    assert fb(bws=0) == _lib.TBA_ERR_INVALID_ARG
+    assert fb(x=_lm(hidden_stride=60)) == _lib.TBA_ERR_INVALID_ARG
+    # workspace: the stored fp32 logits of one chunk (2 Qwen groups = 16384 rows) dominate
+    b = L.tba_lmhead_fwd_bwd_workspace_bytes(64, 1024, 3584, 152064, 8, 0)
+    assert b >= 16384 * 152064 * 4 + 2 * 16384 * 152064 * 2
+    assert L.tba_lmhead_fwd_bwd_workspace_bytes(64, 1024, 3584, 152064, 8, 1) < b   # one group per chunk
+    assert L.tba_lmhead_fwd_bwd_workspace_bytes(9, 4, 64, 100, 4, 0) == 0          # 9 % 4 != 0
+    assert L.tba_lmhead_fwd_bwd_workspace_bytes(0, 4, 64, 100, 4, 0) == 256
