@@ -28,6 +28,9 @@ constexpr int LM_THREADS = 192;
 constexpr uint32_t LM_IDESC = tc_idesc_bf16(LM_BM, LM_BN);
 static_assert(LM_BK == TC_BK, "one 128-byte swizzle row per K block");
 constexpr size_t LM_SMEM = 1024 + (size_t)LM_STAGES * LM_STAGE_BYTES + 256;
+// + the logits-store staging (one-call schedule): per epilogue warp two 32 x 32 fp32 boxes
+constexpr int LM_ZSTG_BYTES = 2 * 32 * 32 * 4;
+constexpr size_t LM_SMEM_Z = 1024 + (size_t)LM_STAGES * LM_STAGE_BYTES + 1024 + 4 * LM_ZSTG_BYTES;
 
 // The same load multicast to the CTAs of `mask` (same shared offset in each; each destination's
 // mbarrier at `bar`'s offset receives the complete_tx).
@@ -109,7 +112,9 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
                                                  int row_in, int lane, uint64_t* tfull, uint32_t tempty_addr,
                                                  bool cluster_arrive, const int64_t* __restrict__ tokens,
                                                  const RowScale& rs, float2* __restrict__ part,
-                                                 float* __restrict__ zy_out, int h = 0) {
+                                                 float* __restrict__ zy_out, int h = 0,
+                                                 const CUtensorMap* zmap = nullptr, uint32_t zstg = 0,
+                                                 uint32_t* zcnt = nullptr) {
   const float sc = rs.sc;
   const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
   const int64_t row = (int64_t)rb * LM_BM + row_in;
@@ -137,7 +142,23 @@ __device__ __forceinline__ void lm_epilogue_item(const LmGrid& g, int rb, int gr
     for (int c = 0; c < ((H == 1 || u == h) ? LM_BN / 32 : 0); ++c) {
       float v[32];
       tmem_ld32(tmem_lane + col0 + c * 32, v);
-      if (g.zst && in_rows) {
+      if (zmap) {  // logits store through shared memory + one TMA bulk store per 32 x 32 box
+        const uint32_t buf = zstg + (*zcnt & 1u) * (32 * 32 * 4);
+        if (*zcnt >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)  // 16-byte chunk q4 of this row at (q4 ^ row % 8): conflict-free
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 128 + ((q4 ^ (lane & 7)) << 4)),
+                       "f"(v[4 * q4]), "f"(v[4 * q4 + 1]), "f"(v[4 * q4 + 2]), "f"(v[4 * q4 + 3])
+                       : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(zmap, buf, (int)(nb + c * 32), (int)(rb * LM_BM + (row_in & ~31)));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++*zcnt;
+      } else if (g.zst && in_rows) {
         float* zp = g.zst + row * g.zst_ld + nb + c * 32;
         if (nb + c * 32 + 32 <= g.V) {
 #pragma unroll
@@ -209,7 +230,7 @@ template <int MC>
 __global__ void __launch_bounds__(LM_THREADS, 1)
     lmhead_fwd(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
                const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
-               float2* __restrict__ part, float* __restrict__ zy_out) {
+               float2* __restrict__ part, float* __restrict__ zy_out, const __grid_constant__ CUtensorMap tmZ) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -322,14 +343,19 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     const int row_in = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint32_t j = 0;
+    // one-call schedule: the logits go out through per-warp staging boxes and TMA stores
+    const bool zt = g.zst != nullptr && MC == 1;
+    const uint32_t zstg = smem_u32(smem + LM_STAGES * LM_STAGE_BYTES + 1024) + (uint32_t)q * LM_ZSTG_BYTES;
+    uint32_t zcnt = 0;
     for (int64_t it = unit0; it < n_items; it += n_units) {
       int rb, grp;
       lm_item(g, nact, it, rb, grp);
       rb = g.act[rb];
       rb = rb * MC + (int)crank;
       lm_epilogue_item(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, smem_u32(tempty), false, tokens, rs,
-                       part, zy_out);
+                       part, zy_out, 0, zt ? &tmZ : nullptr, zstg, &zcnt);
     }
+    if (zt && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   if (MC > 1) cluster_sync_all();  // no CTA leaves while its partner may still write into it
@@ -363,7 +389,8 @@ template <int NT, int H = 1>
 __global__ void __launch_bounds__(64 + 128 * H, 1)
     lmhead_fwd_2sm(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
                    const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
-                   float2* __restrict__ part, float* __restrict__ zy_out) {
+                   float2* __restrict__ part, float* __restrict__ zy_out,
+                   const __grid_constant__ CUtensorMap tmZ /* unused: this kernel stores logits directly */) {
   constexpr int L2_STAGES = L2Cfg<NT>::STAGES, L2_A_BYTES = L2Cfg<NT>::A_BYTES, L2_B_BYTES = L2Cfg<NT>::B_BYTES,
                 L2_STAGE_BYTES = L2Cfg<NT>::STAGE_BYTES, NACC = 2 / NT;
   extern __shared__ uint8_t smem_raw[];
@@ -615,10 +642,13 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
   g.zst = zst;
   g.zst_ld = zst_ld;
-  CUtensorMap mh, mw;
+  CUtensorMap mh, mw, mz;
   if (!make_map(&mh, x->hidden, rows, x->d, x->hidden_stride, LM_BM) ||
       !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN / mc))
     return TBA_ERR_CUDA;
+  const bool ztma = zst && mode == 1;  // the single-SM kernel stores the logits with TMA
+  if (ztma ? !make_store_map_f32(&mz, zst, rows, x->vocab, zst_ld) : false) return TBA_ERR_CUDA;
+  if (!ztma) mz = CUtensorMap{};
   char* pw = static_cast<char*>(part_ws);
   float2* part = reinterpret_cast<float2*>(pw);
   pw += align_up((size_t)g.n_groups * H * (size_t)rows * sizeof(float2), 256);
@@ -637,9 +667,10 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
               : mode == 3 ? lmhead_fwd_2sm<1, 1>
               : mode == 2 ? lmhead_fwd<2>
                           : lmhead_fwd<1>;
-  const size_t smem = mode >= 4 ? L2Cfg<2>::SMEM : mode == 3 ? L2Cfg<1>::SMEM : LM_SMEM;
+  const size_t smem = mode >= 4 ? L2Cfg<2>::SMEM : mode == 3 ? L2Cfg<1>::SMEM : ztma ? LM_SMEM_Z : LM_SMEM;
   if (!attr[mode - 1][dev]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(mode == 1 ? LM_SMEM_Z : smem)) !=
+        cudaSuccess)
       return TBA_ERR_CUDA;
     attr[mode - 1][dev] = true;
   }
@@ -663,7 +694,7 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   const int64_t max_items = (int64_t)n_units_total * g.n_groups;  // the active count is known on the device only
   if (units > max_items) units = max_items;
   cfg.gridDim = dim3((unsigned)(units * mc));
-  if (cudaLaunchKernelEx(&cfg, kern, mh, mw, g, x->tokens, x->mask, rs, part, zy) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, kern, mh, mw, g, x->tokens, x->mask, rs, part, zy, mz) != cudaSuccess)
     return TBA_ERR_CUDA;
   const int64_t blocks = (rows + 255) / 256 < 4096 ? (rows + 255) / 256 : 4096;
   lmhead_combine<<<(unsigned)blocks, 256, 0, s>>>(part, zy, rows, g.n_groups * H, x->vocab, x->tokens, x->mask, rs,
