@@ -2,7 +2,9 @@
  * host, copy them to the device with the CUDA runtime, run the VarGrad TB head forward and
  * backward through the C ABI, and print the loss, the per-sequence log-probs and a checksum
  * of dlogits; then the same sequences' log-probs from hidden states through the LM-head-fused
- * forward. The test suite runs it and compares with the fp64 oracle.
+ * forward, and the loss with its gradients w.r.t. the hidden states and the LM-head weight
+ * from the one-call LM-head forward + backward. The test suite runs it and compares with the
+ * fp64 oracle.
  *
  *   gcc -O2 -I include -I /usr/local/cuda/include examples/c_abi_example.c \
  *       -L paper_2503_18929_b200 -ltba -L /usr/local/cuda/lib64 -lcudart -o c_abi_example
@@ -155,5 +157,27 @@ int main(void) {
   CK(cudaMemcpy(seq, d_seq, sizeof(seq), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(&status, d_status, sizeof(status), cudaMemcpyDeviceToHost));
   for (int s = 0; s < N; ++s) printf("lmhead seq %d logp %.12g\n", s, seq[s]);
+
+  /* Training step through the LM head in one call: loss, dL/dhidden (fp32) and dL/dW (fp32),
+   * the [N, T, V] logits never allocated. */
+  void *d_bws, *d_dh, *d_dw;
+  const size_t bws = tba_lmhead_fwd_bwd_workspace_bytes(N, T, D, V, (int32_t)K, 0);
+  CK(cudaMalloc(&d_bws, bws));
+  CK(cudaMalloc(&d_dh, sizeof(float) * N * T * D));
+  CK(cudaMalloc(&d_dw, sizeof(float) * V * D));
+  TB(tba_lmhead_tb_loss_fwd_bwd(&lm, NULL, d_ref, d_rew, beta, (int32_t)K, (double)N, 2.0 / (double)N, 0, d_lws,
+                                d_seq, d_ntok, d_logz, d_resid, d_partial, d_dh, TBA_FP32, D, (float*)d_dw, D, 0,
+                                NULL, d_bws, d_status, NULL));
+  CK(cudaDeviceSynchronize());
+  float* h_dh = (float*)malloc(sizeof(float) * N * T * D);
+  float* h_dw = (float*)malloc(sizeof(float) * V * D);
+  CK(cudaMemcpy(partial, d_partial, sizeof(partial), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h_dh, d_dh, sizeof(float) * N * T * D, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h_dw, d_dw, sizeof(float) * V * D, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&status, d_status, sizeof(status), cudaMemcpyDeviceToHost));
+  double sh = 0.0, sw = 0.0;
+  for (int64_t i = 0; i < N * T * D; ++i) sh += fabs((double)h_dh[i]);
+  for (int64_t i = 0; i < V * D; ++i) sw += fabs((double)h_dw[i]);
+  printf("lmhead loss %.12g dhidden_abs_sum %.9g dweight_abs_sum %.9g\n", partial[0], sh, sw);
   return status != 0;
 }

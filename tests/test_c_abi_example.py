@@ -70,3 +70,14 @@ def test_c_example_runs_and_matches_oracle():
     ell, _ = O.lmhead_seq_logprob(hid.reshape(6, 4, 64), w, tok, mask)
     got = [float(x) for x in re.findall(r"lmhead seq \d+ logp (\S+)", out.stdout)]
     np.testing.assert_allclose(got, ell, rtol=0, atol=1e-5)
+    # the one-call LM-head training step: loss and the gradient sums
+    z = O.lmhead_logits(hid, w).reshape(6, 4, 257)
+    rl = O.vargrad_head(z, tok, mask, ref, rew, 0.5, 3)
+    dH, dW = O.lmhead_grads(hid, w, rl["dlogits"].reshape(24, 257))
+    m = re.search(r"lmhead loss (\S+) dhidden_abs_sum (\S+) dweight_abs_sum (\S+)", out.stdout)
+    assert m, out.stdout
+    assert abs(float(m.group(1)) - rl["loss"]) <= 1e-4 * abs(rl["loss"])
+    # |sum|x| - sum|x_ref|| <= sum |x - x_ref| <= the per-element bound of DESIGN.md R21, summed
+    AZ = np.abs(rl["dlogits"].reshape(24, 257))
+    assert abs(float(m.group(2)) - np.abs(dH).sum()) <= (2.0 ** -8 + 4 * 257 ** 0.5 * 2.0 ** -24) * (AZ @ np.abs(w)).sum()
+    assert abs(float(m.group(3)) - np.abs(dW).sum()) <= (2.0 ** -8 + 4 * 24 ** 0.5 * 2.0 ** -24) * (AZ.T @ np.abs(hid)).sum()
