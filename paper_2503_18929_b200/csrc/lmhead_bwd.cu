@@ -301,14 +301,15 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
           uint16_t* zr = z.dz + m * z.Vp + v0;
           if (v0 + 32 <= z.V) {
             store_bf16x32(zr, v);
+            if (z.dzt)
 #pragma unroll
-            for (int e = 0; e < 32; ++e) z.dzt[(v0 + e) * z.C + m] = to_bf16(v[e]);
+              for (int e = 0; e < 32; ++e) z.dzt[(v0 + e) * z.C + m] = to_bf16(v[e]);
           } else {
             for (int e = 0; e < 32; ++e)
               if (v0 + e < z.V) {
                 const uint16_t b = to_bf16(v[e]);
                 zr[e] = b;
-                z.dzt[(v0 + e) * z.C + m] = b;
+                if (z.dzt) z.dzt[(v0 + e) * z.C + m] = b;
               }
           }
         }
@@ -365,7 +366,10 @@ struct G2 {
 };
 constexpr uint32_t G2_IDESC = tc_idesc_bf16(256, GB_BN);
 
-template <int NT>
+// MN = true: both operands MN-major (A = dZ [K = rows, M = V], B = Hc [K = rows, N = d], read as
+// stored, no transposed copies): each 128-wide operand slab is two TMA boxes of {64 MN, 64 K}
+// placed 8 KB apart (the descriptor's LBO).
+template <int NT, bool MN = false>
 __global__ void __launch_bounds__(GB_THREADS, 1)
     tc_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs a) {
   using C = G2<NT>;
@@ -436,12 +440,27 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         for (int64_t kb = 0; kb < g.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           if (leader) mbar_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
-          tma_load_2d_pair(smem_u32(sA + stage * G2_A_BYTES), &tmA, (int)(kb * TC_BK), (int)(mb * 256 + crank * 128),
-                           smem_u32(&full[stage]), pol_a, true);
+          if (MN) {
 #pragma unroll
-          for (int u = 0; u < NT; ++u)
-            tma_load_2d_pair(smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2)), &tmB, (int)(kb * TC_BK),
-                             (int)((nb * NT + u) * GB_BN + crank * 128), smem_u32(&full[stage]), pol_b, true);
+            for (int hb = 0; hb < 2; ++hb)
+              tma_load_2d_pair(smem_u32(sA + stage * G2_A_BYTES + hb * 8192), &tmA,
+                               (int)(mb * 256 + crank * 128 + hb * 64), (int)(kb * TC_BK), smem_u32(&full[stage]),
+                               pol_a, true);
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+#pragma unroll
+              for (int hb = 0; hb < 2; ++hb)
+                tma_load_2d_pair(smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2) + hb * 8192), &tmB,
+                                 (int)((nb * NT + u) * GB_BN + crank * 128 + hb * 64), (int)(kb * TC_BK),
+                                 smem_u32(&full[stage]), pol_b, true);
+          } else {
+            tma_load_2d_pair(smem_u32(sA + stage * G2_A_BYTES), &tmA, (int)(kb * TC_BK),
+                             (int)(mb * 256 + crank * 128), smem_u32(&full[stage]), pol_a, true);
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+              tma_load_2d_pair(smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2)), &tmB, (int)(kb * TC_BK),
+                               (int)((nb * NT + u) * GB_BN + crank * 128), smem_u32(&full[stage]), pol_b, true);
+          }
           if (++stage == G2_STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -462,13 +481,17 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         for (int64_t kb = 0; kb < g.nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * G2_A_BYTES));
+          const uint32_t sa = smem_u32(sA + stage * G2_A_BYTES);
+          const uint64_t a0 = MN ? umma_desc_mn_sw128(sa, 8192) : umma_desc_sw128(sa);
+          constexpr uint32_t kstep = MN ? (16 * 128) >> 4 : 2;  // K = 16: 16 rows of 128 B, or +32 B in a row
+          constexpr uint32_t IDESC = MN ? (G2_IDESC | kIdescMajorMN) : G2_IDESC;
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
 #pragma unroll
             for (int u = 0; u < NT; ++u) {
-              const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2)));
-              umma_bf16_pair<G2_IDESC>(d_tmem + u * GB_BN, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
+              const uint32_t sb = smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2));
+              const uint64_t b0 = MN ? umma_desc_mn_sw128(sb, 8192) : umma_desc_sw128(sb);
+              umma_bf16_pair<IDESC>(d_tmem + u * GB_BN, a0 + kstep * k, b0 + kstep * k, (kb | k) != 0);
             }
           umma_commit_pair(&empty[stage]);
           if (++stage == G2_STAGES) {
@@ -590,6 +613,7 @@ __global__ void __launch_bounds__(256) lmb_gather_t(const uint16_t* __restrict__
     tp[2] = val.z;
     tp[3] = val.w;
   }
+  if (!dst_t) return;
   __syncthreads();
 #pragma unroll
   for (int p = 0; p < 2; ++p) {
@@ -665,6 +689,7 @@ __global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __rest
     tp[0] = lo;
     tp[1] = hi;
   }
+  if (!z.dzt) return;  // dW reads dz itself (MN-major operand)
   __syncthreads();
   // dz^T: 128 vocabulary rows of 64 chunk rows (128 B each): 8 threads x 16 B per row
 #pragma unroll
@@ -723,14 +748,14 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
   return launch_status();
 }
 
-template <int NT>
+template <int NT, bool MN = false>
 int launch_gemm2(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int64_t max_pair_tiles,
                  cudaStream_t s) {
   static bool attr[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
   if (!attr[dev]) {
-    if (cudaFuncSetAttribute(tc_gemm2<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2<NT>::SMEM) !=
+    if (cudaFuncSetAttribute(tc_gemm2<NT, MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2<NT>::SMEM) !=
         cudaSuccess)
       return TBA_ERR_CUDA;
     attr[dev] = true;
@@ -749,11 +774,12 @@ int launch_gemm2(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a
   int64_t pairs = device_sms() / 2;
   cfg.gridDim = dim3((unsigned)(pairs * 2));
   int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, tc_gemm2<NT>, &cfg) == cudaSuccess && ncl > 0 && ncl < pairs) pairs = ncl;
+  if (cudaOccupancyMaxActiveClusters(&ncl, tc_gemm2<NT, MN>, &cfg) == cudaSuccess && ncl > 0 && ncl < pairs)
+    pairs = ncl;
   if (pairs > max_pair_tiles) pairs = max_pair_tiles;
   if (pairs < 1) pairs = 1;
   cfg.gridDim = dim3((unsigned)(pairs * 2));
-  if (cudaLaunchKernelEx(&cfg, tc_gemm2<NT>, ma, mb, a) != cudaSuccess) return TBA_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, tc_gemm2<NT, MN>, ma, mb, a) != cudaSuccess) return TBA_ERR_CUDA;
   return TBA_OK;
 }
 
@@ -784,6 +810,8 @@ struct LmbCtx {
   LmbWs w;
   CUtensorMap m_hc, m_w, m_dz, m_wt, m_dzt, m_hct;
   int swz, ninner, pol, pair, wide;  // pair: bit 0 dH, bit 1 dW on the cta_group::2 kernel; wide: NT = 2
+  bool dwmn;                         // dW reads dZ and Hc as MN-major operands (no transposed copies)
+  CUtensorMap m_dzmn, m_hcmn;
   CUtensorMap m_wt2, m_hct2;   // B operands with 128-row boxes for the pair kernel (A boxes are 128 rows already)
 };
 
@@ -793,6 +821,7 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   static const int pol = env_int("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
   static const int pair = env_int("TBA_LMB_2SM", 3);  // measured: 196-203 ms vs 218-223 (one-call Qwen step)
   static const int wide = env_int("TBA_LMB_NT2", 3);  // bit 0 dH, bit 1 dW: 256 x 512 pair tiles
+  static const int dwmn = env_int("TBA_LMB_DW_MN", 1);
   const int64_t d = x->d, V = x->vocab;
   k.x = x;
   k.C = C;
@@ -803,6 +832,7 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   k.pol = pol;
   k.pair = pair;
   k.wide = wide;
+  k.dwmn = dwmn != 0 && (pair & 2) != 0;
   if (need_wt) {
     const dim3 grid((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64));
     lmb_gather_t<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x->weight), x->weight_stride, d, nullptr,
@@ -814,6 +844,9 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
       !make_map(&k.m_dzt, k.w.dzt, V, C, C, GB_BM) || !make_map(&k.m_hct, k.w.hct, d, C, C, GB_BN))
     return TBA_ERR_CUDA;
   if (pair && (!make_map(&k.m_wt2, k.w.wt, d, V, k.Vp, 128) || !make_map(&k.m_hct2, k.w.hct, d, C, C, 128)))
+    return TBA_ERR_CUDA;
+  // MN-major boxes {64 along V (or d), 64 rows}
+  if (k.dwmn && (!make_map(&k.m_dzmn, k.w.dz, C, V, k.Vp, 64) || !make_map(&k.m_hcmn, k.w.hc, C, d, d, 64)))
     return TBA_ERR_CUDA;
   return TBA_OK;
 }
@@ -828,13 +861,13 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
   const int64_t nt_v = (V + GB_BN - 1) / GB_BN, nt_d = (d + GB_BN - 1) / GB_BN;
   const dim3 ggrid((unsigned)((d + 63) / 64), (unsigned)(C / 64));
   lmb_gather_t<<<ggrid, 256, 0, s>>>(static_cast<const uint16_t*>(x->hidden), x->hidden_stride, d, k.w.idx, n_valid, 0,
-                                     chunk0, C, 1, k.w.hc, k.w.hct, C);
+                                     chunk0, C, 1, k.w.hc, (dw && !k.dwmn) ? k.w.hct : nullptr, C);
   if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
   dz.V = V;
   dz.Vp = k.Vp;
   dz.C = C;
   dz.dz = k.w.dz;
-  dz.dzt = k.w.dzt;
+  dz.dzt = (dw && !k.dwmn) ? k.w.dzt : nullptr;
   int rc;
   if (zst) {  // 2'. dz from the stored logits (chunk0 == 0: the chunk's own row list)
     dz.idx = k.w.idx;
@@ -892,8 +925,11 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
     b.pol = (k.pol >> 2) & 3;
     b.st = StoreArgs{dw, dw_stride, nullptr, 0, dw_add ? 1 : 0,
                      ((reinterpret_cast<uintptr_t>(dw) | (uintptr_t)(dw_stride * 4)) & 15) == 0};
-    rc = (k.pair & 2) ? ((k.wide & 2) ? launch_gemm2<2>(k.m_dzt, k.m_hct2, b, ((V + 255) / 256) * nt_d, s)
-                                      : launch_gemm2<1>(k.m_dzt, k.m_hct2, b, ((V + 255) / 256) * nt_d, s))
+    const int64_t mt = ((V + 255) / 256) * nt_d;
+    rc = k.dwmn ? ((k.wide & 2) ? launch_gemm2<2, true>(k.m_dzmn, k.m_hcmn, b, mt, s)
+                                : launch_gemm2<1, true>(k.m_dzmn, k.m_hcmn, b, mt, s))
+         : (k.pair & 2) ? ((k.wide & 2) ? launch_gemm2<2>(k.m_dzt, k.m_hct2, b, mt, s)
+                                      : launch_gemm2<1>(k.m_dzt, k.m_hct2, b, mt, s))
                       : launch_gemm<EPI_STORE>(k.m_dzt, k.m_hct, b, ((V + GB_BM - 1) / GB_BM) * nt_d, s);
   }
   return rc;

@@ -23,6 +23,16 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
 
+// MN-major operand, 128-byte swizzle: 64 MN-contiguous bf16 (128 B) per K row, K rows 128 B apart
+// (8-row groups 1024 B apart: SBO), the next 64-wide MN block `lbo_bytes` further (LBO) — the
+// layout TMA writes for boxes of {64 MN, K} placed lbo_bytes apart. Instruction bits 15/16 mark
+// A/B as MN-major. Advancing K by 16 moves the start address by 16 x 128 B.
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr, uint32_t lbo_bytes) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16) | (64ull << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+constexpr uint32_t kIdescMajorMN = (1u << 15) | (1u << 16);
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
                                             uint64_t pol) {
   asm volatile(
