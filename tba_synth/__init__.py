@@ -152,6 +152,27 @@ WORKLOADS["qwen_shard"] = dataclasses.replace(WORKLOADS["qwen"], name="qwen_shar
 # Pythia TL;DR in fp32 logits/dlogits: the paper's PFT runs were fp32 without DeepSpeed.
 WORKLOADS["pythia_fp32"] = dataclasses.replace(WORKLOADS["pythia"], name="pythia_fp32", dtype="fp32",
                                                note="Pythia-410M TL;DR shape with fp32 logits (PFT precision, P:593)")
+# The paper's own batch shapes (its hyperparameter tables; BASELINE.json's configs differ):
+# GSM8K Table 3: 7 prompts x K=20, responses up to 512 tokens, Rho-1B vocabulary.
+WORKLOADS["gsm8k_t3"] = dataclasses.replace(WORKLOADS["rhomath"], name="gsm8k_t3", B=7,
+                                            note="paper Table 3 (GSM8K): 7 x K=20, T=512, V=32000")
+# GSM8K K ablation (`tab:k_ablate`): K=40 with fewer prompts; 140/40 is not whole, so 3 x 40
+# (the largest whole-group batch not above Table 3's 140; DESIGN.md R-presets).
+WORKLOADS["gsm8k_k40"] = dataclasses.replace(WORKLOADS["rhomath"], name="gsm8k_k40", B=3, K=40,
+                                             note="paper K ablation tab:k_ablate (GSM8K): 3 x K=40, T=512, V=32000")
+# TL;DR Table 4: 8 prompts x K=20, 128-token responses, Pythia vocabulary.
+WORKLOADS["tldr_t4"] = dataclasses.replace(WORKLOADS["pythia"], name="tldr_t4", B=8, K=20, T=128,
+                                           len_lo=128, len_hi=128,
+                                           note="paper Table 4 (TL;DR): 8 x K=20, T=128, V=50304")
+# MATH Table 5: 32 prompts x K=16; responses up to 3072 - 1024 = 2048 tokens, length
+# mix unstated: L_s ~ U{256..2048} (DESIGN.md R-presets). The whole batch is 319 GB of bf16
+# logits; `math_t5_shard` is its per-GPU share at 8xB200 (4 groups, 39.9 GB).
+WORKLOADS["math_t5"] = dataclasses.replace(WORKLOADS["qwen"], name="math_t5", B=32, K=16, T=2048,
+                                           len_lo=256, len_hi=2048,
+                                           note="paper Table 5 (MATH): 32 x K=16, T<=2048, V=152064")
+WORKLOADS["math_t5_shard"] = dataclasses.replace(WORKLOADS["math_t5"], name="math_t5_shard", B=4,
+                                                 note="paper Table 5 (MATH) per-GPU shard at 8xB200: "
+                                                      "4 x K=16, T<=2048, V=152064")
 # One Qwen group (8 x 1024 rows, 2.5 GB of logits): the slice `ncu --set full` replays.
 WORKLOADS["qwen_group"] = dataclasses.replace(WORKLOADS["qwen"], name="qwen_group", B=1,
                                               note="one Qwen2.5-7B MATH group: 1 x K=8, T=1024, V=152064 (profiling)")

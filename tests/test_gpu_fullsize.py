@@ -151,3 +151,29 @@ def test_qwen_group_metamorphic_permutation_and_shift():
     rew2 = inp["log_reward"] + w.beta * 0.75
     o3, ws3 = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], rew2, w.beta, K, float(N))
     H.assert_seq_close(o3.resid.cpu().numpy(), o.resid.cpu().numpy(), "shifted resid", rel=1e-9, abs_=1e-9)
+
+
+@pytest.mark.parametrize("name,seed,groups", [("gsm8k_t3", 0, [0, 6]), ("gsm8k_k40", 1, [0, 2]),
+                                              ("tldr_t4", 2, [3, 7])])
+def test_paper_table_batch_shapes_full(name, seed, groups):
+    """The paper's own batch shapes (Tables 3 and 4, the K = 40 ablation) at full size."""
+    w = syn.WORKLOADS[name]
+    inp, o, d = run_full(w, seed)
+    ref = H.oracle_seq_values(w, seed, 0, w.B)
+    H.assert_seq_close(o.seq_logp.cpu().numpy(), ref["ell"], f"seq_logp (all {w.N} sequences)")
+    np.testing.assert_array_equal(o.n_tokens.cpu().numpy(), ref["n_tok"])
+    loss, logz, eps = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, w.K)
+    H.assert_seq_close(o.log_z.cpu().numpy(), logz, "log_z")
+    H.assert_seq_close(o.resid.cpu().numpy(), eps, "resid")
+    H.assert_seq_close([o.partial[0].item()], [loss], "loss")
+    check_groups(w, seed, inp, o, d, groups, n_rows_sample=16)
+    check_properties(w, inp, o, d)
+
+
+def test_math_t5_two_groups_ragged_2048():
+    """Table 5's MATH shape (K = 16, responses up to 2048 tokens, V = 152064): two whole groups
+    (20 GB of logits), one compared with the oracle sequence by sequence."""
+    w = syn.WORKLOADS["math_t5_shard"]
+    inp, o, d = run_full(w, 3, 0, 2)
+    check_groups(w, 3, inp, o, d, [1], n_rows_sample=12)
+    check_properties(w, inp, o, d, n_rows=32)

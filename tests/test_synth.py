@@ -88,3 +88,16 @@ def test_rewards_and_ref():
     ref = syn.ref_logp(w, 0)
     e_v = 6 - (np.log(w.V) + 2.65)
     assert np.all(np.abs(ref - e_v * w.T) <= 20.0 + 1e-3)
+
+
+def test_paper_table_presets():
+    """Batch shapes of the paper's hyperparameter tables."""
+    W = syn.WORKLOADS
+    assert (W["gsm8k_t3"].B, W["gsm8k_t3"].K, W["gsm8k_t3"].T) == (7, 20, 512)       # effective batch 140
+    assert W["gsm8k_k40"].K == 40 and W["gsm8k_k40"].N <= 140
+    assert (W["tldr_t4"].B, W["tldr_t4"].K, W["tldr_t4"].T) == (8, 20, 128)          # effective batch 160
+    assert (W["math_t5"].N, W["math_t5"].T, W["math_t5"].beta) == (512, 2048, 0.005)  # 3072 - 1024
+    assert W["math_t5_shard"].B * 8 == W["math_t5"].B
+    L = syn.seq_lengths(W["math_t5"], 0)
+    assert L.min() >= 256 and L.max() <= 2048 and len(L) == 512
+    assert np.all(syn.seq_lengths(W["tldr_t4"], 0) == 128)
