@@ -333,6 +333,8 @@ int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const d
  *   (>= d). dhidden must not alias hidden. accumulate = 0 overwrites (masked rows of dhidden
  *   are written with 0), accumulate = 1 adds into the existing contents (micro-batching).
  *   d_log_z (TB only, nullable): dL/dlog Z_i for a learned log Z, as in tba_tb_loss_bwd.
+ * dhidden may be summed over up to 4 slices of the vocabulary (split-K: fixed slice bounds that
+ * depend on d, vocab and the SM count only, added in slice order).
  * Deterministic: fixed tile order, no atomics. bwd_workspace: 256-byte aligned, of
  * tba_lmhead_bwd_workspace_bytes(n_seq, seq_len, d, vocab, chunk_rows) bytes. */
 size_t tba_lmhead_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t d, int64_t vocab,

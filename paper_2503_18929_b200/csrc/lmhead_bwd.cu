@@ -20,6 +20,8 @@
 // cta_group::2 form with 256 x 512 tiles per SM pair (half the single-SM kernel's L2 -> SM feed).
 // The one-call schedule (launch_lmhead_fwd_bwd) takes chunks of whole groups: the forward stores
 // the chunk's fp32 logits and lmb_dz_from_z replaces step 2's recompute GEMM.
+#include <cmath>
+
 #include "tc_sm100.cuh"
 
 namespace tba {
@@ -66,6 +68,9 @@ struct GemmArgs {
   int pol;             // bit 0: A loads evict_last, bit 1: B loads evict_last
   DzArgs dz;
   StoreArgs st;
+  int ksplit;          // tc_gemm2 only: > 1 splits K into ksplit slices; slice sl of tile (m, n) stores
+  float* part;         // its fp32 partial at part[(sl * cap + m) * part_ld + n] (lmb_splitk_reduce sums them)
+  int64_t part_ld;
 };
 
 __device__ __forceinline__ int64_t chunk_count(const int* n_valid, int64_t chunk0, int64_t cap) {
@@ -403,6 +408,10 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
   g.n_inner = a.n_inner;
   const int64_t n_tiles = g.n_mt * g.n_nt;
   const bool has_k = g.nkb > 0;
+  // split-K (K static, ksplit <= nkb): unit u = slice (u / n_tiles) of tile (u % n_tiles), k blocks
+  // [sl nkb / S, (sl + 1) nkb / S): the slice boundaries depend on K and S only, never on the tiling.
+  const int S = a.ksplit > 1 ? a.ksplit : 1;
+  const int64_t n_units = n_tiles * S;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < G2_STAGES; ++s) {
@@ -434,10 +443,11 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
       const uint64_t pol_a = l2_policy(a.pol & 1), pol_b = l2_policy(a.pol & 2);
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = pair0; t < n_tiles; t += n_pairs) {
+      for (int64_t u = pair0; u < n_units; u += n_pairs) {
+        const int64_t t = u % n_tiles, sl = u / n_tiles;
         int64_t mb, nb;
         tile_of(g, t, mb, nb);
-        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+        for (int64_t kb = sl * g.nkb / S, kb1 = (sl + 1) * g.nkb / S; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           if (leader) mbar_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
           if (MN) {
@@ -473,12 +483,13 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t j = 0;
-      for (int64_t t = pair0; t < n_tiles; t += n_pairs, ++j) {
+      for (int64_t u = pair0; u < n_units; u += n_pairs, ++j) {
+        const int64_t sl = u / n_tiles, kb0 = sl * g.nkb / S;
         const uint32_t acc = j % NACC, aph = (j / NACC) & 1u;
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * NT * GB_BN;
-        for (int64_t kb = 0; kb < g.nkb; ++kb) {
+        for (int64_t kb = kb0, kb1 = (sl + 1) * g.nkb / S; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(sA + stage * G2_A_BYTES);
@@ -488,10 +499,10 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)
 #pragma unroll
-            for (int u = 0; u < NT; ++u) {
-              const uint32_t sb = smem_u32(sB + stage * G2_B_BYTES + u * (128 * TC_BK * 2));
+            for (int nu = 0; nu < NT; ++nu) {
+              const uint32_t sb = smem_u32(sB + stage * G2_B_BYTES + nu * (128 * TC_BK * 2));
               const uint64_t b0 = MN ? umma_desc_mn_sw128(sb, 8192) : umma_desc_sw128(sb);
-              umma_bf16_pair<IDESC>(d_tmem + u * GB_BN, a0 + kstep * k, b0 + kstep * k, (kb | k) != 0);
+              umma_bf16_pair<IDESC>(d_tmem + nu * GB_BN, a0 + kstep * k, b0 + kstep * k, kb != kb0 || k != 0);
             }
           umma_commit_pair(&empty[stage]);
           if (++stage == G2_STAGES) {
@@ -510,7 +521,8 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(tempty_leader) : "r"(smem_u32(tempty)));
     const StoreArgs& st = a.st;
     uint32_t j = 0;
-    for (int64_t t = pair0; t < n_tiles; t += n_pairs, ++j) {
+    for (int64_t u = pair0; u < n_units; u += n_pairs, ++j) {
+      const int64_t t = u % n_tiles, sl = u / n_tiles;
       int64_t mb, nb;
       tile_of(g, t, mb, nb);
       const uint32_t acc = j % NACC, aph = (j / NACC) & 1u;
@@ -532,7 +544,22 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0.f;
         }
-        if (in && (has_k || !st.add)) store_row32(st, orow, n0, a.N, v);
+        if (S > 1) {
+          if (in) {  // fp32 partial of slice sl (part_ld is a multiple of 4 floats)
+            float* p = a.part + (sl * a.cap + m) * a.part_ld + n0;
+            if (n0 + 32 <= a.N) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                reinterpret_cast<float4*>(p)[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (n0 + e < a.N) p[e] = v[e];
+            }
+          }
+        } else if (in && (has_k || !st.add)) {
+          store_row32(st, orow, n0, a.N, v);
+        }
       }
       if (has_k) {
         tc_fence_before();
@@ -706,12 +733,49 @@ __global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __rest
   }
 }
 
+// dH rows from the split-K partials of tc_gemm2: out[row_map[m]] (+)= sum over slices, in slice order
+// (fixed order: deterministic). One thread per 4 consecutive columns; rows m < the chunk's count.
+__global__ void __launch_bounds__(256) lmb_splitk_reduce(const float* __restrict__ part, int64_t part_ld, int S,
+                                                         int64_t cap, const int* __restrict__ n_valid, int64_t chunk0,
+                                                         int64_t N, StoreArgs st) {
+  const int64_t M = chunk_count(n_valid, chunk0, cap);
+  const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (n >= N) return;
+  for (int64_t m = blockIdx.y; m < M; m += gridDim.y) {
+    float4 acc = __ldg(reinterpret_cast<const float4*>(part + m * part_ld + n));
+    for (int sl = 1; sl < S; ++sl) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(part + (sl * cap + m) * part_ld + n));
+      acc.x += q.x;
+      acc.y += q.y;
+      acc.z += q.z;
+      acc.w += q.w;
+    }
+    const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+    const int64_t orow = st.row_map ? (int64_t)st.row_map[m] : m;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (n + e >= N) break;
+      if (st.out_bf16) {
+        uint16_t* o = static_cast<uint16_t*>(st.D) + orow * st.ldd + n + e;
+        *o = to_bf16(st.add ? v[e] + bf16_to_f(*o) : v[e]);
+      } else {
+        float* o = static_cast<float*>(st.D) + orow * st.ldd + n + e;
+        *o = st.add ? v[e] + *o : v[e];
+      }
+    }
+  }
+}
+
+constexpr int LMB_KSPLIT_MAX = 4;
+
 struct LmbWs {
   int* idx;  // [rows] + the count at idx[rows]
   uint16_t *wt, *hc, *hct, *dz, *dzt;
+  float* part;  // dH split-K partials [LMB_KSPLIT_MAX][C][lmb_dp(d)]
 };
 
 inline int64_t lmb_vp(int64_t V) { return (V + 7) / 8 * 8; }
+inline int64_t lmb_dp(int64_t d) { return (d + 3) / 4 * 4; }
 
 LmbWs lmb_layout(void* base, int64_t rows, int64_t d, int64_t V, int64_t C) {
   char* p = static_cast<char*>(base);
@@ -728,6 +792,7 @@ LmbWs lmb_layout(void* base, int64_t rows, int64_t d, int64_t V, int64_t C) {
   w.hct = reinterpret_cast<uint16_t*>(take((size_t)d * (size_t)C * 2));
   w.dz = reinterpret_cast<uint16_t*>(take((size_t)C * (size_t)lmb_vp(V) * 2));
   w.dzt = reinterpret_cast<uint16_t*>(take((size_t)V * (size_t)C * 2));
+  w.part = reinterpret_cast<float*>(take((size_t)LMB_KSPLIT_MAX * (size_t)C * (size_t)lmb_dp(d) * 4));
   return w;
 }
 
@@ -796,7 +861,8 @@ size_t lmhead_bwd_ws_bytes(int64_t rows, int64_t d, int64_t V, int64_t chunk_row
   const int64_t C = lmhead_bwd_chunk(rows, chunk_rows);
   return align_up((size_t)(rows + 1) * sizeof(int), 256) + align_up((size_t)d * (size_t)lmb_vp(V) * 2, 256) +
          2 * align_up((size_t)C * (size_t)d * 2, 256) + align_up((size_t)C * (size_t)lmb_vp(V) * 2, 256) +
-         align_up((size_t)V * (size_t)C * 2, 256);
+         align_up((size_t)V * (size_t)C * 2, 256) +
+         align_up((size_t)LMB_KSPLIT_MAX * (size_t)C * (size_t)lmb_dp(d) * 4, 256);
 }
 
 namespace {
@@ -811,9 +877,43 @@ struct LmbCtx {
   CUtensorMap m_hc, m_w, m_dz, m_wt, m_dzt, m_hct;
   int swz, ninner, pol, pair, wide;  // pair: bit 0 dH, bit 1 dW on the cta_group::2 kernel; wide: NT = 2
   bool dwmn;                         // dW reads dZ and Hc as MN-major operands (no transposed copies)
+  int dh_split;                      // dH split-K slices on the pair kernel (lmb_dh_split)
   CUtensorMap m_dzmn, m_hcmn;
   CUtensorMap m_wt2, m_hct2;   // B operands with 128-row boxes for the pair kernel (A boxes are 128 rows already)
 };
+
+// dH = dZ W has few output tiles and a long K (= V): (C/256) x (d/512) pair tiles leave the last
+// wave mostly idle (Qwen: 448 tiles on 74 pairs = 6.05 waves run as 7). Split K into S slices
+// (TBA_LMB_KSPLIT: 0 auto, else forced 1..4). Auto: the smallest S whose waves over the nominal chunk
+// (LMB_DEFAULT_CHUNK rows) come within 4 % of perfect balance. S depends on (d, V, SMs) only, so the
+// one-call and two-call schedules split alike and their dH stay bitwise equal.
+int lmb_dh_split(int64_t d, int64_t V, int nt) {
+  static const int knob = env_int("TBA_LMB_KSPLIT", 0);
+  const int64_t nkb = (V + TC_BK - 1) / TC_BK;
+  int S = 1;
+  if (knob > 0) {
+    S = knob;
+  } else {
+    const double pairs = (double)(device_sms() / 2 > 0 ? device_sms() / 2 : 1);
+    const double tiles = (double)((LMB_DEFAULT_CHUNK / 256) * ((d + nt * GB_BN - 1) / (nt * GB_BN)));
+    const double ideal = tiles / pairs;
+    double best = 1e30;
+    for (int c = 1; c <= LMB_KSPLIT_MAX; ++c) {
+      const double waves = std::ceil(tiles * c / pairs) / c;
+      if (waves <= 1.04 * ideal) {
+        S = c;
+        break;
+      }
+      if (waves < best - 1e-9) {
+        best = waves;
+        S = c;
+      }
+    }
+  }
+  if (S > LMB_KSPLIT_MAX) S = LMB_KSPLIT_MAX;
+  if (S > nkb) S = (int)nkb;
+  return S < 1 ? 1 : S;
+}
 
 int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, void* bws, bool need_wt, cudaStream_t s) {
   static const int swz = [] { int v = env_int("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
@@ -833,6 +933,7 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   k.pair = pair;
   k.wide = wide;
   k.dwmn = dwmn != 0 && (pair & 2) != 0;
+  k.dh_split = (pair & 1) ? lmb_dh_split(d, V, (wide & 1) ? 2 : 1) : 1;
   if (need_wt) {
     const dim3 grid((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64));
     lmb_gather_t<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x->weight), x->weight_stride, d, nullptr,
@@ -906,9 +1007,20 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
     const int64_t esz = dh_dt == TBA_BF16 ? 2 : 4;
     b.st = StoreArgs{dh, dh_stride, k.w.idx + chunk0, dh_dt == TBA_BF16, dh_add ? 1 : 0,
                      ((reinterpret_cast<uintptr_t>(dh) | (uintptr_t)(dh_stride * esz)) & 15) == 0};
-    rc = (k.pair & 1) ? ((k.wide & 1) ? launch_gemm2<2>(k.m_dz, k.m_wt2, b, (C / 256 + 1) * nt_d, s)
-                                      : launch_gemm2<1>(k.m_dz, k.m_wt2, b, (C / 256 + 1) * nt_d, s))
-                      : launch_gemm<EPI_STORE>(k.m_dz, k.m_wt, b, (C / GB_BM) * nt_d, s);
+    if (k.pair & 1) {
+      b.ksplit = k.dh_split;
+      b.part = k.w.part;
+      b.part_ld = lmb_dp(d);
+      const int64_t units = (C / 256 + 1) * nt_d * k.dh_split;
+      rc = (k.wide & 1) ? launch_gemm2<2>(k.m_dz, k.m_wt2, b, units, s) : launch_gemm2<1>(k.m_dz, k.m_wt2, b, units, s);
+      if (!rc && k.dh_split > 1) {
+        const dim3 rg((unsigned)(((d + 3) / 4 + 255) / 256), (unsigned)(C < 65535 ? C : 65535));
+        lmb_splitk_reduce<<<rg, 256, 0, s>>>(k.w.part, b.part_ld, k.dh_split, C, n_valid, chunk0, d, b.st);
+        rc = launch_status();
+      }
+    } else {
+      rc = launch_gemm<EPI_STORE>(k.m_dz, k.m_wt, b, (C / GB_BM) * nt_d, s);
+    }
     if (rc) return rc;
   }
   if (dw) {  // 4. dW (+)= dZ^T H: M = V, N = d, K = the chunk's rows

@@ -276,10 +276,35 @@ def test_lmhead_bwd_pair_kernel_bitwise(tmp_path):
     # (forward kernel TBA_LM_MC, backward TBA_LMB_2SM, TBA_LMB_NT2): single-SM everywhere first
     for cfg in (("1", "0", "0"), ("1", "3", "0"), ("1", "3", "3"), ("3", "3", "3"), ("4", "3", "3"), ("2", "0", "0")):
         f = tmp_path / f"r{''.join(cfg)}.pt"
-        env = dict(os.environ, TBA_LM_MC=cfg[0], TBA_LMB_2SM=cfg[1], TBA_LMB_NT2=cfg[2])
+        env = dict(os.environ, TBA_LM_MC=cfg[0], TBA_LMB_2SM=cfg[1], TBA_LMB_NT2=cfg[2], TBA_LMB_KSPLIT="1")
         subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
         out[cfg] = torch.load(f)
     base = out[("1", "0", "0")]
     for cfg, r in out.items():
         for k in base:
             assert torch.equal(base[k], r[k]), (cfg, k)
+
+
+def test_lmhead_bwd_dh_split_k(tmp_path):
+    """dH = dZ W split along K (= V) into 2-4 slices on the pair kernel (TBA_LMB_KSPLIT): each slice is
+    one K-ordered fp32 accumulation and the slices are summed in slice order, so everything but dH is
+    bitwise the unsplit result, and dH differs only by fp32 reassociation (well inside R21's bound)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for ks in ("1", "2", "3", "4"):
+        f = tmp_path / f"k{ks}.pt"
+        env = dict(os.environ, TBA_LMB_2SM="3", TBA_LMB_NT2="3", TBA_LMB_KSPLIT=ks)
+        subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
+        out[ks] = torch.load(f)
+    base = out["1"]
+    scale = base["dh"].float().abs().max().item()
+    for ks, r in out.items():
+        for k in base:
+            if k == "dh":
+                err = (r[k].float() - base[k].float()).abs().max().item()
+                assert err <= 2 ** -7 * scale, (ks, err, scale)   # a bf16 rounding step at most
+            else:
+                assert torch.equal(base[k], r[k]), (ks, k)
