@@ -741,16 +741,21 @@ __global__ void __launch_bounds__(256) lmb_splitk_reduce(const float* __restrict
   const int64_t M = chunk_count(n_valid, chunk0, cap);
   const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (n >= N) return;
+  const bool full4 = n + 4 <= N;  // the tail reads only the columns the GEMM wrote
   for (int64_t m = blockIdx.y; m < M; m += gridDim.y) {
-    float4 acc = __ldg(reinterpret_cast<const float4*>(part + m * part_ld + n));
-    for (int sl = 1; sl < S; ++sl) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(part + (sl * cap + m) * part_ld + n));
-      acc.x += q.x;
-      acc.y += q.y;
-      acc.z += q.z;
-      acc.w += q.w;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int sl = 0; sl < S; ++sl) {
+      const float* q = part + (sl * cap + m) * part_ld + n;
+      if (full4) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(q));
+        v[0] += w.x;
+        v[1] += w.y;
+        v[2] += w.z;
+        v[3] += w.w;
+      } else {
+        for (int e = 0; e < 4 && n + e < N; ++e) v[e] += __ldg(q + e);
+      }
     }
-    const float v[4] = {acc.x, acc.y, acc.z, acc.w};
     const int64_t orow = st.row_map ? (int64_t)st.row_map[m] : m;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {

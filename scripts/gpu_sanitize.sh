@@ -13,3 +13,10 @@ done
 timeout 900 compute-sanitizer --tool racecheck --kernel-name regex=tc_gemm2 python scripts/sanitize_case.py > gpurun_out/sanitize_racecheck_pair.log 2>&1
 echo "racecheck (pair GEMMs) rc=$?"; grep -E "RACECHECK SUMMARY" gpurun_out/sanitize_racecheck_pair.log
 grep -oE "in lmhead_bwd.cu:[0-9]+" gpurun_out/sanitize_racecheck_pair.log | sort | uniq -c
+# dH split-K (forced on at the small dims, where auto picks S = 1): the slice partials and their reduction
+# (initcheck unfiltered, as above: a kernel filter hides the writes of the input generators)
+for tool in memcheck initcheck; do
+  if [ $tool = initcheck ]; then F=""; else F="--kernel-name regex=lmb_|tc_gemm"; fi
+  TBA_LMB_KSPLIT=3 timeout 900 compute-sanitizer --tool $tool $F --error-exitcode 9 python scripts/sanitize_case.py > gpurun_out/sanitize_ksplit_$tool.log 2>&1
+  echo "$tool (TBA_LMB_KSPLIT=3) rc=$?"; grep -E "ERROR SUMMARY|sanitize cases done" gpurun_out/sanitize_ksplit_$tool.log | tail -2
+done
