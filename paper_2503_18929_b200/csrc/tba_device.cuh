@@ -363,8 +363,26 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
     if (s >= n_seq) break;
     double acc = 0.0;
     int cnt = 0;
-    for (int64_t t = lane; t < T; t += 32) {
-      const int64_t r = s * T + t;
+    const int64_t base = s * T;
+    int64_t t = lane;
+    // 8 positions per lane in flight (masks first, then the predicated log-prob loads), summed in
+    // the same t order as the tail loop: bitwise the plain loop, without one load latency per step.
+    for (; t + 32 * 7 < T; t += 32 * 8) {
+      uint8_t mk[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mk[u] = mask[base + t + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = mk[u] ? __ldcg(lp + base + t + 32 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (mk[u]) {
+          acc += v[u];
+          ++cnt;
+        }
+    }
+    for (; t < T; t += 32) {
+      const int64_t r = base + t;
       if (mask[r]) {
         acc += __ldcg(lp + r);  // L2-coherent: lp may have been written by other CTAs of this grid
         ++cnt;
