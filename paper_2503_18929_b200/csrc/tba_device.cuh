@@ -366,12 +366,13 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
     const int64_t base = s * T;
     int64_t t = lane;
     // 8 positions per lane in flight (masks first, then the predicated log-prob loads), summed in
-    // the same t order as the tail loop: bitwise the plain loop, without one load latency per step.
-    for (; t + 32 * 7 < T; t += 32 * 8) {
+    // t order: bitwise the plain one-position loop, without one load latency per position.
+    // (lp is read L2-coherent: it may have been written by other CTAs of this grid)
+    for (; t < T; t += 32 * 8) {
       uint8_t mk[8];
       double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) mk[u] = mask[base + t + 32 * u];
+      for (int u = 0; u < 8; ++u) mk[u] = (t + 32 * u < T) ? mask[base + t + 32 * u] : (uint8_t)0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = mk[u] ? __ldcg(lp + base + t + 32 * u) : 0.0;
 #pragma unroll
@@ -380,13 +381,6 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
           acc += v[u];
           ++cnt;
         }
-    }
-    for (; t < T; t += 32) {
-      const int64_t r = base + t;
-      if (mask[r]) {
-        acc += __ldcg(lp + r);  // L2-coherent: lp may have been written by other CTAs of this grid
-        ++cnt;
-      }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -455,20 +449,37 @@ __device__ __forceinline__ void tb_group_head(int64_t g, int K, const double* __
                                               const double* seq_logp, double* __restrict__ log_z,
                                               double* __restrict__ resid, double* __restrict__ group_sq) {
   const int64_t s0 = g * K;
+  // delta_j for 8 sequences at a time (loads in flight together); sums in j order as before
+  auto delta8 = [&](int j0, double (&d)[8]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u < K) d[u] = ref_logp[s0 + j0 + u] - __ldcg(seq_logp + s0 + j0 + u) + log_reward[s0 + j0 + u] * inv_beta;
+  };
   double lz;
   if (log_z_param) {
     lz = log_z_param[g];
   } else {
     double sum = 0.0;
-    for (int j = 0; j < K; ++j) sum += ref_logp[s0 + j] - __ldcg(seq_logp + s0 + j) + log_reward[s0 + j] * inv_beta;
+    for (int j0 = 0; j0 < K; j0 += 8) {
+      double d[8];
+      delta8(j0, d);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < K) sum += d[u];
+    }
     lz = sum / (double)K;
   }
   double sq = 0.0;
-  for (int j = 0; j < K; ++j) {
-    const double delta = ref_logp[s0 + j] - __ldcg(seq_logp + s0 + j) + log_reward[s0 + j] * inv_beta;
-    const double e = lz - delta;
-    resid[s0 + j] = e;
-    sq += e * e;
+  for (int j0 = 0; j0 < K; j0 += 8) {
+    double d[8];
+    delta8(j0, d);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u < K) {
+        const double e = lz - d[u];
+        resid[s0 + j0 + u] = e;
+        sq += e * e;
+      }
   }
   log_z[g] = lz;
   group_sq[g] = sq;
@@ -477,8 +488,17 @@ __device__ __forceinline__ void tb_group_head(int64_t g, int K, const double* __
 // Final fixed-order reduction of the per-group sums of squares (+ optional fused all-reduce).
 __device__ __forceinline__ void tb_finish(const double* group_sq, int64_t groups, int64_t n_seq, double inv_n_global,
                                           double* partial, const PeerArgs& pa) {
+  // serial group order (deterministic); 16 loads in flight per batch instead of one latency per group
   double tot = 0.0;
-  for (int64_t i = 0; i < groups; ++i) tot += __ldcg(group_sq + i);
+  int64_t i = 0;
+  for (; i + 16 <= groups; i += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldcg(group_sq + i + u);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) tot += v[u];
+  }
+  for (; i < groups; ++i) tot += __ldcg(group_sq + i);
   const double p[3] = {tot * inv_n_global, (double)n_seq, (double)groups};
   if (pa.world > 0) {
     peer_allreduce3(pa, p, partial);
