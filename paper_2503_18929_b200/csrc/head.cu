@@ -9,7 +9,7 @@ namespace {
 // Eq. 3 when log_z_param != NULL; Eq. 5 residual eps = log Z_i - delta. The last CTA (counter)
 // reduces the per-group sums of squares in group order.
 template <bool HEAD>
-__global__ void __launch_bounds__(256) seq_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(1024) seq_head(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
                                                 int64_t n_seq, int64_t T, int K, const double* __restrict__ ref_logp,
                                                 const double* __restrict__ log_reward,
                                                 const double* __restrict__ log_z_param, double inv_beta,
@@ -252,7 +252,9 @@ bool launch_fwd_head(const tba_rows* x, const WsLayout& w, const RowScale& rs, i
 
 int launch_seq_head(bool head, const WsLayout& w, const uint8_t* mask, const HeadArgs& ha, cudaStream_t s) {
   if (head) {
-    seq_head<true><<<(unsigned)(ha.n_seq / ha.K), 256, 0, s>>>(
+    // one warp per sequence of the group (K > 8: more than one round of 8 warps otherwise)
+    const int threads = ha.K <= 8 ? 256 : (ha.K >= 32 ? 1024 : 32 * ha.K);
+    seq_head<true><<<(unsigned)(ha.n_seq / ha.K), threads, 0, s>>>(
         w.lp, mask, ha.n_seq, ha.T, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.inv_n_global,
         ha.seq_logp, ha.n_tokens, ha.log_z, ha.resid, w.group_sq, ha.partial, w.counter, ha.pa);
   } else {

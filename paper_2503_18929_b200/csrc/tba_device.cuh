@@ -350,15 +350,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 
 
 // ------------------------------------------------------------------------------ a2 + a3
-// Per-sequence sums: warp w of a CTA takes sequences w, w+8, ... of the CTA's `per` sequences,
+// Per-sequence sums: warp w of a CTA takes sequences w, w+nw, ... of the CTA's `per` sequences,
 // lane-strided fp64 partial sums over t in a fixed order, then a fixed xor butterfly.
 __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const uint8_t* __restrict__ mask,
                                          int64_t n_seq, int64_t T, int64_t s0, int per,
                                          double* __restrict__ seq_logp, int32_t* __restrict__ n_tokens,
                                          int* my_count) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
   int tot = 0;
-  for (int j = warp; j < per; j += 8) {
+  for (int j = warp; j < per; j += nw) {
     const int64_t s = s0 + j;
     if (s >= n_seq) break;
     double acc = 0.0;
