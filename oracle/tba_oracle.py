@@ -23,7 +23,9 @@ Pins (tests/test_oracle.py): worked values of S:52, S:
 the closed form log Z = log(0.5e + 0.5) at pi_theta = pi* (Eq. 2); softmax rows sum to 1
 within 1e-12; shift invariance; scipy's logsumexp; brute-force products of
 probabilities; L = mean within-group population variance; per-group shift invariance;
-the independent Appendix-A advantage form; central finite differences of the loss.
+the independent Appendix-A advantage form; central finite differences of the loss;
+token_logprob_rows + sequence_sums against the brute-force product row by row; dlogits_row
+against central differences of token_logprob, the S:133 worked rows and ``dlogits``.
 TBA' (Eq. 16) pins (tests/test_oracle_tbap.py): Dr. GRPO equality at beta = 0 on-policy
 (P:616), the Eq. 7 / Eq. 16 link A = -beta*eps, clip/IcePop worked values, the band
 (0, inf) no-op, per-group shift invariance, finite differences with coefficients held fixed.
@@ -70,25 +72,44 @@ def token_logprob(z: np.ndarray, y: int) -> tuple[float, float]:
 
 
 # ----------------------------------------------------------------------------- a2
+def token_logprob_rows(z_rows: np.ndarray, tokens) -> tuple[np.ndarray, np.ndarray]:
+    """``token_logprob`` of each row of z_rows [n, V] at its token (tokens [n]): the per-token
+    terms of log pi_theta(y|x) (Eqs. 4-5) for a batch of VALID rows, wherever they come from
+    (the full-size harness regenerates sampled rows from the seed). Returns (lp [n], lse [n])."""
+    n = len(tokens)
+    lp = np.empty(n)
+    lse = np.empty(n)
+    for i in range(n):
+        lp[i], lse[i] = token_logprob(z_rows[i], int(tokens[i]))
+    return lp, lse
+
+
+def sequence_sums(lp: np.ndarray, mask: np.ndarray):
+    """a2: ell_s = sum_{t: mu=1} lp_{s,t} (``math.fsum``, exact) and n_tok_s = sum_t mu_{s,t}.
+    lp [N, T] holds the token log-probs at valid positions (other entries are ignored)."""
+    N = lp.shape[0]
+    ell = np.array([math.fsum(lp[s][mask[s] == 1]) for s in range(N)])
+    ntok = np.asarray(mask).sum(1).astype(np.int64)
+    return ell, ntok
+
+
 def seq_logprob(logits: np.ndarray, tokens: np.ndarray, mask: np.ndarray):
     """ell_s = sum_t mu_{s,t} log softmax(z_{s,t})[y_{s,t}] and n_tok_s = sum_t mu_{s,t}.
 
     logits [N, T, V] (fp64-convertible), tokens [N, T] int, mask [N, T] 0/1. Tokens at
-    masked positions are ignored (reading R5). The sum over t uses
-    ``math.fsum`` (exact). Returns (ell [N] fp64, n_tok [N] int64, lse [N, T] fp64 with
-    NaN at masked positions)."""
+    masked positions are ignored (reading R5). ``token_logprob_rows`` over the
+    valid rows, then ``sequence_sums``. Returns (ell [N] fp64, n_tok [N] int64,
+    lse [N, T] fp64 with NaN at masked positions)."""
     N, T = tokens.shape
-    ell = np.zeros(N, dtype=np.float64)
-    ntok = np.zeros(N, dtype=np.int64)
+    lp = np.zeros((N, T))
     lse = np.full((N, T), np.nan)
-    for s in range(N):
-        terms = []
-        for t in range(T):
-            if mask[s, t]:
-                lp, lse[s, t] = token_logprob(logits[s, t], int(tokens[s, t]))
-                terms.append(lp)
-        ell[s] = math.fsum(terms)
-        ntok[s] = len(terms)
+    valid = np.asarray(mask).reshape(-1) == 1
+    if valid.any():
+        z = np.asarray(logits).reshape(N * T, -1)[valid]
+        lpv, lsev = token_logprob_rows(z, np.asarray(tokens).reshape(-1)[valid])
+        lp.reshape(-1)[valid] = lpv
+        lse.reshape(-1)[valid] = lsev
+    ell, ntok = sequence_sums(lp, mask)
     return ell, ntok, lse
 
 

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 1800 python -m pytest tests -q -m gpu -x 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python bench.py > gpurun_out/r2_bench0.json 2> gpurun_out/r2_bench0.err
+tail -c 3000 gpurun_out/r2_bench0.json

@@ -3,28 +3,47 @@
 // same integer round-to-nearest-even to bf16. Holds none of the method's arithmetic; it only
 // fills device buffers with synthetic logits so that 20 GB inputs need not cross PCIe.
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace {
 
 constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ uint64_t hash_at(uint64_t key, uint64_t i) { return mix64(key + (i + 1) * GAMMA); }
+__host__ __device__ __forceinline__ uint64_t hash_at(uint64_t key, uint64_t i) { return mix64(key + (i + 1) * GAMMA); }
 
-__device__ __forceinline__ float irwin_hall(uint64_t h) {
+__host__ __device__ __forceinline__ float irwin_hall(uint64_t h) {
   int64_t acc = (int64_t)(h & 0xFFFF) + (int64_t)((h >> 16) & 0xFFFF) + (int64_t)((h >> 32) & 0xFFFF) +
                 (int64_t)((h >> 48) & 0xFFFF) - 131070;
   return (float)((double)acc * (1.0 / 16384.0));
 }
 
-__device__ __forceinline__ uint16_t bf16_rne(float x) {
-  uint32_t b = __float_as_uint(x);
+__host__ __device__ __forceinline__ uint32_t f32_bits(float x) {
+#ifdef __CUDA_ARCH__
+  return __float_as_uint(x);
+#else
+  uint32_t b;
+  std::memcpy(&b, &x, 4);
+  return b;
+#endif
+}
+
+__host__ __device__ __forceinline__ uint64_t umulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+__host__ __device__ __forceinline__ uint16_t bf16_rne(float x) {
+  uint32_t b = f32_bits(x);
   return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
 }
 
@@ -33,7 +52,7 @@ __global__ void synth_logits_kernel(void* out, uint64_t key_logits, uint64_t key
                                     int64_t row0, int64_t nrows, int64_t V, int64_t row_stride) {
   for (int64_t r = blockIdx.y; r < nrows; r += gridDim.y) {
     const uint64_t grow = (uint64_t)(row0 + r);
-    const uint64_t y = __umul64hi(hash_at(key_tok, grow), (uint64_t)V);
+    const uint64_t y = umulhi64(hash_at(key_tok, grow), (uint64_t)V);
     const float peak = (float)(4 * (int)(hash_at(key_peak, grow) & 3ull));
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < row_stride;
          c += (int64_t)gridDim.x * blockDim.x) {
@@ -110,6 +129,28 @@ int tba_synth_logits(void* out, int dtype, uint64_t key_logits, uint64_t key_tok
   else
     synth_logits_kernel<false><<<grid, block, 0, stream>>>(out, key_logits, key_tok, key_peak, row0, nrows, V, row_stride);
   return (int)cudaGetLastError();
+}
+
+// HOST twin (no GPU needed): the same element function on the CPU, for an arbitrary list of
+// global rows, packed [nrows, V] (bf16 bits or fp32). Lets the test harness regenerate the
+// oracle's input rows ~100x faster than the NumPy twin (which pins it bit for bit,
+// tests/test_synth.py). Returns 0, or 1 on a bad argument.
+int tba_synth_logits_host(void* out, int dtype, uint64_t key_logits, uint64_t key_tok, uint64_t key_peak,
+                          const int64_t* rows, int64_t nrows, int64_t V) {
+  if (!out || !rows || nrows < 0 || V <= 0 || (dtype != 0 && dtype != 1)) return 1;
+  for (int64_t r = 0; r < nrows; ++r) {
+    const uint64_t grow = (uint64_t)rows[r];
+    const uint64_t y = umulhi64(hash_at(key_tok, grow), (uint64_t)V);
+    const float peak = (float)(4 * (int)(hash_at(key_peak, grow) & 3ull));
+    const uint64_t base = grow * (uint64_t)V;
+    for (int64_t c = 0; c < V; ++c) {
+      float z = irwin_hall(hash_at(key_logits, base + (uint64_t)c));
+      if ((uint64_t)c == y) z = z + peak;
+      if (dtype == 0) static_cast<uint16_t*>(out)[r * V + c] = bf16_rne(z);
+      else static_cast<float*>(out)[r * V + c] = z;
+    }
+  }
+  return 0;
 }
 
 }  // extern "C"

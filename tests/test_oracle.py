@@ -145,6 +145,31 @@ def test_seq_logprob_brute_force_product():
         assert ntok[s] == int(mask[s].sum())
 
 
+def test_row_terms_and_sequence_sums_brute_force():
+    """token_logprob_rows + sequence_sums (what the full-size harness calls on regenerated rows)
+    against the plain product of probabilities, row by row, with no reference to seq_logprob."""
+    rng = np.random.default_rng(11)
+    logits, tokens, mask, _, _ = _rand_instance(rng, 2, 2, 5, 6, scale=1.5)
+    N, T, V = logits.shape
+    valid = np.flatnonzero(mask.reshape(-1))
+    lp_v, lse_v = O.token_logprob_rows(logits.reshape(N * T, V)[valid], tokens.reshape(-1)[valid])
+    for i, r in enumerate(valid):
+        e = np.exp(logits.reshape(N * T, V)[r])
+        assert abs(math.exp(lp_v[i]) - e[tokens.reshape(-1)[r]] / e.sum()) < 1e-15
+        assert abs(math.exp(lse_v[i]) - e.sum()) < 1e-13 * e.sum()
+    lp = np.full((N, T), np.nan)                  # entries at masked positions must be ignored
+    lp.reshape(-1)[valid] = lp_v
+    ell, ntok = O.sequence_sums(lp, mask)
+    for s in range(N):
+        prod = 1.0
+        for t in range(T):
+            if mask[s, t]:
+                e = np.exp(logits[s, t])
+                prod *= e[tokens[s, t]] / e.sum()
+        assert abs(math.exp(ell[s]) - prod) < 1e-14 * max(1.0, prod)
+        assert ntok[s] == int(mask[s].sum())
+
+
 def test_masked_positions_ignored():
     rng = np.random.default_rng(2)
     logits, tokens, mask, _, _ = _rand_instance(rng, 1, 2, 6, 7)
@@ -237,6 +262,38 @@ def test_dlogits_finite_differences(K):  # north_star / S:160: relative e
         fd[idx] = (loss_of(lp) - loss_of(lm)) / (2 * step)
     rel = np.max(np.abs(fd - an)) / np.max(np.abs(an))
     assert rel < 1e-6, rel
+
+
+def test_dlogits_row_pins():
+    """dlogits_row (the expected value of every sampled full-size row comparison): (i) central
+    finite differences of the token log-prob it scales, times 2 eps g / N (App. A P:446-451);
+    (ii) the S:133 worked rows (-0.25, +0.25); (iii) equal to the FD-pinned ``dlogits`` at
+    (s, t) on random instances with grad_out != 1 and N_global != N."""
+    rng = np.random.default_rng(21)
+    for V in (2, 3, 7):
+        z = rng.normal(0, 1.5, V)
+        y = int(rng.integers(0, V))
+        eps, n, g = float(rng.normal()), int(rng.integers(4, 40)), float(rng.normal())
+        d = O.dlogits_row(z, y, eps, n, g)
+        h = 1e-6
+        for v in range(V):
+            zp, zm = z.copy(), z.copy()
+            zp[v] += h
+            zm[v] -= h
+            fd = (O.token_logprob(zp, y)[0] - O.token_logprob(zm, y)[0]) / (2 * h) * 2 * eps * g / n
+            assert abs(d[v] - fd) <= 1e-8 * max(1.0, abs(fd))
+    gold = GOLD["log_z_r10_uniform"]
+    for j in range(2):
+        row = O.dlogits_row(np.zeros(2), gold["tokens"][j], gold["eps"][j], 2)
+        np.testing.assert_allclose(row, gold["dlogits_rows"][j], atol=1e-15)
+    logits, tokens, mask, ref, rew = _rand_instance(rng, 2, 3, 4, 9)
+    _, _, eps = O.vargrad_tb_loss(O.seq_logprob(logits, tokens, mask)[0], ref, rew, 0.5, 3, n_global=20)
+    full = O.dlogits(logits, tokens, mask, eps, 20, grad_out=-1.75)
+    for s in range(6):
+        for t in range(4):
+            if mask[s, t]:
+                np.testing.assert_allclose(O.dlogits_row(logits[s, t], int(tokens[s, t]), eps[s], 20, -1.75),
+                                           full[s, t], rtol=0, atol=1e-16)
 
 
 def test_dlogits_rows_sum_zero_and_masked_zero():

@@ -101,3 +101,18 @@ def test_paper_table_presets():
     L = syn.seq_lengths(W["math_t5"], 0)
     assert L.min() >= 256 and L.max() <= 2048 and len(L) == 512
     assert np.all(syn.seq_lengths(W["tldr_t4"], 0) == 128)
+
+
+def test_host_twin_bit_identical_to_numpy():
+    """The C host twin (used by the full-size oracle harness) equals the NumPy twin bit for bit,
+    bf16 and fp32, on rows spanning small and 64-bit-scale indices and an unaligned vocabulary."""
+    rows = np.array([0, 1, 77, 65535, 524287, 2 ** 33 + 5], dtype=np.int64)
+    for V in (1000, 50257, 152064):
+        for dt in ("bf16", "fp32"):
+            a = syn.logits_rows(5, V, rows, dt)
+            b = syn.logits_rows_host(5, V, rows, dt)
+            assert a.dtype == b.dtype
+            np.testing.assert_array_equal(a.view(np.uint16 if dt == "bf16" else np.uint32),
+                                          b.view(np.uint16 if dt == "bf16" else np.uint32))
+    np.testing.assert_array_equal(syn.logits_rows_f64_host(2, 999, [3, 4], "bf16"),
+                                  syn.logits_rows_f64(2, 999, [3, 4], "bf16"))
