@@ -49,51 +49,137 @@ def host_logits(w: syn.Workload, seed: int, g0: int, ng: int) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------- parallel oracle
+# Full-size oracle runs: input rows are regenerated from the seed by tba_synth's C host twin
+# (bit-identical to its NumPy twin) in a persistent pool of spawned worker processes (one per
+# host core); every value is computed by oracle/ functions (token_logprob_rows, sequence_sums,
+# dlogits_row) — the pool only distributes rows.
+_POOL = None
+RECORD: list = []   # parity maxima per (test, config, seed, quantity); written by conftest
+
+
+def n_workers() -> int:
+    return max(1, len(os.sched_getaffinity(0)))
+
+
+def pool():
+    global _POOL
+    if _POOL is None:
+        import multiprocessing as mp
+        _POOL = ProcessPoolExecutor(n_workers(), mp_context=mp.get_context("spawn"))
+    return _POOL
+
+
+def record(test: str, config: str, seed: int, quantity: str, n: int, max_abs_err: float, max_err_over_tol: float,
+           **extra):
+    RECORD.append(dict(test=test, config=config, seed=int(seed), quantity=quantity, n=int(n),
+                       max_abs_err=float(max_abs_err), max_err_over_tol=float(max_err_over_tol), **extra))
+
+
 def _rows_lp(args):
     seed, V, dtype, rows, toks = args
-    z = syn.logits_rows_f64(seed, V, rows, dtype)
-    out = np.empty(len(rows))
-    lse = np.empty(len(rows))
-    for i in range(len(rows)):
-        out[i], lse[i] = O.token_logprob(z[i], int(toks[i]))
-    return out, lse
+    return O.token_logprob_rows(syn.logits_rows_f64_host(seed, V, rows, dtype), toks)
 
 
-def oracle_seq_values(w: syn.Workload, seed: int, g0: int, ng: int, workers: int | None = None,
-                      chunk_rows: int = 64):
-    """Oracle a1-a3 for groups g0..g0+ng-1, regenerating rows from the seed in worker
-    processes (only valid rows are evaluated). Returns dict(ell, n_tok, log_z, eps,
-    lse_by_row)."""
+def oracle_seq_values(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: int = 64):
+    """Oracle a1-a2 for groups g0..g0+ng-1 (only valid rows are evaluated). Returns
+    dict(ell, n_tok, lse [N, T], tokens, mask, ref_logp, log_reward)."""
     gi = syn.group_inputs(w, seed, g0, ng)
     tok, mask = gi["tokens"], gi["mask"]
     N, T = tok.shape
     base = g0 * w.K * T
     valid = np.flatnonzero(mask.reshape(-1))
-    jobs = []
-    for i in range(0, len(valid), chunk_rows):
-        v = valid[i:i + chunk_rows]
-        jobs.append((seed, w.V, w.dtype, base + v, tok.reshape(-1)[v]))
-    workers = workers or max(1, len(os.sched_getaffinity(0)))
-    lp = np.zeros(N * T)
+    jobs = [(seed, w.V, w.dtype, base + valid[i:i + chunk_rows], tok.reshape(-1)[valid[i:i + chunk_rows]])
+            for i in range(0, len(valid), chunk_rows)]
+    res = list(pool().map(_rows_lp, jobs)) if len(jobs) > 1 else [_rows_lp(j) for j in jobs]
+    lp = np.full(N * T, np.nan)
     lse = np.full(N * T, np.nan)
-    if workers > 1 and len(jobs) > 1:
-        with ProcessPoolExecutor(workers) as ex:
-            res = list(ex.map(_rows_lp, jobs))
-    else:
-        res = [_rows_lp(j) for j in jobs]
     pos = 0
     for a, b in res:
         v = valid[pos:pos + len(a)]
         lp[v], lse[v] = a, b
         pos += len(a)
-    lp = lp.reshape(N, T)
-    ell = np.array([math.fsum(lp[s][mask[s] == 1]) for s in range(N)])
-    ntok = mask.sum(1).astype(np.int64)
+    ell, ntok = O.sequence_sums(lp.reshape(N, T), mask)
     return dict(ell=ell, n_tok=ntok, lse=lse.reshape(N, T), **gi)
+
+
+def _cmp_rows(args):
+    """Worker: compare GPU dlogits rows (read from a /dev/shm memmap) with oracle dlogits_row."""
+    path, shape, gdt, i0, i1, seed, V, in_dt, rows, toks, eps, n_global, grad_out, out_dt = args
+    mm = np.memmap(path, dtype=np.uint16 if gdt == "bf16" else np.float32, mode="r", shape=shape)
+    g = mm[i0:i1]
+    g = syn.bf16_bits_to_f64(g) if gdt == "bf16" else g.astype(np.float64)
+    z = syn.logits_rows_f64_host(seed, V, rows, in_dt)
+    n_bad, max_abs, max_ratio, worst = 0, 0.0, 0.0, None
+    for i in range(len(rows)):
+        want = O.dlogits_row(z[i], int(toks[i]), float(eps[i]), n_global, grad_out)
+        c = 2.0 * float(eps[i]) / n_global * grad_out
+        if out_dt == "bf16":
+            rb = O.round_bf16(want)
+            err = np.abs(g[i] - rb)
+            ratio = err / O.bf16_ulp(rb)
+            ratio[(np.abs(g[i]) < 2.0 ** -126) & (np.abs(rb) < 2.0 ** -126)] = 0.0
+            ok = ratio <= 1.0
+            abs_err = np.abs(g[i] - want)
+        else:
+            abs_err = np.abs(g[i] - want)
+            ratio = abs_err / (2e-6 * max(1.0, abs(c)))
+            ok = ratio <= 1.0
+        bad = int((~ok).sum())
+        if bad and worst is None:
+            j = int(np.argmax(ratio))
+            worst = (int(rows[i]), j, float(g[i][j]), float(want[j]), c)
+        n_bad += bad
+        max_abs = max(max_abs, float(abs_err.max()))
+        max_ratio = max(max_ratio, float(ratio.max()))
+    return n_bad, max_abs, max_ratio, worst
+
+
+def compare_dlogits_rows(d, w: syn.Workload, seed: int, flat_rows, row_base: int, tokens_flat, eps_of_row,
+                         n_global: int, grad_out: float = 1.0, what: str = "", chunk: int = 2048, sub: int = 16):
+    """Element-wise comparison of GPU dlogits rows (``d`` viewed [rows, V], local row indices
+    ``flat_rows``, all VALID) with oracle dlogits_row on the regenerated logits (global row =
+    row_base + local). tokens_flat / eps_of_row: per local row arrays. Raises on any element
+    outside the tolerance; returns (n_rows, max_abs_err, max_err_over_tol)."""
+    import torch
+    flat_rows = np.asarray(flat_rows, dtype=np.int64)
+    V = w.V
+    dv = d.reshape(-1, V) if d.is_contiguous() else d.view(-1, V)
+    gdt = "bf16" if d.dtype == torch.bfloat16 else "fp32"
+    path = f"/dev/shm/tba_parity_{os.getpid()}.bin"
+    cap = min(chunk, len(flat_rows))
+    tot_bad, max_abs, max_ratio, worst = 0, 0.0, 0.0, None
+    if cap == 0:
+        return 0, 0.0, 0.0
+    mm = np.memmap(path, dtype=np.uint16 if gdt == "bf16" else np.float32, mode="w+", shape=(cap, V))
+    try:
+        host = torch.from_numpy(mm.view(np.int16) if gdt == "bf16" else mm)
+        for c0 in range(0, len(flat_rows), cap):
+            rr = flat_rows[c0:c0 + cap]
+            idx = torch.from_numpy(rr).to(d.device)
+            rows_dev = dv.index_select(0, idx)
+            host[:len(rr)].copy_(rows_dev.view(torch.int16) if gdt == "bf16" else rows_dev)
+            mm.flush()
+            del rows_dev
+            jobs = [(path, (cap, V), gdt, i, min(i + sub, len(rr)), seed, V, w.dtype, row_base + rr[i:i + sub],
+                     tokens_flat[rr[i:i + sub]], eps_of_row[rr[i:i + sub]], n_global, grad_out, gdt)
+                    for i in range(0, len(rr), sub)]
+            for nb, ma, mr, wst in pool().map(_cmp_rows, jobs):
+                tot_bad += nb
+                max_abs = max(max_abs, ma)
+                max_ratio = max(max_ratio, mr)
+                worst = worst or wst
+    finally:
+        del mm
+        os.unlink(path)
+    if tot_bad:
+        raise AssertionError(f"dlogits {what}: {tot_bad} elements outside tolerance; first: global row {worst[0]} "
+                             f"col {worst[1]} gpu {worst[2]} oracle {worst[3]} c={worst[4]}")
+    return len(flat_rows), max_abs, max_ratio
 
 
 # --------------------------------------------------------------------------- tolerances
 def assert_seq_close(gpu, ref, what, rel=1e-4, abs_=1e-5):
+    """|gpu - ref| <= max(rel |ref|, abs_) element-wise; returns max err / tol."""
     gpu = np.asarray(gpu, np.float64)
     ref = np.asarray(ref, np.float64)
     tol = np.maximum(rel * np.abs(ref), abs_)
@@ -101,7 +187,7 @@ def assert_seq_close(gpu, ref, what, rel=1e-4, abs_=1e-5):
     if bad.any():
         i = np.flatnonzero(bad)[:5]
         raise AssertionError(f"{what}: {bad.sum()} mismatches, e.g. idx {i}: gpu {gpu[i]} oracle {ref[i]}")
-    return float(np.max(np.abs(gpu - ref) / np.maximum(np.abs(ref), abs_ / rel))) if len(ref) else 0.0
+    return float(np.max(np.abs(gpu - ref) / tol)) if len(ref) else 0.0
 
 
 def assert_dlogits_close(gpu_row, ref_row, c_seq, dtype: str, what=""):

@@ -1,12 +1,15 @@
-"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(SURVEY §8(d) oracle-coverage plan).
 
-Per-sequence values are compared with the fp64 oracle on every sequence the oracle can
-afford (all of Pythia and red-teaming; sampled whole groups of RhoMath and of the Qwen
-per-GPU shard), dlogits on seeded samples of rows; properties that hold at any size
-(loss = sum eps^2 / N, sum_v dlogits = 0, masked rows zero, group permutation and reward
-shift metamorphics, bitwise determinism) are checked on the full outputs."""
-import dataclasses
-
+* toy, Pythia and red-teaming: every per-sequence value and EVERY dlogits row against the
+  fp64 oracle;
+* RhoMath and the Qwen per-GPU shard: every per-sequence value (all groups), dlogits on 4096
+  seeded random valid rows plus every row of two whole groups;
+* the paper's own table shapes and Table 5's MATH shard: every per-sequence value of the
+  groups they hold, sampled dlogits rows.
+Properties that hold at any size (loss = sum eps^2 / N, sum_v dlogits = 0, masked rows zero,
+group permutation / reward-shift metamorphics, bitwise determinism) are checked on the full
+outputs. Every comparison's maxima go to tests/_harness.RECORD (-> $TBA_PARITY_OUT)."""
 import numpy as np
 import pytest
 
@@ -35,34 +38,35 @@ def run_full(w, seed, g0=0, ng=None):
     return inp, o, d
 
 
-def check_groups(w, seed, inp, o, d, groups, n_rows_sample=48):
-    """Oracle on whole groups `groups` (per-sequence values) + sampled rows of dlogits."""
-    K, T = w.K, w.T
-    N = inp["tokens"].shape[0]
-    sl, nt = o.seq_logp.cpu().numpy(), o.n_tokens.cpu().numpy()
-    lz, eps = o.log_z.cpu().numpy(), o.resid.cpu().numpy()
-    rng = np.random.default_rng(seed + 100)
-    for g in groups:
-        ref = H.oracle_seq_values(w, seed, g, 1)
-        s = slice(g * K, (g + 1) * K)
-        H.assert_seq_close(sl[s], ref["ell"], f"seq_logp group {g}")
-        np.testing.assert_array_equal(nt[s], ref["n_tok"])
-        loss_g, logz_g, eps_g = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, K,
-                                                  n_global=N)
-        H.assert_seq_close(lz[g:g + 1], logz_g, f"log_z group {g}")
-        H.assert_seq_close(eps[s], eps_g, f"resid group {g}")
-        # sampled valid rows of this group: oracle dlogits row vs GPU row
-        mask = ref["mask"]
-        valid = np.flatnonzero(mask.reshape(-1))
-        pick = rng.choice(valid, size=min(n_rows_sample, len(valid)), replace=False)
-        rows_global = g * K * T + pick
-        z = syn.logits_rows_f64(seed, w.V, rows_global, w.dtype)
-        for i, r in enumerate(pick):
-            sj, t = divmod(int(r), T)
-            y = int(ref["tokens"][sj, t])
-            want = O.dlogits_row(z[i], y, eps_g[sj], N)
-            got = d[g * K + sj, t].float().cpu().numpy().astype(np.float64)
-            H.assert_dlogits_close(got, want, 2 * eps_g[sj] / N, w.dtype, f"g={g} s={sj} t={t}")
+def check_seq_values(test, w, seed, o, g0, ng, N):
+    """Every per-sequence value of groups g0..g0+ng-1 (ell, n_tok, log Z, eps) and the loss of
+    those groups against the oracle. Returns the oracle dict (eps_global, tokens, mask...)."""
+    K = w.K
+    ref = H.oracle_seq_values(w, seed, g0, ng)
+    s = slice(g0 * K, (g0 + ng) * K)
+    sl, nt = o.seq_logp.cpu().numpy()[s], o.n_tokens.cpu().numpy()[s]
+    lz, eps = o.log_z.cpu().numpy()[g0:g0 + ng], o.resid.cpu().numpy()[s]
+    r = H.assert_seq_close(sl, ref["ell"], f"{test} seq_logp")
+    H.record(test, w.name, seed, "seq_logp", len(sl), np.max(np.abs(sl - ref["ell"])), r)
+    np.testing.assert_array_equal(nt, ref["n_tok"])                       # token counts: bit-exact
+    H.record(test, w.name, seed, "n_tokens (bit-exact)", len(nt), 0.0, 0.0)
+    loss_g, logz_g, eps_g = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, K, n_global=N)
+    r = H.assert_seq_close(lz, logz_g, f"{test} log_z")
+    H.record(test, w.name, seed, "log_z", len(lz), np.max(np.abs(lz - logz_g)), r)
+    r = H.assert_seq_close(eps, eps_g, f"{test} resid")
+    H.record(test, w.name, seed, "resid", len(eps), np.max(np.abs(eps - eps_g)), r)
+    if ng * K == o.resid.shape[0]:                                        # the whole call: the loss too
+        p0 = o.partial[0].item()
+        r = H.assert_seq_close([p0], [loss_g], f"{test} loss")
+        H.record(test, w.name, seed, "loss", 1, abs(p0 - loss_g), r)
+    ref["eps_g"] = eps_g
+    return ref
+
+
+def check_dlogits(test, w, seed, d, rows_local, tokens_flat, eps_of_row, N, what):
+    n, ma, mr = H.compare_dlogits_rows(d, w, seed, rows_local, 0, tokens_flat, eps_of_row, N, what=f"{test} {what}")
+    H.record(test, w.name, seed, f"dlogits ({what})", n, ma, mr,
+             tol="1 bf16 ulp" if d.dtype == torch.bfloat16 else "2e-6*max(1,|c|)")
 
 
 def check_properties(w, inp, o, d, n_rows=64, seed=0):
@@ -77,7 +81,7 @@ def check_properties(w, inp, o, d, n_rows=64, seed=0):
     mask = inp["mask"].cpu().numpy()
     rng = np.random.default_rng(seed)
     flat = d.view(-1, w.V)
-    rows = rng.choice(N * w.T, size=n_rows, replace=False)
+    rows = rng.choice(N * w.T, size=min(n_rows, N * w.T), replace=False)
     for r in rows:
         row = flat[r].float()
         if mask.reshape(-1)[r]:
@@ -85,52 +89,70 @@ def check_properties(w, inp, o, d, n_rows=64, seed=0):
             assert abs(row.double().sum().item()) <= 4e-3 * c + 1e-6             # sum_v (onehot - p) = 0
         else:
             assert torch.count_nonzero(row).item() == 0                         # masked rows are zero
+    masked = np.flatnonzero(mask.reshape(-1) == 0)
+    for i in range(0, len(masked), 4096):                                     # every masked row is +0
+        idx = torch.from_numpy(masked[i:i + 4096]).to(d.device)
+        assert torch.count_nonzero(flat.index_select(0, idx).view(torch.int16)).item() == 0
 
 
-def test_pythia_full_all_sequences():
-    w = syn.WORKLOADS["pythia"]
-    inp, o, d = run_full(w, 0)
-    ref = H.oracle_seq_values(w, 0, 0, w.B)
-    H.assert_seq_close(o.seq_logp.cpu().numpy(), ref["ell"], "seq_logp (all 256 sequences)")
-    np.testing.assert_array_equal(o.n_tokens.cpu().numpy(), ref["n_tok"])
-    loss, logz, eps = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, w.K)
-    H.assert_seq_close(o.log_z.cpu().numpy(), logz, "log_z")
-    H.assert_seq_close(o.resid.cpu().numpy(), eps, "resid")
-    H.assert_seq_close([o.partial[0].item()], [loss], "loss")
-    check_groups(w, 0, inp, o, d, [0, 37], n_rows_sample=32)
+def _row_plan(w, seed, mask_flat, whole_groups, n_random):
+    """Local valid rows: every row of `whole_groups` plus n_random seeded random valid rows."""
+    valid = np.flatnonzero(mask_flat)
+    gr = w.K * w.T
+    rows = [valid[(valid >= g * gr) & (valid < (g + 1) * gr)] for g in whole_groups]
+    rng = np.random.default_rng(1000 + seed)
+    rows.append(rng.choice(valid, size=min(n_random, len(valid)), replace=False))
+    return np.unique(np.concatenate(rows))
+
+
+@pytest.mark.parametrize("name,seed", [("toy", 0), ("pythia", 0), ("redteam", 1)])
+def test_full_compare_every_value_and_row(name, seed):
+    """Toy, Pythia and red-teaming compared in full: all sequences, every dlogits row."""
+    w = syn.WORKLOADS[name]
+    test = f"full_{name}"
+    inp, o, d = run_full(w, seed)
+    ref = check_seq_values(test, w, seed, o, 0, w.B, w.N)
+    mask_flat = ref["mask"].reshape(-1)
+    eps_row = np.repeat(ref["eps_g"], w.T)
+    check_dlogits(test, w, seed, d, np.flatnonzero(mask_flat), ref["tokens"].reshape(-1), eps_row, w.N,
+                  "every valid row")
     check_properties(w, inp, o, d)
 
 
-def test_redteam_full_unaligned_rows():
-    w = syn.WORKLOADS["redteam"]
-    inp, o, d = run_full(w, 1)
-    ref = H.oracle_seq_values(w, 1, 0, w.B)
-    H.assert_seq_close(o.seq_logp.cpu().numpy(), ref["ell"], "seq_logp (all 1024 sequences)")
-    loss, logz, eps = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, w.K)
-    H.assert_seq_close(o.resid.cpu().numpy(), eps, "resid")
-    H.assert_seq_close([o.partial[0].item()], [loss], "loss")
-    check_groups(w, 1, inp, o, d, [5, 127], n_rows_sample=32)
-    check_properties(w, inp, o, d)
-
-
-def test_rhomath_full_ragged_sampled_groups():
-    w = syn.WORKLOADS["rhomath"]
-    inp, o, d = run_full(w, 2)
-    check_groups(w, 2, inp, o, d, [0, 17, 31], n_rows_sample=24)
-    check_properties(w, inp, o, d)
-
-
-def test_qwen_shard_bench_configuration():
-    w = syn.WORKLOADS["qwen_shard"]  # exactly what bench.py times at N=1
-    inp, o, d = run_full(w, 0)
-    check_groups(w, 0, inp, o, d, [3], n_rows_sample=16)
+@pytest.mark.parametrize("name,seed,groups", [("rhomath", 2, [0, 31]), ("qwen_shard", 0, [2, 7])])
+def test_large_all_sequences_plus_rows(name, seed, groups):
+    """RhoMath and the Qwen shard: every per-sequence value; dlogits on 4096 seeded random
+    valid rows plus every row of two whole groups."""
+    w = syn.WORKLOADS[name]
+    test = f"large_{name}"
+    inp, o, d = run_full(w, seed)
+    ref = check_seq_values(test, w, seed, o, 0, w.B, w.N)
+    mask_flat = ref["mask"].reshape(-1)
+    rows = _row_plan(w, seed, mask_flat, groups, 4096)
+    eps_row = np.repeat(ref["eps_g"], w.T)
+    check_dlogits(test, w, seed, d, rows, ref["tokens"].reshape(-1), eps_row, w.N,
+                  f"groups {groups} whole + 4096 random rows")
     check_properties(w, inp, o, d, n_rows=32)
-    # bitwise determinism of a second run over the same buffers
-    o2, ws2 = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta,
-                              w.K, float(w.N))
-    assert torch.equal(o2.seq_logp, o.seq_logp) and torch.equal(o2.partial, o.partial)
-    d2 = tba.vargrad_bwd(inp["logits"], inp["tokens"], inp["mask"], ws2, o2.resid, 2.0 / w.N)
-    assert torch.equal(d2.view(torch.int16), d.view(torch.int16))
+    if name == "qwen_shard":  # bitwise determinism of a second run over the same buffers
+        o2, ws2 = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"],
+                                  w.beta, w.K, float(w.N))
+        assert torch.equal(o2.seq_logp, o.seq_logp) and torch.equal(o2.partial, o.partial)
+        d2 = tba.vargrad_bwd(inp["logits"], inp["tokens"], inp["mask"], ws2, o2.resid, 2.0 / w.N)
+        assert torch.equal(d2.view(torch.int16), d.view(torch.int16))
+
+
+@pytest.mark.parametrize("name,seed", [("pythia", 1), ("pythia", 2), ("redteam", 0), ("redteam", 2),
+                                       ("rhomath", 0), ("rhomath", 1)])
+def test_parity_seeds_sequence_values(name, seed):
+    """Parity seeds {0, 1, 2}: every per-sequence value and the loss, plus 512
+    random dlogits rows, on the other seeds of the smaller configs."""
+    w = syn.WORKLOADS[name]
+    test = f"seeds_{name}"
+    inp, o, d = run_full(w, seed)
+    ref = check_seq_values(test, w, seed, o, 0, w.B, w.N)
+    rows = _row_plan(w, seed, ref["mask"].reshape(-1), [], 512)
+    check_dlogits(test, w, seed, d, rows, ref["tokens"].reshape(-1), np.repeat(ref["eps_g"], w.T), w.N,
+                  "512 random rows")
 
 
 def test_qwen_group_metamorphic_permutation_and_shift():
@@ -153,27 +175,28 @@ def test_qwen_group_metamorphic_permutation_and_shift():
     H.assert_seq_close(o3.resid.cpu().numpy(), o.resid.cpu().numpy(), "shifted resid", rel=1e-9, abs_=1e-9)
 
 
-@pytest.mark.parametrize("name,seed,groups", [("gsm8k_t3", 0, [0, 6]), ("gsm8k_k40", 1, [0, 2]),
-                                              ("tldr_t4", 2, [3, 7])])
-def test_paper_table_batch_shapes_full(name, seed, groups):
-    """The paper's own batch shapes (Tables 3 and 4, the K = 40 ablation) at full size."""
+@pytest.mark.parametrize("name,seed", [("gsm8k_t3", 0), ("gsm8k_k40", 1), ("tldr_t4", 2)])
+def test_paper_table_batch_shapes_full(name, seed):
+    """The paper's own batch shapes (Tables 3 and 4, the K = 40 ablation) at full size: every
+    per-sequence value, 1024 random dlogits rows plus every row of group 0."""
     w = syn.WORKLOADS[name]
+    test = f"paper_{name}"
     inp, o, d = run_full(w, seed)
-    ref = H.oracle_seq_values(w, seed, 0, w.B)
-    H.assert_seq_close(o.seq_logp.cpu().numpy(), ref["ell"], f"seq_logp (all {w.N} sequences)")
-    np.testing.assert_array_equal(o.n_tokens.cpu().numpy(), ref["n_tok"])
-    loss, logz, eps = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, w.K)
-    H.assert_seq_close(o.log_z.cpu().numpy(), logz, "log_z")
-    H.assert_seq_close(o.resid.cpu().numpy(), eps, "resid")
-    H.assert_seq_close([o.partial[0].item()], [loss], "loss")
-    check_groups(w, seed, inp, o, d, groups, n_rows_sample=16)
+    ref = check_seq_values(test, w, seed, o, 0, w.B, w.N)
+    rows = _row_plan(w, seed, ref["mask"].reshape(-1), [0], 1024)
+    check_dlogits(test, w, seed, d, rows, ref["tokens"].reshape(-1), np.repeat(ref["eps_g"], w.T), w.N,
+                  "group 0 whole + 1024 random rows")
     check_properties(w, inp, o, d)
 
 
 def test_math_t5_two_groups_ragged_2048():
     """Table 5's MATH shape (K = 16, responses up to 2048 tokens, V = 152064): two whole groups
-    (20 GB of logits), one compared with the oracle sequence by sequence."""
+    (20 GB of logits), every per-sequence value, 1024 random dlogits rows."""
     w = syn.WORKLOADS["math_t5_shard"]
+    test = "paper_math_t5"
     inp, o, d = run_full(w, 3, 0, 2)
-    check_groups(w, 3, inp, o, d, [1], n_rows_sample=12)
+    ref = check_seq_values(test, w, 3, o, 0, 2, 2 * w.K)
+    rows = _row_plan(w, 3, ref["mask"].reshape(-1), [], 1024)
+    check_dlogits(test, w, 3, d, rows, ref["tokens"].reshape(-1), np.repeat(ref["eps_g"], w.T), 2 * w.K,
+                  "1024 random rows")
     check_properties(w, inp, o, d, n_rows=32)

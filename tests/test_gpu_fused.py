@@ -193,3 +193,33 @@ def test_cuda_graph_capture_replays_bitwise():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out.partial, ref_p) and torch.equal(d.view(torch.int16), ref_d.view(torch.int16))
+
+
+@pytest.mark.parametrize("name,seed,sched", [("pythia", 5, "fused"), ("redteam", 6, "fused"),
+                                             ("pythia", 8, "pipelined")])
+def test_one_call_schedules_against_oracle(name, seed, sched):
+    """The one-launch / pipelined schedules compared with the fp64 ORACLE directly (not only with
+    the two-call CUDA path): every per-sequence value, the loss and every dlogits row."""
+    import numpy as np
+
+    from oracle import tba_oracle as O
+    w = syn.WORKLOADS[name]
+    inp = H.device_inputs(w, seed)
+    call = tba.vargrad_fused if sched == "fused" else tba.vargrad_pipelined
+    o, _, d, _ = call(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta, w.K,
+                      float(w.N), check_status=True)
+    torch.cuda.synchronize()
+    ref = H.oracle_seq_values(w, seed, 0, w.B)
+    test = f"{sched}_vs_oracle"
+    sl = o.seq_logp.cpu().numpy()
+    H.record(test, name, seed, "seq_logp", w.N, np.max(np.abs(sl - ref["ell"])),
+             H.assert_seq_close(sl, ref["ell"], "seq_logp"))
+    np.testing.assert_array_equal(o.n_tokens.cpu().numpy(), ref["n_tok"])
+    loss, logz, eps = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, w.K)
+    for q, g, want in (("log_z", o.log_z, logz), ("resid", o.resid, eps), ("loss", o.partial[:1], [loss])):
+        g = g.cpu().numpy()
+        H.record(test, name, seed, q, len(g), np.max(np.abs(g - want)), H.assert_seq_close(g, want, q))
+    rows = np.flatnonzero(ref["mask"].reshape(-1))
+    n, ma, mr = H.compare_dlogits_rows(d, w, seed, rows, 0, ref["tokens"].reshape(-1), np.repeat(eps, w.T), w.N,
+                                       what=test)
+    H.record(test, name, seed, "dlogits (every valid row)", n, ma, mr, tol="1 bf16 ulp")
