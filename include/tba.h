@@ -45,7 +45,7 @@ extern "C" {
 typedef struct CUstream_st* tba_stream_t; /* == cudaStream_t */
 
 enum tba_status { TBA_OK = 0, TBA_ERR_INVALID_ARG = 1, TBA_ERR_INVALID_CONFIG = 2, TBA_ERR_CUDA = 3 };
-enum tba_dev_status { TBA_DEV_TOKEN_RANGE = 1, TBA_DEV_NONFINITE_ROW = 2, TBA_DEV_PEER_TIMEOUT = 4 };
+enum tba_dev_status { TBA_DEV_TOKEN_RANGE = 1, TBA_DEV_NONFINITE_ROW = 2 };
 enum tba_dtype { TBA_BF16 = 0, TBA_FP32 = 1 };
 
 #define TBA_ABI_VERSION 1
@@ -142,36 +142,6 @@ int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* work
                     const double* resid, double grad_scale, const double* grad_out, void* dlogits,
                     int32_t dlogits_dtype, int64_t dlogits_row_stride, double* d_log_z, int32_t K,
                     tba_stream_t stream);
-
-/* Forward with the loss all-reduce fused into the head kernel over peer memory:
- * instead of a separate NCCL all-reduce of `partial`, the head's last CTA exchanges the three
- * partials with every rank through CUDA-IPC-mapped buffers (P2P stores over NVLink) and
- * returns the GLOBAL { L, N_global, B_global } in `partial` on every rank, bit-identical across
- * ranks (summed in rank order). Set-up (host, once): every rank allocates its slot buffer
- * (2 * world * 4 doubles) and flag buffer (world uint32, zeroed) with tba_ipc_alloc, exchanges
- * the 64-byte handles, opens the peers' with tba_ipc_open, and uploads the [world] pointer
- * arrays. `epoch` must be > 0 and increase by 1 per call on every rank; every rank must own >= 1
- * group. A peer that does not arrive within timeout_s sets TBA_DEV_PEER_TIMEOUT and NaN. */
-typedef struct tba_peer_reduce {
-  double* const*       slots;  /* device array [world] of device pointers (rank q's slot buffer) */
-  unsigned int* const* flags;  /* device array [world] of device pointers (rank q's flags)       */
-  int32_t              rank, world;
-  uint32_t             epoch;
-  double               timeout_s;
-} tba_peer_reduce;
-
-int tba_tb_loss_fwd_peer(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
-                         const double* log_reward, double beta, int32_t K, double n_seq_global,
-                         void* workspace, double* seq_logp, int32_t* n_tokens, double* log_z,
-                         double* resid, double* partial, const tba_peer_reduce* pr,
-                         int32_t* dev_status, tba_stream_t stream);
-
-/* CUDA IPC helpers (host-side set-up of the peer buffers): allocate + zero + export a 64-byte
- * handle; open a peer's handle; close / free. */
-int tba_ipc_alloc(size_t bytes, void** dev_ptr, void* handle64);
-int tba_ipc_open(const void* handle64, void** dev_ptr);
-int tba_ipc_close(void* dev_ptr);
-int tba_ipc_free(void* dev_ptr);
 
 /* One-launch forward + backward: the outputs of tba_tb_loss_fwd followed
  * by tba_tb_loss_bwd with grad_scale = 2 g / n_seq_global fixed at call time (g = 1 when the

@@ -169,10 +169,14 @@ def advantages(ell, ref_logp, log_reward, beta: float, K: int) -> np.ndarray:
 
 # ----------------------------------------------------------------------------- a5
 def grad_logprob_row(z: np.ndarray, y: int) -> np.ndarray:
-    """d log softmax(z)[y] / dz = onehot(y) - softmax(z)."""
+    """d log softmax(z)[y] / dz = onehot(y) - softmax(z).
+
+    The token's entry 1 - p_y is formed as sum_{v != y} p_v (the same quantity: the softmax sums
+    to 1), so it keeps its relative accuracy when p_y -> 1 instead of cancelling in fp64."""
     lp, _ = log_softmax_row(z)
-    g = -np.exp(lp)
-    g[y] += 1.0
+    p = np.exp(lp)
+    g = -p
+    g[y] = np.sum(np.delete(p, y))
     return g
 
 

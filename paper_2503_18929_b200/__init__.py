@@ -5,7 +5,7 @@ this package only marshals PyTorch tensors into it. There is no CPU fallback: th
 raise if the extension is missing.
 """
 from ._lib import TbaError, load as load_library  # noqa: F401
-from .dist import PeerReducer, group_range, token_balanced_ranges  # noqa: F401
+from .dist import allreduce_partial_async, group_range, token_balanced_ranges  # noqa: F401
 from .ops import (CapturedStep, LmHeadTBLoss, TBAPrimeLoss, VarGradTBLoss, lmhead_bwd_workspace_bytes,  # noqa: F401
                   lmhead_seq_logprob, lmhead_tb_loss, lmhead_tbap_bwd, lmhead_vargrad_bwd, lmhead_vargrad_fwd_bwd,
                   lmhead_fwd_bwd_workspace_bytes, lmhead_tbap_fwd, lmhead_token_logprob,
@@ -21,4 +21,4 @@ __all__ = ["CapturedStep", "seq_logprob", "token_logprob", "vargrad_tb_loss", "V
            "lmhead_tbap_fwd", "lmhead_tb_loss", "LmHeadTBLoss", "lmhead_vargrad_bwd", "lmhead_tbap_bwd",
            "lmhead_bwd_workspace_bytes", "lmhead_vargrad_fwd_bwd", "lmhead_fwd_bwd_workspace_bytes",
            "lmhead_workspace_bytes", "make_lmhead",
-           "group_range", "token_balanced_ranges", "PeerReducer", "load_library", "TbaError"]
+           "group_range", "token_balanced_ranges", "allreduce_partial_async", "load_library", "TbaError"]

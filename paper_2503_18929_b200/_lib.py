@@ -20,13 +20,11 @@ TBA_BF16, TBA_FP32 = 0, 1
 EXPORTS = ("tba_abi_version", "tba_status_string", "tba_workspace_bytes", "tba_seq_logprob", "tba_token_logprob",
            "tba_vargrad_tb_loss_fwd", "tba_vargrad_tb_loss_bwd", "tba_tb_loss_fwd", "tba_tb_loss_bwd", "tba_tb_loss_fused",
            "tba_tb_loss_pipelined", "tba_tb_loss_fwd_deferred",
-           "tba_tbap_loss_fwd", "tba_tbap_loss_bwd", "tba_tbap_loss_fwd_deferred", "tba_tb_loss_fwd_peer",
-           "tba_ipc_alloc", "tba_ipc_open", "tba_ipc_close", "tba_ipc_free",
+           "tba_tbap_loss_fwd", "tba_tbap_loss_bwd", "tba_tbap_loss_fwd_deferred",
            "tba_lmhead_workspace_bytes", "tba_lmhead_seq_logprob", "tba_lmhead_tb_loss_fwd",
            "tba_lmhead_token_logprob", "tba_lmhead_tbap_loss_fwd", "tba_lmhead_bwd_workspace_bytes",
            "tba_lmhead_tb_loss_bwd", "tba_lmhead_tbap_loss_bwd", "tba_lmhead_fwd_bwd_workspace_bytes",
            "tba_lmhead_tb_loss_fwd_bwd")
-TBA_DEV_PEER_TIMEOUT = 4
 TBA_IS_NONE, TBA_IS_CLIP, TBA_IS_ICEPOP = 0, 1, 2
 
 
@@ -45,11 +43,6 @@ class TbaLmhead(ctypes.Structure):
 
 class TbaTbOpts(ctypes.Structure):
     _fields_ = [("inv_temp", ctypes.c_double), ("log_z_param", ctypes.c_void_p)]
-
-
-class TbaPeerReduce(ctypes.Structure):
-    _fields_ = [("slots", ctypes.c_void_p), ("flags", ctypes.c_void_p), ("rank", ctypes.c_int32),
-                ("world", ctypes.c_int32), ("epoch", ctypes.c_uint32), ("timeout_s", ctypes.c_double)]
 
 
 class TbaError(ValueError):
@@ -99,9 +92,6 @@ def load(path: str | None = None) -> ctypes.CDLL:
         L.tba_tb_loss_pipelined.argtypes = [RP, OP, P, P, D, I32, D, D, I32, P, P, P, P, P, P, P, I32, I64, P, P, P, P]
         L.tba_tb_loss_fwd_deferred.restype = ctypes.c_int
         L.tba_tb_loss_fwd_deferred.argtypes = [RP, OP, P, P, D, I32, D, P, P, P, P, P, P, P, I32, I64, P, P]
-        PP = ctypes.POINTER(TbaPeerReduce)
-        L.tba_tb_loss_fwd_peer.restype = ctypes.c_int
-        L.tba_tb_loss_fwd_peer.argtypes = [RP, OP, P, P, D, I32, D, P, P, P, P, P, P, PP, P, P]
         LP = ctypes.POINTER(TbaLmhead)
         L.tba_lmhead_workspace_bytes.restype = SZ
         L.tba_lmhead_workspace_bytes.argtypes = [I64, I64, I64]
@@ -124,14 +114,6 @@ def load(path: str | None = None) -> ctypes.CDLL:
         L.tba_lmhead_tb_loss_fwd_bwd.restype = ctypes.c_int
         L.tba_lmhead_tb_loss_fwd_bwd.argtypes = [LP, OP, P, P, D, I32, D, D, I32, P, P, P, P, P, P, P, I32, I64, P,
                                                  I64, I32, P, P, P, P]
-        L.tba_ipc_alloc.restype = ctypes.c_int
-        L.tba_ipc_alloc.argtypes = [SZ, ctypes.POINTER(ctypes.c_void_p), P]
-        L.tba_ipc_open.restype = ctypes.c_int
-        L.tba_ipc_open.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
-        L.tba_ipc_close.restype = ctypes.c_int
-        L.tba_ipc_close.argtypes = [P]
-        L.tba_ipc_free.restype = ctypes.c_int
-        L.tba_ipc_free.argtypes = [P]
         L.tba_tbap_loss_fwd.restype = ctypes.c_int
         L.tba_tbap_loss_fwd.argtypes = [RP, P, P, P, D, I32, I32, D, D, D, P, P, P, P, P, P, P, P]
         L.tba_tbap_loss_fwd_deferred.restype = ctypes.c_int

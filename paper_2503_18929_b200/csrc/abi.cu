@@ -10,7 +10,7 @@ namespace {
 // The Eq. 4/5 group-head arguments shared by the two-call and deferred forwards.
 HeadArgs tb_head_args(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
                       double beta, int32_t K, double n_seq_global, const WsLayout& w, double* seq_logp,
-                      int32_t* n_tokens, double* log_z, double* resid, double* partial, const PeerArgs& pa) {
+                      int32_t* n_tokens, double* log_z, double* resid, double* partial) {
   HeadArgs ha{};
   ha.T = x->seq_len;
   ha.K = K;
@@ -27,7 +27,6 @@ HeadArgs tb_head_args(const tba_rows* x, const tba_tb_opts* opts, const double* 
   ha.resid = resid;
   ha.group_sq = w.group_sq;
   ha.partial = partial;
-  ha.pa = pa;
   return ha;
 }
 
@@ -82,8 +81,6 @@ int tba_seq_logprob(const tba_rows* x, void* workspace, double* seq_logp, int32_
   ha.n_seq = x->n_seq;
   ha.seq_logp = seq_logp;
   ha.n_tokens = n_tokens;
-  ha.pa = PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, dev_status};
-  if (launch_fwd_head(x, w, make_scale(1.0), dev_status, ha, s, &rc)) return rc;
   rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
   if (rc) return rc;
   return launch_seq_head(false, w, x->mask, ha, s);
@@ -104,34 +101,9 @@ int tba_token_logprob(const tba_rows* x, double inv_temp, void* workspace, doubl
   return launch_token_lp(w, x->mask, rows, tok_logp, s);
 }
 
-static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
-                            const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
-                            double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
-                            int32_t* dev_status, const tba_peer_reduce* pr, tba_stream_t stream);
-
 int tba_tb_loss_fwd(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp, const double* log_reward,
                     double beta, int32_t K, double n_seq_global, void* workspace, double* seq_logp, int32_t* n_tokens,
                     double* log_z, double* resid, double* partial, int32_t* dev_status, tba_stream_t stream) {
-  return tb_loss_fwd_impl(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
-                          resid, partial, dev_status, nullptr, stream);
-}
-
-int tba_tb_loss_fwd_peer(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
-                         const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
-                         double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
-                         const tba_peer_reduce* pr, int32_t* dev_status, tba_stream_t stream) {
-  if (!pr || !pr->slots || !pr->flags || pr->world < 1 || pr->rank < 0 || pr->rank >= pr->world || pr->epoch == 0 ||
-      !(pr->timeout_s > 0.0))
-    return TBA_ERR_INVALID_ARG;
-  if (x && x->n_seq == 0) return TBA_ERR_INVALID_ARG;  // every rank must own >= 1 group to join the reduction
-  return tb_loss_fwd_impl(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens, log_z,
-                          resid, partial, dev_status, pr, stream);
-}
-
-static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
-                            const double* log_reward, double beta, int32_t K, double n_seq_global, void* workspace,
-                            double* seq_logp, int32_t* n_tokens, double* log_z, double* resid, double* partial,
-                            int32_t* dev_status, const tba_peer_reduce* pr, tba_stream_t stream) {
   if (!(std::isfinite(beta) && beta > 0.0)) return TBA_ERR_INVALID_CONFIG;
   if (K < 2) return TBA_ERR_INVALID_CONFIG;
   int rc = check_opts(opts);
@@ -149,47 +121,14 @@ static int tb_loss_fwd_impl(const tba_rows* x, const tba_tb_opts* opts, const do
     return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   WsLayout w = ws_layout(workspace, x->n_seq, x->seq_len);
-  PeerArgs pa{nullptr, nullptr, 0, 0, 0u, 0ull, dev_status};
-  if (pr) {
-    pa.slots = pr->slots;
-    pa.flags = pr->flags;
-    pa.rank = pr->rank;
-    pa.world = pr->world;
-    pa.epoch = pr->epoch;
-    pa.timeout_ns = (unsigned long long)(pr->timeout_s * 1e9);
-  }
   const RowScale rs = make_scale(opt_inv_temp(opts));
-  HeadArgs ha = tb_head_args(x, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens, log_z, resid,
-                             partial, pa);
-  if (launch_fwd_head(x, w, rs, dev_status, ha, s, &rc)) return rc;
+  const HeadArgs ha = tb_head_args(x, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
+                                   log_z, resid, partial);
   if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
   rc = launch_fwd_rows(x, w, rs, dev_status, s);
   if (rc) return rc;
   return launch_seq_head(true, w, x->mask, ha, s);
 }
-
-// ---- CUDA IPC helpers for the peer reduction buffers (host-side, not on the hot path)
-int tba_ipc_alloc(size_t bytes, void** dev_ptr, void* handle64) {
-  if (!dev_ptr || !handle64 || bytes == 0) return TBA_ERR_INVALID_ARG;
-  if (cudaMalloc(dev_ptr, bytes) != cudaSuccess) return TBA_ERR_CUDA;
-  if (cudaMemset(*dev_ptr, 0, bytes) != cudaSuccess) return TBA_ERR_CUDA;
-  cudaIpcMemHandle_t h;
-  if (cudaIpcGetMemHandle(&h, *dev_ptr) != cudaSuccess) return TBA_ERR_CUDA;
-  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
-  memcpy(handle64, &h, sizeof(h));
-  return TBA_OK;
-}
-
-int tba_ipc_open(const void* handle64, void** dev_ptr) {
-  if (!handle64 || !dev_ptr) return TBA_ERR_INVALID_ARG;
-  cudaIpcMemHandle_t h;
-  memcpy(&h, handle64, sizeof(h));
-  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
-}
-
-int tba_ipc_close(void* dev_ptr) { return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
-
-int tba_ipc_free(void* dev_ptr) { return cudaFree(dev_ptr) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
 
 int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* workspace, const double* resid,
                     double grad_scale, const double* grad_out, void* dlogits, int32_t dlogits_dtype,
@@ -213,7 +152,7 @@ int tba_tb_loss_bwd(const tba_rows* x, const tba_tb_opts* opts, const void* work
   if (x->seq_len == 0) return TBA_OK;
   if (!workspace || reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   const WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
-  return launch_bwd(false, x, w.stats, resid, nullptr, grad_scale, grad_out, make_scale(opt_inv_temp(opts)),
+  return launch_bwd(false, x, w.stats, w.qy, resid, nullptr, grad_scale, grad_out, make_scale(opt_inv_temp(opts)),
                     dlogits, dlogits_dtype, dlogits_row_stride, s);
 }
 
@@ -261,6 +200,7 @@ int tba_tb_loss_fused(const tba_rows* x, const tba_tb_opts* opts, const double* 
   a.log_reward = log_reward;
   a.log_z_param = opts ? opts->log_z_param : nullptr;
   a.stats = w.stats;
+  a.qy = w.qy;
   a.lp = w.lp;
   a.seq_logp = seq_logp;
   a.n_tokens = n_tokens;
@@ -347,21 +287,20 @@ int tba_tb_loss_pipelined(const tba_rows* x, const tba_tb_opts* opts, const doub
     xc.tokens = x->tokens + r0;
     xc.mask = x->mask + r0;
     xc.n_seq = gc * K;
-    const WsLayout wc{w.stats + r0, w.lp + r0, w.group_sq + g0, nullptr, nullptr};
+    const WsLayout wc{w.stats + r0, w.lp + r0, w.group_sq + g0, nullptr, nullptr, w.qy + r0};
     // forward of chunk c after the writer of chunk c-2: at most two chunks of logits live in L2
     if (two && c >= 2 && cudaStreamWaitEvent(s, evB[c % 2], 0) != cudaSuccess) rc = TBA_ERR_CUDA;
     if (!rc) rc = launch_fwd_rows(&xc, wc, rs, dev_status, s);
     if (rc) break;
     HeadArgs ha = tb_head_args(&xc, opts, ref_logp + s0, log_reward + s0, beta, K, n_seq_global, wc, seq_logp + s0,
-                               n_tokens + s0, log_z + g0, resid + s0, partial,
-                               PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+                               n_tokens + s0, log_z + g0, resid + s0, partial);
     if (ha.log_z_param) ha.log_z_param += g0;
     rc = launch_seq_head(true, wc, xc.mask, ha, s);  // wc.counter == NULL: no per-chunk reduction
     if (rc) break;
     if (two && (cudaEventRecord(evF[c % 2], s) != cudaSuccess || cudaStreamWaitEvent(sb, evF[c % 2], 0) != cudaSuccess))
       rc = TBA_ERR_CUDA;
     if (!rc)
-      rc = launch_bwd(false, &xc, wc.stats, resid + s0, nullptr, grad_scale, nullptr, rs,
+      rc = launch_bwd(false, &xc, wc.stats, wc.qy, resid + s0, nullptr, grad_scale, nullptr, rs,
                       static_cast<char*>(dlogits) + r0 * dlogits_row_stride * oesz, dlogits_dtype, dlogits_row_stride,
                       two ? sb : s);
     if (!rc && two && cudaEventRecord(evB[c % 2], sb) != cudaSuccess) rc = TBA_ERR_CUDA;
@@ -402,7 +341,7 @@ int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const d
   rc = launch_single(x, w, make_scale(opt_inv_temp(opts)), dev_status, grad_unscaled, g_dtype, g_row_stride, s);
   if (rc) return rc;
   const HeadArgs ha = tb_head_args(x, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
-                                   log_z, resid, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+                                   log_z, resid, partial);
   return launch_seq_head(true, w, x->mask, ha, s);
 }
 
@@ -497,7 +436,7 @@ int tba_tbap_loss_bwd(const tba_rows* x, const void* workspace, const float* coe
   if (!workspace || !coef) return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return TBA_ERR_INVALID_ARG;
   const WsLayout w = ws_layout(const_cast<void*>(workspace), x->n_seq, x->seq_len);
-  return launch_bwd(true, x, w.stats, nullptr, coef, grad_scale, grad_out, make_scale(1.0), dlogits, dlogits_dtype,
+  return launch_bwd(true, x, w.stats, w.qy, nullptr, coef, grad_scale, grad_out, make_scale(1.0), dlogits, dlogits_dtype,
                     dlogits_row_stride, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -604,7 +543,7 @@ int tba_lmhead_tb_loss_fwd(const tba_lmhead* x, const tba_tb_opts* opts, const d
   xr.n_seq = x->n_seq;
   xr.seq_len = x->seq_len;
   const HeadArgs ha = tb_head_args(&xr, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
-                                   log_z, resid, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+                                   log_z, resid, partial);
   return launch_seq_head(true, w, x->mask, ha, s);
 }
 
@@ -729,7 +668,7 @@ int tba_lmhead_tb_loss_fwd_bwd(const tba_lmhead* x, const tba_tb_opts* opts, con
   xr.n_seq = x->n_seq;
   xr.seq_len = x->seq_len;
   const HeadArgs ha = tb_head_args(&xr, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
-                                   log_z, resid, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+                                   log_z, resid, partial);
   rc = launch_lmhead_fwd_bwd(x, rs, w, ha, K, grad_scale, 1.0 / n_seq_global, dhidden, dhidden_dtype,
                              dhidden_row_stride, dweight, dweight_row_stride, accumulate != 0, groups_per_chunk,
                              bwd_workspace, dev_status, s);

@@ -14,8 +14,9 @@ template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false>
 __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                 int64_t stride, const int64_t* __restrict__ tokens,
                                                 const uint8_t* __restrict__ mask, RowScale rs,
-                                                float2* __restrict__ stats, double* __restrict__ lp,
-                                                int32_t* dev_status, TO* __restrict__ g_out, int64_t ostride) {
+                                                float2* __restrict__ stats, float* __restrict__ qy,
+                                                double* __restrict__ lp, int32_t* dev_status,
+                                                TO* __restrict__ g_out, int64_t ostride) {
   namespace cg = cooperative_groups;
   constexpr int NW = NT / 32;
   const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -25,7 +26,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   __shared__ double sm_s[NW];
   __shared__ float part_m, part_M2;  // this CTA's partial, read by the cluster through DSMEM
   __shared__ double part_s;
-  __shared__ float sh_M2, sh_L2S;
+  __shared__ float sh_M2, sh_L2S, sh_qy;
   __shared__ int64_t sh_y;
   const bool live = row < rows;
   const bool valid = live && mask[row] != 0;  // uniform over the cluster
@@ -35,10 +36,11 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   float M = -INFINITY, M2 = 0.f;
   double S = 0.0;
   if (valid) {
-    if (threadIdx.x == 0) sh_y = tokens[row];
+    const int64_t yt = tokens[row];
+    if (threadIdx.x == 0) sh_y = yt;
     OnlineState st;
     st.init(rs);
-    fwd_accumulate<T, 4, true>(rp, V, gt, CS * NT, st, make_policy(true));
+    fwd_accumulate<T, 4, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
     combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     if (lane == 0) {
       sm_m[warp] = M;
@@ -81,7 +83,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     return;
   }
   if (!valid) {
-    bwd_row<T, TO, 4>(rp, op, V, gt, CS * NT, false, 0.f, 0.f, 0.f, 0.f, -1);
+    bwd_row<T, TO, 4>(rp, op, V, gt, CS * NT, false, 0.f, 0.f, 0.f, 0.f, -1, 0.f);
     if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     return;
   }
@@ -90,13 +92,15 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     const bool ok = (y >= 0 && y < V);
     if (rank == 0) {
       const float zy = ok ? Elem<T>::load1(rp + y) : 0.f;
-      finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+      finalize_row(M, M2, S, zy, ok, row, rs, stats, qy, lp, dev_status);
     }
+    const double ey = ok ? exp2((double)Elem<T>::load1(rp + y) * (double)rs.sc - (double)M2) : 0.0;
     sh_M2 = M2;
-    sh_L2S = (float)log2(S);
+    sh_L2S = (float)log2(S + ey);
+    sh_qy = (float)(S / (S + ey));
   }
   __syncthreads();
-  bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
+  bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
                                 make_policy(false));
   if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
@@ -105,134 +109,12 @@ template <class T, class TO, int NT, int U2 = 4, bool REV = false>
 __global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                   int64_t stride, const int64_t* __restrict__ tokens,
                                                   const uint8_t* __restrict__ mask, RowScale rs,
-                                                  float2* __restrict__ stats, double* __restrict__ lp,
-                                                  int32_t* dev_status, TO* __restrict__ g_out, int64_t ostride) {
-  row_single_body<T, TO, NT, 1, U2, REV>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out,
+                                                  float2* __restrict__ stats, float* __restrict__ qy,
+                                                  double* __restrict__ lp, int32_t* dev_status,
+                                                  TO* __restrict__ g_out, int64_t ostride) {
+  row_single_body<T, TO, NT, 1, U2, REV>(logits, rows, V, stride, tokens, mask, rs, stats, qy, lp, dev_status, g_out,
                                          ostride);
 }
-
-template <class T, class TO, int NT, int U2 = 4>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
-    row_single2(const T* __restrict__ logits, int64_t rows, int64_t V, int64_t stride,
-                const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
-                float2* __restrict__ stats, double* __restrict__ lp, int32_t* dev_status, TO* __restrict__ g_out,
-                int64_t ostride) {
-  row_single_body<T, TO, NT, 2, U2>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out, ostride);
-}
-
-template <class T, class TO, int NT, int U2 = 4>
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(NT)
-    row_single4(const T* __restrict__ logits, int64_t rows, int64_t V, int64_t stride,
-                const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
-                float2* __restrict__ stats, double* __restrict__ lp, int32_t* dev_status, TO* __restrict__ g_out,
-                int64_t ostride) {
-  row_single_body<T, TO, NT, 4, U2>(logits, rows, V, stride, tokens, mask, rs, stats, lp, dev_status, g_out, ostride);
-}
-
-// Pipelined deferred pass (cfg 7): persistent 2-CTA clusters (one CTA of 1024 threads per SM),
-// each CTA split into two teams of 16 warps. In round j, team A streams HALF of row j from HBM
-// (pass 1) while team B re-reads half of row j-1 from L2 and writes its gradient (pass 2); the two
-// CTAs of the cluster then exchange their row-j partials through DSMEM. Every SM thus keeps an HBM
-// read stream and a write stream busy at all times, while only ~148 rows (45 MB at V = 152064)
-// are in flight, so the re-reads stay in L2.
-template <class T, class TO>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024, 1)
-    row_single_pipe(const T* __restrict__ logits, int64_t rows, int64_t V, int64_t stride,
-                    const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
-                    float2* __restrict__ stats, double* __restrict__ lp, int32_t* dev_status, TO* __restrict__ g_out,
-                    int64_t ostride, int64_t n_clusters) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  constexpr int NTH = 1024;  // threads per row across the cluster (2 CTAs x 512-thread team)
-  const int rank = (int)cl.block_rank();
-  const int64_t cid = (int64_t)blockIdx.x / 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool teamA = warp < 16;
-  const int gt = rank * 512 + (threadIdx.x & 511);
-  __shared__ float wm[16], wm2[16];
-  __shared__ double wsum[16];
-  __shared__ float part_m[2], part_M2[2];
-  __shared__ double part_s[2];
-  __shared__ float st_M2[2], st_L2S[2];
-  __shared__ int64_t st_y[2], st_row[2];
-  __shared__ int st_valid[2];
-  const int64_t nrc = cid < rows ? (rows - cid + n_clusters - 1) / n_clusters : 0;
-  const uint64_t pol_last = make_policy(true), pol_first = make_policy(false);
-  for (int64_t j = 0; j <= nrc; ++j) {
-    const int b = (int)(j & 1);
-    if (teamA) {
-      if (j < nrc) {
-        const int64_t row = cid + j * n_clusters;
-        if (mask[row]) {
-          OnlineState st;
-          st.init(rs);
-          fwd_accumulate<T, 4, true>(logits + row * stride, V, gt, NTH, st, pol_last);
-          float M, M2;
-          double S;
-          combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
-          if (lane == 0) {
-            wm[warp] = M;
-            wm2[warp] = M2;
-            wsum[warp] = S;
-          }
-          asm volatile("bar.sync 1, 512;" ::: "memory");
-          if (warp == 0) {
-            const bool act = lane < 16;
-            combine_lanes(act ? wm[lane] : -INFINITY, act ? wm2[lane] : 0.f, act ? wsum[lane] : 0.0, act, rs.sc, M,
-                          M2, S);
-            if (lane == 0) {
-              part_m[b] = M;
-              part_M2[b] = M2;
-              part_s[b] = S;
-            }
-          }
-        }
-      }
-    } else if (j >= 1) {
-      const int pb = b ^ 1;
-      const int64_t row = st_row[pb];
-      const bool valid = st_valid[pb] != 0;
-      bwd_row<T, TO, 4, true>(logits + row * stride, g_out + row * ostride, V, gt, NTH, valid, rs.sc, st_M2[pb],
-                              st_L2S[pb], (float)rs.inv_temp, st_y[pb], pol_first);
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (warp == 0 && j < nrc) {
-      const int64_t row = cid + j * n_clusters;
-      const bool valid = mask[row] != 0;
-      float M = -INFINITY, M2 = 0.f;
-      double S = 0.0;
-      if (valid) {
-        const bool act = lane < 2;
-        float pm = -INFINITY, pm2 = 0.f;
-        double ps = 0.0;
-        if (act) {
-          pm = *cl.map_shared_rank(&part_m[b], lane);
-          pm2 = *cl.map_shared_rank(&part_M2[b], lane);
-          ps = *cl.map_shared_rank(&part_s[b], lane);
-        }
-        combine_lanes(pm, pm2, ps, act, rs.sc, M, M2, S);
-      }
-      if (lane == 0) {
-        int64_t y = -1;
-        if (valid) {
-          y = tokens[row];
-          const bool ok = (y >= 0 && y < V);
-          if (rank == 0) {
-            const float zy = ok ? Elem<T>::load1(logits + row * stride + y) : 0.f;
-            finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
-          }
-          st_M2[b] = M2;
-          st_L2S[b] = (float)log2(S);
-        }
-        st_y[b] = y;
-        st_row[b] = row;
-        st_valid[b] = valid;
-      }
-    }
-    __syncthreads();  // row j's statistics are visible to team B in round j+1
-  }
-}
-
 
 // ------------------------------------------------------------------------------ launch
 }  // namespace
@@ -249,31 +131,15 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
     // sweeps the row backwards (cfg 8 / 9 = cfg 4 / 0 reversed): the row's most recently streamed
     // vectors are re-read first, while still in L2 (Qwen 8.13 -> 7.96 ms, scripts/gpu_ab_rev.sh).
     const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
-    int cfg = rb <= 128 * 1024 ? 9 : 8;
-    const int ecfg = env_int("TBA_SINGLE_CFG", -1);
-    if (ecfg >= 0 && ecfg <= 9) cfg = ecfg;
-#define TBA_SINGLE1(KERN_, T_, TO_, NT_, CS_, U2_, ...)                                                        \
-  KERN_<T_, TO_, NT_, U2_, ##__VA_ARGS__><<<(unsigned)(rows * CS_), NT_, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab, \
-                                                             x->row_stride, x->tokens, x->mask, rs, w.stats,      \
-                                                             w.lp, dev_status, static_cast<TO_*>(grad_unscaled),  \
-                                                             g_row_stride)
-#define TBA_SINGLE(T_, TO_)                                          \
-  do {                                                               \
-    if (cfg == 0) TBA_SINGLE1(row_single1, T_, TO_, 256, 1, 4);      \
-    else if (cfg == 1) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 4); \
-    else if (cfg == 2) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 4); \
-    else if (cfg == 3) TBA_SINGLE1(row_single4, T_, TO_, 512, 4, 4); \
-    else if (cfg == 4) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 8); \
-    else if (cfg == 5) TBA_SINGLE1(row_single2, T_, TO_, 512, 2, 8); \
-    else if (cfg == 6) TBA_SINGLE1(row_single2, T_, TO_, 256, 2, 4); \
-    else if (cfg == 8) TBA_SINGLE1(row_single1, T_, TO_, 512, 1, 8, true); \
-    else if (cfg == 9) TBA_SINGLE1(row_single1, T_, TO_, 256, 1, 4, true); \
-    else {                                                           \
-      const int64_t ncl = (int64_t)device_sms() / 2;                 \
-      row_single_pipe<T_, TO_><<<(unsigned)(2 * ncl), 1024, 0, s>>>( \
-          static_cast<const T_*>(x->logits), rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, \
-          w.lp, dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride, ncl);                        \
-    }                                                                \
+    const bool small = rb <= 128 * 1024;
+#define TBA_SINGLE1(T_, TO_, NT_, U2_)                                                                          \
+  row_single1<T_, TO_, NT_, U2_, true><<<(unsigned)rows, NT_, 0, s>>>(                                         \
+      static_cast<const T_*>(x->logits), rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, w.qy, w.lp, \
+      dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride)
+#define TBA_SINGLE(T_, TO_)                   \
+  do {                                        \
+    if (small) TBA_SINGLE1(T_, TO_, 256, 4);  \
+    else TBA_SINGLE1(T_, TO_, 512, 8);        \
   } while (0)
     if (x->dtype == TBA_BF16) {
       if (g_dtype == TBA_BF16) TBA_SINGLE(uint16_t, uint16_t);

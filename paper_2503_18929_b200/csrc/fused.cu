@@ -61,21 +61,18 @@ __global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
       const int64_t row = gr0 + rin;
       if (rin < rows_per_group && a.mask[row]) {
         const T* rp = logits + row * a.stride;
+        const int64_t y = a.tokens[row];
+        const bool ok = (y >= 0 && y < a.V);
         float zy = 0.f;
-        bool ok = true;
-        if (gt == 0) {
-          const int64_t y = a.tokens[row];
-          ok = (y >= 0 && y < a.V);
-          if (ok) zy = Elem<T>::load1(rp + y);
-        }
+        if (gt == 0 && ok) zy = Elem<T>::load1(rp + y);
         OnlineState st;
         st.init(a.rs);
-        fwd_accumulate<T, kFusedU, false, (TPR_F == 64 ? 1 : 0)>(rp, a.V, gt, TPR_F, st);  // as the two-call path
+        fwd_accumulate<T, kFusedU, false, (TPR_F == 64 ? 1 : 0)>(rp, a.V, gt, TPR_F, st, ok ? y : -1);  // as two-call
         float M, M2;
         double S;
         combine_lanes(st.m, st.R2, st.s, true, a.rs.sc, M, M2, S);
         if (WPR == 1) {
-          if (lane == 0) finalize_row(M, M2, S, zy, ok, row, a.rs, a.stats, a.lp, a.dev_status);
+          if (lane == 0) finalize_row(M, M2, S, zy, ok, row, a.rs, a.stats, a.qy, a.lp, a.dev_status);
         } else {
           if (lane == 0) {
             sm_m[grp][wig] = M;
@@ -87,7 +84,7 @@ __global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
             const bool act = lane < WPR;
             combine_lanes(act ? sm_m[grp][lane] : -INFINITY, act ? sm_M2[grp][lane] : 0.f,
                           act ? sm_s[grp][lane] : 0.0, act, a.rs.sc, M, M2, S);
-            if (lane == 0) finalize_row(M, M2, S, zy, ok, row, a.rs, a.stats, a.lp, a.dev_status);
+            if (lane == 0) finalize_row(M, M2, S, zy, ok, row, a.rs, a.stats, a.qy, a.lp, a.dev_status);
           }
         }
       }
@@ -152,17 +149,18 @@ __global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
       if (rin < rows_per_group) {
         const int64_t row = gr0 + rin;
         const bool valid = a.mask[row] != 0;
-        float M2 = 0.f, L2S = 0.f, c = 0.f;
+        float M2 = 0.f, L2S = 0.f, c = 0.f, qy = 0.f;
         int64_t y = -1;
         if (valid) {
           const float2 stt = __ldcg(a.stats + row);
           M2 = stt.x;
           L2S = stt.y;
+          qy = __ldcg(a.qy + row);
           c = (float)(a.grad_scale * a.rs.inv_temp * __ldcg(a.resid + row / a.T));
           y = a.tokens[row];
         }
         bwd_row<T, TO, 4>(logits + row * a.stride, dlogits + row * a.ostride, a.V, tid, TPR_B, valid, a.rs.sc, M2,
-                          L2S, c, y);
+                          L2S, c, y, qy);
       }
     }
   }

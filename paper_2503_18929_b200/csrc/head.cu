@@ -1,5 +1,5 @@
-// a2 + a3: per-sequence sums and the group heads (VarGrad TB, Eqs. 4-5; TBA', Eq. 16), the
-// forward-with-fused-head variant, and the small helper kernels.
+// a2 + a3: per-sequence sums and the group heads (VarGrad TB, Eqs. 4-5; TBA', Eq. 16) and the
+// small helper kernels.
 #include "tba_device.cuh"
 
 namespace tba {
@@ -16,8 +16,7 @@ __global__ void __launch_bounds__(1024) seq_head(const double* __restrict__ lp, 
                                                 double inv_n_global, double* __restrict__ seq_logp,
                                                 int32_t* __restrict__ n_tokens, double* __restrict__ log_z,
                                                 double* __restrict__ resid, double* __restrict__ group_sq,
-                                                double* __restrict__ partial, unsigned int* counter,
-                                                PeerArgs pa = PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr}) {
+                                                double* __restrict__ partial, unsigned int* counter) {
   const int per = HEAD ? K : 8;
   const int64_t s0 = (int64_t)blockIdx.x * per;
   seq_sums(lp, mask, n_seq, T, s0, per, seq_logp, n_tokens, nullptr);
@@ -37,67 +36,10 @@ __global__ void __launch_bounds__(1024) seq_head(const double* __restrict__ lp, 
   if (am_last && threadIdx.x == 0) {
     __threadfence();
     *counter = 0u;
-    tb_finish(group_sq, (int64_t)gridDim.x, n_seq, inv_n_global, partial, pa);
+    tb_finish(group_sq, (int64_t)gridDim.x, n_seq, inv_n_global, partial);
   }
 }
 
-
-// Forward rows + per-sequence sums (+ group head) in ONE kernel: every CTA, after its rows, adds
-// its row counts to per-unit counters (unit = one sequence for log-probs, one group of K
-// sequences for the TB head); the CTA that completes a unit computes that unit's sums (and
-// head), and the CTA completing the last group reduces the loss partials. Saves the separate
-// seq_head launch and its latency.
-template <class T, int TPR, int U, int NP>
-__global__ void __launch_bounds__(256) row_fwd_head(const T* __restrict__ logits, int64_t rows, int64_t V,
-                                                     int64_t stride, const int64_t* __restrict__ tokens,
-                                                     const uint8_t* __restrict__ mask, RowScale rs,
-                                                     float2* __restrict__ stats, double* __restrict__ lp,
-                                                     int32_t* dev_status, HeadArgs ha) {
-  constexpr int RPC = 256 / TPR, WPRS = TPR / 32 > 0 ? TPR / 32 : 1;
-  __shared__ float sm_m[RPC][WPRS], sm_M2[RPC][WPRS];
-  __shared__ double sm_s[RPC][WPRS];
-  __shared__ int64_t sh_done[RPC + 1];
-  __shared__ int sh_ndone;
-  const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
-  const int64_t row0 = (int64_t)blockIdx.x * RPC;
-  const int64_t row = row0 + grp;
-  if (row < rows && mask[row] != 0) {
-    fwd_row_group<T, TPR, U, NP, true>(logits, row, V, stride, tokens, rs, stats, lp, dev_status, sm_m, sm_M2, sm_s,
-                                       grp, gt);
-  }
-  __syncthreads();
-  const int64_t unit_rows = (int64_t)ha.K * ha.T;
-  if (threadIdx.x == 0) {
-    int nd = 0;
-    const int64_t r1 = row0 + RPC < rows ? row0 + RPC : rows;
-    for (int64_t r = row0; r < r1;) {
-      const int64_t u = r / unit_rows;
-      const int64_t ue = (u + 1) * unit_rows < r1 ? (u + 1) * unit_rows : r1;
-      const unsigned cnt = (unsigned)(ue - r);
-      if (atomicAdd(&ha.units_done[u], cnt) + cnt == (unsigned)unit_rows) sh_done[nd++] = u;
-      r = ue;
-    }
-    sh_ndone = nd;
-    if (nd) __threadfence();
-  }
-  __syncthreads();
-  for (int i = 0; i < sh_ndone; ++i) {
-    const int64_t u = sh_done[i];
-    seq_sums(lp, mask, ha.n_seq, ha.T, u * ha.K, ha.K, ha.seq_logp, ha.n_tokens, nullptr);
-    if (!ha.head) continue;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tb_group_head(u, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.seq_logp, ha.log_z,
-                    ha.resid, ha.group_sq);
-      __threadfence();
-      const int64_t groups = ha.n_seq / ha.K;
-      if (atomicAdd(ha.groups_done, 1u) + 1u == (unsigned)groups) {
-        __threadfence();
-        tb_finish(ha.group_sq, groups, ha.n_seq, ha.inv_n_global, ha.partial, ha.pa);
-      }
-    }
-  }
-}
 
 // ------------------------------------------------------------------------------ TBA' head (Eq. 16)
 // One CTA per group: sequence sums as seq_head; thread 0 forms A_j = (r_j - rbar) -
@@ -206,49 +148,11 @@ __global__ void dlogz_kernel(const double* __restrict__ resid, int64_t groups, i
 __global__ void tb_finish_kernel(const double* __restrict__ group_sq, int64_t groups, int64_t n_seq,
                                  double inv_n_global, double* __restrict__ partial) {
   if (threadIdx.x == 0 && blockIdx.x == 0)
-    tb_finish(group_sq, groups, n_seq, inv_n_global, partial, PeerArgs{nullptr, nullptr, 0, 0, 0u, 0ull, nullptr});
+    tb_finish(group_sq, groups, n_seq, inv_n_global, partial);
 }
 
 // ------------------------------------------------------------------------------ launch
 }  // namespace
-
-// Forward rows with the per-unit sums / TB head fused in (row_fwd_head). Returns false when the
-// separate kernels must be used instead (no rows, or the TMA forward selected for A/B).
-bool launch_fwd_head(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, HeadArgs& ha,
-                     cudaStream_t s, int* rc) {
-  const int64_t rows = x->n_seq * x->seq_len;
-  const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
-  if (rows == 0 || (switches().fwd_tma && x->vocab * esz > kSmallRowBytes)) return false;
-  // Off by default: measured on B200 (scripts/gpu_ab_head.sh) the per-row fence + unit counters
-  // cost as much as the separate seq_head launch saves (Qwen 9.305 vs 9.283 ms, RhoMath 7.03 vs
-  // 6.98; only the launch-bound toy gains, 0.056 vs 0.060). TBA_FUSE_HEAD=1 selects it.
-  if (env_int("TBA_FUSE_HEAD", 0) == 0) return false;
-  if (cudaMemsetAsync(w.fused, 0, fused_counter_bytes(x->n_seq), s) != cudaSuccess) {
-    *rc = TBA_ERR_CUDA;
-    return true;
-  }
-  ha.units_done = w.fused + 2;
-  ha.groups_done = w.fused + 1;
-  const int tpr = fwd_tpr(x->vocab, esz);
-  const int np = env_int("TBA_FWD_NP", 1);
-  const unsigned grid = (unsigned)((rows + 256 / tpr - 1) / (256 / tpr));
-#define TBA_HEAD(T_, TPR_, NP_)                                                                                    \
-  row_fwd_head<T_, TPR_, kU, NP_><<<grid, 256, 0, s>>>(static_cast<const T_*>(x->logits), rows, x->vocab,         \
-                                                       x->row_stride, x->tokens, x->mask, rs, w.stats, w.lp,      \
-                                                       dev_status, ha)
-  if (x->dtype == TBA_BF16) {
-    if (tpr == 64 && np == 1) TBA_HEAD(uint16_t, 64, 1);
-    else if (tpr == 64) TBA_HEAD(uint16_t, 64, 0);
-    else TBA_HEAD(uint16_t, 32, 0);
-  } else {
-    if (tpr == 64 && np == 1) TBA_HEAD(float, 64, 1);
-    else if (tpr == 64) TBA_HEAD(float, 64, 0);
-    else TBA_HEAD(float, 32, 0);
-  }
-#undef TBA_HEAD
-  *rc = cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
-  return true;
-}
 
 int launch_seq_head(bool head, const WsLayout& w, const uint8_t* mask, const HeadArgs& ha, cudaStream_t s) {
   if (head) {
@@ -256,7 +160,7 @@ int launch_seq_head(bool head, const WsLayout& w, const uint8_t* mask, const Hea
     const int threads = ha.K <= 8 ? 256 : (ha.K >= 32 ? 1024 : 32 * ha.K);
     seq_head<true><<<(unsigned)(ha.n_seq / ha.K), threads, 0, s>>>(
         w.lp, mask, ha.n_seq, ha.T, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.inv_n_global,
-        ha.seq_logp, ha.n_tokens, ha.log_z, ha.resid, w.group_sq, ha.partial, w.counter, ha.pa);
+        ha.seq_logp, ha.n_tokens, ha.log_z, ha.resid, w.group_sq, ha.partial, w.counter);
   } else {
     seq_head<false><<<(unsigned)((ha.n_seq + 7) / 8), 256, 0, s>>>(
         w.lp, mask, ha.n_seq, ha.T, 8, nullptr, nullptr, nullptr, 0.0, 0.0, ha.seq_logp, ha.n_tokens, nullptr,

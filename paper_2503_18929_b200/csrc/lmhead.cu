@@ -365,166 +365,6 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   }
 }
 
-// cta_group::2 variant: an SM pair (cluster of 2) computes a 256 x 256 logit tile per MMA
-// (M = 256 across the pair: each CTA holds its 128 hidden rows and half of the weight tile in
-// shared memory, and its 128 accumulator rows in its own TMEM). Per SM and stage only 32 KB
-// (16 KB hidden + 16 KB weight) are loaded and read by the tensor core, 2/3 of the single-SM
-// kernel's operand traffic. Both CTAs' TMA loads signal the leader's full barrier; the leader's
-// lane issues the MMA and its commits arrive on both CTAs' barriers (multicast); the four
-// epilogue warps of both CTAs release an accumulator on the leader's barrier (count 8).
-// NT = 2: 256 x 512 pair tiles (two N = 256 MMAs per K step share the hidden stage; one
-// accumulator of 512 columns, so the softmax epilogue of a tile is not overlapped with the next
-// tile's MMAs): per SM 48 KB per 128 x 512 x 64 of work, half the single-SM kernel's L2 feed.
-template <int NT>
-struct L2Cfg {
-  static constexpr int STAGES = NT == 1 ? 6 : 4;
-  static constexpr int A_BYTES = LM_BM * LM_BK * 2;              // 16 KB: this CTA's 128 hidden rows
-  static constexpr int B_BYTES = NT * (LM_BN / 2) * LM_BK * 2;   // this CTA's halves of the NT weight tiles
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
-};
-constexpr uint32_t L2_IDESC = tc_idesc_bf16(2 * LM_BM, LM_BN);
-
-template <int NT, int H = 1>
-__global__ void __launch_bounds__(64 + 128 * H, 1)
-    lmhead_fwd_2sm(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LmGrid g,
-                   const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, RowScale rs,
-                   float2* __restrict__ part, float* __restrict__ zy_out,
-                   const __grid_constant__ CUtensorMap tmZ /* unused: this kernel stores logits directly */) {
-  constexpr int L2_STAGES = L2Cfg<NT>::STAGES, L2_A_BYTES = L2Cfg<NT>::A_BYTES, L2_B_BYTES = L2Cfg<NT>::B_BYTES,
-                L2_STAGE_BYTES = L2Cfg<NT>::STAGE_BYTES, NACC = 2 / NT;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + L2_STAGES * L2_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L2_STAGES * L2_STAGE_BYTES);
-  uint64_t* empty = full + L2_STAGES;
-  uint64_t* tfull = empty + L2_STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_ctarank();
-  const bool leader = crank == 0;
-  const int64_t unit0 = blockIdx.x / 2, n_units = gridDim.x / 2;
-  const int nact = *g.n_act;
-  const int64_t n_items = (int64_t)nact * g.n_groups;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < L2_STAGES; ++s) {
-      mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
-      mbar_init(&empty[s], 1);  // the leader's multicast commit
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8 * H);  // leader: 4 H epilogue warps x 2 CTAs
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer (both CTAs)
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmH)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-      const uint64_t pol_w = l2_policy(g.pol & 1), pol_h = l2_policy(g.pol & 2);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t it = unit0; it < n_items; it += n_units) {
-        int rb, grp;
-        lm_item(g, nact, it, rb, grp);
-        rb = g.act[rb];
-        rb = rb * 2 + (int)crank;
-        const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
-        for (int t = t0; t < t1; t += NT) {
-          for (int kb = 0; kb < g.nkb; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1u);
-            if (leader) mbar_expect_tx(&full[stage], 2 * L2_STAGE_BYTES);
-            tma_load_2d_pair(smem_u32(sA + stage * L2_A_BYTES), &tmH, kb * LM_BK, rb * LM_BM, smem_u32(&full[stage]),
-                             pol_h, (g.pol & 4) == 0);
-#pragma unroll
-            for (int u = 0; u < NT; ++u)
-              tma_load_2d_pair(smem_u32(sB + stage * L2_B_BYTES + u * (L2_B_BYTES / NT)), &tmW, kb * LM_BK,
-                               (t + u) * LM_BN + (int)crank * (LM_BN / 2), smem_u32(&full[stage]), pol_w,
-                               (g.pol & 4) == 0);
-            if (++stage == L2_STAGES) {
-              stage = 0;
-              phase ^= 1u;
-            }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---- MMA issuer (leader only)
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t j = 0;
-      for (int64_t it = unit0; it < n_items; it += n_units) {
-        int rb, grp;
-        lm_item(g, nact, it, rb, grp);
-        rb = g.act[rb];
-        const int t0 = grp * g.G, t1 = min(g.n_tiles, t0 + g.G);
-        for (int t = t0; t < t1; t += NT, ++j) {
-          const uint32_t acc = j % NACC, aph = (j / NACC) & 1u;
-          mbar_wait(&tempty[acc], aph ^ 1u);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem + acc * NT * LM_BN;
-          for (int kb = 0; kb < g.nkb; ++kb) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint64_t a0 = umma_desc_sw128(smem_u32(sA + stage * L2_A_BYTES));
-#pragma unroll
-            for (int k = 0; k < LM_BK / 16; ++k)
-#pragma unroll
-              for (int u = 0; u < NT; ++u) {
-                const uint64_t b0 = umma_desc_sw128(smem_u32(sB + stage * L2_B_BYTES + u * (L2_B_BYTES / NT)));
-                umma_bf16_pair<L2_IDESC>(d_tmem + u * LM_BN, a0 + 2u * k, b0 + 2u * k, (kb | k) != 0);
-              }
-            umma_commit_pair(&empty[stage]);
-            if (++stage == L2_STAGES) {
-              stage = 0;
-              phase ^= 1u;
-            }
-          }
-          umma_commit_pair(&tfull[acc]);
-        }
-      }
-    }
-  } else {  // ---- epilogue (both CTAs): release on the leader's tempty
-    const int q = warp & 3;
-    const int h = (warp - 2) / 4;  // warp-half (H = 2)
-    const int row_in = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    uint32_t tempty_leader;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(tempty_leader) : "r"(smem_u32(tempty)));
-    uint32_t j = 0;
-    for (int64_t it = unit0; it < n_items; it += n_units) {
-      int rb, grp;
-      lm_item(g, nact, it, rb, grp);
-      rb = g.act[rb];
-      rb = rb * 2 + (int)crank;
-      lm_epilogue_item<NT, H>(g, rb, grp, j, tmem + lane_addr, row_in, lane, tfull, tempty_leader, true, tokens, rs,
-                              part, zy_out, h);
-    }
-  }
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-}
-
 // Ordered list of the row-block units (MCu row blocks of 128 rows) that hold a valid row: one
 // CTA, chunks of 1024 units, ballot + warp-total scan. Masked tails of short responses then cost
 // no GEMM work and the persistent CTAs stay balanced over the units that remain.
@@ -595,49 +435,27 @@ __global__ void lmhead_combine(const float2* __restrict__ part, const float* __r
 
 }  // namespace
 
-// A/B knobs (read once): TBA_LM_G vocab tiles per work item (>= LM_G keeps the workspace bound),
-// TBA_LM_SWZ row blocks per raster super-row.
-int lm_g() {
-  static int g = [] { int v = env_int("TBA_LM_G", LM_G); return v >= LM_G ? v : LM_G; }();
-  return g;
-}
-int lm_swz() {
-  static int v = [] { int x = env_int("TBA_LM_SWZ", LM_RB_SWZ); return x >= 1 ? x : LM_RB_SWZ; }();
-  return v;
-}
-
 size_t lmhead_partial_bytes(int64_t rows, int64_t V) {
-  // the most partials any G >= LM_G makes: two per group with the split epilogue (TBA_LM_MC=5)
-  const int64_t groups = 2 * (((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G);
+  const int64_t groups = ((V + LM_BN - 1) / LM_BN + LM_G - 1) / LM_G;
   const int64_t blocks = (rows + LM_BM - 1) / LM_BM;
   return align_up((size_t)groups * (size_t)rows * sizeof(float2), 256) + align_up((size_t)rows * sizeof(float), 256) +
          align_up((size_t)(blocks + 1) * sizeof(int), 256);
-}
-
-// TBA_LM_MC: 1 single-SM kernel, 2 cluster pair with weight multicast, 3 cta_group::2 pair (256 x 256
-// tiles), 4 cta_group::2 pair with 256 x 512 tiles, 5 the same with eight epilogue warps.
-int lm_mc() {
-  static int v = [] { int x = env_int("TBA_LM_MC", 1); return (x >= 2 && x <= 5) ? x : 1; }();
-  return v;
 }
 
 int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
                        cudaStream_t s, float* zst, int64_t zst_ld) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
-  const int mode = lm_mc();
-  const int mc = mode == 1 ? 1 : 2;  // CTAs per cluster
+  constexpr int mc = 1;  // one CTA per work item (the cluster / cta_group::2 variants measured slower)
   const int n_rb = (int)((rows + LM_BM - 1) / LM_BM);
   const int n_units_total = (n_rb + mc - 1) / mc;  // row-block units (pairs when mc = 2)
   LmGrid g;
   g.rows = rows;
   g.V = x->vocab;
   g.n_tiles = (int)((x->vocab + LM_BN - 1) / LM_BN);
-  g.G = lm_g();
-  if (mode >= 4 && (g.G & 1)) ++g.G;  // a wide tile holds two vocabulary tiles of one group
-  const int H = mode == 5 ? 2 : 1;      // partials per group
-  g.swz = (lm_swz() + mc - 1) / mc;  // the raster counts row blocks: a pair unit holds two
-  g.pol = env_int("TBA_LM_POL", 1) & 7;
+  g.G = LM_G;
+  g.swz = LM_RB_SWZ;
+  g.pol = 1;  // weight tiles evict_last (54.4-55.5 vs 62-63 ms with evict_normal)
   g.n_groups = (g.n_tiles + g.G - 1) / g.G;
   g.nkb = (int)((x->d + LM_BK - 1) / LM_BK);
   g.zst = zst;
@@ -646,12 +464,12 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   if (!make_map(&mh, x->hidden, rows, x->d, x->hidden_stride, LM_BM) ||
       !make_map(&mw, x->weight, x->vocab, x->d, x->weight_stride, LM_BN / mc))
     return TBA_ERR_CUDA;
-  const bool ztma = zst && mode == 1;  // the single-SM kernel stores the logits with TMA
+  const bool ztma = zst != nullptr;  // the logits store goes out through TMA
   if (ztma ? !make_store_map_f32(&mz, zst, rows, x->vocab, zst_ld) : false) return TBA_ERR_CUDA;
   if (!ztma) mz = CUtensorMap{};
   char* pw = static_cast<char*>(part_ws);
   float2* part = reinterpret_cast<float2*>(pw);
-  pw += align_up((size_t)g.n_groups * H * (size_t)rows * sizeof(float2), 256);
+  pw += align_up((size_t)g.n_groups * (size_t)rows * sizeof(float2), 256);
   float* zy = reinterpret_cast<float*>(pw);
   pw += align_up((size_t)rows * sizeof(float), 256);
   int* act = reinterpret_cast<int*>(pw);
@@ -659,45 +477,28 @@ int launch_lmhead_rows(const tba_lmhead* x, void* part_ws, const WsLayout& w, co
   g.n_act = act + n_rb;
   lm_compact_units<<<1, 1024, 0, s>>>(x->mask, rows, mc, n_units_total, act, act + n_rb);
   if (cudaGetLastError() != cudaSuccess) return TBA_ERR_CUDA;
-  static bool attr[5][64] = {};  // per variant and device; benign race: idempotent
+  static bool attr[64] = {};  // per device; benign race: idempotent
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return TBA_ERR_CUDA;
-  auto kern = mode == 5   ? lmhead_fwd_2sm<2, 2>
-              : mode == 4 ? lmhead_fwd_2sm<2, 1>
-              : mode == 3 ? lmhead_fwd_2sm<1, 1>
-              : mode == 2 ? lmhead_fwd<2>
-                          : lmhead_fwd<1>;
-  const size_t smem = mode >= 4 ? L2Cfg<2>::SMEM : mode == 3 ? L2Cfg<1>::SMEM : ztma ? LM_SMEM_Z : LM_SMEM;
-  if (!attr[mode - 1][dev]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(mode == 1 ? LM_SMEM_Z : smem)) !=
-        cudaSuccess)
+  auto kern = lmhead_fwd<1>;
+  const size_t smem = ztma ? LM_SMEM_Z : LM_SMEM;
+  if (!attr[dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM_Z) != cudaSuccess)
       return TBA_ERR_CUDA;
-    attr[mode - 1][dev] = true;
+    attr[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[1];
-  cfg.blockDim = dim3(mode == 5 ? 64 + 256 : LM_THREADS);
+  cfg.blockDim = dim3(LM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  int64_t units = device_sms() / mc;
-  if (mc > 1) {
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = mc;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cfg.gridDim = dim3((unsigned)(units * mc));
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl > 0 && ncl < units) units = ncl;
-  }
+  int64_t units = device_sms();
   const int64_t max_items = (int64_t)n_units_total * g.n_groups;  // the active count is known on the device only
   if (units > max_items) units = max_items;
   cfg.gridDim = dim3((unsigned)(units * mc));
   if (cudaLaunchKernelEx(&cfg, kern, mh, mw, g, x->tokens, x->mask, rs, part, zy, mz) != cudaSuccess)
     return TBA_ERR_CUDA;
   const int64_t blocks = (rows + 255) / 256 < 4096 ? (rows + 255) / 256 : 4096;
-  lmhead_combine<<<(unsigned)blocks, 256, 0, s>>>(part, zy, rows, g.n_groups * H, x->vocab, x->tokens, x->mask, rs,
+  lmhead_combine<<<(unsigned)blocks, 256, 0, s>>>(part, zy, rows, g.n_groups, x->vocab, x->tokens, x->mask, rs,
                                                   w.stats, w.lp, dev_status);
   return launch_status();
 }

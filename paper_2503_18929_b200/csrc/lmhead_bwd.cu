@@ -660,12 +660,13 @@ __global__ void __launch_bounds__(256) lmb_gather_t(const uint16_t* __restrict__
 // vocabulary columns; row i of the chunk is batch row r = idx[i], its logits at zst + (r - zrow0) * zst_ld.
 //   dz [i, v] = c_r (1[v = y_r] - 2^(z sc - M2 - log2 S))  (bf16)  and  dz^T [v, i] the same
 // (rows i in [n, n rounded up to 128) are written as 0 so the GEMM tiles over them read zeros).
-__global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __restrict__ n_valid, int64_t cap,
-                                                     const float* __restrict__ zst, int64_t zst_ld, int64_t zrow0) {
+__global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __restrict__ n_valid, int64_t chunk0,
+                                                     int64_t cap, const float* __restrict__ zst, int64_t zst_ld,
+                                                     int64_t zrow0) {
   __shared__ uint16_t tile[64][130];  // 65-word rows: the column reads below hit distinct banks
   __shared__ float s_c[64], s_m2[64], s_l2s[64];
   __shared__ long long s_y[64], s_off[64];
-  const int64_t n = chunk_count(n_valid, 0, cap);
+  const int64_t n = chunk_count(n_valid, chunk0, cap);
   const int64_t n_pad = (n + 127) / 128 * 128;
   const int64_t i0 = (int64_t)blockIdx.y * 64, v0 = (int64_t)blockIdx.x * 128;
   if (i0 >= n_pad) return;
@@ -675,7 +676,7 @@ __global__ void __launch_bounds__(256) lmb_dz_from_z(DzArgs z, const int* __rest
     float c = 0.f, M2 = 0.f, L2S = 0.f;
     long long y = -1, off = -1;
     if (i < n) {
-      const int64_t r = z.idx[i];
+      const int64_t r = z.idx[chunk0 + i];
       const float2 st = z.stats[r];
       M2 = st.x;
       L2S = st.y;
@@ -773,6 +774,30 @@ __global__ void __launch_bounds__(256) lmb_splitk_reduce(const float* __restrict
 
 constexpr int LMB_KSPLIT_MAX = 4;
 
+// Kernel selection of the backward GEMMs, read ONCE per process (A/B and test switches; the
+// defaults are the measured best): pair bit 0 dH / bit 1 dW on the cta_group::2
+// kernel, wide = 256 x 512 pair tiles, dwmn = dW reads dZ and Hc as MN-major operands.
+struct LmbKnobs {
+  int swz, ninner, pol, pair, wide, dwmn, ksplit;
+};
+const LmbKnobs& lmb_knobs() {
+  static const LmbKnobs k = [] {
+    LmbKnobs v;
+    v.swz = env_once("TBA_LMB_SWZ", 32);
+    if (v.swz < 1) v.swz = 32;
+    v.ninner = env_once("TBA_LMB_NINNER", 3);
+    v.pol = env_once("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
+    v.pair = env_once("TBA_LMB_2SM", 3);   // measured: 196-203 ms vs 218-223 (one-call Qwen step)
+    v.wide = env_once("TBA_LMB_NT2", 3);
+    v.dwmn = env_once("TBA_LMB_DW_MN", 1) != 0 && (v.pair & 2) != 0;
+    v.ksplit = env_once("TBA_LMB_KSPLIT", 0);
+    return v;
+  }();
+  return k;
+}
+// The transposed copies dZ^T [V, C] and Hc^T [d, C] exist only for the K-major dW forms.
+inline bool lmb_need_transposed() { return !lmb_knobs().dwmn; }
+
 struct LmbWs {
   int* idx;  // [rows] + the count at idx[rows]
   uint16_t *wt, *hc, *hct, *dz, *dzt;
@@ -794,9 +819,10 @@ LmbWs lmb_layout(void* base, int64_t rows, int64_t d, int64_t V, int64_t C) {
   w.idx = reinterpret_cast<int*>(take((size_t)(rows + 1) * sizeof(int)));
   w.wt = reinterpret_cast<uint16_t*>(take((size_t)d * (size_t)lmb_vp(V) * 2));
   w.hc = reinterpret_cast<uint16_t*>(take((size_t)C * (size_t)d * 2));
-  w.hct = reinterpret_cast<uint16_t*>(take((size_t)d * (size_t)C * 2));
+  const bool tr = lmb_need_transposed();
+  w.hct = reinterpret_cast<uint16_t*>(take(tr ? (size_t)d * (size_t)C * 2 : 0));
   w.dz = reinterpret_cast<uint16_t*>(take((size_t)C * (size_t)lmb_vp(V) * 2));
-  w.dzt = reinterpret_cast<uint16_t*>(take((size_t)V * (size_t)C * 2));
+  w.dzt = reinterpret_cast<uint16_t*>(take(tr ? (size_t)V * (size_t)C * 2 : 0));
   w.part = reinterpret_cast<float*>(take((size_t)LMB_KSPLIT_MAX * (size_t)C * (size_t)lmb_dp(d) * 4));
   return w;
 }
@@ -864,9 +890,10 @@ int64_t lmhead_bwd_chunk(int64_t rows, int64_t chunk_rows) {
 
 size_t lmhead_bwd_ws_bytes(int64_t rows, int64_t d, int64_t V, int64_t chunk_rows) {
   const int64_t C = lmhead_bwd_chunk(rows, chunk_rows);
+  const bool tr = lmb_need_transposed();
   return align_up((size_t)(rows + 1) * sizeof(int), 256) + align_up((size_t)d * (size_t)lmb_vp(V) * 2, 256) +
-         2 * align_up((size_t)C * (size_t)d * 2, 256) + align_up((size_t)C * (size_t)lmb_vp(V) * 2, 256) +
-         align_up((size_t)V * (size_t)C * 2, 256) +
+         align_up((size_t)C * (size_t)d * 2, 256) + (tr ? align_up((size_t)d * (size_t)C * 2, 256) : 0) +
+         align_up((size_t)C * (size_t)lmb_vp(V) * 2, 256) + (tr ? align_up((size_t)V * (size_t)C * 2, 256) : 0) +
          align_up((size_t)LMB_KSPLIT_MAX * (size_t)C * (size_t)lmb_dp(d) * 4, 256);
 }
 
@@ -893,7 +920,7 @@ struct LmbCtx {
 // (LMB_DEFAULT_CHUNK rows) come within 4 % of perfect balance. S depends on (d, V, SMs) only, so the
 // one-call and two-call schedules split alike and their dH stay bitwise equal.
 int lmb_dh_split(int64_t d, int64_t V, int nt) {
-  static const int knob = env_int("TBA_LMB_KSPLIT", 0);
+  const int knob = lmb_knobs().ksplit;
   const int64_t nkb = (V + TC_BK - 1) / TC_BK;
   int S = 1;
   if (knob > 0) {
@@ -921,23 +948,19 @@ int lmb_dh_split(int64_t d, int64_t V, int nt) {
 }
 
 int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, void* bws, bool need_wt, cudaStream_t s) {
-  static const int swz = [] { int v = env_int("TBA_LMB_SWZ", 32); return v >= 1 ? v : 32; }();
-  static const int ninner = env_int("TBA_LMB_NINNER", 3);
-  static const int pol = env_int("TBA_LMB_POL", 0x8);  // dW: keep Hc^T in L2 (measured 198 vs 203 ms)
-  static const int pair = env_int("TBA_LMB_2SM", 3);  // measured: 196-203 ms vs 218-223 (one-call Qwen step)
-  static const int wide = env_int("TBA_LMB_NT2", 3);  // bit 0 dH, bit 1 dW: 256 x 512 pair tiles
-  static const int dwmn = env_int("TBA_LMB_DW_MN", 1);
+  const LmbKnobs& kn = lmb_knobs();
+  const int pair = kn.pair, wide = kn.wide;
   const int64_t d = x->d, V = x->vocab;
   k.x = x;
   k.C = C;
   k.Vp = lmb_vp(V);
   k.w = lmb_layout(bws, idx_rows, d, V, C);
-  k.swz = swz;
-  k.ninner = ninner;
-  k.pol = pol;
+  k.swz = kn.swz;
+  k.ninner = kn.ninner;
+  k.pol = kn.pol;
   k.pair = pair;
   k.wide = wide;
-  k.dwmn = dwmn != 0 && (pair & 2) != 0;
+  k.dwmn = kn.dwmn != 0;
   k.dh_split = (pair & 1) ? lmb_dh_split(d, V, (wide & 1) ? 2 : 1) : 1;
   if (need_wt) {
     const dim3 grid((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64));
@@ -947,10 +970,10 @@ int lmb_prepare(LmbCtx& k, const tba_lmhead* x, int64_t idx_rows, int64_t C, voi
   }
   if (!make_map(&k.m_hc, k.w.hc, C, d, d, GB_BM) || !make_map(&k.m_w, x->weight, V, d, x->weight_stride, GB_BN) ||
       !make_map(&k.m_dz, k.w.dz, C, V, k.Vp, GB_BM) || !make_map(&k.m_wt, k.w.wt, d, V, k.Vp, GB_BN) ||
-      !make_map(&k.m_dzt, k.w.dzt, V, C, C, GB_BM) || !make_map(&k.m_hct, k.w.hct, d, C, C, GB_BN))
+      (!k.dwmn && (!make_map(&k.m_dzt, k.w.dzt, V, C, C, GB_BM) || !make_map(&k.m_hct, k.w.hct, d, C, C, GB_BN))))
     return TBA_ERR_CUDA;
-  if (pair && (!make_map(&k.m_wt2, k.w.wt, d, V, k.Vp, 128) || !make_map(&k.m_hct2, k.w.hct, d, C, C, 128)))
-    return TBA_ERR_CUDA;
+  if (pair && !make_map(&k.m_wt2, k.w.wt, d, V, k.Vp, 128)) return TBA_ERR_CUDA;
+  if (pair && !k.dwmn && !make_map(&k.m_hct2, k.w.hct, d, C, C, 128)) return TBA_ERR_CUDA;
   // MN-major boxes {64 along V (or d), 64 rows}
   if (k.dwmn && (!make_map(&k.m_dzmn, k.w.dz, C, V, k.Vp, 64) || !make_map(&k.m_hcmn, k.w.hc, C, d, d, 64)))
     return TBA_ERR_CUDA;
@@ -975,10 +998,10 @@ int lmb_chunk(const LmbCtx& k, const int* n_valid, int64_t chunk0, DzArgs dz, co
   dz.dz = k.w.dz;
   dz.dzt = (dw && !k.dwmn) ? k.w.dzt : nullptr;
   int rc;
-  if (zst) {  // 2'. dz from the stored logits (chunk0 == 0: the chunk's own row list)
+  if (zst) {  // 2'. dz from the stored logits (rows idx[chunk0 ..] of the group chunk's own row list)
     dz.idx = k.w.idx;
     const dim3 grid((unsigned)((V + 127) / 128), (unsigned)(C / 64));
-    lmb_dz_from_z<<<grid, 256, 0, s>>>(dz, n_valid, C, zst, zst_ld, zrow0);
+    lmb_dz_from_z<<<grid, 256, 0, s>>>(dz, n_valid, chunk0, C, zst, zst_ld, zrow0);
     rc = launch_status();
   } else {  // 2. dz tiles recomputed: M = the chunk's rows, N = V, K = d
     GemmArgs a{};
@@ -1113,8 +1136,8 @@ int64_t lmhead_fb_groups(int64_t groups, int64_t rows_per_group, int32_t groups_
 
 size_t lmhead_fb_ws_bytes(int64_t n_seq, int64_t T, int64_t d, int64_t V, int32_t K, int32_t groups_per_chunk) {
   const int64_t gpc = lmhead_fb_groups(n_seq / K, (int64_t)K * T, groups_per_chunk);
-  const int64_t R = gpc * K * T;  // rows per chunk
-  const int64_t C = lmhead_bwd_chunk(R, R);
+  const int64_t R = gpc * K * T;  // rows per chunk (all stored as fp32 logits)
+  const int64_t C = lmhead_bwd_chunk(R, R < LMB_DEFAULT_CHUNK ? R : LMB_DEFAULT_CHUNK);  // GEMM sub-chunk
   return lmhead_bwd_ws_bytes(R, d, V, C) + align_up((size_t)R * (size_t)lmb_vp(V) * 4, 256) +
          lmhead_partial_bytes(R, V);
 }
@@ -1125,7 +1148,10 @@ int launch_lmhead_fwd_bwd(const tba_lmhead* x, const RowScale& rs, const WsLayou
                           int32_t* dev_status, cudaStream_t s) {
   const int64_t T = x->seq_len, groups = x->n_seq / K, rows = x->n_seq * T;
   const int64_t gpc = lmhead_fb_groups(groups, (int64_t)K * T, groups_per_chunk);
-  const int64_t R = gpc * K * T, C = lmhead_bwd_chunk(R, R);
+  // R rows per group chunk (their fp32 logits stored); the compaction / GEMM chunk C is capped at
+  // LMB_DEFAULT_CHUNK, so one group larger than that (Table 5: K = 16 x T = 2048) runs as several
+  // sub-chunks of its stored logits instead of growing every backward buffer with the group.
+  const int64_t R = gpc * K * T, C = lmhead_bwd_chunk(R, R < LMB_DEFAULT_CHUNK ? R : LMB_DEFAULT_CHUNK);
   int rc = TBA_OK;
   if (!accumulate) rc = lmb_zero_outputs(x, rows, dh, dh_dt, dh_stride, dw, dw_stride, false, s);
   if (rc) return rc;
@@ -1146,7 +1172,7 @@ int launch_lmhead_fwd_bwd(const tba_lmhead* x, const RowScale& rs, const WsLayou
     xc.tokens = x->tokens + r0;
     xc.mask = x->mask + r0;
     xc.n_seq = gc * K;
-    const WsLayout wc{w.stats + r0, w.lp + r0, w.group_sq + g0, nullptr, nullptr};
+    const WsLayout wc{w.stats + r0, w.lp + r0, w.group_sq + g0, nullptr, nullptr, w.qy + r0};
     // forward of the chunk, logits kept (row r0 + i at zst + i * Vp)
     rc = launch_lmhead_rows(&xc, part_ws, wc, rs, dev_status, s, zst, k.Vp);
     if (rc) break;
@@ -1165,8 +1191,9 @@ int launch_lmhead_fwd_bwd(const tba_lmhead* x, const RowScale& rs, const WsLayou
     // backward of the chunk from the stored logits
     lmb_compact_rows<<<1, 1024, 0, s>>>(xc.mask, rc_rows, r0, k.w.idx, n_valid);
     if ((rc = launch_status())) break;
-    rc = lmb_chunk(k, n_valid, 0, dz0, zst, k.Vp, r0, dh, dh_dt, dh_stride, accumulate, dw, dw_stride,
-                   accumulate || c > 0, s);
+    for (int64_t sub = 0; sub * C < rc_rows && !rc; ++sub)  // sub-chunks past *n_valid do no work
+      rc = lmb_chunk(k, n_valid, sub * C, dz0, zst, k.Vp, r0, dh, dh_dt, dh_stride, accumulate, dw, dw_stride,
+                     accumulate || c > 0 || sub > 0, s);
   }
   if (!rc) rc = launch_tb_finish(w.group_sq, groups, x->n_seq, inv_n_global, ha0.partial, s);
   return rc;

@@ -1,6 +1,6 @@
 // Device building blocks shared by the kernels of libtba.so (kernel overview: tba_iface.cuh):
 // PTX wrappers, the online log-sum-exp state and the row forward (a1), the per-sequence sums and
-// group head (a2, a3) with the fused peer all-reduce, the row gradient writer (a5) and the
+// group head (a2, a3), the row gradient writer (a5) and the
 // acquire/release flags. Header-only; internal linkage in every translation unit.
 #pragma once
 #include "tba_iface.cuh"
@@ -160,6 +160,8 @@ struct OnlineState {
     chunk(z);
     s += (double)ex2(fmaf(z, sc, -R2));
   }
+  // the sampled token's element: it takes part in the max, not in the sum (finalize_row adds it)
+  __device__ __forceinline__ void add1_excl(float z) { chunk(z); }
 };
 
 // Combine (m, R2, s) partial states held by the lanes of a warp (`active` lanes only). Result
@@ -177,14 +179,23 @@ __device__ __forceinline__ void combine_lanes(float m, float R2, double s, bool 
   S = v;
 }
 
-__device__ __forceinline__ void finalize_row(float M, float M2, double S, float zy, bool tok_ok, int64_t row,
+// Sx = the sum over the row's elements OTHER than the sampled token's (relative to M2; the token's
+// element was excluded from the online sums). The token's term e_y = 2^(z_y sc - M2) is formed here
+// in fp64 (z_y sc exact in fp64), so that 1 - p_y = Sx / (Sx + e_y) and
+//   lp = log p_y = (z_y - M)(a - ln2 sc) - log1p(Sx / e_y)
+// keep full relative accuracy when p_y -> 1 (a confident token: 1 - p_y far below fp32's epsilon,
+// where sum-then-subtract would cancel). a = inv_temp; sc = fl(log2(e) a) (§5.1).
+__device__ __forceinline__ void finalize_row(float M, float M2, double Sx, float zy, bool tok_ok, int64_t row,
                                              const RowScale& rs, float2* __restrict__ stats,
-                                             double* __restrict__ lp, int32_t* dev_status) {
+                                             float* __restrict__ qy, double* __restrict__ lp,
+                                             int32_t* dev_status) {
+  const double ey = tok_ok ? exp2((double)zy * (double)rs.sc - (double)M2) : 0.0;
+  const double S = Sx + ey;
   const bool finite = (M > -INFINITY) && (M < INFINITY) && (S > 0.0) && (S < INFINITY);
   const double log2s = log2(S);
   stats[row] = make_float2(M2, (float)log2s);
-  // lp = a (z_y - M) - ln sum_v e^{kappa a (z_v - M)},  a = inv_temp, kappa a = sc / log2(e)  (§5.1)
-  double v = rs.inv_temp * ((double)zy - (double)M) - kLN2 * (log2s + (double)M2 - (double)M * (double)rs.sc);
+  qy[row] = (float)(Sx / S);  // 1 - p_y
+  double v = ey > 0.0 ? ((double)zy - (double)M) * (rs.inv_temp - kLN2 * (double)rs.sc) - log1p(Sx / ey) : -INFINITY;
   if (!tok_ok) v = nan("");
   lp[row] = v;
   if (dev_status) {
@@ -197,7 +208,7 @@ __device__ __forceinline__ void finalize_row(float M, float M2, double S, float 
 // fp32 pair accumulators (<= 4U terms each) folded into the fp64 partial once per call.
 // NP of the VEC/2 element pairs of every vector take the FMA-pipe exp2 instead of MUFU.
 template <class T, int U, int NP = 0>
-__device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st) {
+__device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st, int uy = -1, int ey = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   float z[U][VEC];
@@ -211,6 +222,13 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 #pragma unroll
     for (int e = 0; e < VEC; e += 2) cm = fmaxf(cm, fmaxf(z[u][e], z[u][e + 1]));
   st.chunk(cm);
+  if ((unsigned)uy < (unsigned)U) {  // the sampled token's element (vector uy, slot ey): in the max, not the sum
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (u == uy && e == ey) z[u][e] = -INFINITY;
+  }
   const uint64_t l2e = f2_pack(st.sc, st.sc), nr2 = f2_pack(-st.R2, -st.R2);
   uint64_t acc[VEC / 2];
 #pragma unroll
@@ -238,31 +256,45 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
   st.s += (double)(a + b);
 }
 
-// LDG-streamed partial state of one row over threads tid, tid+nthr, ...
+// LDG-streamed partial state of one row over threads tid, tid+nthr, ... The sampled token's element
+// (index y; y < 0 or >= V: none) enters the max but not the sum (finalize_row adds its term).
 template <class T, int U, bool POL = false, int NP = 0>
 __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_t V, int tid, int nthr,
-                                               OnlineState& st, uint64_t pol = 0) {
+                                               OnlineState& st, int64_t y, uint64_t pol = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(row, V);
   const int64_t nvec = (V - h) / VEC;
   const int64_t tail0 = h + nvec * VEC;
-  if (tid < h) st.add1(E::load1(row + tid));
-  for (int64_t i = tail0 + tid; i < V; i += nthr) st.add1(E::load1(row + i));
+  if (tid < h) {
+    const float z = E::load1(row + tid);
+    if (tid == y) st.add1_excl(z);
+    else st.add1(z);
+  }
+  for (int64_t i = tail0 + tid; i < V; i += nthr) {
+    const float z = E::load1(row + i);
+    if (i == y) st.add1_excl(z);
+    else st.add1(z);
+  }
+  // The token's vector ky (row vectors < 2^28: 32-bit) is this thread's vector number jy =
+  // (ky - tid) / nthr when ky = tid mod nthr; du counts down to it by U per iteration.
+  const int ky = (y >= h && y < tail0) ? (int)((y - h) / VEC) : -1;
+  const int ey = ky >= 0 ? (int)((y - h) - (int64_t)ky * VEC) : 0;
+  int du = (ky >= tid && (ky - tid) % nthr == 0) ? (ky - tid) / nthr : -(1 << 30);
   const uint4* vp = reinterpret_cast<const uint4*>(row + h);
   const int64_t step = (int64_t)nthr * U;
-  const int64_t nfull = nvec / step;
+  const int nfull = (int)(nvec / step);
   int64_t k0 = tid;
-  for (int64_t it = 0; it < nfull; ++it, k0 += step) {
+  for (int it = 0; it < nfull; ++it, k0 += step, du -= U) {
     uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
       v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
-    fwd_consume<T, U, NP>(v, st);
+    fwd_consume<T, U, NP>(v, st, du, ey);
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
-    fwd_consume<T, 1>(v1, st);
+    fwd_consume<T, 1>(v1, st, k == ky ? 0 : -1, ey);
   }
 }
 
@@ -270,29 +302,27 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 template <class T, int TPR, int U, int NP, bool FENCE = false>
 __device__ __forceinline__ void fwd_row_group(const T* __restrict__ logits, int64_t row, int64_t V, int64_t stride,
                                               const int64_t* __restrict__ tokens, const RowScale& rs,
-                                              float2* __restrict__ stats, double* __restrict__ lp,
+                                              float2* __restrict__ stats, float* __restrict__ qy,
+                                              double* __restrict__ lp,
                                               int32_t* dev_status, float (*sm_m)[TPR / 32 > 0 ? TPR / 32 : 1],
                                               float (*sm_M2)[TPR / 32 > 0 ? TPR / 32 : 1],
                                               double (*sm_s)[TPR / 32 > 0 ? TPR / 32 : 1], int grp, int gt) {
   constexpr int WPR = TPR / 32;
   const int lane = threadIdx.x & 31, wig = gt >> 5;
   const T* rp = logits + row * stride;
+  const int64_t y = tokens[row];
+  const bool ok = (y >= 0 && y < V);
   float zy = 0.f;
-  bool ok = true;
-  if (gt == 0) {
-    const int64_t y = tokens[row];
-    ok = (y >= 0 && y < V);
-    if (ok) zy = Elem<T>::load1(rp + y);
-  }
+  if (gt == 0 && ok) zy = Elem<T>::load1(rp + y);
   OnlineState st;
   st.init(rs);
-  fwd_accumulate<T, U, false, NP>(rp, V, gt, TPR, st);
+  fwd_accumulate<T, U, false, NP>(rp, V, gt, TPR, st, ok ? y : -1);
   float M, M2;
   double S;
   combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
   if (WPR == 1) {
     if (lane == 0) {
-      finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+      finalize_row(M, M2, S, zy, ok, row, rs, stats, qy, lp, dev_status);
       if (FENCE) __threadfence();  // publish lp / stats before the unit counters move
     }
     return;
@@ -308,7 +338,7 @@ __device__ __forceinline__ void fwd_row_group(const T* __restrict__ logits, int6
     combine_lanes(act ? sm_m[grp][lane] : -INFINITY, act ? sm_M2[grp][lane] : 0.f, act ? sm_s[grp][lane] : 0.0, act,
                   rs.sc, M, M2, S);
     if (lane == 0) {
-      finalize_row(M, M2, S, zy, ok, row, rs, stats, lp, dev_status);
+      finalize_row(M, M2, S, zy, ok, row, rs, stats, qy, lp, dev_status);
       if (FENCE) __threadfence();
     }
   }
@@ -404,52 +434,6 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
   if (my_count) *my_count = tot;
 }
 
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ void peer_allreduce3(const PeerArgs& pa, const double (&p)[3], double* partial) {
-  const int par = (int)(pa.epoch & 1u);
-  for (int q = 0; q < pa.world; ++q) {
-    double* dst = pa.slots[q] + ((size_t)par * pa.world + pa.rank) * 4;
-    dst[0] = p[0];
-    dst[1] = p[1];
-    dst[2] = p[2];
-  }
-  __threadfence_system();
-  for (int q = 0; q < pa.world; ++q)
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pa.flags[q] + pa.rank), "r"(pa.epoch) : "memory");
-  const unsigned int* mine = pa.flags[pa.rank];
-  const unsigned long long t0 = globaltimer_ns();
-  bool timeout = false;
-  for (int q = 0; q < pa.world && !timeout; ++q) {
-    for (;;) {
-      unsigned int v;
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + q) : "memory");
-      if ((int)(v - pa.epoch) >= 0) break;
-      if (globaltimer_ns() - t0 > pa.timeout_ns) {
-        timeout = true;
-        break;
-      }
-      __nanosleep(256);
-    }
-  }
-  if (timeout) {
-    if (pa.dev_status) atomicOr(pa.dev_status, TBA_DEV_PEER_TIMEOUT);
-    partial[0] = partial[1] = partial[2] = nan("");
-    return;
-  }
-  const volatile double* my = pa.slots[pa.rank] + (size_t)par * pa.world * 4;
-  double t[3] = {0.0, 0.0, 0.0};
-  for (int q = 0; q < pa.world; ++q)
-    for (int k = 0; k < 3; ++k) t[k] += my[q * 4 + k];
-  partial[0] = t[0];
-  partial[1] = t[1];
-  partial[2] = t[2];
-}
-
 // Eq. 4 (or the learned log Z of Eq. 3) and the Eq. 5 residuals of group g, by one thread.
 __device__ __forceinline__ void tb_group_head(int64_t g, int K, const double* __restrict__ ref_logp,
                                               const double* __restrict__ log_reward,
@@ -493,9 +477,9 @@ __device__ __forceinline__ void tb_group_head(int64_t g, int K, const double* __
   group_sq[g] = sq;
 }
 
-// Final fixed-order reduction of the per-group sums of squares (+ optional fused all-reduce).
+// Final fixed-order reduction of the per-group sums of squares.
 __device__ __forceinline__ void tb_finish(const double* group_sq, int64_t groups, int64_t n_seq, double inv_n_global,
-                                          double* partial, const PeerArgs& pa) {
+                                          double* partial) {
   // serial group order (deterministic); 16 loads in flight per batch instead of one latency per group
   double tot = 0.0;
   int64_t i = 0;
@@ -507,14 +491,9 @@ __device__ __forceinline__ void tb_finish(const double* group_sq, int64_t groups
     for (int u = 0; u < 16; ++u) tot += v[u];
   }
   for (; i < groups; ++i) tot += __ldcg(group_sq + i);
-  const double p[3] = {tot * inv_n_global, (double)n_seq, (double)groups};
-  if (pa.world > 0) {
-    peer_allreduce3(pa, p, partial);
-  } else {
-    partial[0] = p[0];
-    partial[1] = p[1];
-    partial[2] = p[2];
-  }
+  partial[0] = tot * inv_n_global;
+  partial[1] = (double)n_seq;
+  partial[2] = (double)groups;
 }
 
 // ------------------------------------------------------------------------------ a5
@@ -550,9 +529,11 @@ __device__ __forceinline__ void store_vals(TO* o, const float (&d)[N]) {
 
 // REV: walk the row's vectors from the end (the deferred pass re-reads a row it has just streamed:
 // its last vectors are the most recently touched in L2).
+// dz_v = -c p_v for v != y and c (1 - p_y) at the token, with 1 - p_y = qy from the forward (exact
+// when p_y -> 1, where c - c p_y would cancel).
 template <class T, class TO, int U, bool POL = false, bool REV = false>
 __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid, int nthr,
-                                        bool valid, float sc, float M2, float L2S, float c, int64_t y,
+                                        bool valid, float sc, float M2, float L2S, float c, int64_t y, float qy,
                                         uint64_t pol = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
@@ -565,7 +546,7 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
     float d = 0.f;
     if (valid) {
       const float p = ex2(fmaf(E::load1(rp + i), sc, -M2) - L2S);
-      d = (i == y) ? fmaf(-c, p, c) : -c * p;
+      d = (i == y) ? c * qy : -c * p;
     }
     Out<TO>::put1(op + i, d);
   };
@@ -603,7 +584,7 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
           const int e = (int)((y - h) - k * VEC);
 #pragma unroll
           for (int q = 0; q < VEC; ++q)
-            if (q == e) d[q] += c;
+            if (q == e) d[q] = c * qy;
         }
         store_vals<TO, VEC>(ob + k * VEC, d);
       }

@@ -8,14 +8,12 @@
 //                                   ex2 per element (packed FFMA2/FADD2; 1 of 4 pairs on the FMA
 //                                   pipe), gather z[y]; writes per-row (M2, log2 S) and the token
 //                                   log-prob (fp64).
-//                row_fwd_tma   a1   alternative: persistent, warp-specialised, cp.async.bulk ring.
 //   head.cu      seq_head      a2+a3 per-sequence fixed-order fp64 sums of token log-probs
 //                                   (log pi(y|x)) and token counts; per group Eq. 4 log Z (or a
 //                                   learned log Z, Eq. 3) and the Eq. 5 residuals; the last CTA
 //                                   reduces the per-group sums of squares (+ peer all-reduce).
 //                tbap_head     a2+a3' TBA' (Eq. 16): per-group advantages, per-token IS-weighted
 //                                   coefficients.
-//                row_fwd_head  a1-a3 forward rows with the head fused in (A/B option).
 //   bwd.cu       row_bwd       a5   stream each valid row again: dz = c (1[v=y] - softmax); c per
 //                                   sequence (TB) or per token (TBA'); masked rows zero-filled.
 //   fused.cu     tb_fused      a1-a5 in one persistent launch (NEXT 2 (i)).
@@ -47,26 +45,7 @@ struct RowScale {
   double inv_temp;
 };
 
-// One-shot all-reduce of the 3 loss partials fused into the head kernel, over peer memory
-// (NVLink P2P stores / loads through CUDA IPC mappings): the last CTA of every rank
-// writes its partial into slot [rank] of every peer's buffer, releases a per-peer flag with the
-// call's epoch, waits (acquire, bounded by a timeout) for all ranks' flags, and sums the slots in
-// rank order — every rank computes bit-identical totals, with no NCCL launch. Slots are double-
-// buffered by epoch parity (a rank cannot get two epochs ahead of a peer that has not read).
-struct PeerArgs {
-  double* const* slots;         // [world] device pointers: rank q's buffer of 2 x world x 4 doubles
-  unsigned int* const* flags;   // [world] device pointers: rank q's [world] epoch flags
-  int rank, world;
-  unsigned int epoch;
-  unsigned long long timeout_ns;
-  int32_t* dev_status;
-};
-
-// Forward rows + per-sequence sums (+ group head) in ONE kernel: every CTA, after its rows, adds
-// its row counts to per-unit counters (unit = one sequence for log-probs, one group of K
-// sequences for the TB head); the CTA that completes a unit computes that unit's sums (and
-// head), and the CTA completing the last group reduces the loss partials. Saves the separate
-// seq_head launch and its latency.
+// Arguments of the per-sequence sums and the Eq. 4/5 group head (seq_head).
 struct HeadArgs {
   int64_t T;
   int K;             // sequences per unit (1 = log-probs only)
@@ -82,9 +61,6 @@ struct HeadArgs {
   double* resid;
   double* group_sq;
   double* partial;
-  unsigned int* units_done;   // [n_units]
-  unsigned int* groups_done;  // [1]
-  PeerArgs pa;
 };
 
 // One persistent launch for the whole VarGrad TB step: forward rows, the group head and the
@@ -103,6 +79,7 @@ struct FusedArgs {
   const double* log_reward;
   const double* log_z_param;
   float2* stats;
+  float* qy;
   double* lp;
   double* seq_logp;
   int32_t* n_tokens;
@@ -138,6 +115,7 @@ struct WsLayout {
   double* group_sq;
   unsigned int* counter;
   unsigned int* fused;
+  float* qy;  // per row: 1 - p_y (the token's complement probability, exact when p_y -> 1)
 };
 
 inline size_t fused_counter_bytes(int64_t n_seq) { return (size_t)(2 + 2 * n_seq) * sizeof(unsigned int); }
@@ -158,13 +136,16 @@ inline WsLayout ws_layout(void* ws, int64_t n_seq, int64_t T) {
   l.counter = reinterpret_cast<unsigned int*>(p + off);
   off = align_up(off + 4 * sizeof(unsigned int), 256);
   l.fused = reinterpret_cast<unsigned int*>(p + off);  // work, groups_done, rows_done[n_seq], ready[n_seq]
+  off = align_up(off + fused_counter_bytes(n_seq), 256);
+  l.qy = reinterpret_cast<float*>(p + off);
   return l;
 }
 
 inline size_t ws_bytes(int64_t n_seq, int64_t T) {
   const size_t rows = (size_t)n_seq * (size_t)T;
   return align_up(rows * sizeof(float2), 256) + align_up(rows * sizeof(double), 256) +
-         align_up((size_t)n_seq * sizeof(double), 256) + 256 + align_up(fused_counter_bytes(n_seq), 256);
+         align_up((size_t)n_seq * sizeof(double), 256) + 256 + align_up(fused_counter_bytes(n_seq), 256) +
+         align_up(rows * sizeof(float), 256);
 }
 
 inline int validate_rows(const tba_rows* x) {
@@ -209,47 +190,24 @@ inline int device_sms() {
   return n;
 }
 
-inline int env_int(const char* name, int dflt) {
+// Environment overrides of the two non-default schedules' chunking (tba_tb_loss_fused's lookahead,
+// tba_tb_loss_pipelined's default chunk), read ONCE per process; never consulted by the default
+// two-call path.
+inline int env_once(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
 }
 
-// A/B switches (read once): TBA_FWD_IMPL=tma selects the TMA-ring forward, TBA_TMA_CFG its
-// configuration, TBA_FWD_TPR / TBA_BWD_TPR force threads per row. Defaults are the measured best.
-struct Switches {
-  int fwd_tma, tma_cfg, fwd_tpr, bwd_tpr;
-};
-inline const Switches& switches() {
-  static Switches s = [] {
-    Switches v;
-    const char* e = getenv("TBA_FWD_IMPL");
-    v.fwd_tma = (e && e[0] == 't') ? 1 : 0;
-    v.tma_cfg = env_int("TBA_TMA_CFG", 0);
-    v.fwd_tpr = env_int("TBA_FWD_TPR", 0);
-    v.bwd_tpr = env_int("TBA_BWD_TPR", 0);
-    return v;
-  }();
-  return s;
-}
+// Forward threads per row, measured on B200: 64 threads (4 rows per CTA) is best
+// or within 1 % for V = 32000 ... 152064; one warp for short rows.
+inline int fwd_tpr(int64_t V, int64_t esz) { return (V * esz / 16) < 1024 ? 32 : 64; }
 
-inline bool valid_tpr(int t) { return t == 32 || t == 64 || t == 128 || t == 256; }
-
-// Forward threads per row, measured on B200 (scripts/gpu_ab_tpr.sh): 64 threads
-// (4 rows per CTA) is best or within 1 % for V = 32000 ... 152064; one warp for short rows.
-inline int fwd_tpr(int64_t V, int64_t esz) {
-  if (valid_tpr(switches().fwd_tpr)) return switches().fwd_tpr;
-  return (V * esz / 16) < 1024 ? 32 : 64;
-}
-
-// Backward threads per row (scripts/gpu_ab_bwd.sh): one CTA per long row, one warp per short row.
-inline int bwd_tpr(int64_t V, int64_t esz) {
-  if (valid_tpr(switches().bwd_tpr)) return switches().bwd_tpr;
-  return V * esz <= kSmallRowBytes ? 32 : 256;
-}
+// Backward threads per row: one CTA per long row, one warp per short row.
+inline int bwd_tpr(int64_t V, int64_t esz) { return V * esz <= kSmallRowBytes ? 32 : 256; }
 
 // Groups of look-ahead in the fused schedule: as many groups of logits as fit in ~35 % of L2.
 inline int fused_lookahead(int64_t group_bytes, int groups) {
-  const int env = env_int("TBA_FUSED_D", -1);
+  static const int env = env_once("TBA_FUSED_D", -1);
   int d;
   if (env >= 0) {
     d = env;
@@ -267,7 +225,8 @@ inline int fused_lookahead(int64_t group_bytes, int groups) {
 // Groups per chunk of the pipelined schedule: chunks of <= ~1/4 of L2, so that chunk c (being
 // re-read by the gradient writer) and chunk c+1 (being read by the forward) both stay resident.
 inline int pipe_groups(int64_t group_bytes, int64_t groups) {
-  int d = env_int("TBA_PIPE_GROUPS", 0);
+  static const int env = env_once("TBA_PIPE_GROUPS", 0);
+  int d = env;
   if (d <= 0) {
     int dev = 0, l2 = 0;
     cudaGetDevice(&dev);
@@ -315,10 +274,6 @@ inline int launch_status() { return cudaGetLastError() == cudaSuccess ? TBA_OK :
 int launch_fwd_rows(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, cudaStream_t s);
 
 // head.cu
-// Forward rows with the sums / TB head fused in (row_fwd_head, TBA_FUSE_HEAD=1). Returns false
-// when the separate kernels must be used instead; otherwise *rc holds the status.
-bool launch_fwd_head(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status, HeadArgs& ha,
-                     cudaStream_t s, int* rc);
 // seq_head: HEAD = false -> log pi(y|x) and counts only (ha.K ignored); true -> + Eq. 4/5 head.
 int launch_seq_head(bool head, const WsLayout& w, const uint8_t* mask, const HeadArgs& ha, cudaStream_t s);
 int launch_tbap_head(const WsLayout& w, const uint8_t* mask, const float* gen_logp, int64_t n_seq, int64_t T, int K,
@@ -333,7 +288,8 @@ int launch_dlogz(const double* resid, int64_t groups, int K, double grad_scale, 
                  double* d_log_z, cudaStream_t s);
 
 // bwd.cu — a5: per_row = false: c = resid[s] (TB); true: c = coef[row] (TBA').
-int launch_bwd(bool per_row, const tba_rows* x, const float2* stats, const double* resid, const float* coef,
+int launch_bwd(bool per_row, const tba_rows* x, const float2* stats, const float* qy, const double* resid,
+               const float* coef,
                double gs, const double* go, const RowScale& rs, void* dlogits, int32_t odt, int64_t ostride,
                cudaStream_t s);
 

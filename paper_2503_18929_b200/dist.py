@@ -41,70 +41,53 @@ def token_balanced_ranges(group_tokens, world: int) -> list[tuple[int, int]]:
     return [(cuts[i], cuts[i + 1]) for i in range(world)]
 
 
-class PeerReducer:
-    """Buffers for the loss all-reduce fused into the head kernel over peer memory
-    (tba_tb_loss_fwd_peer; CUDA IPC mappings, P2P over NVLink). Collective: every rank of
-    ``group`` constructs it once on its device; ``next_args()`` returns the per-call struct
-    (the epoch increases by one per call on every rank)."""
+class PartialAllreduce:
+    """The loss partials' all-reduce running on a side stream: the backward never
+    waits for it, because the gradient needs only the static N_global. ``wait()`` makes the
+    caller's current stream wait for it and returns the global [L, N_global, B_global]."""
 
-    def __init__(self, group, device, timeout_s: float = 10.0):
-        import ctypes
+    def __init__(self, out, event, stream):
+        self.out, self.event, self.stream = out, event, stream
 
+    def wait(self):
         import torch
-        import torch.distributed as dist
+        torch.cuda.current_stream(self.out.device).wait_event(self.event)
+        self.out.record_stream(torch.cuda.current_stream(self.out.device))
+        return self.out
 
-        from . import _lib
-        L = _lib.load()
-        self._L = L
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        self.timeout_s = float(timeout_s)
-        self.device = torch.device(device)
-        own = []
-        handles = []
-        with torch.cuda.device(self.device):
-            for nbytes in (2 * self.world * 4 * 8, max(self.world * 4, 16)):
-                ptr = ctypes.c_void_p()
-                h = ctypes.create_string_buffer(64)
-                _lib.check(L.tba_ipc_alloc(nbytes, ctypes.byref(ptr), h), "tba_ipc_alloc")
-                own.append(ptr.value)
-                handles.append(h.raw)
-        self._own = own
-        gathered = [None] * self.world
-        dist.all_gather_object(gathered, handles, group=group)
-        self._opened = []
-        slots, flags = [], []
-        with torch.cuda.device(self.device):
-            for q in range(self.world):
-                if q == self.rank:
-                    slots.append(own[0])
-                    flags.append(own[1])
-                    continue
-                ptrs = []
-                for h in gathered[q]:
-                    p = ctypes.c_void_p()
-                    _lib.check(L.tba_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)), "tba_ipc_open")
-                    self._opened.append(p.value)
-                    ptrs.append(p.value)
-                slots.append(ptrs[0])
-                flags.append(ptrs[1])
-        # device arrays of device pointers
-        self.slots_arr = torch.tensor(slots, dtype=torch.int64, device=self.device)
-        self.flags_arr = torch.tensor(flags, dtype=torch.int64, device=self.device)
-        self.epoch = 0
-        dist.barrier(group=group)
 
-    def next_args(self):
-        from ._lib import TbaPeerReduce
-        self.epoch += 1
-        return TbaPeerReduce(self.slots_arr.data_ptr(), self.flags_arr.data_ptr(), self.rank, self.world,
-                             self.epoch, self.timeout_s)
+_SIDE: dict = {}
 
-    def close(self):
-        import torch
-        torch.cuda.synchronize(self.device)
-        for p in self._opened:
-            self._L.tba_ipc_close(p)
-        for p in self._own:
-            self._L.tba_ipc_free(p)
-        self._opened, self._own = [], []
+
+def allreduce_partial_async(partial, group) -> PartialAllreduce:
+    """All-reduce (sum) a copy of ``partial`` (fp64 [3], on the current stream's device) on a side
+    stream ordered after the current stream's work so far; the current stream does not wait. The
+    result is read through ``PartialAllreduce.wait()`` (event-ordered)."""
+    import torch
+    import torch.distributed as dist
+    dev = partial.device
+    key = (dev.type, dev.index)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
+    side = _SIDE[key]
+    if side is None:  # CPU tensors (gloo tests): nothing to overlap
+        out = partial.clone()
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+        return _CpuDone(out)
+    cur = torch.cuda.current_stream(dev)
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        out = partial.clone()
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    partial.record_stream(side)
+    return PartialAllreduce(out, ev, side)
+
+
+class _CpuDone:
+    def __init__(self, out):
+        self.out = out
+
+    def wait(self):
+        return self.out

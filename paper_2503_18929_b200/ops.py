@@ -134,7 +134,7 @@ def _opts(inv_temp: float, log_z_param):
 
 def vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, n_seq_global: float,
                 workspace=None, out: _Fwd | None = None, check_status: bool = _CHECK, inv_temp: float = 1.0,
-                log_z_param=None, peer=None):
+                log_z_param=None):
     """Raw TB forward (tba_tb_loss_fwd; tba_vargrad_tb_loss_fwd when inv_temp = 1 and no learned
     log Z). log_z_param: optional fp64 [N/K] learned log Z(x_i) (Eq. 3). Returns (_Fwd, workspace)."""
     L = _lib.load()
@@ -155,13 +155,7 @@ def vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int,
         args = (ref_logp.data_ptr(), log_reward.data_ptr(), float(beta), int(K), float(n_seq_global), ws.data_ptr(),
                 o.seq_logp.data_ptr(), o.n_tokens.data_ptr(), o.log_z.data_ptr() if N else None, o.resid.data_ptr(),
                 o.partial.data_ptr(), _ptr(st), _stream(dev))
-        if peer is not None:  # dist.PeerReducer: partial becomes the all-reduced global value
-            pr = peer.next_args()
-            a = list(args)
-            st_ptr, stream = a[-2], a[-1]
-            check(L.tba_tb_loss_fwd_peer(ctypes.byref(x), ctypes.byref(opts) if opts is not None else None,
-                                         *a[:-2], ctypes.byref(pr), st_ptr, stream), "tba_tb_loss_fwd_peer")
-        elif opts is None:
+        if opts is None:
             check(L.tba_vargrad_tb_loss_fwd(ctypes.byref(x), *args), "tba_vargrad_tb_loss_fwd")
         else:
             check(L.tba_tb_loss_fwd(ctypes.byref(x), ctypes.byref(opts), *args), "tba_tb_loss_fwd")
@@ -212,19 +206,26 @@ class VarGradTBLoss(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, logits, log_z_param, tokens, mask, ref_logp, log_reward, beta, K, n_global, group,
-                dlogits_dtype, inv_temp, aux, peer=None):
+                dlogits_dtype, inv_temp, aux, overlap=False):
         lzp = None if log_z_param is None else log_z_param.detach().contiguous()
         o, ws = vargrad_fwd(logits, tokens, mask, ref_logp, log_reward, beta, K, n_global, inv_temp=inv_temp,
-                            log_z_param=lzp, peer=peer)
-        if group is not None and peer is None:
-            import torch.distributed as dist
-            dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
+                            log_z_param=lzp)
+        pending = None
+        if group is not None:
+            if overlap:  # side-stream all-reduce; the returned loss is this rank's share
+                from .dist import allreduce_partial_async
+                pending = allreduce_partial_async(o.partial, group)
+            else:
+                import torch.distributed as dist
+                dist.all_reduce(o.partial, op=dist.ReduceOp.SUM, group=group)
         ctx.save_for_backward(logits, tokens, mask, ws, o.resid)
         ctx.n_global, ctx.K, ctx.inv_temp = n_global, K, inv_temp
         ctx.dlogits_dtype = dlogits_dtype
         ctx.lzp = lzp
         if aux is not None:
             aux.update(seq_logp=o.seq_logp, n_tokens=o.n_tokens, log_z=o.log_z, resid=o.resid, partial=o.partial)
+            if pending is not None:
+                aux["global_partial"] = pending
         return o.partial[0]
 
     @staticmethod
@@ -238,7 +239,7 @@ class VarGradTBLoss(torch.autograd.Function):
 
 def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int, *, n_seq_global=None,
                     group=None, dlogits_dtype=None, return_aux: bool = False, log_z=None, inv_temp: float = 1.0,
-                    peer=None):
+                    overlap_allreduce: bool = False):
     """The trajectory-balance loss, autograd-enabled.
 
     Default: the VarGrad loss of Eq. 5 with the detached K-sample log Z of Eq. 4.
@@ -247,8 +248,11 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
     logits [N, T, V] bf16/fp32 (N = groups*K, group-major); tokens int64 [N, T]; mask
     uint8/bool [N, T]; ref_logp, log_reward fp64 [N] (log_reward is r_phi). With ``group``
     each rank passes its own whole groups and the partial sums are all-reduced once;
-    ``n_seq_global`` defaults to N * world. ``peer`` (a ``dist.PeerReducer``) replaces the NCCL
-    all-reduce by the one fused into the head kernel over peer memory. Returns the 0-dim fp64
+    ``n_seq_global`` defaults to N * world. With ``overlap_allreduce`` the all-reduce runs on a side
+    stream and the returned (differentiable) loss is this rank's share sum_own eps^2 / N_global —
+    whose gradient is exactly the global loss's, since L = sum over ranks of the shares — while
+    ``aux["global_partial"].wait()`` gives the global [L, N_global, B_global]; the backward never
+    waits for the collective (N_global is static). Returns the 0-dim fp64
     loss (and an aux dict with seq_logp, n_tokens, log_z, resid, partial when ``return_aux``)."""
     N = tokens.shape[0]
     if n_seq_global is None:
@@ -259,7 +263,8 @@ def vargrad_tb_loss(logits, tokens, mask, ref_logp, log_reward, beta: float, K: 
             n_seq_global = N
     aux = {} if return_aux else None
     loss = VarGradTBLoss.apply(logits, log_z, tokens, mask, ref_logp, log_reward, float(beta), int(K),
-                               float(n_seq_global), group, dlogits_dtype, float(inv_temp), aux, peer)
+                               float(n_seq_global), group, dlogits_dtype, float(inv_temp), aux,
+                               bool(overlap_allreduce))
     return (loss, aux) if return_aux else loss
 
 
@@ -644,6 +649,8 @@ class LmHeadTBLoss(torch.autograd.Function):
         ctx.n_global, ctx.K, ctx.inv_temp, ctx.lzp, ctx.chunk_rows = n_global, K, inv_temp, lzp, chunk_rows
         if aux is not None:
             aux.update(seq_logp=o.seq_logp, n_tokens=o.n_tokens, log_z=o.log_z, resid=o.resid, partial=o.partial)
+            if pending is not None:
+                aux["global_partial"] = pending
         return o.partial[0]
 
     @staticmethod

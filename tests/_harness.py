@@ -178,6 +178,29 @@ def compare_dlogits_rows(d, w: syn.Workload, seed: int, flat_rows, row_base: int
 
 
 # --------------------------------------------------------------------------- tolerances
+def seq_tols(ell_ref, K, rel=1e-4, abs_=1e-5):
+    """Bars for log Z and the residuals, propagated from the per-sequence log-prob bar
+    (|d ell_s| <= max(rel |ell_s|, abs_), north_star): log Z_i = mean_j(rho + r/beta - ell_j) and
+    eps_s = log Z_i - delta_s are exact fp64 combinations of the ell's, so they inherit
+    |d log Z_i| <= mean_j tol(ell_j) and |d eps_s| <= tol(ell_s) + mean_j tol(ell_j)
+    (reading R23: log Z of a group can be ~0 while its ell's are ~-2000)."""
+    t = np.maximum(rel * np.abs(np.asarray(ell_ref, np.float64)), abs_)
+    tz = t.reshape(-1, K).mean(1)
+    return tz, t + np.repeat(tz, K)
+
+
+def assert_close_tol(gpu, ref, tol, what):
+    """|gpu - ref| <= tol element-wise (tol an array); returns max err / tol."""
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    tol = np.maximum(np.asarray(tol, np.float64), np.maximum(1e-4 * np.abs(ref), 1e-5))
+    bad = ~((np.abs(gpu - ref) <= tol) | (gpu == ref))
+    if bad.any():
+        i = np.flatnonzero(bad)[:5]
+        raise AssertionError(f"{what}: {bad.sum()} mismatches, e.g. idx {i}: gpu {gpu[i]} oracle {ref[i]} tol {tol[i]}")
+    return float(np.max(np.abs(gpu - ref) / tol)) if len(ref) else 0.0
+
+
 def assert_seq_close(gpu, ref, what, rel=1e-4, abs_=1e-5):
     """|gpu - ref| <= max(rel |ref|, abs_) element-wise; returns max err / tol."""
     gpu = np.asarray(gpu, np.float64)

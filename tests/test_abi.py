@@ -207,7 +207,8 @@ def test_lmhead_bwd_validation(L):
 def test_lmhead_bwd_workspace_bytes(L):
     rows, d, V, C = 65536, 3584, 152064, 16384
     b = L.tba_lmhead_bwd_workspace_bytes(64, 1024, d, V, C)
-    need = d * V * 2 + 2 * C * d * 2 + 2 * C * V * 2 + rows * 4   # W^T, Hc, Hc^T, dZ, dZ^T, row list
+    # W^T, Hc, dZ, row list (dW reads dZ and Hc as MN-major operands: no transposed copies by default)
+    need = d * V * 2 + C * d * 2 + C * V * 2 + rows * 4
     need += 4 * C * d * 4                                           # dH split-K partials (<= 4 fp32 slices)
     assert need <= b < need + 16 * 256
     # the chunk is rounded up to 128 rows and capped at the batch
@@ -238,7 +239,13 @@ def test_lmhead_fwd_bwd_validation_and_workspace(L):
     assert fb(x=_lm(hidden_stride=60)) == _lib.TBA_ERR_INVALID_ARG
     # workspace: the stored fp32 logits of one chunk (2 Qwen groups = 16384 rows) dominate
     b = L.tba_lmhead_fwd_bwd_workspace_bytes(64, 1024, 3584, 152064, 8, 0)
-    assert b >= 16384 * 152064 * 4 + 2 * 16384 * 152064 * 2
+    assert b >= 16384 * 152064 * 4 + 16384 * 152064 * 2
+    # one group larger than the 16384-row GEMM chunk (Table 5: K = 16 x T = 2048 = 32768 rows): the
+    # stored logits cover the group, every other backward buffer stays at the 16384-row chunk
+    big = L.tba_lmhead_fwd_bwd_workspace_bytes(16, 2048, 3584, 152064, 16, 0)
+    zst = 32768 * 152064 * 4
+    assert zst < big < zst + 16384 * 152064 * 2 + 3584 * 152064 * 2 + 4 * 16384 * 3584 * 4 + 16384 * 3584 * 2 + \
+        32768 * 152064 // 1024 * 16 + (1 << 24)
     assert L.tba_lmhead_fwd_bwd_workspace_bytes(64, 1024, 3584, 152064, 8, 1) < b   # one group per chunk
     assert L.tba_lmhead_fwd_bwd_workspace_bytes(9, 4, 64, 100, 4, 0) == 0          # 9 % 4 != 0
     assert L.tba_lmhead_fwd_bwd_workspace_bytes(0, 4, 64, 100, 4, 0) == 256

@@ -51,10 +51,11 @@ def check_seq_values(test, w, seed, o, g0, ng, N):
     np.testing.assert_array_equal(nt, ref["n_tok"])                       # token counts: bit-exact
     H.record(test, w.name, seed, "n_tokens (bit-exact)", len(nt), 0.0, 0.0)
     loss_g, logz_g, eps_g = O.vargrad_tb_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, K, n_global=N)
-    r = H.assert_seq_close(lz, logz_g, f"{test} log_z")
-    H.record(test, w.name, seed, "log_z", len(lz), np.max(np.abs(lz - logz_g)), r)
-    r = H.assert_seq_close(eps, eps_g, f"{test} resid")
-    H.record(test, w.name, seed, "resid", len(eps), np.max(np.abs(eps - eps_g)), r)
+    tz, te = H.seq_tols(ref["ell"], K)              # propagated from the ell bar (reading R23)
+    r = H.assert_close_tol(lz, logz_g, tz, f"{test} log_z")
+    H.record(test, w.name, seed, "log_z", len(lz), np.max(np.abs(lz - logz_g)), r, tol="propagated from ell (R23)")
+    r = H.assert_close_tol(eps, eps_g, te, f"{test} resid")
+    H.record(test, w.name, seed, "resid", len(eps), np.max(np.abs(eps - eps_g)), r, tol="propagated from ell (R23)")
     if ng * K == o.resid.shape[0]:                                        # the whole call: the loss too
         p0 = o.partial[0].item()
         r = H.assert_seq_close([p0], [loss_g], f"{test} loss")

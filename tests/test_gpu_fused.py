@@ -144,22 +144,16 @@ def test_deferred_scale_matches_oracle(name, w):
     assert torch.allclose(G2.double(), G.double(), rtol=2 ** -8, atol=1e-30)
 
 
-@pytest.mark.parametrize("cfg", ["0", "1", "2", "3", "4", "5", "6", "7"])
-def test_deferred_all_cluster_shapes(cfg, monkeypatch):
-    """Every (threads, cluster size) configuration of the deferred kernel gives the same G."""
-    monkeypatch.setenv("TBA_SINGLE_CFG", cfg)
-    w = W("redteam", B=2, K=4, T=5, len_lo=1, len_hi=5)   # odd row length, ragged
+@pytest.mark.parametrize("V", [5003, 50257, 80000])
+def test_deferred_both_row_classes(V):
+    """The deferred kernel's two row classes (<= 128 KB rows: 256 threads; longer: 512 threads with 8
+    vectors in flight) give the oracle's dlogits once the row scale is applied."""
+    w = W("redteam", B=2, K=4, T=5, V=V, len_lo=1, len_hi=5)   # ragged; odd row length at 50257
     inp = H.device_inputs(w, 2)
     o, _, G = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
                                        inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=torch.float32,
                                        check_status=True)
-    monkeypatch.setenv("TBA_SINGLE_CFG", "0")
-    o0, _, G0 = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
-                                         inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=torch.float32)
     torch.cuda.synchronize()
-    # different threads per row => different fp32 partial-sum order: equal to rounding
-    H.assert_seq_close(o.seq_logp.cpu().numpy(), o0.seq_logp.cpu().numpy(), "seq_logp", rel=1e-7, abs_=1e-7)
-    assert torch.allclose(G, G0, rtol=1e-5, atol=1e-8)
     from oracle import tba_oracle as O
     h = inp["host"]
     ref = O.vargrad_head(H.host_logits(w, 2, 0, w.B), h["tokens"], h["mask"], h["ref_logp"], h["log_reward"], w.beta,

@@ -264,22 +264,21 @@ torch.save({"dh": dh.cpu(), "dw": dw.cpu(), "ell": f.seq_logp.cpu(), "resid": o.
 
 
 def test_lmhead_bwd_pair_kernel_bitwise(tmp_path):
-    """Every kernel variant gives bitwise the single-SM results (each logit / gradient element is
-    one K-ordered fp32 accumulation whatever the tile shape): the forward on the multicast pair
-    (TBA_LM_MC=2) and the cta_group::2 pair with 256 x 256 (3) or 256 x 512 tiles (4), the backward
-    GEMMs on the pair kernel (TBA_LMB_2SM=3) with 256 x 256 or 256 x 512 tiles (TBA_LMB_NT2=3)."""
+    """Every backward GEMM kernel gives bitwise the single-SM results (each gradient element is one
+    K-ordered fp32 accumulation whatever the tile shape): the pair kernel (TBA_LMB_2SM=3) with 256 x 256
+    or 256 x 512 tiles (TBA_LMB_NT2=3), K-major or MN-major dW (TBA_LMB_DW_MN)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    # (forward kernel TBA_LM_MC, backward TBA_LMB_2SM, TBA_LMB_NT2): single-SM everywhere first
-    for cfg in (("1", "0", "0"), ("1", "3", "0"), ("1", "3", "3"), ("3", "3", "3"), ("4", "3", "3"), ("2", "0", "0")):
+    # (TBA_LMB_DW_MN, TBA_LMB_2SM, TBA_LMB_NT2): single-SM everywhere first
+    for cfg in (("0", "0", "0"), ("0", "3", "0"), ("0", "3", "3"), ("1", "3", "3"), ("1", "3", "0")):
         f = tmp_path / f"r{''.join(cfg)}.pt"
-        env = dict(os.environ, TBA_LM_MC=cfg[0], TBA_LMB_2SM=cfg[1], TBA_LMB_NT2=cfg[2], TBA_LMB_KSPLIT="1")
+        env = dict(os.environ, TBA_LMB_DW_MN=cfg[0], TBA_LMB_2SM=cfg[1], TBA_LMB_NT2=cfg[2], TBA_LMB_KSPLIT="1")
         subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env, check=True, timeout=300)
         out[cfg] = torch.load(f)
-    base = out[("1", "0", "0")]
+    base = out[("0", "0", "0")]
     for cfg, r in out.items():
         for k in base:
             assert torch.equal(base[k], r[k]), (cfg, k)

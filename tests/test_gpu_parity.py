@@ -381,20 +381,3 @@ def test_token_logprob_matches_oracle(inv_temp):
     sl, _ = tba.seq_logprob(inp["logits"], inp["tokens"], inp["mask"])
     if inv_temp == 1.0:
         H.assert_seq_close(tl.sum(1).cpu().numpy(), sl.cpu().numpy(), "sum of token log-probs", rel=1e-9, abs_=1e-9)
-
-
-def test_fused_head_option_bitwise(monkeypatch):
-    """TBA_FUSE_HEAD=1 (forward rows + sums + head in one kernel) gives the same bits."""
-    w = W("rhomath", B=3, K=4, T=9, V=4093, len_lo=0, len_hi=9)
-    inp = H.device_inputs(w, 5)
-    a, wa = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta,
-                            w.K, w.N)
-    sa, na = tba.seq_logprob(inp["logits"], inp["tokens"], inp["mask"])
-    monkeypatch.setenv("TBA_FUSE_HEAD", "1")
-    b, wb = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta,
-                            w.K, w.N)
-    sb, nb = tba.seq_logprob(inp["logits"], inp["tokens"], inp["mask"])
-    torch.cuda.synchronize()
-    for f in ("seq_logp", "n_tokens", "log_z", "resid", "partial"):
-        assert torch.equal(getattr(a, f), getattr(b, f)), f
-    assert torch.equal(sa, sb) and torch.equal(na, nb)

@@ -264,6 +264,15 @@ def test_dlogits_finite_differences(K):  # north_star / S:160: relative e
     assert rel < 1e-6, rel
 
 
+def test_grad_token_entry_confident_closed_form():
+    """The token's entry 1 - p_y of a confident row against its closed form 2 / (e^40 + 2) for
+    z = (40, 0, 0), y = 0 (8.5e-18: fp64's 1 - p_y would cancel to 0); the other entries -p_v."""
+    g = O.grad_logprob_row(np.array([40.0, 0.0, 0.0]), 0)
+    assert abs(g[0] - 2.0 / (math.exp(40.0) + 2.0)) <= 1e-13 * g[0]
+    np.testing.assert_allclose(g[1:], -1.0 / (math.exp(40.0) + 2.0), rtol=1e-13)
+    assert abs(g.sum()) <= 1e-30
+
+
 def test_dlogits_row_pins():
     """dlogits_row (the expected value of every sampled full-size row comparison): (i) central
     finite differences of the token log-prob it scales, times 2 eps g / N (App. A P:446-451);

@@ -62,5 +62,6 @@ def test_bench_uses_oracle_only_in_baseline_legs():
             for n in ast.walk(fn):
                 if isinstance(n, ast.ImportFrom) and n.module and n.module.startswith("oracle"):
                     users.add(fn.name)
-    # the two bounded-sample timers of the cpu_baseline legs / --impl reference arm
-    assert users == {"oracle_sample", "oracle_lmhead_sample"}
+    # the bounded-sample timers of the cpu_baseline legs / --impl reference arm (the multi-process
+    # pool's per-group oracle call, and the LM-head sample)
+    assert users == {"_oracle_group", "oracle_lmhead_sample"}
