@@ -43,6 +43,25 @@ cudaEvent_t* pipe_events() {
   return ev[dev];
 }
 
+// Any byte overlap between the LM-head backward's outputs (dhidden, dweight) and its inputs (hidden,
+// weight, both re-read chunk by chunk) or each other.
+bool lm_outputs_overlap(const tba_lmhead* x, const void* dh, int64_t dh_stride, int32_t dh_dt, const float* dw,
+                        int64_t dw_stride) {
+  const int64_t rows = x->n_seq * x->seq_len, d = x->d, V = x->vocab, dhe = esz_of(dh_dt);
+  auto span_hit = [](const void* a, int64_t na, int64_t sa, int64_t ea, const void* b, int64_t nb, int64_t sb,
+                     int64_t eb, int64_t cols) {
+    if (!a || !b || na <= 0 || nb <= 0) return false;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+    const uintptr_t a1 = a0 + (uintptr_t)(((na - 1) * sa + cols) * ea), b1 = b0 + (uintptr_t)(((nb - 1) * sb + cols) * eb);
+    return a0 < b1 && b0 < a1;
+  };
+  return span_hit(dh, rows, dh_stride, dhe, x->hidden, rows, x->hidden_stride, 2, d) ||
+         span_hit(dh, rows, dh_stride, dhe, x->weight, V, x->weight_stride, 2, d) ||
+         span_hit(dw, V, dw_stride, 4, x->hidden, rows, x->hidden_stride, 2, d) ||
+         span_hit(dw, V, dw_stride, 4, x->weight, V, x->weight_stride, 2, d) ||
+         span_hit(dh, rows, dh_stride, dhe, dw, V, dw_stride, 4, d);
+}
+
 }  // namespace
 
 // ================================================================================ C ABI
@@ -124,7 +143,8 @@ int tba_tb_loss_fwd(const tba_rows* x, const tba_tb_opts* opts, const double* re
   const RowScale rs = make_scale(opt_inv_temp(opts));
   const HeadArgs ha = tb_head_args(x, opts, ref_logp, log_reward, beta, K, n_seq_global, w, seq_logp, n_tokens,
                                    log_z, resid, partial);
-  if (cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
+  // the head's counter is zeroed by the forward kernel (no memset node between the PDL-chained kernels)
+  if (x->seq_len == 0 && cudaMemsetAsync(w.counter, 0, sizeof(unsigned int), s) != cudaSuccess) return TBA_ERR_CUDA;
   rc = launch_fwd_rows(x, w, rs, dev_status, s);
   if (rc) return rc;
   return launch_seq_head(true, w, x->mask, ha, s);
@@ -329,7 +349,8 @@ int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const d
   if (!partial) return TBA_ERR_INVALID_ARG;
   rc = validate_out(x, grad_unscaled, g_dtype, g_row_stride);
   if (rc) return rc;
-  if (grad_unscaled && grad_unscaled == x->logits) return TBA_ERR_INVALID_ARG;  // pass 2 re-reads the row
+  if (grad_unscaled && out_overlaps_rows(x, grad_unscaled, g_row_stride, g_dtype))
+    return TBA_ERR_INVALID_ARG;  // pass 2 re-reads the row
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (x->n_seq == 0)
     return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
@@ -395,7 +416,7 @@ static int tbap_fwd_impl(const tba_rows* x, const float* gen_logp, const double*
   if (grad_unscaled) {
     rc = validate_out(x, grad_unscaled, g_dtype, g_row_stride);
     if (rc) return rc;
-    if (grad_unscaled == x->logits) return TBA_ERR_INVALID_ARG;
+    if (out_overlaps_rows(x, grad_unscaled, g_row_stride, g_dtype)) return TBA_ERR_INVALID_ARG;
     rc = launch_single(x, w, make_scale(1.0), dev_status, grad_unscaled, g_dtype, g_row_stride, s);
   } else {
     rc = launch_fwd_rows(x, w, make_scale(1.0), dev_status, s);
@@ -566,9 +587,10 @@ static int lmhead_bwd_impl(const tba_lmhead* x, const void* workspace, const dou
     if (dh_dtype != TBA_BF16 && dh_dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
     if (dh_stride < x->d || reinterpret_cast<uintptr_t>(dhidden) % (dh_dtype == TBA_BF16 ? 2 : 4))
       return TBA_ERR_INVALID_ARG;
-    if (dhidden == x->hidden) return TBA_ERR_INVALID_ARG;  // hidden is re-read chunk by chunk
   }
   if (dweight && (dw_stride < x->d || reinterpret_cast<uintptr_t>(dweight) % 4)) return TBA_ERR_INVALID_ARG;
+  if (lm_outputs_overlap(x, dhidden, dh_stride, dh_dtype, dweight, dw_stride))
+    return TBA_ERR_INVALID_ARG;  // hidden and the weight are re-read chunk by chunk
   const int64_t rows = x->n_seq * x->seq_len;
   if (!dhidden && !dweight) return TBA_OK;
   if (rows > 0) {
@@ -644,11 +666,12 @@ int tba_lmhead_tb_loss_fwd_bwd(const tba_lmhead* x, const tba_tb_opts* opts, con
   if (!std::isfinite(grad_scale) || !partial) return TBA_ERR_INVALID_ARG;
   if (dhidden) {
     if (dhidden_dtype != TBA_BF16 && dhidden_dtype != TBA_FP32) return TBA_ERR_INVALID_ARG;
-    if (dhidden_row_stride < x->d || reinterpret_cast<uintptr_t>(dhidden) % (dhidden_dtype == TBA_BF16 ? 2 : 4) ||
-        dhidden == x->hidden)
+    if (dhidden_row_stride < x->d || reinterpret_cast<uintptr_t>(dhidden) % (dhidden_dtype == TBA_BF16 ? 2 : 4))
       return TBA_ERR_INVALID_ARG;
   }
   if (dweight && (dweight_row_stride < x->d || reinterpret_cast<uintptr_t>(dweight) % 4)) return TBA_ERR_INVALID_ARG;
+  if (lm_outputs_overlap(x, dhidden, dhidden_row_stride, dhidden_dtype, dweight, dweight_row_stride))
+    return TBA_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (x->n_seq == 0 || x->seq_len == 0) {  // no rows: the two calls handle these shapes
     rc = tba_lmhead_tb_loss_fwd(x, opts, ref_logp, log_reward, beta, K, n_seq_global, workspace, seq_logp, n_tokens,

@@ -14,6 +14,8 @@ __global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int
                                                double grad_scale, const double* __restrict__ grad_out, RowScale rs,
                                                TO* __restrict__ dlogits, int64_t ostride) {
   constexpr int RPC = 256 / TPR;
+  pdl_trigger();
+  pdl_wait();
   const int64_t row = (int64_t)blockIdx.x * RPC + threadIdx.x / TPR;
   if (row >= rows) return;
   const int tid = threadIdx.x % TPR;
@@ -35,7 +37,7 @@ __global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int
 
 // ------------------------------------------------------------------------------ launch
 template <class T, class TO, bool PER_ROW>
-void launch_bwd_t(const tba_rows* x, const float2* stats, const float* qy, const double* resid, const float* coef,
+int launch_bwd_t(const tba_rows* x, const float2* stats, const float* qy, const double* resid, const float* coef,
                   double gs,
                   const double* go, const RowScale& rs, TO* out, int64_t ostride, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
@@ -43,9 +45,9 @@ void launch_bwd_t(const tba_rows* x, const float2* stats, const float* qy, const
   const int64_t rpc = 256 / tpr;
   const unsigned grid = (unsigned)((rows + rpc - 1) / rpc);
   auto lg = static_cast<const T*>(x->logits);
-#define TBA_BWD(TPR_)                                                                                              \
-  row_bwd<T, TO, TPR_, kU, PER_ROW><<<grid, 256, 0, s>>>(lg, rows, x->seq_len, x->vocab, x->row_stride, x->tokens, \
-                                                        x->mask, stats, qy, resid, coef, gs, go, rs, out, ostride)
+#define TBA_BWD(TPR_)                                                                                             \
+  return launch_pdl(row_bwd<T, TO, TPR_, kU, PER_ROW>, dim3(grid), dim3(256), 0, s, lg, rows, x->seq_len, x->vocab, \
+                    x->row_stride, x->tokens, x->mask, stats, qy, resid, coef, gs, go, rs, out, ostride)
   if (tpr == 32) TBA_BWD(32);
   else TBA_BWD(256);
 #undef TBA_BWD
@@ -58,18 +60,16 @@ int launch_bwd_dt(const tba_rows* x, const float2* stats, const float* qy, const
   if (x->n_seq * x->seq_len == 0) return TBA_OK;
   if (x->dtype == TBA_BF16) {
     if (odt == TBA_BF16)
-      launch_bwd_t<uint16_t, uint16_t, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits),
-                                                ostride, s);
-    else
-      launch_bwd_t<uint16_t, float, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
-  } else {
-    if (odt == TBA_BF16)
-      launch_bwd_t<float, uint16_t, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits), ostride,
-                                             s);
-    else
-      launch_bwd_t<float, float, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs, static_cast<float*>(dlogits), ostride, s);
+      return launch_bwd_t<uint16_t, uint16_t, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs,
+                                                       static_cast<uint16_t*>(dlogits), ostride, s);
+    return launch_bwd_t<uint16_t, float, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs, static_cast<float*>(dlogits),
+                                                  ostride, s);
   }
-  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  if (odt == TBA_BF16)
+    return launch_bwd_t<float, uint16_t, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs, static_cast<uint16_t*>(dlogits),
+                                                  ostride, s);
+  return launch_bwd_t<float, float, PER_ROW>(x, stats, qy, resid, coef, gs, go, rs, static_cast<float*>(dlogits),
+                                             ostride, s);
 }
 
 }  // namespace

@@ -90,14 +90,12 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   if (threadIdx.x == 0) {
     const int64_t y = sh_y;
     const bool ok = (y >= 0 && y < V);
-    if (rank == 0) {
-      const float zy = ok ? Elem<T>::load1(rp + y) : 0.f;
-      finalize_row(M, M2, S, zy, ok, row, rs, stats, qy, lp, dev_status);
-    }
-    const double ey = ok ? exp2((double)Elem<T>::load1(rp + y) * (double)rs.sc - (double)M2) : 0.0;
-    sh_M2 = M2;
-    sh_L2S = (float)log2(S + ey);
-    sh_qy = (float)(S / (S + ey));
+    const float zy = ok ? Elem<T>::load1(rp + y) : 0.f;
+    finalize_row(M, M2, S, zy, ok, row, rs, stats, qy, lp, dev_status);  // CS == 1: this CTA owns the row
+    const float2 st2 = stats[row];  // written just above by this thread
+    sh_M2 = st2.x;
+    sh_L2S = st2.y;
+    sh_qy = qy[row];
   }
   __syncthreads();
   bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,

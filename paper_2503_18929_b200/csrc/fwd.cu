@@ -10,10 +10,15 @@ __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits
                                                      int64_t stride, const int64_t* __restrict__ tokens,
                                                      const uint8_t* __restrict__ mask, RowScale rs,
                                                      float2* __restrict__ stats, float* __restrict__ qy,
-                                                     double* __restrict__ lp, int32_t* dev_status) {
+                                                     double* __restrict__ lp, int32_t* dev_status,
+                                                     unsigned int* zero_counter) {
   constexpr int RPC = 256 / TPR, WPRS = TPR / 32 > 0 ? TPR / 32 : 1;
   __shared__ float sm_m[RPC][WPRS], sm_M2[RPC][WPRS];
   __shared__ double sm_s[RPC][WPRS];
+  pdl_trigger();
+  pdl_wait();
+  // the head's last-CTA counter (read only by the next kernel, after this grid completes)
+  if (zero_counter && blockIdx.x == 0 && threadIdx.x == 0) *zero_counter = 0u;
   const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
   const int64_t row = (int64_t)blockIdx.x * RPC + grp;
   if (row >= rows || mask[row] == 0) return;
@@ -22,23 +27,19 @@ __global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits
 }
 
 template <class T>
-void launch_fwd_rows_t(const T* lg, const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
+int launch_fwd_rows_t(const T* lg, const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
                        cudaStream_t s, int tpr) {
   const int64_t rows = x->n_seq * x->seq_len;
   const int64_t rpc = 256 / tpr;
   const unsigned grid = (unsigned)((rows + rpc - 1) / rpc);
-#define TBA_ROWS(TPR_)                                                                                               \
-  row_fwd_rows<T, TPR_, kU><<<grid, 256, 0, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, \
-                                                 w.qy, w.lp, dev_status)
+#define TBA_ROWS(TPR_, NP_)                                                                                     \
+  return launch_pdl(row_fwd_rows<T, TPR_, kU, NP_>, dim3(grid), dim3(256), 0, s, lg, rows, x->vocab, x->row_stride, \
+                    x->tokens, x->mask, rs, w.stats, w.qy, w.lp, dev_status, w.counter)
   // 64 threads per row: 1 of the 4 element pairs per 16-byte vector takes the FMA-pipe exp2
   // (exp2_poly2) instead of MUFU — relieves the XU pipe (75 % busy), +3 % forward bandwidth on
   // every BASELINE shape; 2 of 4 over-loads the FMA/ALU pipes.
-  if (tpr == 64) {
-    row_fwd_rows<T, 64, kU, 1><<<grid, 256, 0, s>>>(lg, rows, x->vocab, x->row_stride, x->tokens, x->mask, rs,
-                                                    w.stats, w.qy, w.lp, dev_status);
-    return;
-  }
-  TBA_ROWS(32);
+  if (tpr == 64) TBA_ROWS(64, 1);
+  TBA_ROWS(32, 0);
 #undef TBA_ROWS
 }
 
@@ -49,9 +50,9 @@ int launch_fwd_rows(const tba_rows* x, const WsLayout& w, const RowScale& rs, in
   if (rows == 0) return TBA_OK;
   const int64_t esz = x->dtype == TBA_BF16 ? 2 : 4;
   const int tpr = fwd_tpr(x->vocab, esz);
-  if (x->dtype == TBA_BF16) launch_fwd_rows_t<uint16_t>(static_cast<const uint16_t*>(x->logits), x, w, rs, dev_status, s, tpr);
-  else launch_fwd_rows_t<float>(static_cast<const float*>(x->logits), x, w, rs, dev_status, s, tpr);
-  return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+  return x->dtype == TBA_BF16
+             ? launch_fwd_rows_t<uint16_t>(static_cast<const uint16_t*>(x->logits), x, w, rs, dev_status, s, tpr)
+             : launch_fwd_rows_t<float>(static_cast<const float*>(x->logits), x, w, rs, dev_status, s, tpr);
 }
 
 }  // namespace tba

@@ -19,6 +19,8 @@ __global__ void __launch_bounds__(1024) seq_head(const double* __restrict__ lp, 
                                                 double* __restrict__ partial, unsigned int* counter) {
   const int per = HEAD ? K : 8;
   const int64_t s0 = (int64_t)blockIdx.x * per;
+  pdl_trigger();
+  pdl_wait();
   seq_sums(lp, mask, n_seq, T, s0, per, seq_logp, n_tokens, nullptr);
   if (!HEAD) return;
   __syncthreads();
@@ -158,15 +160,14 @@ int launch_seq_head(bool head, const WsLayout& w, const uint8_t* mask, const Hea
   if (head) {
     // one warp per sequence of the group (K > 8: more than one round of 8 warps otherwise)
     const int threads = ha.K <= 8 ? 256 : (ha.K >= 32 ? 1024 : 32 * ha.K);
-    seq_head<true><<<(unsigned)(ha.n_seq / ha.K), threads, 0, s>>>(
-        w.lp, mask, ha.n_seq, ha.T, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.inv_n_global,
-        ha.seq_logp, ha.n_tokens, ha.log_z, ha.resid, w.group_sq, ha.partial, w.counter);
-  } else {
-    seq_head<false><<<(unsigned)((ha.n_seq + 7) / 8), 256, 0, s>>>(
-        w.lp, mask, ha.n_seq, ha.T, 8, nullptr, nullptr, nullptr, 0.0, 0.0, ha.seq_logp, ha.n_tokens, nullptr,
-        nullptr, nullptr, nullptr, nullptr);
+    return launch_pdl(seq_head<true>, dim3((unsigned)(ha.n_seq / ha.K)), dim3(threads), 0, s, w.lp, mask, ha.n_seq,
+                      ha.T, ha.K, ha.ref_logp, ha.log_reward, ha.log_z_param, ha.inv_beta, ha.inv_n_global,
+                      ha.seq_logp, ha.n_tokens, ha.log_z, ha.resid, w.group_sq, ha.partial, w.counter);
   }
-  return launch_status();
+  return launch_pdl(seq_head<false>, dim3((unsigned)((ha.n_seq + 7) / 8)), dim3(256), 0, s, w.lp, mask, ha.n_seq,
+                    ha.T, 8, (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, 0.0, 0.0,
+                    ha.seq_logp, ha.n_tokens, (double*)nullptr, (double*)nullptr, (double*)nullptr, (double*)nullptr,
+                    (unsigned int*)nullptr);
 }
 
 int launch_tbap_head(const WsLayout& w, const uint8_t* mask, const float* gen_logp, int64_t n_seq, int64_t T, int K,

@@ -8,6 +8,14 @@
 namespace tba {
 namespace {
 // ------------------------------------------------------------------------------ PTX helpers
+// Programmatic dependent launch (PDL): kernels of the path are launched with the programmatic
+// stream-serialisation attribute (launch_pdl). Each one first lets its dependents launch (they are
+// scheduled into the SMs its last wave frees, instead of after a drain and a launch gap), then waits
+// until the previous kernel in the stream has completed and its writes are visible. Both are no-ops
+// for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -189,13 +197,23 @@ __device__ __forceinline__ void finalize_row(float M, float M2, double Sx, float
                                              const RowScale& rs, float2* __restrict__ stats,
                                              float* __restrict__ qy, double* __restrict__ lp,
                                              int32_t* dev_status) {
-  const double ey = tok_ok ? exp2((double)zy * (double)rs.sc - (double)M2) : 0.0;
-  const double S = Sx + ey;
-  const bool finite = (M > -INFINITY) && (M < INFINITY) && (S > 0.0) && (S < INFINITY);
-  const double log2s = log2(S);
+  // log2 of the token's term and of the others' sum; everything below stays in the log domain, so
+  // neither a confident token (p_y -> 1) nor a hopeless one (e_y below fp64's range) loses accuracy
+  const double xy = tok_ok ? (double)zy * (double)rs.sc - (double)M2 : -INFINITY;   // exact in fp64
+  const double lx = log2(Sx);                                                     // -inf if Sx = 0
+  const double d = xy - lx;                                                       // log2(e_y / Sx)
+  const double t = exp2(-fabs(d));                                                // in [0, 1]
+  const double log2s = fmax(xy, lx) + log1p(t) * 1.4426950408889634;               // log2(Sx + e_y)
+  const double q = d > 0.0 ? t / (1.0 + t) : 1.0 / (1.0 + t);                     // 1 - p_y = Sx / S
+  // lp = a (z_y - M) - ln2 (log2 S + M2 - M sc), with log2 S + M2 - M sc written so that the
+  // exact (z_y - M) sc cancels: p_y -> 1 gives (z_y - M)(a - ln2 sc) - log1p(Sx / e_y)
+  double v = d > 0.0 ? ((double)zy - (double)M) * (rs.inv_temp - kLN2 * (double)rs.sc) - log1p(t)
+                     : rs.inv_temp * ((double)zy - (double)M) - kLN2 * (lx + (double)M2 - (double)M * (double)rs.sc) -
+                           log1p(t);
+  if (xy == -INFINITY) v = -INFINITY;
+  const bool finite = (M > -INFINITY) && (M < INFINITY) && (log2s > -INFINITY) && (log2s < INFINITY);
   stats[row] = make_float2(M2, (float)log2s);
-  qy[row] = (float)(Sx / S);  // 1 - p_y
-  double v = ey > 0.0 ? ((double)zy - (double)M) * (rs.inv_temp - kLN2 * (double)rs.sc) - log1p(Sx / ey) : -INFINITY;
+  qy[row] = (float)q;
   if (!tok_ok) v = nan("");
   lp[row] = v;
   if (dev_status) {
@@ -207,7 +225,7 @@ __device__ __forceinline__ void finalize_row(float M, float M2, double Sx, float
 // Consume U 16-byte vectors of one row: chunk max, rare re-base, sum of 2^x (FFMA2 + MUFU + FADD2),
 // fp32 pair accumulators (<= 4U terms each) folded into the fp64 partial once per call.
 // NP of the VEC/2 element pairs of every vector take the FMA-pipe exp2 instead of MUFU.
-template <class T, int U, int NP = 0>
+template <class T, int U, int NP = 0, bool EXCL = false>
 __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st, int uy = -1, int ey = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
@@ -222,7 +240,7 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 #pragma unroll
     for (int e = 0; e < VEC; e += 2) cm = fmaxf(cm, fmaxf(z[u][e], z[u][e + 1]));
   st.chunk(cm);
-  if ((unsigned)uy < (unsigned)U) {  // the sampled token's element (vector uy, slot ey): in the max, not the sum
+  if (EXCL) {  // the sampled token's element (vector uy, slot ey): in the max, not the sum
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -290,11 +308,15 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 #pragma unroll
     for (int u = 0; u < U; ++u)
       v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
-    fwd_consume<T, U, NP>(v, st, du, ey);
+    // the (rare) iteration holding the token's vector runs a separate copy of the consume: a branch,
+    // not per-element selects in the hot loop
+    if ((unsigned)du < (unsigned)U) fwd_consume<T, U, NP, true>(v, st, du, ey);
+    else fwd_consume<T, U, NP>(v, st);
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
-    fwd_consume<T, 1>(v1, st, k == ky ? 0 : -1, ey);
+    if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
+    else fwd_consume<T, 1>(v1, st);
   }
 }
 

@@ -166,6 +166,19 @@ inline int validate_rows(const tba_rows* x) {
   return TBA_OK;
 }
 
+inline int64_t esz_of(int32_t dt) { return dt == TBA_BF16 ? 2 : 4; }
+
+// Do [a, a + span_a) and [b, b + span_b) intersect, each the bytes of `rows` rows of `vocab`
+// elements at the given row stride (the last row ends at its vocab-th element)?
+inline bool ranges_overlap(const void* a, int64_t rows, int64_t a_stride, int64_t vocab, int64_t a_esz, const void* b,
+                           int64_t b_stride, int64_t b_esz) {
+  if (rows <= 0) return false;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  const uintptr_t a1 = a0 + (uintptr_t)(((rows - 1) * a_stride + vocab) * a_esz);
+  const uintptr_t b1 = b0 + (uintptr_t)(((rows - 1) * b_stride + vocab) * b_esz);
+  return a0 < b1 && b0 < a1;
+}
+
 inline int validate_out(const tba_rows* x, const void* dlogits, int32_t odt, int64_t ostride) {
   if (odt != TBA_BF16 && odt != TBA_FP32) return TBA_ERR_INVALID_ARG;
   if (ostride < x->vocab) return TBA_ERR_INVALID_ARG;
@@ -174,9 +187,21 @@ inline int validate_out(const tba_rows* x, const void* dlogits, int32_t odt, int
   const int64_t oesz = odt == TBA_BF16 ? 2 : 4;
   if (ostride > INT64_MAX / 8 / oesz / rows) return TBA_ERR_INVALID_ARG;
   if (!dlogits || reinterpret_cast<uintptr_t>(dlogits) % oesz) return TBA_ERR_INVALID_ARG;
-  if (dlogits == x->logits && (odt != x->dtype || ostride != x->row_stride))
-    return TBA_ERR_INVALID_ARG;  // aliasing is only supported element-for-element
+  // Aliasing: only element-for-element (same base, dtype and row stride); any other overlap of the
+  // two byte ranges would let one row's writes clobber logits another thread still reads.
+  if (dlogits == x->logits) {
+    if (odt != x->dtype || ostride != x->row_stride) return TBA_ERR_INVALID_ARG;
+  } else if (ranges_overlap(x->logits, rows, x->row_stride, x->vocab, esz_of(x->dtype), dlogits, ostride, oesz)) {
+    return TBA_ERR_INVALID_ARG;
+  }
   return TBA_OK;
+}
+
+// The output of a row pass that re-reads its rows (deferred scale) may not overlap them at all.
+inline bool out_overlaps_rows(const tba_rows* x, const void* out, int64_t ostride, int32_t odt) {
+  const int64_t rows = x->n_seq * x->seq_len;
+  return rows > 0 && ranges_overlap(x->logits, rows, x->row_stride, x->vocab, esz_of(x->dtype), out, ostride,
+                                    odt == TBA_BF16 ? 2 : 4);
 }
 
 inline int device_sms() {
@@ -266,6 +291,23 @@ inline int check_opts(const tba_tb_opts* o) {
 inline double opt_inv_temp(const tba_tb_opts* o) { return o ? o->inv_temp : 1.0; }
 
 inline int launch_status() { return cudaGetLastError() == cudaSuccess ? TBA_OK : TBA_ERR_CUDA; }
+
+// Launch with programmatic dependent launch (see pdl_trigger / pdl_wait in tba_device.cuh): the
+// kernel may be scheduled before the previous kernel in `s` finishes and waits for it on the device.
+template <class... KArgs, class... Args>
+inline int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
+}
 
 // ------------------------------------------------------------------------------ launchers
 // Defined in the kernel TUs; each returns a TBA_* status (launch errors included).

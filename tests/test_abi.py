@@ -112,6 +112,14 @@ def test_bwd_arg_errors(L):
     assert bwd(out=FAKE + 1) == _lib.TBA_ERR_INVALID_ARG
     assert bwd(out=FAKE, dt=1) == _lib.TBA_ERR_INVALID_ARG      # aliasing with a different dtype
     assert bwd(out=FAKE, ors=128) == _lib.TBA_ERR_INVALID_ARG   # aliasing with a different stride
+    # partial overlap: dlogits starting two rows into the logits, or ending inside them
+    rows = x.n_seq * x.seq_len
+    assert bwd(out=FAKE + 2 * 100 * 2) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(out=FAKE - (rows - 1) * 100 * 2) == _lib.TBA_ERR_INVALID_ARG
+    assert bwd(out=FAKE + 2, ors=100) == _lib.TBA_ERR_INVALID_ARG
+    # disjoint ranges pass validation (then fail only at the launch on this GPU-less host)
+    far = FAKE + rows * 100 * 2 + 0x10000
+    assert bwd(out=far) != _lib.TBA_ERR_INVALID_ARG
 
 
 def test_empty_batch_is_ok_without_gpu_work(L):
