@@ -75,6 +75,23 @@ def build(force: bool = False, verbose: bool = False) -> dict:
     return out
 
 
+def build_variant(name: str, defines, out_root: str = "/tmp/tba_variants", verbose: bool = False) -> str:
+    """A/B builds (developer tool, never the product): libtba.so compiled with extra -D defines into
+    out_root/name/; load one with TBA_LIBRARY=<path> (paper_2503_18929_b200._lib)."""
+    srcs, _, _ = TARGETS["tba"]
+    objdir = os.path.join(out_root, name, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    lib = os.path.join(out_root, name, "libtba.so")
+    flags = [f"-D{d}" for d in defines]
+    objs = [os.path.join(objdir, os.path.splitext(os.path.basename(s_))[0] + ".o") for s_ in srcs]
+    jobs = [([nvcc(), *ARCH, *CFLAGS, *flags, "-c", "-o", o, s_], s_) for s_, o in zip(srcs, objs)]
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(_run, c, w, verbose) for c, w in jobs]:
+            f.result()
+    _run([nvcc(), *ARCH, *LDFLAGS, "-o", lib, *objs], name + " (link)", verbose)
+    return lib
+
+
 def build_c_example(out: str | None = None) -> str:
     """Compile examples/c_abi_example.c against include/tba.h and libtba.so (plain C + CUDA runtime)."""
     build()

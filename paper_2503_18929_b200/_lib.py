@@ -10,7 +10,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtba.so")
+# TBA_LIBRARY: load an A/B build of the same library instead (developer switch, _build.build_variant)
+LIB_PATH = os.environ.get("TBA_LIBRARY") or os.path.join(_HERE, "libtba.so")
 
 TBA_OK, TBA_ERR_INVALID_ARG, TBA_ERR_INVALID_CONFIG, TBA_ERR_CUDA = 0, 1, 2, 3
 TBA_DEV_TOKEN_RANGE, TBA_DEV_NONFINITE_ROW = 1, 2

@@ -13,7 +13,11 @@ namespace {
 // scheduled into the SMs its last wave frees, instead of after a drain and a launch gap), then waits
 // until the previous kernel in the stream has completed and its writes are visible. Both are no-ops
 // for a kernel launched without the attribute.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+#ifndef TBA_AB_NO_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -193,10 +197,8 @@ __device__ __forceinline__ void combine_lanes(float m, float R2, double s, bool 
 //   lp = log p_y = (z_y - M)(a - ln2 sc) - log1p(Sx / e_y)
 // keep full relative accuracy when p_y -> 1 (a confident token: 1 - p_y far below fp32's epsilon,
 // where sum-then-subtract would cancel). a = inv_temp; sc = fl(log2(e) a) (§5.1).
-__device__ __forceinline__ void finalize_row(float M, float M2, double Sx, float zy, bool tok_ok, int64_t row,
-                                             const RowScale& rs, float2* __restrict__ stats,
-                                             float* __restrict__ qy, double* __restrict__ lp,
-                                             int32_t* dev_status) {
+__device__ __forceinline__ void row_stats(float M, float M2, double Sx, float zy, bool tok_ok, const RowScale& rs,
+                                          float2& stats, float& qy, double& lpv) {
   // log2 of the token's term and of the others' sum; everything below stays in the log domain, so
   // neither a confident token (p_y -> 1) nor a hopeless one (e_y below fp64's range) loses accuracy
   const double xy = tok_ok ? (double)zy * (double)rs.sc - (double)M2 : -INFINITY;   // exact in fp64
@@ -211,10 +213,23 @@ __device__ __forceinline__ void finalize_row(float M, float M2, double Sx, float
                      : rs.inv_temp * ((double)zy - (double)M) - kLN2 * (lx + (double)M2 - (double)M * (double)rs.sc) -
                            log1p(t);
   if (xy == -INFINITY) v = -INFINITY;
-  const bool finite = (M > -INFINITY) && (M < INFINITY) && (log2s > -INFINITY) && (log2s < INFINITY);
-  stats[row] = make_float2(M2, (float)log2s);
-  qy[row] = (float)q;
   if (!tok_ok) v = nan("");
+  stats = make_float2(M2, (float)log2s);
+  qy = (float)q;
+  lpv = v;
+}
+
+__device__ __forceinline__ void finalize_row(float M, float M2, double Sx, float zy, bool tok_ok, int64_t row,
+                                             const RowScale& rs, float2* __restrict__ stats,
+                                             float* __restrict__ qy, double* __restrict__ lp,
+                                             int32_t* dev_status) {
+  float2 st;
+  float q;
+  double v;
+  row_stats(M, M2, Sx, zy, tok_ok, rs, st, q, v);
+  const bool finite = (M > -INFINITY) && (M < INFINITY) && (st.y > -INFINITY) && (st.y < INFINITY);
+  stats[row] = st;
+  qy[row] = q;
   lp[row] = v;
   if (dev_status) {
     int f = (tok_ok ? 0 : TBA_DEV_TOKEN_RANGE) | (finite ? 0 : TBA_DEV_NONFINITE_ROW);
@@ -310,8 +325,12 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
       v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
     // the (rare) iteration holding the token's vector runs a separate copy of the consume: a branch,
     // not per-element selects in the hot loop
+#ifdef TBA_AB_NO_EXCL
+    fwd_consume<T, U, NP>(v, st);
+#else
     if ((unsigned)du < (unsigned)U) fwd_consume<T, U, NP, true>(v, st, du, ey);
     else fwd_consume<T, U, NP>(v, st);
+#endif
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
