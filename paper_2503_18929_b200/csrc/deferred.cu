@@ -456,7 +456,11 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
                   void* grad_unscaled, int32_t g_dtype, int64_t g_row_stride, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
+#ifdef TBA_AB_DEFER_L2
+  const int cs = 0;
+#else
   const int cs = smem_cluster_size(x, grad_unscaled, g_dtype, g_row_stride);
+#endif
   if (cs > 0) {
     DsArgs a{x->logits, grad_unscaled, x->tokens, x->mask, w.stats, w.qy, w.lp, dev_status, nullptr, rows,
              x->vocab, x->row_stride, g_row_stride, rs};

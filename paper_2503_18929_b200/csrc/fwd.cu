@@ -6,7 +6,7 @@ namespace {
 // TPR threads per row, 256/TPR rows per CTA (TPR = 32 ... 256). Each row group meets on its own
 // named barrier (ids 1..8); a masked row's group exits as a whole.
 template <class T, int TPR, int U, int NP = 0>
-__global__ void __launch_bounds__(256) row_fwd_rows(const T* __restrict__ logits, int64_t rows, int64_t V,
+__global__ void __launch_bounds__(256, 4) row_fwd_rows(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                      int64_t stride, const int64_t* __restrict__ tokens,
                                                      const uint8_t* __restrict__ mask, RowScale rs,
                                                      float2* __restrict__ stats, float* __restrict__ qy,

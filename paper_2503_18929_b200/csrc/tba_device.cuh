@@ -255,7 +255,7 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 #pragma unroll
     for (int e = 0; e < VEC; e += 2) cm = fmaxf(cm, fmaxf(z[u][e], z[u][e + 1]));
   st.chunk(cm);
-  if (EXCL) {  // the sampled token's element (vector uy, slot ey): in the max, not the sum
+  if (EXCL && uy >= 0) {  // the sampled token's element (vector uy, slot ey): in the max, not the sum
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -309,26 +309,27 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
     if (i == y) st.add1_excl(z);
     else st.add1(z);
   }
-  // The token's vector ky (row vectors < 2^28: 32-bit) is this thread's vector number jy =
-  // (ky - tid) / nthr when ky = tid mod nthr; du counts down to it by U per iteration.
+  // The token's vector ky (row vectors < 2^28: 32-bit) is vector round jy = ky / nthr of thread
+  // ky % nthr, i.e. main-loop iteration ity = jy / U — the same for every thread of the row, so the
+  // slow copy of the consume step is taken by the whole row group in one iteration (a uniform
+  // branch); inside it only the owning thread masks the element.
   const int ky = (y >= h && y < tail0) ? (int)((y - h) / VEC) : -1;
   const int ey = ky >= 0 ? (int)((y - h) - (int64_t)ky * VEC) : 0;
-  int du = (ky >= tid && (ky - tid) % nthr == 0) ? (ky - tid) / nthr : -(1 << 30);
+  const int ity = ky >= 0 ? ky / nthr / U : -1;
+  const int uy = (ky >= 0 && ky % nthr == tid) ? (ky / nthr) % U : -1;
   const uint4* vp = reinterpret_cast<const uint4*>(row + h);
   const int64_t step = (int64_t)nthr * U;
   const int nfull = (int)(nvec / step);
   int64_t k0 = tid;
-  for (int it = 0; it < nfull; ++it, k0 += step, du -= U) {
+  for (int it = 0; it < nfull; ++it, k0 += step) {
     uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
       v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
-    // the (rare) iteration holding the token's vector runs a separate copy of the consume: a branch,
-    // not per-element selects in the hot loop
 #ifdef TBA_AB_NO_EXCL
     fwd_consume<T, U, NP>(v, st);
 #else
-    if ((unsigned)du < (unsigned)U) fwd_consume<T, U, NP, true>(v, st, du, ey);
+    if (it == ity) fwd_consume<T, U, NP, true>(v, st, uy, ey);
     else fwd_consume<T, U, NP>(v, st);
 #endif
   }

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2503_18929_b200.dist import group_range, token_balanced_ranges
+from paper_2503_18929_b200.dist import allreduce_partial_async, group_range, token_balanced_ranges
 
 
 def _free_port():
@@ -47,7 +47,9 @@ def _worker(rank, world, port, B, K, out_q):
     else:  # a rank with zero groups contributes zero partials
         part, d = np.zeros(3), np.zeros((0, 3, 7))
     t = torch.tensor(part, dtype=torch.float64)
+    pend = allreduce_partial_async(t, dist.group.WORLD)  # the side-stream form (CPU: in place)
     dist.all_reduce(t)  # the path's only collective
+    assert torch.equal(pend.wait(), t)
     out_q.put((rank, g0, g1, t.numpy().copy(), d))
     dist.barrier()
     dist.destroy_process_group()

@@ -125,6 +125,8 @@ def _run(z, tokens, mask, ref, rew, beta, dtype, out_dtype, test, what):
             if od == "bf16":
                 rb = O.round_bf16(r["dlogits"][s, t])
                 ratio = np.abs(dd[s, t] - rb) / O.bf16_ulp(rb)
+                ftz = 2.0 ** -126 * max(1.0, abs(c))
+                ratio[(np.abs(dd[s, t]) < ftz) & (np.abs(rb) < ftz)] = 0.0
             else:
                 ratio = np.abs(dd[s, t] - r["dlogits"][s, t]) / (2e-6 * max(1.0, abs(c)))
             worst_ratio = max(worst_ratio, float(ratio.max()))
