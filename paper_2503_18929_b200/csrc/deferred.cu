@@ -129,11 +129,11 @@ __global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, 
 //     the SAME tiles in shared memory: G = inv_temp (1[v=y] - softmax), 16-byte streaming stores.
 // Rows whose output is not 16-byte aligned at the input's element offset, or whose part would not
 // fit the ring, use row_single1 (above).
-constexpr int DS_TILE = 8192;   // bytes per slot = one bulk copy
-constexpr int DS_SLOTS = 27;    // 216 KB ring
+constexpr int DS_TILE = 16384;  // bytes per slot = one bulk copy
+constexpr int DS_SLOTS = 13;    // 208 KB ring
 constexpr int DS_NCW = 16;      // consumer warps
 constexpr int DS_THREADS = (DS_NCW + 1) * 32;
-constexpr int DS_LOOKAHEAD = 4;  // slots a part leaves free at least
+constexpr int DS_LOOKAHEAD = 3;  // slots a part leaves free at least
 constexpr size_t DS_SMEM = (size_t)DS_SLOTS * DS_TILE;
 
 struct DsArgs {
@@ -289,13 +289,22 @@ __global__ void __launch_bounds__(DS_THREADS, 1) row_smem(DsArgs a) {
       for (int64_t t0 = 0; t0 < nvp; t0 += TV) {
         mbar_wait(&full[slot], phase);
         const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)slot * DS_TILE);
+        if (t0 + TV <= nvp) {  // a full tile: U vectors per thread, one consume step
+          uint4 v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t k = t0 + ct + u * NC;  // vector within the part
-          if (k < nvp) {
-            uint4 v1[1] = {sv[ct + u * NC]};
-            if (q.v0 + k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
-            else fwd_consume<T, 1>(v1, st);
+          for (int u = 0; u < U; ++u) v[u] = sv[ct + u * NC];
+          const int64_t kr = ky - q.v0 - t0 - ct;  // the token's vector relative to this thread's first
+          if (kr >= 0 && kr < (int64_t)U * NC && kr % NC == 0) fwd_consume<T, U, 1, true>(v, st, (int)(kr / NC), ey);
+          else fwd_consume<T, U, 1>(v, st);
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t k = t0 + ct + u * NC;  // vector within the part
+            if (k < nvp) {
+              uint4 v1[1] = {sv[ct + u * NC]};
+              if (q.v0 + k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
+              else fwd_consume<T, 1>(v1, st);
+            }
           }
         }
         if (++slot == DS_SLOTS) {

@@ -92,7 +92,7 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
 // 2^x for a pair of fp32 on the FMA pipe (offloads MUFU.EX2, which the forward saturates first):
 // Cody-Waite split x = n + f, |f| <= 1/2, by the 1.5*2^23 rounding trick; degree-5 minimax
 // polynomial for 2^f (max relative error 2.3e-7 with fp32 Horner, the order of ex2.approx);
-// 2^n added to the exponent field. Inputs clamped at -125 (ex2.approx.ftz flushes there too).
+// 2^n added to the exponent field. Inputs below -125 give +0 (ex2.approx.ftz flushes below -126).
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   float a, b;
   f2_unpack(x, a, b);
@@ -109,8 +109,11 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   uint32_t plo, phi, tlo, thi;
   asm("mov.b64 {%0, %1}, %2;" : "=r"(plo), "=r"(phi) : "l"(p));
   asm("mov.b64 {%0, %1}, %2;" : "=r"(tlo), "=r"(thi) : "l"(t));
+  // below -125 the result is flushed to +0, as ex2.approx.ftz does below -126 (the clamp alone would
+  // leave a floor of 2^-125 per element: a confident row's 1 - p_y would never fall below ~V 2^-127)
+  const uint32_t rlo = a < -125.f ? 0u : plo + (tlo << 23), rhi = b < -125.f ? 0u : phi + (thi << 23);
   uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(plo + (tlo << 23)), "r"(phi + (thi << 23)));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(rlo), "r"(rhi));
   return r;
 }
 
@@ -197,25 +200,38 @@ __device__ __forceinline__ void combine_lanes(float m, float R2, double s, bool 
 //   lp = log p_y = (z_y - M)(a - ln2 sc) - log1p(Sx / e_y)
 // keep full relative accuracy when p_y -> 1 (a confident token: 1 - p_y far below fp32's epsilon,
 // where sum-then-subtract would cancel). a = inv_temp; sc = fl(log2(e) a) (§5.1).
+// log2 of a positive fp64 value from its exponent and an fp32 log2 of its mantissa (absolute error
+// ~1e-7): cheap, and defined over fp64's whole range (Sx can be far below fp32's)
+__device__ __forceinline__ double log2_fast(double x) {
+  if (!(x > 0.0)) return x == 0.0 ? -INFINITY : nan("");
+  if (isinf(x)) return INFINITY;
+  int e;
+  const double m = frexp(x, &e);  // x = m 2^e, m in [0.5, 1)
+  return (double)e + (double)__log2f((float)m);
+}
+
 __device__ __forceinline__ void row_stats(float M, float M2, double Sx, float zy, bool tok_ok, const RowScale& rs,
                                           float2& stats, float& qy, double& lpv) {
   // log2 of the token's term and of the others' sum; everything below stays in the log domain, so
-  // neither a confident token (p_y -> 1) nor a hopeless one (e_y below fp64's range) loses accuracy
+  // neither a confident token (p_y -> 1) nor a hopeless one (e_y below fp64's range) loses accuracy.
+  // The transcendentals run in fp32 on quantities in [0, 1] (absolute error ~1e-7 nats per token,
+  // relative for log1p of a small t); the large terms are exact fp64.
   const double xy = tok_ok ? (double)zy * (double)rs.sc - (double)M2 : -INFINITY;   // exact in fp64
-  const double lx = log2(Sx);                                                     // -inf if Sx = 0
+  const double lx = log2_fast(Sx);                                                // -inf if Sx = 0
   const double d = xy - lx;                                                       // log2(e_y / Sx)
-  const double t = exp2(-fabs(d));                                                // in [0, 1]
-  const double log2s = fmax(xy, lx) + log1p(t) * 1.4426950408889634;               // log2(Sx + e_y)
-  const double q = d > 0.0 ? t / (1.0 + t) : 1.0 / (1.0 + t);                     // 1 - p_y = Sx / S
+  const float t = fabs(d) < 160.0 ? exp2f(-(float)fabs(d)) : 0.f;                  // in [0, 1]
+  const double l1p = (double)log1pf(t);                                            // ln(1 + t)
+  const double log2s = fmax(xy, lx) + l1p * 1.4426950408889634;                     // log2(Sx + e_y)
+  const float q = d > 0.0 ? t / (1.f + t) : 1.f / (1.f + t);                       // 1 - p_y = Sx / S
   // lp = a (z_y - M) - ln2 (log2 S + M2 - M sc), with log2 S + M2 - M sc written so that the
   // exact (z_y - M) sc cancels: p_y -> 1 gives (z_y - M)(a - ln2 sc) - log1p(Sx / e_y)
-  double v = d > 0.0 ? ((double)zy - (double)M) * (rs.inv_temp - kLN2 * (double)rs.sc) - log1p(t)
+  double v = d > 0.0 ? ((double)zy - (double)M) * (rs.inv_temp - kLN2 * (double)rs.sc) - l1p
                      : rs.inv_temp * ((double)zy - (double)M) - kLN2 * (lx + (double)M2 - (double)M * (double)rs.sc) -
-                           log1p(t);
+                           l1p;
   if (xy == -INFINITY) v = -INFINITY;
   if (!tok_ok) v = nan("");
   stats = make_float2(M2, (float)log2s);
-  qy = (float)q;
+  qy = q;
   lpv = v;
 }
 
