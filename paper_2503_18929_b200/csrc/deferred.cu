@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, 
 }
 
 // ------------------------------------------------------------------------------ SMEM-resident rows
+#ifdef TBA_AB_DEFER_SMEM
 // The row pass with the row kept ON CHIP between its two passes, so the HBM traffic is exactly 2V
 // read + 2V write per valid row (the 4V floor) whatever L2 does. Persistent: one CTA per SM, CS CTAs
 // (an SM pair for rows of up to ~376 KB: a bf16 Qwen row is 304 KB) per cluster; cluster c takes
@@ -401,8 +402,10 @@ __global__ void __launch_bounds__(DS_THREADS, 1) row_smem(DsArgs a) {
   }
   if (CS > 1) ds_cluster_sync();  // no CTA leaves while its peer may still write into it
 }
+#endif  // TBA_AB_DEFER_SMEM
 
 // ------------------------------------------------------------------------------ launch
+#ifdef TBA_AB_DEFER_SMEM
 // Can row_smem take this call? Every row's output must be 16-byte aligned at the element where the
 // input row's 16-byte-aligned interior starts (rows and outputs repeat their alignment with a period
 // of at most 16 rows), and one CTA's part of a row must leave DS_LOOKAHEAD slots of the ring free.
@@ -457,19 +460,22 @@ int launch_smem_t(const DsArgs& a, int cs, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
 }
 
+#endif  // TBA_AB_DEFER_SMEM
+
 }  // namespace
 
-// deferred-scale row pass: row_smem (rows kept on chip: exact 4V) when the rows fit the ring and the
-// output alignment allows it, else row_single1
+// deferred-scale row pass: row_single1, the L2 two-pass kernel; row_smem (rows kept
+// on chip, exact 4V) only in the TBA_AB_DEFER_SMEM A/B build
 int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int32_t* dev_status,
                   void* grad_unscaled, int32_t g_dtype, int64_t g_row_stride, cudaStream_t s) {
   const int64_t rows = x->n_seq * x->seq_len;
   if (rows == 0) return TBA_OK;
-#ifdef TBA_AB_DEFER_L2
-  const int cs = 0;
-#else
+#ifdef TBA_AB_DEFER_SMEM
   const int cs = smem_cluster_size(x, grad_unscaled, g_dtype, g_row_stride);
+#else
+  const int cs = 0;  // row_smem measured slower than the L2 two-pass kernel: A/B build only
 #endif
+#ifdef TBA_AB_DEFER_SMEM
   if (cs > 0) {
     DsArgs a{x->logits, grad_unscaled, x->tokens, x->mask, w.stats, w.qy, w.lp, dev_status, nullptr, rows,
              x->vocab, x->row_stride, g_row_stride, rs};
@@ -477,6 +483,9 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
       return g_dtype == TBA_BF16 ? launch_smem_t<uint16_t, uint16_t>(a, cs, s) : launch_smem_t<uint16_t, float>(a, cs, s);
     return g_dtype == TBA_BF16 ? launch_smem_t<float, uint16_t>(a, cs, s) : launch_smem_t<float, float>(a, cs, s);
   }
+#else
+  (void)cs;
+#endif
   // Fallback: the row is streamed twice through L2 (rows <= 128 KB: 256 threads per row; longer: 512
   // threads with 8 vectors per thread in pass 2, swept backwards so its most recently streamed
   // vectors are re-read first).

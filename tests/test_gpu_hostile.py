@@ -164,3 +164,48 @@ def test_hostile_bf16_in_fp32_out_large_c():
     z, tokens, mask, ref, rew = _inputs(152064, "bf16", 3, ["peak_last_vec", "ramp_up_small", "ninf_block",
                                                               "peak_last_elem"], big_c=True)
     _run(z, tokens, mask, ref, rew, 1.0, "bf16", torch.float32, "hostile_large_c", "bf16 in, fp32 out, |c|~10")
+
+
+@pytest.mark.parametrize("peak", [16.0, 24.0])
+def test_confident_sequences(peak):
+    """Confident sequences, the common case of a trained policy: every token's logit stands `peak`
+    above N(0, 1) noise at V = 32000, so 1 - p_y ~ V e^(0.5 - peak) (5e-3 and 2e-6) and a 256-token
+    response has |ell| of 1e-3 .. 1: log p_y and 1 - p_y must keep their RELATIVE accuracy (R24;
+    summing the token's term with the others in fp32 would lose ~2e-7 of p_y per token, 1e-4 of ell
+    here). Every per-sequence value, and dlogits including each row's token entry, against the oracle."""
+    V, Tc, Kc = 32000, 256, 4
+    Nc = 2 * Kc
+    rng = np.random.default_rng(int(peak))
+    z = rng.normal(0.0, 1.0, (Nc, Tc, V))
+    tokens = rng.integers(0, V, (Nc, Tc))
+    z[np.arange(Nc)[:, None], np.arange(Tc)[None, :], tokens] += peak
+    z = _bf16(z)
+    mask = np.ones((Nc, Tc), np.uint8)
+    mask[3, 200:] = 0
+    ref = (rng.normal(0.0, 1e-3, Nc)).astype(np.float32).astype(np.float64)
+    rew = (rng.normal(0.0, 1.0, Nc)).astype(np.float32).astype(np.float64)
+    dev = "cuda"
+    lg = torch.from_numpy(z).to(dev, torch.bfloat16)
+    tk, mk = torch.from_numpy(tokens).to(dev), torch.from_numpy(mask).to(dev)
+    o, ws = tba.vargrad_fwd(lg, tk, mk, torch.from_numpy(ref).to(dev), torch.from_numpy(rew).to(dev), 1.0, Kc,
+                            float(Nc), check_status=True)
+    d = tba.vargrad_bwd(lg, tk, mk, ws, o.resid, 2.0 / Nc)
+    torch.cuda.synchronize()
+    r = O.vargrad_head(z, tokens, mask, ref, rew, 1.0, Kc)
+    sl = o.seq_logp.cpu().numpy()
+    # the literal bar (rel 1e-4, abs 1e-5) is loose at |ell| ~ 1e-3: hold the sequence log-probs to
+    # 1e-5 RELATIVE as well, which summing through fp32 with the token's term included would miss
+    rr = H.assert_close_tol(sl, r["ell"], 1e-5 * np.abs(r["ell"]) + 1e-12, f"confident peak {peak} seq_logp")
+    H.record("hostile_confident", f"V=32000 peak={peak}", 0, "seq_logp (rel 1e-5)", Nc, np.max(np.abs(sl - r["ell"])),
+             rr, ell_range=[float(np.min(r["ell"])), float(np.max(r["ell"]))])
+    dd = d.float().cpu().numpy().astype(np.float64)
+    worst = 0.0
+    for s in range(Nc):
+        c = 2.0 * r["eps"][s] / Nc
+        for t in range(Tc):
+            H.assert_dlogits_close(dd[s, t], r["dlogits"][s, t], c, "bf16", f"confident s={s} t={t}")
+            if mask[s, t]:
+                y = int(tokens[s, t])
+                rb = O.round_bf16(np.array([r["dlogits"][s, t, y]]))[0]
+                worst = max(worst, abs(dd[s, t, y] - rb) / O.bf16_ulp(np.array([rb]))[0])
+    H.record("hostile_confident", f"V=32000 peak={peak}", 0, "dlogits token entries (ulp)", Nc * Tc, 0.0, worst)
