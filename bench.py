@@ -128,6 +128,7 @@ def cpu_model() -> str:
 
 def _oracle_inputs(w: syn.Workload, seed: int, g: int, t_prefix: int):
     """Group g's first t_prefix positions (inputs only; generation is not oracle work)."""
+    t_prefix = min(t_prefix, w.T)
     gi = syn.group_inputs(w, seed, g, 1)
     rows = (np.arange(g * w.K, (g + 1) * w.K)[:, None] * w.T + np.arange(t_prefix)[None, :]).reshape(-1)
     lg = syn.logits_rows_f64_host(seed, w.V, rows, w.dtype).reshape(w.K, t_prefix, w.V)

@@ -337,6 +337,29 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
   const int64_t step = (int64_t)nthr * U;
   const int nfull = (int)(nvec / step);
   int64_t k0 = tid;
+#ifdef TBA_AB_SPLIT_LOOP
+  // A/B: the iterations before and after the token's in two loops without a per-iteration test
+  auto fast = [&](int n) {
+    for (int it = 0; it < n; ++it, k0 += step) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
+      fwd_consume<T, U, NP>(v, st);
+    }
+  };
+  const int n1 = (ity >= 0 && ity < nfull) ? ity : nfull;
+  fast(n1);
+  if (n1 < nfull) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
+    fwd_consume<T, U, NP, true>(v, st, uy, ey);
+    k0 += step;
+    fast(nfull - n1 - 1);
+  }
+#else
   for (int it = 0; it < nfull; ++it, k0 += step) {
     uint4 v[U];
 #pragma unroll
@@ -349,6 +372,7 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
     else fwd_consume<T, U, NP>(v, st);
 #endif
   }
+#endif
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
     if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
