@@ -305,6 +305,13 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
   st.s += (double)(a + b);
 }
 
+#ifdef TBA_AB_NOINLINE_SLOW
+template <class T, int U, int NP>
+__device__ __noinline__ void fwd_consume_excl(const uint4 (&v)[U], OnlineState& st, int uy, int ey) {
+  fwd_consume<T, U, NP, true>(v, st, uy, ey);
+}
+#endif
+
 // LDG-streamed partial state of one row over threads tid, tid+nthr, ... The sampled token's element
 // (index y; y < 0 or >= V: none) enters the max but not the sum (finalize_row adds its term).
 template <class T, int U, bool POL = false, int NP = 0>
@@ -331,7 +338,9 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
   // branch); inside it only the owning thread masks the element.
   const int ky = (y >= h && y < tail0) ? (int)((y - h) / VEC) : -1;
   const int ey = ky >= 0 ? (int)((y - h) - (int64_t)ky * VEC) : 0;
-  const int ity = ky >= 0 ? ky / nthr / U : -1;
+  // (the warp's lanes share the row, so the iteration is warp-uniform; broadcasting it lets the
+  // compiler branch on a uniform predicate, without a reconvergence barrier in the hot loop)
+  const int ity = __shfl_sync(0xffffffffu, ky >= 0 ? ky / nthr / U : -1, 0);
   const int uy = (ky >= 0 && ky % nthr == tid) ? (ky / nthr) % U : -1;
   const uint4* vp = reinterpret_cast<const uint4*>(row + h);
   const int64_t step = (int64_t)nthr * U;
@@ -368,7 +377,11 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 #ifdef TBA_AB_NO_EXCL
     fwd_consume<T, U, NP>(v, st);
 #else
+#ifdef TBA_AB_NOINLINE_SLOW
+    if (it == ity) fwd_consume_excl<T, U, NP>(v, st, uy, ey);
+#else
     if (it == ity) fwd_consume<T, U, NP, true>(v, st, uy, ey);
+#endif
     else fwd_consume<T, U, NP>(v, st);
 #endif
   }
