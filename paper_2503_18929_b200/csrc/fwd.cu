@@ -20,18 +20,10 @@ __global__ void __launch_bounds__(256, 4) row_fwd_rows(const T* __restrict__ log
   // the head's last-CTA counter (read only by the next kernel, after this grid completes)
   if (zero_counter && blockIdx.x == 0 && threadIdx.x == 0) *zero_counter = 0u;
   const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
-#ifdef TBA_AB_PERSIST_FWD
-  // A/B: persistent row groups (grid = 4 CTAs per SM), each looping over rows with a grid stride
-  for (int64_t row = (int64_t)blockIdx.x * RPC + grp; row < rows; row += (int64_t)gridDim.x * RPC)
-    if (mask[row] != 0)
-      fwd_row_group<T, TPR, U, NP>(logits, row, V, stride, tokens, rs, stats, qy, lp, dev_status, sm_m, sm_M2, sm_s,
-                                   grp, gt);
-#else
   const int64_t row = (int64_t)blockIdx.x * RPC + grp;
   if (row >= rows || mask[row] == 0) return;
   fwd_row_group<T, TPR, U, NP>(logits, row, V, stride, tokens, rs, stats, qy, lp, dev_status, sm_m, sm_M2, sm_s, grp,
                                gt);
-#endif
 }
 
 template <class T>
@@ -39,12 +31,7 @@ int launch_fwd_rows_t(const T* lg, const tba_rows* x, const WsLayout& w, const R
                        cudaStream_t s, int tpr) {
   const int64_t rows = x->n_seq * x->seq_len;
   const int64_t rpc = 256 / tpr;
-#ifdef TBA_AB_PERSIST_FWD
-  const int64_t g0 = (rows + rpc - 1) / rpc, gcap = (int64_t)device_sms() * 4;
-  const unsigned grid = (unsigned)(g0 < gcap ? g0 : gcap);
-#else
   const unsigned grid = (unsigned)((rows + rpc - 1) / rpc);
-#endif
 #define TBA_ROWS(TPR_, NP_)                                                                                     \
   return launch_pdl(row_fwd_rows<T, TPR_, kU, NP_>, dim3(grid), dim3(256), 0, s, lg, rows, x->vocab, x->row_stride, \
                     x->tokens, x->mask, rs, w.stats, w.qy, w.lp, dev_status, w.counter)

@@ -305,13 +305,6 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
   st.s += (double)(a + b);
 }
 
-#ifdef TBA_AB_NOINLINE_SLOW
-template <class T, int U, int NP>
-__device__ __noinline__ void fwd_consume_excl(const uint4 (&v)[U], OnlineState& st, int uy, int ey) {
-  fwd_consume<T, U, NP, true>(v, st, uy, ey);
-}
-#endif
-
 // LDG-streamed partial state of one row over threads tid, tid+nthr, ... The sampled token's element
 // (index y; y < 0 or >= V: none) enters the max but not the sum (finalize_row adds its term).
 template <class T, int U, bool POL = false, int NP = 0>
@@ -338,37 +331,12 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
   // branch); inside it only the owning thread masks the element.
   const int ky = (y >= h && y < tail0) ? (int)((y - h) / VEC) : -1;
   const int ey = ky >= 0 ? (int)((y - h) - (int64_t)ky * VEC) : 0;
-  // (the warp's lanes share the row, so the iteration is warp-uniform; broadcasting it lets the
-  // compiler branch on a uniform predicate, without a reconvergence barrier in the hot loop)
-  const int ity = __shfl_sync(0xffffffffu, ky >= 0 ? ky / nthr / U : -1, 0);
+  const int ity = ky >= 0 ? ky / nthr / U : -1;
   const int uy = (ky >= 0 && ky % nthr == tid) ? (ky / nthr) % U : -1;
   const uint4* vp = reinterpret_cast<const uint4*>(row + h);
   const int64_t step = (int64_t)nthr * U;
   const int nfull = (int)(nvec / step);
   int64_t k0 = tid;
-#ifdef TBA_AB_SPLIT_LOOP
-  // A/B: the iterations before and after the token's in two loops without a per-iteration test
-  auto fast = [&](int n) {
-    for (int it = 0; it < n; ++it, k0 += step) {
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
-      fwd_consume<T, U, NP>(v, st);
-    }
-  };
-  const int n1 = (ity >= 0 && ity < nfull) ? ity : nfull;
-  fast(n1);
-  if (n1 < nfull) {
-    uint4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
-    fwd_consume<T, U, NP, true>(v, st, uy, ey);
-    k0 += step;
-    fast(nfull - n1 - 1);
-  }
-#else
   for (int it = 0; it < nfull; ++it, k0 += step) {
     uint4 v[U];
 #pragma unroll
@@ -377,15 +345,10 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 #ifdef TBA_AB_NO_EXCL
     fwd_consume<T, U, NP>(v, st);
 #else
-#ifdef TBA_AB_NOINLINE_SLOW
-    if (it == ity) fwd_consume_excl<T, U, NP>(v, st, uy, ey);
-#else
     if (it == ity) fwd_consume<T, U, NP, true>(v, st, uy, ey);
-#endif
     else fwd_consume<T, U, NP>(v, st);
 #endif
   }
-#endif
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
     if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
