@@ -35,7 +35,7 @@
     }                                                                         \
   } while (0)
 
-int main(void) {
+int main(int argc, char** argv) {
   const int64_t B = 2, K = 3, N = B * K, T = 4, V = 257;
   const double beta = 0.5;
   float* h_logits = (float*)malloc(sizeof(float) * N * T * V);
@@ -118,6 +118,11 @@ int main(void) {
          partial[2]);
   for (int s = 0; s < N; ++s) printf("seq %d logp %.12g ntok %d\n", s, seq[s], ntok[s]);
   printf("dlogits_abs_sum %.9g row0_sum %.3g\n", cs, rowsum);
+  if (argc > 1) { /* the whole fp32 dlogits tensor, for an element-wise check against the oracle */
+    FILE* f = fopen(argv[1], "wb");
+    if (!f || fwrite(h_d, sizeof(float), (size_t)(N * T * V), f) != (size_t)(N * T * V)) return 3;
+    fclose(f);
+  }
 
   /* The LM-head-fused forward: the same sequences' log-probs from bf16 hidden states [N*T, D]
    * and an LM-head weight [V, D] (entries k/4, k in -2..2: exact in bf16, every logit exact in

@@ -1,5 +1,6 @@
 """The C ABI is usable from plain C: examples/c_abi_example.c builds here (CPU) and, on a GPU,
 its printed loss / per-sequence log-probs match the fp64 oracle on the same inputs."""
+import os
 import re
 import subprocess
 
@@ -7,6 +8,8 @@ import numpy as np
 import pytest
 
 from oracle import tba_oracle as O
+
+from . import _harness as H
 
 
 def _inputs():
@@ -55,7 +58,9 @@ def test_c_example_runs_and_matches_oracle():
         pytest.skip("no GPU")
     from paper_2503_18929_b200 import _build
     exe = _build.build_c_example()
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    import tempfile
+    dump = os.path.join(tempfile.mkdtemp(), "dlogits.f32")
+    out = subprocess.run([exe, dump], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     logits, tok, mask, ref, rew, hid, w = _inputs()
     r = O.vargrad_head(logits, tok, mask, ref, rew, 0.5, 3)
@@ -66,6 +71,12 @@ def test_c_example_runs_and_matches_oracle():
     np.testing.assert_allclose(got, r["ell"], rtol=1e-6)
     cs = float(re.search(r"dlogits_abs_sum (\S+)", out.stdout).group(1))
     assert abs(cs - np.abs(r["dlogits"]).sum()) <= 1e-5 * np.abs(r["dlogits"]).sum()
+    # every element of the fp32 dlogits the C program wrote, against the oracle (R9 bar)
+    d = np.fromfile(dump, dtype=np.float32).astype(np.float64).reshape(r["dlogits"].shape)
+    for s in range(d.shape[0]):
+        c = 2.0 * r["eps"][s] / d.shape[0]
+        for t in range(d.shape[1]):
+            H.assert_dlogits_close(d[s, t], r["dlogits"][s, t], c, "fp32", f"C example s={s} t={t}")
     # the LM-head-fused forward from the lattice hidden states (exact logits)
     ell, _ = O.lmhead_seq_logprob(hid.reshape(6, 4, 64), w, tok, mask)
     got = [float(x) for x in re.findall(r"lmhead seq \d+ logp (\S+)", out.stdout)]
