@@ -749,6 +749,8 @@ def main():
                          "deferred: tba_tb_loss_fwd_deferred (unscaled gradient, 4V bytes; NEXT 2 (ii)); "
                          "pipelined: tba_tb_loss_pipelined (group chunks, writer of chunk c-1 beside the forward "
                          "of chunk c on a second stream)")
+    ap.add_argument("--pipe-one-stream", action="store_true",
+                    help="--schedule pipelined on ONE stream (chunk kernels PDL-chained) instead of two")
     ap.add_argument("--pipe-groups", type=int, default=0,
                     help="groups per chunk for --schedule pipelined (0 = ~L2/4 of logits per chunk)")
     ap.add_argument("--cuda-graph", action="store_true",
@@ -849,7 +851,8 @@ def main():
     def fwd_call():
         if pipelined:
             tba.vargrad_pipelined(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
-                                  dlogits=dlogits, groups_per_chunk=gpc, check_status=False)
+                                  dlogits=dlogits, groups_per_chunk=gpc, check_status=False,
+                                  aux_stream=not args.pipe_one_stream)
         elif fused:
             tba.vargrad_fused(logits, tokens, mask, ref, rew, w.beta, K, n_global, workspace=ws, out=out,
                               dlogits=dlogits, check_status=False)
@@ -1102,7 +1105,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": w.dtype, "data": "synthetic (tba_synth seeded generator, DESIGN.md §6)",
             "config": {"workload": w.name, "objective": args.objective, "schedule": args.schedule, "scaling": "weak",
-                       **({"groups_per_chunk": gpc, "chunks": n_chunks} if pipelined else {}),
+                       **({"groups_per_chunk": gpc, "chunks": n_chunks,
+                           "streams": 1 if args.pipe_one_stream else 2} if pipelined else {}),
                        "cuda_graph": bool(args.cuda_graph), "note": w.note,
                        "B_per_rank": B, "B_global": B * world, "K": K, "T": T,
                        "V": V, "beta": w.beta, "logits_dtype": w.dtype, "dlogits_dtype": w.dtype,
