@@ -256,31 +256,24 @@ def is_weight(lam: float, mode: str, lo: float, hi: float) -> float:
     raise ValueError(mode)
 
 
-def tbap_head(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, K: int, is_mode: str = "clip",
-              is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global: int | None = None, grad_out: float = 1.0,
-              want_grad: bool = True):
-    """TBA' token-level rule, Eq. 16, step by step in the paper's notation:
-      lambda_t = pi_theta(y_t)/pi_gen(y_t)                      per token
-      log Lambda_j = sum_t log(pi_theta(y_t)/pi_ref(y_t)) = ell_j - rho_j
-      A_j = (r_j - rbar) - beta (log Lambda_j - mean_j log Lambda)
-      grad J = sum_j sum_t sg(w(lambda_t) A_j) grad log pi_theta(y_t)
-    normalised by the number of valid tokens (GRPO-style; R15). Returns the
-    surrogate loss L' = -(1/n_tok) sum coef_t lp_t (whose gradient is -grad J / n_tok), ell,
-    n_tok, A, coef [N, T] and, if requested, dlogits = -(coef/n_tok) g (onehot - p)."""
+def tbap_coefficients(lp, mask, gen_logp, ref_logp, log_reward, beta: float, K: int, is_mode: str = "clip",
+                      is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global: int | None = None):
+    """Eq. 16 from the per-token log-probs lp [N, T] (valid positions only are read),
+    step by step in the paper's notation:
+      lambda_t = pi_theta(y_t)/pi_gen(y_t) = exp(lp_t - gen_t)      per token
+      log Lambda_j = ell_j - rho_j,  ell_j = sum_t lp_t              (sequence_sums)
+      A_j = (r_j - rbar) - beta (log Lambda_j - mean_j log Lambda)  per group of K
+      coef_t = w(lambda_t) A_j                                       (a stop-gradient constant)
+    and the surrogate loss L' = -(1/n_tok) sum_t coef_t lp_t (GRPO-style normalisation, P:708;
+    DESIGN.md R15). Returns dict(ell, n_tok, adv, coef [N, T], loss, partial)."""
     if not (math.isfinite(beta) and beta >= 0):
         raise ValueError("invalid-config: beta must be finite and >= 0")
-    N, T = tokens.shape
+    N, T = np.shape(mask)
     if K < 2:
         raise ValueError("invalid-config: K must be >= 2")
     if N % K:
         raise ValueError("invalid-arg: N must be a multiple of K")
-    lp = np.zeros((N, T))
-    for s in range(N):
-        for t in range(T):
-            if mask[s, t]:
-                lp[s, t], _ = token_logprob(logits[s, t], int(tokens[s, t]))
-    ell = np.array([math.fsum(lp[s][mask[s] == 1]) for s in range(N)])
-    ntok = mask.sum(1).astype(np.int64)
+    ell, ntok = sequence_sums(lp, mask)
     ref = np.asarray(ref_logp, np.float64)
     r = np.asarray(log_reward, np.float64)
     A = np.empty(N)
@@ -297,14 +290,38 @@ def tbap_head(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float,
     n = int(ntok.sum()) if n_tok_global is None else n_tok_global
     terms = [coef[s, t] * lp[s, t] for s in range(N) for t in range(T) if mask[s, t]]
     loss = -math.fsum(terms) / n
-    out = dict(lp=lp, ell=ell, n_tok=ntok, adv=A, coef=coef, loss=loss,
-               partial=np.array([loss, float(ntok.sum()), float(N)]))
+    return dict(ell=ell, n_tok=ntok, adv=A, coef=coef, loss=loss,
+                partial=np.array([loss, float(ntok.sum()), float(N)]))
+
+
+def tbap_dlogits_row(z, y: int, coef_t: float, n_tok: int, grad_out: float = 1.0) -> np.ndarray:
+    """One valid row of the TBA' surrogate's gradient: -(coef_t / n_tok) g (onehot(y) - softmax(z))."""
+    return -(coef_t / n_tok) * grad_out * grad_logprob_row(z, y)
+
+
+def tbap_head(logits, tokens, mask, gen_logp, ref_logp, log_reward, beta: float, K: int, is_mode: str = "clip",
+              is_lo: float = 0.0, is_hi: float = 8.0, n_tok_global: int | None = None, grad_out: float = 1.0,
+              want_grad: bool = True):
+    """TBA' token-level rule, Eq. 16: grad J = sum_j sum_t sg(w(lambda_t) A_j)
+    grad log pi_theta(y_t), normalised by the number of valid tokens (GRPO-style; R15).
+    token_logprob_rows over the valid rows, then tbap_coefficients; dlogits (if requested) =
+    tbap_dlogits_row per valid row. Returns the surrogate loss L' = -(1/n_tok) sum coef_t lp_t
+    (whose gradient is -grad J / n_tok), lp, ell, n_tok, A, coef [N, T] and dlogits."""
+    N, T = tokens.shape
+    lp = np.zeros((N, T))
+    valid = np.asarray(mask).reshape(-1) == 1
+    if valid.any():
+        lp.reshape(-1)[valid] = token_logprob_rows(np.asarray(logits).reshape(N * T, -1)[valid],
+                                                   np.asarray(tokens).reshape(-1)[valid])[0]
+    out = tbap_coefficients(lp, mask, gen_logp, ref_logp, log_reward, beta, K, is_mode, is_lo, is_hi, n_tok_global)
+    out["lp"] = lp
+    n = int(out["n_tok"].sum()) if n_tok_global is None else n_tok_global
     if want_grad:
-        d = np.zeros(logits.shape)
+        d = np.zeros(np.shape(logits))
         for s in range(N):
             for t in range(T):
                 if mask[s, t]:
-                    d[s, t] = -(coef[s, t] / n) * grad_out * grad_logprob_row(logits[s, t], int(tokens[s, t]))
+                    d[s, t] = tbap_dlogits_row(logits[s, t], int(tokens[s, t]), out["coef"][s, t], n, grad_out)
         out["dlogits"] = d
     return out
 

@@ -102,17 +102,40 @@ def oracle_seq_values(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: 
     return dict(ell=ell, n_tok=ntok, lse=lse.reshape(N, T), **gi)
 
 
+def oracle_token_lp(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: int = 64):
+    """Oracle per-token log-probs lp [N, T] (0 at masked positions) for groups g0..g0+ng-1, computed
+    by token_logprob_rows on regenerated rows in the worker pool."""
+    gi = syn.group_inputs(w, seed, g0, ng)
+    tok, mask = gi["tokens"], gi["mask"]
+    N, T = tok.shape
+    base = g0 * w.K * T
+    valid = np.flatnonzero(mask.reshape(-1))
+    jobs = [(seed, w.V, w.dtype, base + valid[i:i + chunk_rows], tok.reshape(-1)[valid[i:i + chunk_rows]])
+            for i in range(0, len(valid), chunk_rows)]
+    res = list(pool().map(_rows_lp, jobs)) if len(jobs) > 1 else [_rows_lp(j) for j in jobs]
+    lp = np.zeros(N * T)
+    pos = 0
+    for a, _ in res:
+        lp[valid[pos:pos + len(a)]] = a
+        pos += len(a)
+    return lp.reshape(N, T), gi
+
+
 def _cmp_rows(args):
     """Worker: compare GPU dlogits rows (read from a /dev/shm memmap) with oracle dlogits_row."""
-    path, shape, gdt, i0, i1, seed, V, in_dt, rows, toks, eps, n_global, grad_out, out_dt = args
+    path, shape, gdt, i0, i1, seed, V, in_dt, rows, toks, eps, n_global, grad_out, out_dt, kind = args
     mm = np.memmap(path, dtype=np.uint16 if gdt == "bf16" else np.float32, mode="r", shape=shape)
     g = mm[i0:i1]
     g = syn.bf16_bits_to_f64(g) if gdt == "bf16" else g.astype(np.float64)
     z = syn.logits_rows_f64_host(seed, V, rows, in_dt)
     n_bad, max_abs, max_ratio, worst = 0, 0.0, 0.0, None
     for i in range(len(rows)):
-        want = O.dlogits_row(z[i], int(toks[i]), float(eps[i]), n_global, grad_out)
-        c = 2.0 * float(eps[i]) / n_global * grad_out
+        if kind == "tbap":  # eps holds the per-token coefficient, n_global the token count
+            want = O.tbap_dlogits_row(z[i], int(toks[i]), float(eps[i]), n_global, grad_out)
+            c = -float(eps[i]) / n_global * grad_out
+        else:
+            want = O.dlogits_row(z[i], int(toks[i]), float(eps[i]), n_global, grad_out)
+            c = 2.0 * float(eps[i]) / n_global * grad_out
         if out_dt == "bf16":
             rb = O.round_bf16(want)
             err = np.abs(g[i] - rb)
@@ -136,10 +159,12 @@ def _cmp_rows(args):
 
 
 def compare_dlogits_rows(d, w: syn.Workload, seed: int, flat_rows, row_base: int, tokens_flat, eps_of_row,
-                         n_global: int, grad_out: float = 1.0, what: str = "", chunk: int = 2048, sub: int = 16):
+                         n_global: int, grad_out: float = 1.0, what: str = "", chunk: int = 2048, sub: int = 16,
+                         kind: str = "tb"):
     """Element-wise comparison of GPU dlogits rows (``d`` viewed [rows, V], local row indices
     ``flat_rows``, all VALID) with oracle dlogits_row on the regenerated logits (global row =
-    row_base + local). tokens_flat / eps_of_row: per local row arrays. Raises on any element
+    row_base + local). tokens_flat / eps_of_row: per local row arrays (kind "tbap": eps_of_row holds
+    the per-token TBA' coefficient, n_global the token count, oracle tbap_dlogits_row). Raises on any element
     outside the tolerance; returns (n_rows, max_abs_err, max_err_over_tol)."""
     import torch
     flat_rows = np.asarray(flat_rows, dtype=np.int64)
@@ -162,7 +187,7 @@ def compare_dlogits_rows(d, w: syn.Workload, seed: int, flat_rows, row_base: int
             mm.flush()
             del rows_dev
             jobs = [(path, (cap, V), gdt, i, min(i + sub, len(rr)), seed, V, w.dtype, row_base + rr[i:i + sub],
-                     tokens_flat[rr[i:i + sub]], eps_of_row[rr[i:i + sub]], n_global, grad_out, gdt)
+                     tokens_flat[rr[i:i + sub]], eps_of_row[rr[i:i + sub]], n_global, grad_out, gdt, kind)
                     for i in range(0, len(rr), sub)]
             for nb, ma, mr, wst in pool().map(_cmp_rows, jobs):
                 tot_bad += nb

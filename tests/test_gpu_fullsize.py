@@ -201,3 +201,45 @@ def test_math_t5_two_groups_ragged_2048():
     check_dlogits(test, w, 3, d, rows, ref["tokens"].reshape(-1), np.repeat(ref["eps_g"], w.T), 2 * w.K,
                   "1024 random rows")
     check_properties(w, inp, o, d, n_rows=32)
+
+
+@pytest.mark.parametrize("name,seed,mode", [("qwen_shard", 0, "clip"), ("rhomath", 1, "icepop")])
+def test_tbap_full_size(name, seed, mode):
+    """TBA' (Eq. 16) at full size in bench.py's configuration: every
+    per-sequence value (ell, A), every per-token coefficient w(lambda_t) A_j, the surrogate loss,
+    and dlogits on 4096 seeded random valid rows plus every row of one whole group."""
+    w = syn.WORKLOADS[name]
+    test = f"tbap_{name}"
+    lo, hi = (0.0, 8.0) if mode == "clip" else (0.5, 2.0)
+    inp = H.device_inputs(w, seed)
+    gen = torch.from_numpy(syn.gen_logp(w, seed, 0, w.N)).cuda()
+    n_tok = float(int(inp["host"]["mask"].sum()))
+    o, ws = tba.tbap_fwd(inp["logits"], inp["tokens"], inp["mask"], gen, inp["ref_logp"], inp["log_reward"], w.beta,
+                         w.K, mode, lo, hi, n_tok, check_status=True)
+    d = tba.tbap_bwd(inp["logits"], inp["tokens"], inp["mask"], ws, o.coef, n_tok)
+    torch.cuda.synchronize()
+    lp, gi = H.oracle_token_lp(w, seed, 0, w.B)
+    ref = O.tbap_coefficients(lp, gi["mask"], gen.cpu().numpy(), gi["ref_logp"], gi["log_reward"], w.beta, w.K, mode,
+                              lo, hi, int(n_tok))
+    sl = o.seq_logp.cpu().numpy()
+    H.record(test, name, seed, "seq_logp", w.N, np.max(np.abs(sl - ref["ell"])), H.assert_seq_close(sl, ref["ell"], "ell"))
+    np.testing.assert_array_equal(o.n_tokens.cpu().numpy(), ref["n_tok"])
+    adv = o.adv.cpu().numpy()
+    # A_j inherits ell's bar through beta (log Lambda_j - mean log Lambda): R23 with the factor beta
+    tz, te = H.seq_tols(ref["ell"], w.K)
+    H.record(test, name, seed, "adv", w.N, np.max(np.abs(adv - ref["adv"])),
+             H.assert_close_tol(adv, ref["adv"], w.beta * te, "adv"), tol="beta x propagated (R23)")
+    coef = o.coef.cpu().numpy().astype(np.float64)
+    m = gi["mask"] == 1
+    # coef is stored in fp32: one fp32 rounding of w(lambda) A plus lambda's sensitivity to lp's error
+    ctol = np.abs(ref["coef"]) * (2.0 ** -23) + w.beta * np.repeat(te, w.T).reshape(w.N, w.T) * np.maximum(
+        1.0, np.abs(np.where(m, ref["coef"], 0.0)))
+    r = H.assert_close_tol(coef[m], ref["coef"][m], ctol[m], "coef")
+    H.record(test, name, seed, "coef (every valid token)", int(m.sum()), np.max(np.abs(coef[m] - ref["coef"][m])), r)
+    p0 = o.partial[0].item()
+    H.record(test, name, seed, "loss", 1, abs(p0 - ref["loss"]), H.assert_seq_close([p0], [ref["loss"]], "loss"))
+    rows = _row_plan(w, seed, gi["mask"].reshape(-1), [1], 4096)
+    # the oracle's own coefficients (fp64) scale the oracle rows; the GPU's fp32 coef differs by ~2^-24
+    n, ma, mr = H.compare_dlogits_rows(d, w, seed, rows, 0, gi["tokens"].reshape(-1), ref["coef"].reshape(-1),
+                                       int(n_tok), what=f"{test} dlogits", kind="tbap")
+    H.record(test, name, seed, "dlogits (group 1 whole + 4096 random rows)", n, ma, mr, tol="1 bf16 ulp")

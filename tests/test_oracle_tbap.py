@@ -126,3 +126,23 @@ def test_config_errors():
         O.tbap_head(logits, tokens, mask, gen, ref, rew, -0.1, 3)
     with pytest.raises(ValueError):
         O.tbap_head(logits, tokens, mask, gen, ref, rew, 0.1, 1)
+
+
+def test_tbap_dlogits_row_finite_differences():
+    """tbap_dlogits_row (the expected value of every sampled full-size TBA' row comparison) against
+    central differences of the token log-prob it scales: -(coef / n_tok) g d lp / dz."""
+    import math
+    rng = np.random.default_rng(5)
+    for V in (2, 5, 9):
+        z = rng.normal(0, 1.5, V)
+        y = int(rng.integers(0, V))
+        coef, n, g = float(rng.normal()), int(rng.integers(3, 50)), float(rng.normal())
+        d = O.tbap_dlogits_row(z, y, coef, n, g)
+        h = 1e-6
+        for v in range(V):
+            zp, zm = z.copy(), z.copy()
+            zp[v] += h
+            zm[v] -= h
+            fd = -(coef / n) * g * (O.token_logprob(zp, y)[0] - O.token_logprob(zm, y)[0]) / (2 * h)
+            assert abs(d[v] - fd) <= 1e-8 * max(1.0, abs(fd)), (V, v, d[v], fd)
+        assert abs(math.fsum(d)) <= 1e-15
