@@ -72,15 +72,16 @@ def token_logprob(z: np.ndarray, y: int) -> tuple[float, float]:
 
 
 # ----------------------------------------------------------------------------- a2
-def token_logprob_rows(z_rows: np.ndarray, tokens) -> tuple[np.ndarray, np.ndarray]:
+def token_logprob_rows(z_rows: np.ndarray, tokens, inv_temp: float = 1.0) -> tuple[np.ndarray, np.ndarray]:
     """``token_logprob`` of each row of z_rows [n, V] at its token (tokens [n]): the per-token
     terms of log pi_theta(y|x) (Eqs. 4-5) for a batch of VALID rows, wherever they come from
-    (the full-size harness regenerates sampled rows from the seed). Returns (lp [n], lse [n])."""
+    (the full-size harness regenerates sampled rows from the seed). ``inv_temp`` a: the
+    temperature-scaled policy log softmax(a z) (NEXT 4). Returns (lp [n], lse [n])."""
     n = len(tokens)
     lp = np.empty(n)
     lse = np.empty(n)
     for i in range(n):
-        lp[i], lse[i] = token_logprob(z_rows[i], int(tokens[i]))
+        lp[i], lse[i] = token_logprob(inv_temp * np.asarray(z_rows[i], np.float64), int(tokens[i]))
     return lp, lse
 
 
@@ -196,9 +197,10 @@ def dlogits(logits, tokens, mask, eps, n_global: int, grad_out: float = 1.0) -> 
     return out
 
 
-def dlogits_row(z, y: int, eps_s: float, n_global: int, grad_out: float = 1.0) -> np.ndarray:
-    """One valid row of ``dlogits`` (for sampled-row comparison at full size)."""
-    return 2.0 * eps_s / n_global * grad_out * grad_logprob_row(z, y)
+def dlogits_row(z, y: int, eps_s: float, n_global: int, grad_out: float = 1.0, inv_temp: float = 1.0) -> np.ndarray:
+    """One valid row of ``dlogits`` (for sampled-row comparison at full size); with ``inv_temp`` a
+    the chain rule through log softmax(a z): a (2 eps / N) g (onehot - softmax(a z))."""
+    return inv_temp * (2.0 * eps_s / n_global * grad_out) * grad_logprob_row(inv_temp * np.asarray(z, np.float64), y)
 
 
 # ----------------------------------------------------------------------------- full head
@@ -223,10 +225,16 @@ def vargrad_head(logits, tokens, mask, ref_logp, log_reward, beta: float, K: int
     out = dict(ell=ell, n_tok=ntok, lse=lse, log_z=logz, eps=eps, loss=loss,
                partial=np.array([loss, float(N), float(N // K)]))
     if log_z is not None:
-        out["d_log_z"] = np.array([2.0 * math.fsum(eps[i * K:(i + 1) * K]) / n * grad_out for i in range(N // K)])
+        out["d_log_z"] = learned_log_z_grad(eps, K, n, grad_out)
     if want_grad:
         out["dlogits"] = inv_temp * dlogits(scaled, tokens, mask, eps, n, grad_out)
     return out
+
+
+def learned_log_z_grad(eps, K: int, n_global: int, grad_out: float = 1.0) -> np.ndarray:
+    """dL/dlog Z(x_i) for a learned log Z (Eq. 3, no stop-gradient): (2 / N) g sum_j eps_{iK+j}."""
+    N = len(eps)
+    return np.array([2.0 * math.fsum(eps[i * K:(i + 1) * K]) / n_global * grad_out for i in range(N // K)])
 
 
 def tb_learned_z_loss(ell, ref_logp, log_reward, beta: float, K: int, log_z, n_global: int | None = None):

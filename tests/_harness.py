@@ -76,11 +76,11 @@ def record(test: str, config: str, seed: int, quantity: str, n: int, max_abs_err
 
 
 def _rows_lp(args):
-    seed, V, dtype, rows, toks = args
-    return O.token_logprob_rows(syn.logits_rows_f64_host(seed, V, rows, dtype), toks)
+    seed, V, dtype, rows, toks, inv_temp = args
+    return O.token_logprob_rows(syn.logits_rows_f64_host(seed, V, rows, dtype), toks, inv_temp)
 
 
-def oracle_seq_values(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: int = 64):
+def oracle_seq_values(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: int = 64, inv_temp: float = 1.0):
     """Oracle a1-a2 for groups g0..g0+ng-1 (only valid rows are evaluated). Returns
     dict(ell, n_tok, lse [N, T], tokens, mask, ref_logp, log_reward)."""
     gi = syn.group_inputs(w, seed, g0, ng)
@@ -88,7 +88,7 @@ def oracle_seq_values(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: 
     N, T = tok.shape
     base = g0 * w.K * T
     valid = np.flatnonzero(mask.reshape(-1))
-    jobs = [(seed, w.V, w.dtype, base + valid[i:i + chunk_rows], tok.reshape(-1)[valid[i:i + chunk_rows]])
+    jobs = [(seed, w.V, w.dtype, base + valid[i:i + chunk_rows], tok.reshape(-1)[valid[i:i + chunk_rows]], inv_temp)
             for i in range(0, len(valid), chunk_rows)]
     res = list(pool().map(_rows_lp, jobs)) if len(jobs) > 1 else [_rows_lp(j) for j in jobs]
     lp = np.full(N * T, np.nan)
@@ -110,7 +110,7 @@ def oracle_token_lp(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: in
     N, T = tok.shape
     base = g0 * w.K * T
     valid = np.flatnonzero(mask.reshape(-1))
-    jobs = [(seed, w.V, w.dtype, base + valid[i:i + chunk_rows], tok.reshape(-1)[valid[i:i + chunk_rows]])
+    jobs = [(seed, w.V, w.dtype, base + valid[i:i + chunk_rows], tok.reshape(-1)[valid[i:i + chunk_rows]], 1.0)
             for i in range(0, len(valid), chunk_rows)]
     res = list(pool().map(_rows_lp, jobs)) if len(jobs) > 1 else [_rows_lp(j) for j in jobs]
     lp = np.zeros(N * T)
@@ -123,7 +123,7 @@ def oracle_token_lp(w: syn.Workload, seed: int, g0: int, ng: int, chunk_rows: in
 
 def _cmp_rows(args):
     """Worker: compare GPU dlogits rows (read from a /dev/shm memmap) with oracle dlogits_row."""
-    path, shape, gdt, i0, i1, seed, V, in_dt, rows, toks, eps, n_global, grad_out, out_dt, kind = args
+    path, shape, gdt, i0, i1, seed, V, in_dt, rows, toks, eps, n_global, grad_out, out_dt, kind, inv_temp = args
     mm = np.memmap(path, dtype=np.uint16 if gdt == "bf16" else np.float32, mode="r", shape=shape)
     g = mm[i0:i1]
     g = syn.bf16_bits_to_f64(g) if gdt == "bf16" else g.astype(np.float64)
@@ -134,8 +134,8 @@ def _cmp_rows(args):
             want = O.tbap_dlogits_row(z[i], int(toks[i]), float(eps[i]), n_global, grad_out)
             c = -float(eps[i]) / n_global * grad_out
         else:
-            want = O.dlogits_row(z[i], int(toks[i]), float(eps[i]), n_global, grad_out)
-            c = 2.0 * float(eps[i]) / n_global * grad_out
+            want = O.dlogits_row(z[i], int(toks[i]), float(eps[i]), n_global, grad_out, inv_temp)
+            c = inv_temp * 2.0 * float(eps[i]) / n_global * grad_out
         if out_dt == "bf16":
             rb = O.round_bf16(want)
             err = np.abs(g[i] - rb)
@@ -160,7 +160,7 @@ def _cmp_rows(args):
 
 def compare_dlogits_rows(d, w: syn.Workload, seed: int, flat_rows, row_base: int, tokens_flat, eps_of_row,
                          n_global: int, grad_out: float = 1.0, what: str = "", chunk: int = 2048, sub: int = 16,
-                         kind: str = "tb"):
+                         kind: str = "tb", inv_temp: float = 1.0):
     """Element-wise comparison of GPU dlogits rows (``d`` viewed [rows, V], local row indices
     ``flat_rows``, all VALID) with oracle dlogits_row on the regenerated logits (global row =
     row_base + local). tokens_flat / eps_of_row: per local row arrays (kind "tbap": eps_of_row holds
@@ -187,7 +187,8 @@ def compare_dlogits_rows(d, w: syn.Workload, seed: int, flat_rows, row_base: int
             mm.flush()
             del rows_dev
             jobs = [(path, (cap, V), gdt, i, min(i + sub, len(rr)), seed, V, w.dtype, row_base + rr[i:i + sub],
-                     tokens_flat[rr[i:i + sub]], eps_of_row[rr[i:i + sub]], n_global, grad_out, gdt, kind)
+                     tokens_flat[rr[i:i + sub]], eps_of_row[rr[i:i + sub]], n_global, grad_out, gdt, kind,
+                     inv_temp)
                     for i in range(0, len(rr), sub)]
             for nb, ma, mr, wst in pool().map(_cmp_rows, jobs):
                 tot_bad += nb

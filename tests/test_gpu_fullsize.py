@@ -243,3 +243,39 @@ def test_tbap_full_size(name, seed, mode):
     n, ma, mr = H.compare_dlogits_rows(d, w, seed, rows, 0, gi["tokens"].reshape(-1), ref["coef"].reshape(-1),
                                        int(n_tok), what=f"{test} dlogits", kind="tbap")
     H.record(test, name, seed, "dlogits (group 1 whole + 4096 random rows)", n, ma, mr, tol="1 bf16 ulp")
+
+
+def test_variants_full_size_temperature_and_learned_log_z():
+    """NEXT 4 at the Qwen shard in bench.py's configuration: log pi = log softmax(z / 0.7) and a
+    learned log Z(x_i) (Eq. 3): every per-sequence value, the residuals, dL/dlog Z, the loss and
+    dlogits on 4096 seeded random valid rows plus every row of one whole group."""
+    w = syn.WORKLOADS["qwen_shard"]
+    seed, a = 5, 1.0 / 0.7
+    test = "variants_qwen_shard"
+    inp = H.device_inputs(w, seed)
+    lz = np.random.default_rng(77).normal(-40.0, 5.0, w.B)          # the learned per-prompt log Z (an input)
+    lz_t = torch.from_numpy(lz).cuda()
+    o, ws = tba.vargrad_fwd(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"], inp["log_reward"], w.beta,
+                            w.K, float(w.N), check_status=True, inv_temp=a, log_z_param=lz_t)
+    d, dlz = tba.vargrad_bwd(inp["logits"], inp["tokens"], inp["mask"], ws, o.resid, 2.0 / w.N, inv_temp=a,
+                             log_z_param=lz_t, K=w.K)
+    torch.cuda.synchronize()
+    ref = H.oracle_seq_values(w, seed, 0, w.B, inv_temp=a)
+    sl = o.seq_logp.cpu().numpy()
+    H.record(test, w.name, seed, "seq_logp (inv_temp 1/0.7)", w.N, np.max(np.abs(sl - ref["ell"])),
+             H.assert_seq_close(sl, ref["ell"], "seq_logp"))
+    loss, _, eps = O.tb_learned_z_loss(ref["ell"], ref["ref_logp"], ref["log_reward"], w.beta, w.K, lz, w.N)
+    _, te = H.seq_tols(ref["ell"], w.K)
+    tl = np.maximum(1e-4 * np.abs(ref["ell"]), 1e-5)        # eps = log Z + ell - rho - r/beta: ell's bar alone
+    g = o.resid.cpu().numpy()
+    H.record(test, w.name, seed, "resid (learned log Z)", w.N, np.max(np.abs(g - eps)), H.assert_close_tol(g, eps, tl, "resid"))
+    want = O.learned_log_z_grad(eps, w.K, w.N)
+    got = dlz.cpu().numpy()
+    H.record(test, w.name, seed, "d_log_z", w.B, np.max(np.abs(got - want)),
+             H.assert_close_tol(got, want, 2.0 / w.N * tl.reshape(-1, w.K).sum(1), "d_log_z"))
+    p0 = o.partial[0].item()
+    H.record(test, w.name, seed, "loss", 1, abs(p0 - loss), H.assert_seq_close([p0], [loss], "loss"))
+    rows = _row_plan(w, seed, ref["mask"].reshape(-1), [3], 4096)
+    n, ma, mr = H.compare_dlogits_rows(d, w, seed, rows, 0, ref["tokens"].reshape(-1), np.repeat(eps, w.T), w.N,
+                                       what=f"{test} dlogits", inv_temp=a)
+    H.record(test, w.name, seed, "dlogits (group 3 whole + 4096 random rows)", n, ma, mr, tol="1 bf16 ulp")

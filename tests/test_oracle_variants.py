@@ -78,3 +78,23 @@ def test_inverse_temperature_scaling_identity_and_fd():
         m[idx] -= 1e-5
         fd[idx] = (loss(p) - loss(m)) / 2e-5
     assert np.max(np.abs(fd - h["dlogits"])) / np.max(np.abs(h["dlogits"])) < 1e-6
+
+
+def test_row_functions_with_temperature_equal_the_head():
+    """token_logprob_rows / dlogits_row with inv_temp (what the full-size harness calls) equal the
+    per-row entries of vargrad_head(inv_temp=...) (itself pinned by FD and the scaling identity)."""
+    rng = np.random.default_rng(9)
+    N, T, V, K = 4, 3, 11, 2
+    z = rng.normal(0, 2, (N, T, V))
+    tok = rng.integers(0, V, (N, T))
+    mask = np.ones((N, T), np.uint8)
+    ref, rew = rng.normal(-5, 1, N), rng.normal(0, 1, N)
+    a = 1 / 0.7
+    h = O.vargrad_head(z, tok, mask, ref, rew, 0.4, K, inv_temp=a, grad_out=1.3)
+    lp, _ = O.token_logprob_rows(z.reshape(N * T, V), tok.reshape(-1), inv_temp=a)
+    ell, _ = O.sequence_sums(lp.reshape(N, T), mask)
+    np.testing.assert_allclose(ell, h["ell"], rtol=0, atol=1e-13)
+    for s in range(N):
+        for t in range(T):
+            np.testing.assert_allclose(O.dlogits_row(z[s, t], int(tok[s, t]), h["eps"][s], N, 1.3, inv_temp=a),
+                                       h["dlogits"][s, t], rtol=0, atol=1e-15)
