@@ -171,8 +171,17 @@ def compare_dlogits_rows(d, w: syn.Workload, seed: int, flat_rows, row_base: int
     V = w.V
     dv = d.reshape(-1, V) if d.is_contiguous() else d.view(-1, V)
     gdt = "bf16" if d.dtype == torch.bfloat16 else "fp32"
-    path = f"/dev/shm/tba_parity_{os.getpid()}.bin"
-    cap = min(chunk, len(flat_rows))
+    # the GPU rows go to the workers through a memory-mapped file: /dev/shm when it has room (a
+    # container's /dev/shm can be 64 MB), else the temp directory; the chunk shrinks to fit
+    row_bytes = V * (2 if gdt == "bf16" else 4)
+    import tempfile
+    d_ = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+    free = os.statvfs(d_).f_bavail * os.statvfs(d_).f_frsize
+    if free < 4 * row_bytes * min(chunk, max(len(flat_rows), 1)):
+        d_ = tempfile.gettempdir()
+        free = os.statvfs(d_).f_bavail * os.statvfs(d_).f_frsize
+    path = os.path.join(d_, f"tba_parity_{os.getpid()}.bin")
+    cap = max(1, min(chunk, len(flat_rows), int(free // (2 * row_bytes))))
     tot_bad, max_abs, max_ratio, worst = 0, 0.0, 0.0, None
     if cap == 0:
         return 0, 0.0, 0.0
