@@ -10,7 +10,7 @@ namespace {
 // the UNSCALED gradient G = inv_temp (1[v=y] - softmax) once. HBM bytes: 2V read + 2V write per
 // valid row (the 4V floor); the per-sequence factor grad_scale * g * eps_s is applied by the
 // consumer (the LM-head backward, as a row scale), SURVEY §8(f) NEXT 2.
-template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false>
+template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false, int U1 = 4>
 __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                 int64_t stride, const int64_t* __restrict__ tokens,
                                                 const uint8_t* __restrict__ mask, RowScale rs,
@@ -40,7 +40,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     if (threadIdx.x == 0) sh_y = yt;
     OnlineState st;
     st.init(rs);
-    fwd_accumulate<T, 4, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
+    fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
     combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     if (lane == 0) {
       sm_m[warp] = M;
@@ -103,15 +103,15 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <class T, class TO, int NT, int U2 = 4, bool REV = false>
+template <class T, class TO, int NT, int U2 = 4, bool REV = false, int U1 = 4>
 __global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                   int64_t stride, const int64_t* __restrict__ tokens,
                                                   const uint8_t* __restrict__ mask, RowScale rs,
                                                   float2* __restrict__ stats, float* __restrict__ qy,
                                                   double* __restrict__ lp, int32_t* dev_status,
                                                   TO* __restrict__ g_out, int64_t ostride) {
-  row_single_body<T, TO, NT, 1, U2, REV>(logits, rows, V, stride, tokens, mask, rs, stats, qy, lp, dev_status, g_out,
-                                         ostride);
+  row_single_body<T, TO, NT, 1, U2, REV, U1>(logits, rows, V, stride, tokens, mask, rs, stats, qy, lp, dev_status,
+                                             g_out, ostride);
 }
 
 // ------------------------------------------------------------------------------ SMEM-resident rows
@@ -491,15 +491,29 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
   // vectors are re-read first).
   const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
   const bool small = rb <= 128 * 1024;
-#define TBA_SINGLE1(T_, TO_, NT_, U2_)                                                                          \
-  row_single1<T_, TO_, NT_, U2_, true><<<(unsigned)rows, NT_, 0, s>>>(                                         \
+#define TBA_SINGLE1(T_, TO_, NT_, U2_, ...)                                                                     \
+  row_single1<T_, TO_, NT_, U2_, true, ##__VA_ARGS__><<<(unsigned)rows, NT_, 0, s>>>(                          \
       static_cast<const T_*>(x->logits), rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, w.qy, w.lp, \
       dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride)
+#ifndef TBA_AB_DEFER_CFG
 #define TBA_SINGLE(T_, TO_)                   \
   do {                                        \
     if (small) TBA_SINGLE1(T_, TO_, 256, 4);  \
     else TBA_SINGLE1(T_, TO_, 512, 8);        \
   } while (0)
+#elif TBA_AB_DEFER_CFG == 1  // A/B: 8 vectors per thread in flight in pass 1 too
+#define TBA_SINGLE(T_, TO_)                     \
+  do {                                          \
+    if (small) TBA_SINGLE1(T_, TO_, 256, 4, 8); \
+    else TBA_SINGLE1(T_, TO_, 512, 8, 8);       \
+  } while (0)
+#elif TBA_AB_DEFER_CFG == 2  // A/B: 1024 threads per row
+#define TBA_SINGLE(T_, TO_)                     \
+  do {                                          \
+    if (small) TBA_SINGLE1(T_, TO_, 512, 4);    \
+    else TBA_SINGLE1(T_, TO_, 1024, 8);         \
+  } while (0)
+#endif
   if (x->dtype == TBA_BF16) {
     if (g_dtype == TBA_BF16) TBA_SINGLE(uint16_t, uint16_t);
     else TBA_SINGLE(uint16_t, float);
