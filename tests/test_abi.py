@@ -194,6 +194,7 @@ def test_lmhead_bwd_validation(L):
     assert _lmb(L, x, dhs=32) == bad                      # dhidden row stride < d
     assert _lmb(L, x, dh=FAKE + 2) == bad                 # misaligned fp32 dhidden
     assert _lmb(L, x, dh=FAKE) == bad                     # dhidden aliases hidden
+    assert _lmb(L, x, dh=FAKE + 64) == bad                # dhidden overlaps hidden from its second element on
     assert _lmb(L, x, dws=63) == bad                      # dweight row stride < d
     assert _lmb(L, x, dw=FAKE + 0x20002) == bad           # misaligned dweight
     assert _lmb(L, x, bws=0x200010) == bad                # misaligned bwd workspace
