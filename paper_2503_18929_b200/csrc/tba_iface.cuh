@@ -6,18 +6,21 @@
 //   fwd.cu       row_fwd_rows  a1   stream each valid logits row from HBM once (TPR threads per
 //                                   row, 128-bit loads): online max + sum of 2^(z*sc - R2), one
 //                                   ex2 per element (packed FFMA2/FADD2; 1 of 4 pairs on the FMA
-//                                   pipe), gather z[y]; writes per-row (M2, log2 S) and the token
-//                                   log-prob (fp64).
+//                                   pipe), gather z[y]; the token's own term kept out of the
+//                                   sum; writes per-row (M2, log2 S), 1 - p_y and the token
+//                                   log-prob (fp64). PDL-chained to seq_head and row_bwd.
 //   head.cu      seq_head      a2+a3 per-sequence fixed-order fp64 sums of token log-probs
 //                                   (log pi(y|x)) and token counts; per group Eq. 4 log Z (or a
 //                                   learned log Z, Eq. 3) and the Eq. 5 residuals; the last CTA
-//                                   reduces the per-group sums of squares (+ peer all-reduce).
+//                                   reduces the per-group sums of squares.
 //                tbap_head     a2+a3' TBA' (Eq. 16): per-group advantages, per-token IS-weighted
 //                                   coefficients.
 //   bwd.cu       row_bwd       a5   stream each valid row again: dz = c (1[v=y] - softmax); c per
 //                                   sequence (TB) or per token (TBA'); masked rows zero-filled.
 //   fused.cu     tb_fused      a1-a5 in one persistent launch (NEXT 2 (i)).
-//   deferred.cu  row_single*   a1 + unscaled a5 in one pass per row (NEXT 2 (ii)).
+//   deferred.cu  row_single1   a1 + unscaled a5 in one pass per row (NEXT 2 (ii)); row_smem (rows
+//                                   kept in shared memory) in the TBA_AB_DEFER_SMEM A/B build only.
+//   lmhead*.cu   NEXT 3: the tcgen05 LM-head GEMMs (forward with the softmax epilogue, dz / dH / dW).
 // No float atomics: every output is bitwise reproducible run to run.
 #pragma once
 #include <cstdint>
