@@ -405,8 +405,9 @@ static int tbap_fwd_impl(const tba_rows* x, const float* gen_logp, const double*
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (x->n_seq == 0)  // a rank with zero groups contributes zero partials
     return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
-  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv || !coef ||
-      (x->seq_len > 0 && !gen_logp))
+  // gen_logp and coef are [N, T]: null is legal when T == 0 (an empty tensor has no storage)
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv ||
+      (x->seq_len > 0 && (!gen_logp || !coef)))
     return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(gen_logp) % 4 ||
       reinterpret_cast<uintptr_t>(coef) % 4)
@@ -520,8 +521,9 @@ int tba_lmhead_tbap_loss_fwd(const tba_lmhead* x, const float* gen_logp, const d
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (x->n_seq == 0)
     return cudaMemsetAsync(partial, 0, 3 * sizeof(double), s) == cudaSuccess ? TBA_OK : TBA_ERR_CUDA;
-  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv || !coef ||
-      (x->seq_len > 0 && !gen_logp))
+  // gen_logp and coef are [N, T]: null is legal when T == 0 (an empty tensor has no storage)
+  if (!workspace || !ref_logp || !log_reward || !seq_logp || !n_tokens || !adv ||
+      (x->seq_len > 0 && (!gen_logp || !coef)))
     return TBA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(workspace) % 256 || reinterpret_cast<uintptr_t>(gen_logp) % 4 ||
       reinterpret_cast<uintptr_t>(coef) % 4)
