@@ -33,6 +33,13 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   const T* rp = logits + (live ? row : 0) * stride;
   TO* op = g_out + (live ? row : 0) * ostride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef TBA_AB_DEFER_STASH
+  // A/B: the row's first TBA_AB_DEFER_STASH KB of 16-byte vectors stay in shared memory between the
+  // passes (pass 2 reads them on chip; only the rest must survive in L2)
+  extern __shared__ __align__(16) uint4 ds_stash[];
+  const int64_t nvec_all = (V - head_elems(rp, V)) / Elem<T>::VEC;
+  const int ds_ks = (int)(nvec_all < (int64_t)TBA_AB_DEFER_STASH * 64 ? nvec_all : (int64_t)TBA_AB_DEFER_STASH * 64);
+#endif
   float M = -INFINITY, M2 = 0.f;
   double S = 0.0;
   if (valid) {
@@ -40,7 +47,12 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     if (threadIdx.x == 0) sh_y = yt;
     OnlineState st;
     st.init(rs);
+#ifdef TBA_AB_DEFER_STASH
+    fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true), ds_stash,
+                                ds_ks);
+#else
     fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
+#endif
     combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     if (lane == 0) {
       sm_m[warp] = M;
@@ -98,8 +110,13 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     sh_qy = qy[row];
   }
   __syncthreads();
+#ifdef TBA_AB_DEFER_STASH
+  bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
+                                make_policy(false), ds_stash, ds_ks);
+#else
   bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
                                 make_policy(false));
+#endif
   if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
@@ -491,10 +508,23 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
   // vectors are re-read first).
   const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
   const bool small = rb <= 128 * 1024;
+#ifdef TBA_AB_DEFER_STASH
+  const size_t dsm = (size_t)TBA_AB_DEFER_STASH * 1024;
+#else
+  const size_t dsm = 0;
+#endif
 #define TBA_SINGLE1(T_, TO_, NT_, U2_, ...)                                                                     \
-  row_single1<T_, TO_, NT_, U2_, true, ##__VA_ARGS__><<<(unsigned)rows, NT_, 0, s>>>(                          \
+  do {                                                                                                          \
+    static bool attr_ = false;                                                                                  \
+    if (dsm > 48 * 1024 && !attr_) {                                                                            \
+      cudaFuncSetAttribute(row_single1<T_, TO_, NT_, U2_, true, ##__VA_ARGS__>,                                 \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);                               \
+      attr_ = true;                                                                                             \
+    }                                                                                                           \
+    row_single1<T_, TO_, NT_, U2_, true, ##__VA_ARGS__><<<(unsigned)rows, NT_, dsm, s>>>(                       \
       static_cast<const T_*>(x->logits), rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, w.qy, w.lp, \
-      dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride)
+      dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride);                                             \
+  } while (0)
 #ifndef TBA_AB_DEFER_CFG
 #define TBA_SINGLE(T_, TO_)                   \
   do {                                        \
@@ -506,6 +536,12 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
   do {                                          \
     if (small) TBA_SINGLE1(T_, TO_, 256, 4, 8); \
     else TBA_SINGLE1(T_, TO_, 512, 8, 8);       \
+  } while (0)
+#elif TBA_AB_DEFER_CFG == 3  // A/B: 512 threads per row for every row length
+#define TBA_SINGLE(T_, TO_)                     \
+  do {                                          \
+    if (small) TBA_SINGLE1(T_, TO_, 512, 8);    \
+    else TBA_SINGLE1(T_, TO_, 512, 8);          \
   } while (0)
 #elif TBA_AB_DEFER_CFG == 2  // A/B: 1024 threads per row
 #define TBA_SINGLE(T_, TO_)                     \
