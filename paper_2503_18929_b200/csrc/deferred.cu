@@ -10,7 +10,7 @@ namespace {
 // the UNSCALED gradient G = inv_temp (1[v=y] - softmax) once. HBM bytes: 2V read + 2V write per
 // valid row (the 4V floor); the per-sequence factor grad_scale * g * eps_s is applied by the
 // consumer (the LM-head backward, as a row scale), SURVEY §8(f) NEXT 2.
-template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false, int U1 = 4>
+template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false, int U1 = 4, int STASH_KB = 0>
 __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                 int64_t stride, const int64_t* __restrict__ tokens,
                                                 const uint8_t* __restrict__ mask, RowScale rs,
@@ -33,13 +33,11 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   const T* rp = logits + (live ? row : 0) * stride;
   TO* op = g_out + (live ? row : 0) * ostride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef TBA_AB_DEFER_STASH
-  // A/B: the row's first TBA_AB_DEFER_STASH KB of 16-byte vectors stay in shared memory between the
-  // passes (pass 2 reads them on chip; only the rest must survive in L2)
+  // STASH_KB > 0: the row's first STASH_KB KB of 16-byte vectors stay in shared memory between the
+  // passes (pass 2 reads them on chip; only the rest of the row must survive in L2)
   extern __shared__ __align__(16) uint4 ds_stash[];
   const int64_t nvec_all = (V - head_elems(rp, V)) / Elem<T>::VEC;
-  const int ds_ks = (int)(nvec_all < (int64_t)TBA_AB_DEFER_STASH * 64 ? nvec_all : (int64_t)TBA_AB_DEFER_STASH * 64);
-#endif
+  const int ds_ks = (int)(nvec_all < (int64_t)STASH_KB * 64 ? nvec_all : (int64_t)STASH_KB * 64);
   float M = -INFINITY, M2 = 0.f;
   double S = 0.0;
   if (valid) {
@@ -47,12 +45,8 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     if (threadIdx.x == 0) sh_y = yt;
     OnlineState st;
     st.init(rs);
-#ifdef TBA_AB_DEFER_STASH
-    fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true), ds_stash,
-                                ds_ks);
-#else
-    fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
-#endif
+    fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true),
+                                STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
     combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     if (lane == 0) {
       sm_m[warp] = M;
@@ -110,25 +104,20 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     sh_qy = qy[row];
   }
   __syncthreads();
-#ifdef TBA_AB_DEFER_STASH
   bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
-                                make_policy(false), ds_stash, ds_ks);
-#else
-  bwd_row<T, TO, U2, true, REV>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
-                                make_policy(false));
-#endif
+                                make_policy(false), STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
   if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <class T, class TO, int NT, int U2 = 4, bool REV = false, int U1 = 4>
+template <class T, class TO, int NT, int U2 = 4, bool REV = false, int U1 = 4, int STASH_KB = 0>
 __global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                   int64_t stride, const int64_t* __restrict__ tokens,
                                                   const uint8_t* __restrict__ mask, RowScale rs,
                                                   float2* __restrict__ stats, float* __restrict__ qy,
                                                   double* __restrict__ lp, int32_t* dev_status,
                                                   TO* __restrict__ g_out, int64_t ostride) {
-  row_single_body<T, TO, NT, 1, U2, REV, U1>(logits, rows, V, stride, tokens, mask, rs, stats, qy, lp, dev_status,
-                                             g_out, ostride);
+  row_single_body<T, TO, NT, 1, U2, REV, U1, STASH_KB>(logits, rows, V, stride, tokens, mask, rs, stats, qy, lp,
+                                                       dev_status, g_out, ostride);
 }
 
 // ------------------------------------------------------------------------------ SMEM-resident rows
@@ -508,48 +497,26 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
   // vectors are re-read first).
   const int64_t rb = x->vocab * (x->dtype == TBA_BF16 ? 2 : 4);
   const bool small = rb <= 128 * 1024;
-#ifdef TBA_AB_DEFER_STASH
-  const size_t dsm = (size_t)TBA_AB_DEFER_STASH * 1024;
-#else
-  const size_t dsm = 0;
-#endif
-#define TBA_SINGLE1(T_, TO_, NT_, U2_, ...)                                                                     \
+#define TBA_SINGLE1(T_, TO_, NT_, U2_, U1_, SKB_)                                                                \
   do {                                                                                                          \
     static bool attr_ = false;                                                                                  \
+    const size_t dsm = (size_t)(SKB_) * 1024;                                                                   \
     if (dsm > 48 * 1024 && !attr_) {                                                                            \
-      cudaFuncSetAttribute(row_single1<T_, TO_, NT_, U2_, true, ##__VA_ARGS__>,                                 \
+      cudaFuncSetAttribute(row_single1<T_, TO_, NT_, U2_, true, U1_, SKB_>,                                      \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);                               \
       attr_ = true;                                                                                             \
     }                                                                                                           \
-    row_single1<T_, TO_, NT_, U2_, true, ##__VA_ARGS__><<<(unsigned)rows, NT_, dsm, s>>>(                       \
+    row_single1<T_, TO_, NT_, U2_, true, U1_, SKB_><<<(unsigned)rows, NT_, dsm, s>>>(                            \
       static_cast<const T_*>(x->logits), rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, w.qy, w.lp, \
       dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride);                                             \
   } while (0)
-#ifndef TBA_AB_DEFER_CFG
-#define TBA_SINGLE(T_, TO_)                   \
-  do {                                        \
-    if (small) TBA_SINGLE1(T_, TO_, 256, 4);  \
-    else TBA_SINGLE1(T_, TO_, 512, 8);        \
+  // rows <= 128 KB: 256 threads per row; longer: 512 threads, 8 vectors per thread in flight in pass
+  // 2, and the row's first 104 KB kept in shared memory between the passes
+#define TBA_SINGLE(T_, TO_)                          \
+  do {                                               \
+    if (small) TBA_SINGLE1(T_, TO_, 256, 4, 4, 0);   \
+    else TBA_SINGLE1(T_, TO_, 512, 8, 4, 104);       \
   } while (0)
-#elif TBA_AB_DEFER_CFG == 1  // A/B: 8 vectors per thread in flight in pass 1 too
-#define TBA_SINGLE(T_, TO_)                     \
-  do {                                          \
-    if (small) TBA_SINGLE1(T_, TO_, 256, 4, 8); \
-    else TBA_SINGLE1(T_, TO_, 512, 8, 8);       \
-  } while (0)
-#elif TBA_AB_DEFER_CFG == 3  // A/B: 512 threads per row for every row length
-#define TBA_SINGLE(T_, TO_)                     \
-  do {                                          \
-    if (small) TBA_SINGLE1(T_, TO_, 512, 8);    \
-    else TBA_SINGLE1(T_, TO_, 512, 8);          \
-  } while (0)
-#elif TBA_AB_DEFER_CFG == 2  // A/B: 1024 threads per row
-#define TBA_SINGLE(T_, TO_)                     \
-  do {                                          \
-    if (small) TBA_SINGLE1(T_, TO_, 512, 4);    \
-    else TBA_SINGLE1(T_, TO_, 1024, 8);         \
-  } while (0)
-#endif
   if (x->dtype == TBA_BF16) {
     if (g_dtype == TBA_BF16) TBA_SINGLE(uint16_t, uint16_t);
     else TBA_SINGLE(uint16_t, float);
