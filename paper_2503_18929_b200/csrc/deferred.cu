@@ -511,11 +511,15 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
       dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride);                                             \
   } while (0)
   // rows <= 128 KB: 256 threads per row; longer: 512 threads, 8 vectors per thread in flight in pass
-  // 2, and the row's first 104 KB kept in shared memory between the passes
-#define TBA_SINGLE(T_, TO_)                          \
-  do {                                               \
-    if (small) TBA_SINGLE1(T_, TO_, 256, 4, 4, 0);   \
-    else TBA_SINGLE1(T_, TO_, 512, 8, 4, 104);       \
+  // 2, and the row's first TBA_DEFER_STASH_KB KB kept in shared memory between the passes (DESIGN.md
+  // §5.4; A/B builds may override the size)
+#ifndef TBA_DEFER_STASH_KB
+#define TBA_DEFER_STASH_KB 96
+#endif
+#define TBA_SINGLE(T_, TO_)                                       \
+  do {                                                            \
+    if (small) TBA_SINGLE1(T_, TO_, 256, 4, 4, 0);                \
+    else TBA_SINGLE1(T_, TO_, 512, 8, 4, TBA_DEFER_STASH_KB);     \
   } while (0)
   if (x->dtype == TBA_BF16) {
     if (g_dtype == TBA_BF16) TBA_SINGLE(uint16_t, uint16_t);
