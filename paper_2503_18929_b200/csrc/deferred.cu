@@ -10,6 +10,70 @@ namespace {
 // the UNSCALED gradient G = inv_temp (1[v=y] - softmax) once. HBM bytes: 2V read + 2V write per
 // valid row (the 4V floor); the per-sequence factor grad_scale * g * eps_s is applied by the
 // consumer (the LM-head backward, as a row scale), SURVEY §8(f) NEXT 2.
+// Pass 1 of a long row with a shared-memory stash: the stash part (the row's first ks vectors) is
+// fetched with cp.async straight into shared memory — all of it in flight at once, no registers held —
+// while the threads stream the rest of the row through registers (L2 evict_last, for pass 2); then
+// the stash part is consumed from shared memory. The sampled token's element is excluded as in
+// fwd_accumulate (finalize_row adds it).
+template <class T, int U>
+__device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int64_t V, int tid, int nthr,
+                                                  OnlineState& st, int64_t y, uint4* __restrict__ stash, int ks) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const int64_t h = head_elems(rp, V);
+  const int64_t nvec = (V - h) / VEC;
+  const int64_t tail0 = h + nvec * VEC;
+  const uint4* vp = reinterpret_cast<const uint4*>(rp + h);
+  const uint64_t pol_first = make_policy(false), pol_last = make_policy(true);
+  for (int64_t k = tid; k < ks; k += nthr)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(stash + k)),
+                 "l"(vp + k), "l"(pol_first)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (tid < h) {
+    const float z = E::load1(rp + tid);
+    if (tid == y) st.add1_excl(z);
+    else st.add1(z);
+  }
+  for (int64_t i = tail0 + tid; i < V; i += nthr) {
+    const float z = E::load1(rp + i);
+    if (i == y) st.add1_excl(z);
+    else st.add1(z);
+  }
+  const int64_t ky = (y >= h && y < tail0) ? (y - h) / VEC : -1;
+  const int ey = ky >= 0 ? (int)((y - h) - ky * VEC) : 0;
+  const int64_t step = (int64_t)nthr * U;
+  int64_t k0 = ks + tid;
+  for (; k0 + (int64_t)(U - 1) * nthr < nvec; k0 += step) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldg_pol(vp + k0 + (int64_t)u * nthr, pol_last);
+    const int64_t kr = ky - k0;
+    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, 0, true>(v, st, (int)(kr / nthr), ey);
+    else fwd_consume<T, U>(v, st);
+  }
+  for (int64_t k = k0; k < nvec; k += nthr) {
+    uint4 v1[1] = {ldg_pol(vp + k, pol_last)};
+    if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
+    else fwd_consume<T, 1>(v1, st);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own copies are in shared memory
+  int64_t j0 = tid;
+  for (; j0 + (int64_t)(U - 1) * nthr < ks; j0 += step) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = stash[j0 + (int64_t)u * nthr];
+    const int64_t kr = ky - j0;
+    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, 0, true>(v, st, (int)(kr / nthr), ey);
+    else fwd_consume<T, U>(v, st);
+  }
+  for (int64_t k = j0; k < ks; k += nthr) {
+    uint4 v1[1] = {stash[k]};
+    if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
+    else fwd_consume<T, 1>(v1, st);
+  }
+}
+
 template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false, int U1 = 4, int STASH_KB = 0>
 __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                 int64_t stride, const int64_t* __restrict__ tokens,
@@ -45,8 +109,13 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     if (threadIdx.x == 0) sh_y = yt;
     OnlineState st;
     st.init(rs);
-    fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true),
-                                STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
+#ifdef TBA_AB_DEFER_ASYNC
+    if (STASH_KB > 0)
+      defer_pass1_async<T, U1>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, ds_stash, ds_ks);
+    else
+#endif
+      fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true),
+                                  STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
     combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     if (lane == 0) {
       sm_m[warp] = M;
