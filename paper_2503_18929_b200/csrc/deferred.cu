@@ -109,13 +109,10 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     if (threadIdx.x == 0) sh_y = yt;
     OnlineState st;
     st.init(rs);
-#ifdef TBA_AB_DEFER_ASYNC
-    if (STASH_KB > 0)
+    if (STASH_KB > 0)  // the stash part fetched with cp.async, all of it in flight at once
       defer_pass1_async<T, U1>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, ds_stash, ds_ks);
     else
-#endif
-      fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true),
-                                  STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
+      fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
     combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     if (lane == 0) {
       sm_m[warp] = M;

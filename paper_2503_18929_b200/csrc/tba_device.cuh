@@ -309,8 +309,7 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 // (index y; y < 0 or >= V: none) enters the max but not the sum (finalize_row adds its term).
 template <class T, int U, bool POL = false, int NP = 0>
 __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_t V, int tid, int nthr,
-                                               OnlineState& st, int64_t y, uint64_t pol = 0,
-                                               uint4* __restrict__ stash = nullptr, int ks = 0) {
+                                               OnlineState& st, int64_t y, uint64_t pol = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(row, V);
@@ -343,11 +342,6 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
 #pragma unroll
     for (int u = 0; u < U; ++u)
       v[u] = POL ? ldg_pol(vp + k0 + (int64_t)u * nthr, pol) : ldg_stream(vp + k0 + (int64_t)u * nthr);
-    if (stash != nullptr) {  // keep the row's first ks vectors on chip for a second pass
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (k0 + (int64_t)u * nthr < ks) stash[k0 + (int64_t)u * nthr] = v[u];
-    }
 #ifdef TBA_AB_NO_EXCL
     fwd_consume<T, U, NP>(v, st);
 #else
@@ -357,7 +351,6 @@ __device__ __forceinline__ void fwd_accumulate(const T* __restrict__ row, int64_
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k)};
-    if (stash != nullptr && k < ks) stash[k] = v1[0];
     if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
     else fwd_consume<T, 1>(v1, st);
   }
