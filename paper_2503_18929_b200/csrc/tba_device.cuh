@@ -88,6 +88,11 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 
 // 2^x for a pair of fp32 on the FMA pipe (offloads MUFU.EX2, which the forward saturates first):
 // Cody-Waite split x = n + f, |f| <= 1/2, by the 1.5*2^23 rounding trick; degree-5 minimax
@@ -588,8 +593,10 @@ __device__ __forceinline__ void store_vals(TO* o, const float (&d)[N]) {
 // REV: walk the row's vectors from the end (the deferred pass re-reads a row it has just streamed:
 // its last vectors are the most recently touched in L2).
 // dz_v = -c p_v for v != y and c (1 - p_y) at the token, with 1 - p_y = qy from the forward (exact
-// when p_y -> 1, where c - c p_y would cancel).
-template <class T, class TO, int U, bool POL = false, bool REV = false>
+// when p_y -> 1, where c - c p_y would cancel). TOK_LATE: the token's entry is stored after the loop
+// by the thread that stored its vector (same thread, same address: program order decides) instead
+// of a per-vector test — faster in the deferred pass, slower in row_bwd (measured).
+template <class T, class TO, int U, bool POL = false, bool REV = false, bool TOK_LATE = false>
 __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid, int nthr,
                                         bool valid, float sc, float M2, float L2S, float c, int64_t y, float qy,
                                         uint64_t pol = 0, const uint4* __restrict__ stash = nullptr, int ks = 0) {
@@ -620,7 +627,9 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
     for (int64_t k = tid; k < nvec; k += nthr) store_vals<TO, VEC>(ob + k * VEC, z);
     return;
   }
-  const float nM2 = -M2;
+  // d_v = -c 2^(z_v sc - M2 - L2S) in fp32 pairs (FFMA2 / FADD2 / FMUL2: per lane the same roundings
+  // as the scalar fmaf, subtraction and product)
+  const uint64_t sc2 = f2_pack(sc, sc), nM2 = f2_pack(-M2, -M2), nL2S = f2_pack(-L2S, -L2S), nc = f2_pack(-c, -c);
   const int64_t ky = (y >= h && y < vend) ? (y - h) / VEC : -1;
   for (int64_t k0 = tid; k0 < nvec; k0 += (int64_t)nthr * U) {
     uint4 v[U];
@@ -640,8 +649,13 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
       if (kf < nvec) {
         float d[VEC];
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) d[e] = -c * ex2(fmaf(E::get(v[u], e), sc, nM2) - L2S);
-        if (k == ky) {
+        for (int e = 0; e < VEC; e += 2) {
+          const uint64_t x = fadd2(ffma2(f2_pack(E::get(v[u], e), E::get(v[u], e + 1)), sc2, nM2), nL2S);
+          float a, b;
+          f2_unpack(x, a, b);
+          f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
+        }
+        if (!TOK_LATE && k == ky) {
           const int e = (int)((y - h) - k * VEC);
 #pragma unroll
           for (int q = 0; q < VEC; ++q)
@@ -650,6 +664,10 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
         store_vals<TO, VEC>(ob + k * VEC, d);
       }
     }
+  }
+  if (TOK_LATE && ky >= 0) {
+    const int64_t kf = REV ? nvec - 1 - ky : ky;
+    if (kf % nthr == tid) Out<TO>::put1(op + y, c * qy);
   }
 }
 

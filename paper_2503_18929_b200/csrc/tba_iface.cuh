@@ -18,8 +18,9 @@
 //   bwd.cu       row_bwd       a5   stream each valid row again: dz = c (1[v=y] - softmax); c per
 //                                   sequence (TB) or per token (TBA'); masked rows zero-filled.
 //   fused.cu     tb_fused      a1-a5 in one persistent launch (NEXT 2 (i)).
-//   deferred.cu  row_single1   a1 + unscaled a5 in one pass per row (NEXT 2 (ii)); row_smem (rows
-//                                   kept in shared memory) in the TBA_AB_DEFER_SMEM A/B build only.
+//   deferred.cu  row_single1   a1 + unscaled a5 in one pass per row (NEXT 2 (ii)): pass 1 from HBM
+//                                   (long rows: the first 96 KB into shared memory by cp.async), pass 2
+//                                   from shared memory and L2.
 //   lmhead*.cu   NEXT 3: the tcgen05 LM-head GEMMs (forward with the softmax epilogue, dz / dH / dW).
 // No float atomics: every output is bitwise reproducible run to run.
 #pragma once
