@@ -111,6 +111,72 @@ __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int6
   }
 }
 
+// Pass 2 of the deferred kernel: G over the row, swept backwards through its L2 part (vectors
+// [ks, nvec), the last-streamed ones first, while still in L2) and then its shared-memory stash
+// (vectors [0, ks)); full iterations carry no bounds or stash tests (32-bit vector indices). The
+// arithmetic is bwd_row's (fp32 pairs, the same roundings); the token's entry is stored last by the
+// thread that stored its vector.
+template <class T, class TO, int U>
+__device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid,
+                                            int nthr, float sc, float M2, float L2S, float c, int64_t y, float qy,
+                                            const uint4* __restrict__ stash, int ks) {
+  using E = Elem<T>;
+  constexpr int VEC = E::VEC;
+  const int64_t h = head_elems(rp, V);
+  if (((reinterpret_cast<uint64_t>(op + h) & 15u) != 0) || stash == nullptr) {  // output not co-aligned
+    bwd_row<T, TO, U, true, true, true>(rp, op, V, tid, nthr, true, sc, M2, L2S, c, y, qy, make_policy(false), stash,
+                                       ks);
+    return;
+  }
+  const int nvec = (int)((V - h) / VEC);
+  const int64_t vend = h + (int64_t)nvec * VEC;
+  auto one = [&](int64_t i) {
+    const float p = ex2(fmaf(E::load1(rp + i), sc, -M2) - L2S);
+    Out<TO>::put1(op + i, (i == y) ? c * qy : -c * p);
+  };
+  for (int64_t i = tid; i < h; i += nthr) one(i);
+  for (int64_t i = vend + tid; i < V; i += nthr) one(i);
+  const uint4* vp = reinterpret_cast<const uint4*>(rp + h);
+  TO* ob = op + h;
+  const uint64_t sc2 = f2_pack(sc, sc), nM2 = f2_pack(-M2, -M2), nL2S = f2_pack(-L2S, -L2S), nc = f2_pack(-c, -c);
+  auto emit = [&](const uint4& v, int k) {
+    float d[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) {
+      const uint64_t x = fadd2(ffma2(f2_pack(E::get(v, e), E::get(v, e + 1)), sc2, nM2), nL2S);
+      float a, b;
+      f2_unpack(x, a, b);
+      f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
+    }
+    store_vals<TO, VEC>(ob + (int64_t)k * VEC, d);
+  };
+  const uint64_t pol = make_policy(false);
+  const int nl2 = nvec - ks;  // swept index f in [0, nl2) is vector nvec - 1 - f
+  int f0 = tid;
+  for (; f0 + (U - 1) * nthr < nl2; f0 += nthr * U) {
+    const uint4* p = vp + (nvec - 1 - f0);
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldg_pol(p - u * nthr, pol);
+#pragma unroll
+    for (int u = 0; u < U; ++u) emit(v[u], nvec - 1 - f0 - u * nthr);
+  }
+  for (; f0 < nl2; f0 += nthr) emit(ldg_pol(vp + (nvec - 1 - f0), pol), nvec - 1 - f0);
+  int j0 = tid;
+  for (; j0 + 3 * nthr < ks; j0 += nthr * 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = stash[j0 + u * nthr];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) emit(v[u], j0 + u * nthr);
+  }
+  for (; j0 < ks; j0 += nthr) emit(stash[j0], j0);
+  if (y >= h && y < vend) {
+    const int ky = (int)((y - h) / VEC);
+    if ((ky >= ks ? (nvec - 1 - ky) : ky) % nthr == tid) Out<TO>::put1(op + y, c * qy);
+  }
+}
+
 template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false, int U1 = 4, int STASH_KB = 0>
 __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
                                                 int64_t stride, const int64_t* __restrict__ tokens,
@@ -245,8 +311,11 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   }
   __syncthreads();
   TR(4);
-  bwd_row<T, TO, U2, true, REV, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
-                                make_policy(false), STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
+  if constexpr (STASH_KB > 0 && CS == 1 && REV)
+    defer_pass2<T, TO, U2>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy, ds_stash, ds_ks);
+  else
+    bwd_row<T, TO, U2, true, REV, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
+                                        sh_qy, make_policy(false), STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
   TR(5);
   if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
