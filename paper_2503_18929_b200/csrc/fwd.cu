@@ -35,11 +35,11 @@ int launch_fwd_rows_t(const T* lg, const tba_rows* x, const WsLayout& w, const R
 #define TBA_ROWS(TPR_, NP_)                                                                                     \
   return launch_pdl(row_fwd_rows<T, TPR_, kU, NP_>, dim3(grid), dim3(256), 0, s, lg, rows, x->vocab, x->row_stride, \
                     x->tokens, x->mask, rs, w.stats, w.qy, w.lp, dev_status, w.counter)
-  // 64 threads per row: 1 of the 4 element pairs per 16-byte vector takes the FMA-pipe exp2
-  // (exp2_poly2) instead of MUFU — relieves the XU pipe (75 % busy), +3 % forward bandwidth on
+  // 1 of the 4 element pairs per 16-byte vector (1 of 2 for fp32 rows) takes the FMA-pipe exp2
+  // (exp2_poly2) instead of MUFU — relieves the XU pipe (75 % busy), +1-3 % forward bandwidth on
   // every BASELINE shape; 2 of 4 over-loads the FMA/ALU pipes.
   if (tpr == 64) TBA_ROWS(64, 1);
-  TBA_ROWS(32, 0);
+  TBA_ROWS(32, 1);
 #undef TBA_ROWS
 }
 

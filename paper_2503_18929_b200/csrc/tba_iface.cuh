@@ -227,9 +227,10 @@ inline int env_once(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-// Forward threads per row, measured on B200: 64 threads (4 rows per CTA) is best
-// or within 1 % for V = 32000 ... 152064; one warp for short rows.
-inline int fwd_tpr(int64_t V, int64_t esz) { return (V * esz / 16) < 1024 ? 32 : 64; }
+// Forward threads per row, measured on B200: one warp per row (8 rows per CTA) for
+// rows under 128 KB (Pythia, red-teaming, the GSM8K / RhoMath presets: forward 1-3 % faster with the
+// polynomial offload), 64 threads (4 rows per CTA) for the 304 KB Qwen rows.
+inline int fwd_tpr(int64_t V, int64_t esz) { return (V * esz / 16) < 8192 ? 32 : 64; }
 
 // Backward threads per row: one CTA per long row, one warp per short row.
 inline int bwd_tpr(int64_t V, int64_t esz) { return V * esz <= kSmallRowBytes ? 32 : 256; }
