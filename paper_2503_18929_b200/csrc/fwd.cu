@@ -3,6 +3,17 @@
 
 namespace tba {
 namespace {
+#ifdef TBA_AB_FWD_TRACE
+// per row [smid, globaltimer at the group's start, at its end] (A/B build only,
+// scripts/microbench/fwd_trace.py)
+constexpr int FTR_ROWS = 1 << 19;
+__device__ unsigned long long g_ftrace[FTR_ROWS * 3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c));
+  return c;
+}
+#endif
 // TPR threads per row, 256/TPR rows per CTA (TPR = 32 ... 256). Each row group meets on its own
 // named barrier (ids 1..8); a masked row's group exits as a whole.
 template <class T, int TPR, int U, int NP = 0>
@@ -22,8 +33,19 @@ __global__ void __launch_bounds__(256, 4) row_fwd_rows(const T* __restrict__ log
   const int grp = threadIdx.x / TPR, gt = threadIdx.x % TPR;
   const int64_t row = (int64_t)blockIdx.x * RPC + grp;
   if (row >= rows || mask[row] == 0) return;
+#ifdef TBA_AB_FWD_TRACE
+  if (gt == 0 && row < FTR_ROWS) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_ftrace[row * 3] = sm;
+    g_ftrace[row * 3 + 1] = gtimer();
+  }
+#endif
   fwd_row_group<T, TPR, U, NP>(logits, row, V, stride, tokens, rs, stats, qy, lp, dev_status, sm_m, sm_M2, sm_s, grp,
                                gt);
+#ifdef TBA_AB_FWD_TRACE
+  if (gt == 0 && row < FTR_ROWS) g_ftrace[row * 3 + 2] = gtimer();
+#endif
 }
 
 template <class T>
@@ -56,3 +78,10 @@ int launch_fwd_rows(const tba_rows* x, const WsLayout& w, const RowScale& rs, in
 }
 
 }  // namespace tba
+
+#ifdef TBA_AB_FWD_TRACE
+extern "C" int tba_debug_fwd_trace(void* host, long long n) {
+  if (n > (long long)tba::FTR_ROWS * 3) n = (long long)tba::FTR_ROWS * 3;
+  return cudaMemcpyFromSymbol(host, tba::g_ftrace, (size_t)n * 8) == cudaSuccess ? 0 : 3;
+}
+#endif
