@@ -124,7 +124,7 @@ __device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __rest
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(rp, V);
-  if (((reinterpret_cast<uint64_t>(op + h) & 15u) != 0) || stash == nullptr) {  // output not co-aligned
+  if ((reinterpret_cast<uint64_t>(op + h) & 15u) != 0) {  // output not co-aligned
     bwd_row<T, TO, U, true, true, true>(rp, op, V, tid, nthr, true, sc, M2, L2S, c, y, qy, make_policy(false), stash,
                                        ks);
     return;
@@ -312,8 +312,13 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   }
   __syncthreads();
   TR(4);
+#ifdef TBA_AB_SMALL_P2
+  if constexpr (CS == 1 && REV)
+#else
   if constexpr (STASH_KB > 0 && CS == 1 && REV)
-    defer_pass2<T, TO, U2>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy, ds_stash, ds_ks);
+#endif
+    defer_pass2<T, TO, U2>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
+                           STASH_KB > 0 ? ds_stash : nullptr, STASH_KB > 0 ? ds_ks : 0);
   else
     bwd_row<T, TO, U2, true, REV, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
                                         sh_qy, make_policy(false), STASH_KB > 0 ? ds_stash : nullptr, ds_ks);

@@ -631,6 +631,41 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
   // as the scalar fmaf, subtraction and product)
   const uint64_t sc2 = f2_pack(sc, sc), nM2 = f2_pack(-M2, -M2), nL2S = f2_pack(-L2S, -L2S), nc = f2_pack(-c, -c);
   const int64_t ky = (y >= h && y < vend) ? (y - h) / VEC : -1;
+  if constexpr (!REV && !TOK_LATE) {
+    if (stash == nullptr) {
+      // full iterations with no bounds tests (32-bit vector indices; a row has < 2^31 vectors), then
+      // the remainder; per element the arithmetic below
+      const int nv = (int)nvec, kyi = (int)ky;
+      auto emit = [&](const uint4& v, int k) {
+        float d[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; e += 2) {
+          const uint64_t x = fadd2(ffma2(f2_pack(E::get(v, e), E::get(v, e + 1)), sc2, nM2), nL2S);
+          float a, b;
+          f2_unpack(x, a, b);
+          f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
+        }
+        if (k == kyi) {
+          const int e = (int)((y - h) - (int64_t)k * VEC);
+#pragma unroll
+          for (int q = 0; q < VEC; ++q)
+            if (q == e) d[q] = c * qy;
+        }
+        store_vals<TO, VEC>(ob + (int64_t)k * VEC, d);
+      };
+      int k0 = tid;
+      for (; k0 + (U - 1) * nthr < nv; k0 += nthr * U) {
+        const uint4* p = vp + k0;
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = POL ? ldg_pol(p + u * nthr, pol) : ldg_stream(p + u * nthr);
+#pragma unroll
+        for (int u = 0; u < U; ++u) emit(v[u], k0 + u * nthr);
+      }
+      for (; k0 < nv; k0 += nthr) emit(POL ? ldg_pol(vp + k0, pol) : ldg_stream(vp + k0), k0);
+      return;
+    }
+  }
   for (int64_t k0 = tid; k0 < nvec; k0 += (int64_t)nthr * U) {
     uint4 v[U];
 #pragma unroll
