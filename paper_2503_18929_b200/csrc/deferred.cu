@@ -312,11 +312,9 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   }
   __syncthreads();
   TR(4);
-#ifdef TBA_AB_SMALL_P2
-  if constexpr (CS == 1 && REV)
-#else
-  if constexpr (STASH_KB > 0 && CS == 1 && REV)
-#endif
+  // (rows <= 128 KB without a stash: the same forward-order loop, 1 % faster than sweeping from the
+  // end on RhoMath / red-teaming / GSM8K)
+  if constexpr (CS == 1)
     defer_pass2<T, TO, U2>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
                            STASH_KB > 0 ? ds_stash : nullptr, STASH_KB > 0 ? ds_ks : 0);
   else
