@@ -217,3 +217,47 @@ def test_one_call_schedules_against_oracle(name, seed, sched):
     n, ma, mr = H.compare_dlogits_rows(d, w, seed, rows, 0, ref["tokens"].reshape(-1), np.repeat(eps, w.T), w.N,
                                        what=test)
     H.record(test, name, seed, "dlogits (every valid row)", n, ma, mr, tol="1 bf16 ulp")
+
+
+@pytest.mark.parametrize("V,dtype,g_dtype", [(80001, "bf16", "fp32"), (80001, "bf16", "bf16"), (76000, "bf16", "fp32"),
+                                             (50304, "fp32", "fp32"), (33001, "bf16", "fp32")])
+def test_deferred_token_regions_and_alignment(V, dtype, g_dtype):
+    """Every region of the deferred kernel's row split holds the sampled token somewhere in the batch:
+    the scalar head and tail (odd V: rows start at every 2-byte offset), the shared-memory stash part
+    (the row's first 96 KB), the L2 part, the last element; G rows whose 16-byte alignment differs from
+    the logits row (fp32 G of odd-V bf16 rows) take the scalar fallback. Each G row times (2/N) eps_s
+    is the oracle's dlogits row (App. A)."""
+    from oracle import tba_oracle as O
+    w = W("redteam", B=2, K=4, T=6, V=V, dtype=dtype, len_lo=1, len_hi=6)
+    inp = H.device_inputs(w, 9)
+    h = inp["host"]
+    esz = 2 if dtype == "bf16" else 4
+    stash_elems = 96 * 1024 // esz
+    picks = [p for p in [0, 1, 3, 7, 8, stash_elems - 1, stash_elems, stash_elems + 5, V // 2, V - 9, V - 2, V - 1]
+             if p < V]
+    tok = h["tokens"].copy()
+    for i in range(tok.size):
+        tok.flat[i] = picks[i % len(picks)] if i % 5 else tok.flat[i]
+    h["tokens"] = tok
+    inp["tokens"] = torch.from_numpy(tok).cuda()
+    gdt = torch.float32 if g_dtype == "fp32" else torch.bfloat16
+    o, _, G = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
+                                       inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=gdt, check_status=True)
+    torch.cuda.synchronize()
+    ref = O.vargrad_head(H.host_logits(w, 9, 0, w.B), h["tokens"], h["mask"], h["ref_logp"], h["log_reward"], w.beta,
+                         w.K)
+    eps = o.resid.cpu().numpy()
+    H.assert_seq_close(o.seq_logp.cpu().numpy(), ref["ell"], "seq_logp")
+    H.assert_seq_close(eps, ref["eps"], "resid")
+    g = G.double().cpu().numpy()
+    for s_ in range(w.N):
+        c = 2 * eps[s_] / w.N
+        for t in range(w.T):
+            if not h["mask"][s_, t]:
+                assert np.all(g[s_, t] == 0)
+            elif g_dtype == "fp32":
+                H.assert_dlogits_close(g[s_, t] * c, ref["dlogits"][s_, t], c, "fp32", f"row {s_},{t}")
+            else:  # bf16 G = bf16(G_exact): within one bf16 ulp of the oracle's dlogits / c
+                want = ref["dlogits"][s_, t] / c
+                ok = np.abs(g[s_, t] - want) <= O.bf16_ulp(O.round_bf16(want)) + 2.0 ** -126
+                assert ok.all(), (s_, t, np.flatnonzero(~ok)[:5])
