@@ -13,7 +13,7 @@ for wl in pythia redteam rhomath toy gsm8k_t3 gsm8k_k40 tldr_t4 math_t5_shard py
   timeout 600 python bench.py --workload $wl --no-e2e > gpurun_out/bench_r02_$wl.json 2>/dev/null
 done
 timeout 600 python bench.py --workload qwen_shard --objective tbap --no-e2e --no-cpu-baseline > gpurun_out/bench_r02_qwen_shard_tbap.json 2>/dev/null
-for wl in qwen_shard pythia redteam rhomath; do
+for wl in qwen_shard pythia redteam rhomath math_t5_shard gsm8k_t3 pythia_fp32; do
   timeout 600 python bench.py --workload $wl --schedule deferred --no-e2e --no-cpu-baseline > gpurun_out/bench_r02_${wl}_deferred.json 2>/dev/null
 done
 timeout 600 python bench.py --workload toy --cuda-graph --no-e2e --no-cpu-baseline > gpurun_out/bench_r02_toy_graph.json 2>/dev/null
@@ -36,7 +36,7 @@ for f in sorted(glob.glob('gpurun_out/bench_r02_*.json')):
           'defer', (d.get('variants') or {}).get('deferred_scale', {}).get('ms_per_step'), (d.get('clocks') or {}).get('sm_mhz'))
 PY
 bash scripts/gpu_profile.sh r02 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:row_single -s 3 -c 1 -o gpurun_out/prof_row_single_r02 -f python bench.py --no-e2e --no-cpu-baseline --no-variants --workload qwen_group --schedule deferred --steps 1 --warmup 3 > /dev/null 2>&1
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:row_single -s 6 -c 2 --csv --log-file gpurun_out/dram_deferred_r02.csv python bench.py --no-e2e --no-cpu-baseline --no-variants --schedule deferred --steps 2 --warmup 3 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:row_single -s 3 -c 1 -o gpurun_out/prof_row_single1_r02 -f python bench.py --no-e2e --no-cpu-baseline --no-variants --workload qwen_group --schedule deferred --steps 1 --warmup 3 > /dev/null 2>&1
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:row_single -s 3 -c 2 --csv --log-file gpurun_out/dram_deferred_r02.csv python bench.py --no-e2e --no-cpu-baseline --no-variants --schedule deferred --steps 2 --warmup 3 > /dev/null 2>&1
 bash scripts/gpu_sanitize.sh 2>&1 | tail -14
 ls gpurun_out | head -80
