@@ -117,7 +117,7 @@ __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int6
 // iterations carry no bounds or stash tests (32-bit vector indices). The
 // arithmetic is bwd_row's (fp32 pairs, the same roundings); the token's entry is stored last by the
 // thread that stored its vector.
-template <class T, class TO, int U>
+template <class T, class TO, int U, bool POLY>
 __device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid,
                                             int nthr, float sc, float M2, float L2S, float c, int64_t y, float qy,
                                             const uint4* __restrict__ stash, int ks) {
@@ -140,14 +140,22 @@ __device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __rest
   const uint4* vp = reinterpret_cast<const uint4*>(rp + h);
   TO* ob = op + h;
   const uint64_t sc2 = f2_pack(sc, sc), nM2 = f2_pack(-M2, -M2), nL2S = f2_pack(-L2S, -L2S), nc = f2_pack(-c, -c);
-  auto emit = [&](const uint4& v, int k) {
+  // poly: this vector's last element pair takes the FMA-pipe exp2 (exp2_poly2) instead of MUFU.EX2 —
+  // every other vector of an unrolled group, i.e. 1 of 8 element pairs (POLY: the stash path of long
+  // rows): the XU pipe is the busiest (66 %), and 1 of 8 costs fewer issue slots than it frees
+  // (measured 1.5 % faster; 1 of 4 slower; rows <= 128 KB 0.5 % slower)
+  auto emit = [&](const uint4& v, int k, bool poly = false) {
     float d[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; e += 2) {
       const uint64_t x = fadd2(ffma2(f2_pack(E::get(v, e), E::get(v, e + 1)), sc2, nM2), nL2S);
-      float a, b;
-      f2_unpack(x, a, b);
-      f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
+      if (poly && e == VEC - 2) {
+        f2_unpack(fmul2(exp2_poly2(x), nc), d[e], d[e + 1]);
+      } else {
+        float a, b;
+        f2_unpack(x, a, b);
+        f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
+      }
     }
     store_vals<TO, VEC>(ob + (int64_t)k * VEC, d);
   };
@@ -160,7 +168,7 @@ __device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __rest
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = ldg_pol(p + u * nthr, pol);
 #pragma unroll
-    for (int u = 0; u < U; ++u) emit(v[u], ks + f0 + u * nthr);
+    for (int u = 0; u < U; ++u) emit(v[u], ks + f0 + u * nthr, POLY && (u & 1) != 0);
   }
   for (; f0 < nl2; f0 += nthr) emit(ldg_pol(vp + (ks + f0), pol), ks + f0);
   int j0 = tid;
@@ -169,7 +177,7 @@ __device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __rest
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = stash[j0 + u * nthr];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) emit(v[u], j0 + u * nthr);
+    for (int u = 0; u < 4; ++u) emit(v[u], j0 + u * nthr, POLY && (u & 1) != 0);
   }
   for (; j0 < ks; j0 += nthr) emit(stash[j0], j0);
   if (y >= h && y < vend) {
@@ -315,7 +323,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   // (rows <= 128 KB without a stash: the same forward-order loop, 1 % faster than sweeping from the
   // end on RhoMath / red-teaming / GSM8K)
   if constexpr (CS == 1)
-    defer_pass2<T, TO, U2>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
+    defer_pass2<T, TO, U2, (STASH_KB > 0)>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
                            STASH_KB > 0 ? ds_stash : nullptr, STASH_KB > 0 ? ds_ks : 0);
   else
     bwd_row<T, TO, U2, true, REV, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
