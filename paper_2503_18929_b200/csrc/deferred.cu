@@ -31,7 +31,7 @@ __device__ __forceinline__ unsigned long long clk() {
 // while the threads stream the rest of the row through registers (L2 evict_last, for pass 2); then
 // the stash part is consumed from shared memory. The sampled token's element is excluded as in
 // fwd_accumulate (finalize_row adds it).
-template <class T, int U>
+template <class T, int U, int NP = 0>
 __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int64_t V, int tid, int nthr,
                                                   OnlineState& st, int64_t y, uint4* __restrict__ stash, int ks,
                                                   int64_t trow = 0) {
@@ -83,8 +83,8 @@ __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int6
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = ldg_pol(vp + k0 + (int64_t)u * nthr, pol_last);
     const int64_t kr = ky - k0;
-    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, 0, true>(v, st, (int)(kr / nthr), ey);
-    else fwd_consume<T, U>(v, st);
+    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, NP, true>(v, st, (int)(kr / nthr), ey);
+    else fwd_consume<T, U, NP>(v, st);
   }
   for (int64_t k = k0; k < nvec; k += nthr) {
     uint4 v1[1] = {ldg_pol(vp + k, pol_last)};
@@ -101,8 +101,8 @@ __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int6
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = stash[j0 + (int64_t)u * nthr];
     const int64_t kr = ky - j0;
-    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, 0, true>(v, st, (int)(kr / nthr), ey);
-    else fwd_consume<T, U>(v, st);
+    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, NP, true>(v, st, (int)(kr / nthr), ey);
+    else fwd_consume<T, U, NP>(v, st);
   }
   for (int64_t k = j0; k < ks; k += nthr) {
     uint4 v1[1] = {stash[k]};

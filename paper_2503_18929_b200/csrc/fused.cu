@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
         if (gt == 0 && ok) zy = Elem<T>::load1(rp + y);
         OnlineState st;
         st.init(a.rs);
-        fwd_accumulate<T, kFusedU, false, 1>(rp, a.V, gt, TPR_F, st, ok ? y : -1);  // as two-call
+        fwd_accumulate<T, kFusedU, false, (TPR_F == 64 ? -1 : 1)>(rp, a.V, gt, TPR_F, st, ok ? y : -1);  // as two-call
         float M, M2;
         double S;
         combine_lanes(st.m, st.R2, st.s, true, a.rs.sc, M, M2, S);

@@ -60,8 +60,9 @@ int launch_fwd_rows_t(const T* lg, const tba_rows* x, const WsLayout& w, const R
   // 1 of the 4 element pairs per 16-byte vector (1 of 2 for fp32 rows) takes the FMA-pipe exp2
   // (exp2_poly2) instead of MUFU — relieves the XU pipe (75 % busy), +1-3 % forward bandwidth on
   // every BASELINE shape; 2 of 4 over-loads the FMA/ALU pipes.
-  if (tpr == 64) TBA_ROWS(64, 1);
-  TBA_ROWS(32, 1);
+  // (the 304 KB Qwen rows: 1 of 8 pairs, NP = -1 — 1.3 % faster than 1 of 4 there)
+  if (tpr == 64) TBA_ROWS(64, -1);
+  TBA_ROWS(32, 1);  // (1 of 8 measured equal on the < 128 KB rows)
 #undef TBA_ROWS
 }
 

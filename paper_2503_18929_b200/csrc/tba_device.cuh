@@ -292,7 +292,8 @@ __device__ __forceinline__ void fwd_consume(const uint4 (&v)[U], OnlineState& st
 #pragma unroll
     for (int p = 0; p < VEC / 2; ++p) {
       const uint64_t x = ffma2(f2_pack(z[u][2 * p], z[u][2 * p + 1]), l2e, nr2);
-      const bool poly = (NP >= 1 && p == VEC / 2 - 1) || (NP >= 2 && p == VEC / 2 - 3);
+      const bool poly = (NP >= 1 && p == VEC / 2 - 1) || (NP >= 2 && p == VEC / 2 - 3) ||
+                        (NP == -1 && (u & 1) && p == VEC / 2 - 1);  // -1: 1 of 8 pairs (odd vectors)
       if (poly) {
         acc[p] = fadd2(acc[p], exp2_poly2(x));
       } else {
