@@ -6,7 +6,7 @@ namespace {
 // TPR threads per row, 256/TPR rows per CTA. Row coefficient c = grad_scale * g * inv_temp *
 // (resid[s] for the TB losses, per sequence | coef[row] for per-token rules such as TBA').
 template <class T, class TO, int TPR, int U, bool PER_ROW>
-__global__ void __launch_bounds__(256) row_bwd(const T* __restrict__ logits, int64_t rows, int64_t T_len, int64_t V,
+__global__ void __launch_bounds__(256, TPR == 32 ? 4 : 6) row_bwd(const T* __restrict__ logits, int64_t rows, int64_t T_len, int64_t V,
                                                int64_t stride, const int64_t* __restrict__ tokens,
                                                const uint8_t* __restrict__ mask, const float2* __restrict__ stats,
                                                const float* __restrict__ qy_in, const double* __restrict__ resid,

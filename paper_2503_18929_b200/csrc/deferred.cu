@@ -19,13 +19,11 @@ __device__ __forceinline__ unsigned long long clk() {
 #define TR(i)
 #endif
 
-// A cluster of CS CTAs (NT threads each) per valid row: pass 1 streams the row from HBM with an
-// L2 evict_last policy (online max/sum); the CTAs of the cluster exchange their (max, sum)
-// partials through distributed shared memory; pass 2 re-reads the row — an L2 hit, because the
-// grid keeps only ~40-60 MB of rows in flight (CS and NT are chosen per row size) — and writes
-// the UNSCALED gradient G = inv_temp (1[v=y] - softmax) once. HBM bytes: 2V read + 2V write per
-// valid row (the 4V floor); the per-sequence factor grad_scale * g * eps_s is applied by the
-// consumer (the LM-head backward, as a row scale), SURVEY §8(f) NEXT 2.
+// One CTA per valid row: pass 1 streams the row from HBM with an L2 evict_last policy (online
+// max/sum); pass 2 re-reads the row — from its shared-memory stash and L2 — and writes the UNSCALED
+// gradient G = inv_temp (1[v=y] - softmax) once. HBM bytes: 2V read + 2V write per valid row (the 4V
+// floor) plus the re-reads that miss L2; the per-sequence factor grad_scale * g * eps_s is applied by
+// the consumer (the LM-head backward, as a row scale), SURVEY §8(f) NEXT 2.
 // Pass 1 of a long row with a shared-memory stash: the stash part (the row's first ks vectors) is
 // fetched with cp.async straight into shared memory — all of it in flight at once, no registers held —
 // while the threads stream the rest of the row through registers (L2 evict_last, for pass 2); then
@@ -125,8 +123,7 @@ __device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __rest
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(rp, V);
   if ((reinterpret_cast<uint64_t>(op + h) & 15u) != 0) {  // output not co-aligned
-    bwd_row<T, TO, U, true, true, true>(rp, op, V, tid, nthr, true, sc, M2, L2S, c, y, qy, make_policy(false), stash,
-                                       ks);
+    bwd_row<T, TO, U>(rp, op, V, tid, nthr, true, sc, M2, L2S, c, y, qy);  // the scalar loop
     return;
   }
   const int nvec = (int)((V - h) / VEC);
@@ -186,28 +183,26 @@ __device__ __forceinline__ void defer_pass2(const T* __restrict__ rp, TO* __rest
   }
 }
 
-template <class T, class TO, int NT, int CS, int U2 = 4, bool REV = false, int U1 = 4, int STASH_KB = 0>
-__device__ __forceinline__ void row_single_body(const T* __restrict__ logits, int64_t rows, int64_t V,
-                                                int64_t stride, const int64_t* __restrict__ tokens,
-                                                const uint8_t* __restrict__ mask, RowScale rs,
-                                                float2* __restrict__ stats, float* __restrict__ qy,
-                                                double* __restrict__ lp, int32_t* dev_status,
-                                                TO* __restrict__ g_out, int64_t ostride) {
-  namespace cg = cooperative_groups;
+// One CTA of NT threads per row (grid = rows): pass 1 (online max / sum, the stash part on chip when
+// STASH_KB > 0), the CTA's fixed-order combine, the row statistics, pass 2 (G).
+template <class T, class TO, int NT, int U2, int U1, int STASH_KB>
+__global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, int64_t rows, int64_t V,
+                                                  int64_t stride, const int64_t* __restrict__ tokens,
+                                                  const uint8_t* __restrict__ mask, RowScale rs,
+                                                  float2* __restrict__ stats, float* __restrict__ qy,
+                                                  double* __restrict__ lp, int32_t* dev_status,
+                                                  TO* __restrict__ g_out, int64_t ostride) {
   constexpr int NW = NT / 32;
-  const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-  const int64_t row = (int64_t)blockIdx.x / CS;
-  const int gt = rank * NT + (int)threadIdx.x;  // thread index within the row's cluster
+  const int64_t row = (int64_t)blockIdx.x;
+  const int gt = (int)threadIdx.x;
   __shared__ float sm_m[NW], sm_M2[NW];
   __shared__ double sm_s[NW];
-  __shared__ float part_m, part_M2;  // this CTA's partial, read by the cluster through DSMEM
-  __shared__ double part_s;
   __shared__ float sh_M2, sh_L2S, sh_qy;
   __shared__ int64_t sh_y;
-  const bool live = row < rows;
-  const bool valid = live && mask[row] != 0;  // uniform over the cluster
-  const T* rp = logits + (live ? row : 0) * stride;
-  TO* op = g_out + (live ? row : 0) * ostride;
+  if (row >= rows) return;
+  const bool valid = mask[row] != 0;
+  const T* rp = logits + row * stride;
+  TO* op = g_out + row * ostride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // STASH_KB > 0: the row's first STASH_KB KB of 16-byte vectors stay in shared memory between the
   // passes (pass 2 reads them on chip; only the rest of the row must survive in L2)
@@ -224,8 +219,12 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   }
 #endif
   TR(1);
+  if (!valid) {
+    bwd_row<T, TO, 4>(rp, op, V, gt, NT, false, 0.f, 0.f, 0.f, 0.f, -1, 0.f);
+    return;
+  }
   float zy = 0.f;  // thread 0: the token's logit, loaded while pass 1 runs
-  if (valid) {
+  {
     const int64_t yt = tokens[row];
     if (threadIdx.x == 0) {
       sh_y = yt;
@@ -234,7 +233,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     OnlineState st;
     st.init(rs);
     if (STASH_KB > 0)  // the stash part fetched with cp.async, all of it in flight at once
-      defer_pass1_async<T, U1>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, ds_stash, ds_ks, row);
+      defer_pass1_async<T, U1>(rp, V, gt, NT, st, (yt >= 0 && yt < V) ? yt : -1, ds_stash, ds_ks, row);
     else {
       if (gt == 0) {  // L2 bulk prefetch of the whole (short) row up front: the loads below then hit L2
         const uint64_t pl = make_policy(true);
@@ -248,7 +247,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
                        : "memory");
         }
       }
-      fwd_accumulate<T, U1, true>(rp, V, gt, CS * NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
+      fwd_accumulate<T, U1, true>(rp, V, gt, NT, st, (yt >= 0 && yt < V) ? yt : -1, make_policy(true));
     }
     combine_lanes(st.m, st.R2, st.s, true, rs.sc, M, M2, S);
     TR(3);
@@ -262,40 +261,7 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
       const bool act = lane < NW;
       combine_lanes(act ? sm_m[lane] : -INFINITY, act ? sm_M2[lane] : 0.f, act ? sm_s[lane] : 0.0, act, rs.sc, M,
                     M2, S);
-      if (lane == 0) {
-        part_m = M;
-        part_M2 = M2;
-        part_s = S;
-      }
     }
-  }
-  if constexpr (CS > 1) {
-    cg::cluster_group cl = cg::this_cluster();
-    // phase 1: every CTA's partial is visible cluster-wide (release/acquire)
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (valid && warp == 0) {
-      const bool act = lane < CS;
-      float pm = -INFINITY, pm2 = 0.f;
-      double ps = 0.0;
-      if (act) {
-        pm = *cl.map_shared_rank(&part_m, lane);
-        pm2 = *cl.map_shared_rank(&part_M2, lane);
-        ps = *cl.map_shared_rank(&part_s, lane);
-      }
-      combine_lanes(pm, pm2, ps, act, rs.sc, M, M2, S);
-    }
-    // phase 2 (split): "done reading peers" now, wait only before exiting, so that no CTA's
-    // shared memory disappears while a peer reads it and the barrier latency hides behind pass 2
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  }
-  if (!live) {
-    if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-    return;
-  }
-  if (!valid) {
-    bwd_row<T, TO, 4>(rp, op, V, gt, CS * NT, false, 0.f, 0.f, 0.f, 0.f, -1, 0.f);
-    if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-    return;
   }
   if (threadIdx.x == 0) {  // (M, M2, S) of the whole row in thread 0 (warp 0's combine)
     const int64_t y = sh_y;
@@ -304,15 +270,13 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
     float q;
     double v;
     row_stats(M, M2, S, zy, ok, rs, st2, q, v);
-    if (rank == 0) {  // the cluster's first CTA owns the row's outputs
-      const bool finite = (M > -INFINITY) && (M < INFINITY) && (st2.y > -INFINITY) && (st2.y < INFINITY);
-      stats[row] = st2;
-      qy[row] = q;
-      lp[row] = v;
-      if (dev_status) {
-        const int f = (ok ? 0 : TBA_DEV_TOKEN_RANGE) | (finite ? 0 : TBA_DEV_NONFINITE_ROW);
-        if (f) atomicOr(dev_status, f);
-      }
+    const bool finite = (M > -INFINITY) && (M < INFINITY) && (st2.y > -INFINITY) && (st2.y < INFINITY);
+    stats[row] = st2;
+    qy[row] = q;
+    lp[row] = v;
+    if (dev_status) {
+      const int f = (ok ? 0 : TBA_DEV_TOKEN_RANGE) | (finite ? 0 : TBA_DEV_NONFINITE_ROW);
+      if (f) atomicOr(dev_status, f);
     }
     sh_M2 = st2.x;
     sh_L2S = st2.y;
@@ -322,29 +286,10 @@ __device__ __forceinline__ void row_single_body(const T* __restrict__ logits, in
   TR(4);
   // (rows <= 128 KB without a stash: the same forward-order loop, 1 % faster than sweeping from the
   // end on RhoMath / red-teaming / GSM8K)
-  if constexpr (CS == 1)
-    defer_pass2<T, TO, U2, (STASH_KB > 0)>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
-                           STASH_KB > 0 ? ds_stash : nullptr, STASH_KB > 0 ? ds_ks : 0);
-  else
-    bwd_row<T, TO, U2, true, REV, true>(rp, op, V, gt, CS * NT, true, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y,
-                                        sh_qy, make_policy(false), STASH_KB > 0 ? ds_stash : nullptr, ds_ks);
+  defer_pass2<T, TO, U2, (STASH_KB > 0)>(rp, op, V, gt, NT, rs.sc, sh_M2, sh_L2S, (float)rs.inv_temp, sh_y, sh_qy,
+                                         STASH_KB > 0 ? ds_stash : nullptr, STASH_KB > 0 ? ds_ks : 0);
   TR(5);
-  if constexpr (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
-
-template <class T, class TO, int NT, int U2 = 4, bool REV = false, int U1 = 4, int STASH_KB = 0>
-__global__ void __launch_bounds__(NT) row_single1(const T* __restrict__ logits, int64_t rows, int64_t V,
-                                                  int64_t stride, const int64_t* __restrict__ tokens,
-                                                  const uint8_t* __restrict__ mask, RowScale rs,
-                                                  float2* __restrict__ stats, float* __restrict__ qy,
-                                                  double* __restrict__ lp, int32_t* dev_status,
-                                                  TO* __restrict__ g_out, int64_t ostride) {
-  row_single_body<T, TO, NT, 1, U2, REV, U1, STASH_KB>(logits, rows, V, stride, tokens, mask, rs, stats, qy, lp,
-                                                       dev_status, g_out, ostride);
-}
-
-
-
 
 }  // namespace
 
@@ -363,11 +308,11 @@ int launch_single(const tba_rows* x, const WsLayout& w, const RowScale& rs, int3
     static bool attr_ = false;                                                                                  \
     const size_t dsm = (size_t)(SKB_) * 1024;                                                                   \
     if (dsm > 48 * 1024 && !attr_) {                                                                            \
-      cudaFuncSetAttribute(row_single1<T_, TO_, NT_, U2_, true, U1_, SKB_>,                                      \
+      cudaFuncSetAttribute(row_single1<T_, TO_, NT_, U2_, U1_, SKB_>,                                      \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);                               \
       attr_ = true;                                                                                             \
     }                                                                                                           \
-    row_single1<T_, TO_, NT_, U2_, true, U1_, SKB_><<<(unsigned)rows, NT_, dsm, s>>>(                            \
+    row_single1<T_, TO_, NT_, U2_, U1_, SKB_><<<(unsigned)rows, NT_, dsm, s>>>(                            \
       static_cast<const T_*>(x->logits), rows, x->vocab, x->row_stride, x->tokens, x->mask, rs, w.stats, w.qy, w.lp, \
       dev_status, static_cast<TO_*>(grad_unscaled), g_row_stride);                                             \
   } while (0)

@@ -591,16 +591,14 @@ __device__ __forceinline__ void store_vals(TO* o, const float (&d)[N]) {
   }
 }
 
-// REV: walk the row's vectors from the end (the deferred pass re-reads a row it has just streamed:
-// its last vectors are the most recently touched in L2).
-// dz_v = -c p_v for v != y and c (1 - p_y) at the token, with 1 - p_y = qy from the forward (exact
-// when p_y -> 1, where c - c p_y would cancel). TOK_LATE: the token's entry is stored after the loop
-// by the thread that stored its vector (same thread, same address: program order decides) instead
-// of a per-vector test — faster in the deferred pass, slower in row_bwd (measured).
-template <class T, class TO, int U, bool POL = false, bool REV = false, bool TOK_LATE = false>
+// One row of the gradient writer (a5): dz_v = -c p_v for v != y and c (1 - p_y) at the token, with
+// 1 - p_y = qy from the forward (exact when p_y -> 1, where c - c p_y would cancel); zeros when
+// !valid. Scalar head / tail around the 16-byte-aligned interior; a row whose output is not
+// 16-byte aligned at the same element as its input takes the scalar loop throughout.
+template <class T, class TO, int U, bool POL = false>
 __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict__ op, int64_t V, int tid, int nthr,
                                         bool valid, float sc, float M2, float L2S, float c, int64_t y, float qy,
-                                        uint64_t pol = 0, const uint4* __restrict__ stash = nullptr, int ks = 0) {
+                                        uint64_t pol = 0) {
   using E = Elem<T>;
   constexpr int VEC = E::VEC;
   const int64_t h = head_elems(rp, V);
@@ -621,90 +619,46 @@ __device__ __forceinline__ void bwd_row(const T* __restrict__ rp, TO* __restrict
   for (int64_t i = vend + tid; i < V; i += nthr) one(i);
   const uint4* vp = reinterpret_cast<const uint4*>(rp + h);
   TO* ob = op + h;
+  const int nv = (int)nvec;  // 32-bit vector indices: a row has < 2^31 vectors
   if (!valid) {
     float z[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) z[e] = 0.f;
-    for (int64_t k = tid; k < nvec; k += nthr) store_vals<TO, VEC>(ob + k * VEC, z);
+    for (int k = tid; k < nv; k += nthr) store_vals<TO, VEC>(ob + (int64_t)k * VEC, z);
     return;
   }
   // d_v = -c 2^(z_v sc - M2 - L2S) in fp32 pairs (FFMA2 / FADD2 / FMUL2: per lane the same roundings
   // as the scalar fmaf, subtraction and product)
   const uint64_t sc2 = f2_pack(sc, sc), nM2 = f2_pack(-M2, -M2), nL2S = f2_pack(-L2S, -L2S), nc = f2_pack(-c, -c);
-  const int64_t ky = (y >= h && y < vend) ? (y - h) / VEC : -1;
-  if constexpr (!REV && !TOK_LATE) {
-    if (stash == nullptr) {
-      // full iterations with no bounds tests (32-bit vector indices; a row has < 2^31 vectors), then
-      // the remainder; per element the arithmetic below
-      const int nv = (int)nvec, kyi = (int)ky;
-      auto emit = [&](const uint4& v, int k) {
-        float d[VEC];
+  const int kyi = (y >= h && y < vend) ? (int)((y - h) / VEC) : -1;
+  auto emit = [&](const uint4& v, int k) {
+    float d[VEC];
 #pragma unroll
-        for (int e = 0; e < VEC; e += 2) {
-          const uint64_t x = fadd2(ffma2(f2_pack(E::get(v, e), E::get(v, e + 1)), sc2, nM2), nL2S);
-          float a, b;
-          f2_unpack(x, a, b);
-          f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
-        }
-        if (k == kyi) {
-          const int e = (int)((y - h) - (int64_t)k * VEC);
-#pragma unroll
-          for (int q = 0; q < VEC; ++q)
-            if (q == e) d[q] = c * qy;
-        }
-        store_vals<TO, VEC>(ob + (int64_t)k * VEC, d);
-      };
-      int k0 = tid;
-      for (; k0 + (U - 1) * nthr < nv; k0 += nthr * U) {
-        const uint4* p = vp + k0;
-        uint4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = POL ? ldg_pol(p + u * nthr, pol) : ldg_stream(p + u * nthr);
-#pragma unroll
-        for (int u = 0; u < U; ++u) emit(v[u], k0 + u * nthr);
-      }
-      for (; k0 < nv; k0 += nthr) emit(POL ? ldg_pol(vp + k0, pol) : ldg_stream(vp + k0), k0);
-      return;
+    for (int e = 0; e < VEC; e += 2) {
+      const uint64_t x = fadd2(ffma2(f2_pack(E::get(v, e), E::get(v, e + 1)), sc2, nM2), nL2S);
+      float a, b;
+      f2_unpack(x, a, b);
+      f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
     }
-  }
-  for (int64_t k0 = tid; k0 < nvec; k0 += (int64_t)nthr * U) {
+    if (k == kyi) {
+      const int e = (int)((y - h) - (int64_t)k * VEC);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q)
+        if (q == e) d[q] = c * qy;
+    }
+    store_vals<TO, VEC>(ob + (int64_t)k * VEC, d);
+  };
+  // full iterations with no bounds tests, then the remainder
+  int k0 = tid;
+  for (; k0 + (U - 1) * nthr < nv; k0 += nthr * U) {
+    const uint4* p = vp + k0;
     uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t kf = k0 + (int64_t)u * nthr;
-      const int64_t k = REV ? nvec - 1 - kf : kf;
-      if (kf < nvec) {
-        if (stash != nullptr && k < ks) v[u] = stash[k];  // kept on chip by pass 1
-        else v[u] = POL ? ldg_pol(vp + k, pol) : ldg_stream(vp + k);
-      }
-    }
+    for (int u = 0; u < U; ++u) v[u] = POL ? ldg_pol(p + u * nthr, pol) : ldg_stream(p + u * nthr);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t kf = k0 + (int64_t)u * nthr;
-      const int64_t k = REV ? nvec - 1 - kf : kf;
-      if (kf < nvec) {
-        float d[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; e += 2) {
-          const uint64_t x = fadd2(ffma2(f2_pack(E::get(v[u], e), E::get(v[u], e + 1)), sc2, nM2), nL2S);
-          float a, b;
-          f2_unpack(x, a, b);
-          f2_unpack(fmul2(f2_pack(ex2(a), ex2(b)), nc), d[e], d[e + 1]);
-        }
-        if (!TOK_LATE && k == ky) {
-          const int e = (int)((y - h) - k * VEC);
-#pragma unroll
-          for (int q = 0; q < VEC; ++q)
-            if (q == e) d[q] = c * qy;
-        }
-        store_vals<TO, VEC>(ob + k * VEC, d);
-      }
-    }
+    for (int u = 0; u < U; ++u) emit(v[u], k0 + u * nthr);
   }
-  if (TOK_LATE && ky >= 0) {
-    const int64_t kf = REV ? nvec - 1 - ky : ky;
-    if (kf % nthr == tid) Out<TO>::put1(op + y, c * qy);
-  }
+  for (; k0 < nv; k0 += nthr) emit(POL ? ldg_pol(vp + k0, pol) : ldg_stream(vp + k0), k0);
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
