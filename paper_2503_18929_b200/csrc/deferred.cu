@@ -40,7 +40,7 @@ __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int6
   const int64_t tail0 = h + nvec * VEC;
   const uint4* vp = reinterpret_cast<const uint4*>(rp + h);
   const uint64_t pol_first = make_policy(false), pol_last = make_policy(true);
-  for (int64_t k = tid; k < ks; k += nthr)
+  for (int k = tid; k < ks; k += nthr)
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(stash + k)),
                  "l"(vp + k), "l"(pol_first)
                  : "memory");
@@ -71,20 +71,27 @@ __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int6
     if (i == y) st.add1_excl(z);
     else st.add1(z);
   }
-  const int64_t ky = (y >= h && y < tail0) ? (y - h) / VEC : -1;
-  const int ey = ky >= 0 ? (int)((y - h) - ky * VEC) : 0;
-  const int64_t step = (int64_t)nthr * U;
-  int64_t k0 = ks + tid;
-  for (; k0 + (int64_t)(U - 1) * nthr < nvec; k0 += step) {
+  // 32-bit vector indices (a row has < 2^31 vectors); full iterations are uniform over the CTA, so the
+  // sampled token's iteration is one uniform test per iteration (as in fwd_accumulate)
+  const int nv = (int)nvec;
+  const int ky = (y >= h && y < tail0) ? (int)((y - h) / VEC) : -1;
+  const int ey = ky >= 0 ? (int)((y - h) - (int64_t)ky * VEC) : 0;
+  const int step = nthr * U;
+  const int nfl = (nv - ks) / step;  // full iterations over the L2 part [ks, nv)
+  const int rl = ky - ks;            // the token's index in the L2 part (< 0: not there)
+  const int ityl = rl >= 0 ? rl / step : -1;
+  const int uyl = (rl >= 0 && (rl % step) % nthr == tid) ? (rl % step) / nthr : -1;
+  int k0 = ks + tid;
+  for (int it = 0; it < nfl; ++it, k0 += step) {
     if (PF_VEC > 0 && tid == 0) prefetch(k0 + PF_VEC, k0 + PF_VEC + step);
+    const uint4* p = vp + k0;
     uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ldg_pol(vp + k0 + (int64_t)u * nthr, pol_last);
-    const int64_t kr = ky - k0;
-    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, NP, true>(v, st, (int)(kr / nthr), ey);
+    for (int u = 0; u < U; ++u) v[u] = ldg_pol(p + u * nthr, pol_last);
+    if (it == ityl) fwd_consume<T, U, NP, true>(v, st, uyl, ey);
     else fwd_consume<T, U, NP>(v, st);
   }
-  for (int64_t k = k0; k < nvec; k += nthr) {
+  for (int k = k0; k < nv; k += nthr) {
     uint4 v1[1] = {ldg_pol(vp + k, pol_last)};
     if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
     else fwd_consume<T, 1>(v1, st);
@@ -93,16 +100,18 @@ __device__ __forceinline__ void defer_pass1_async(const T* __restrict__ rp, int6
   if (threadIdx.x == 0 && trow < TR_ROWS) g_trace[trow * 6 + 2] = clk();
 #endif
   asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own copies are in shared memory
-  int64_t j0 = tid;
-  for (; j0 + (int64_t)(U - 1) * nthr < ks; j0 += step) {
+  const int nfs = ks / step;  // full iterations over the stash part [0, ks)
+  const int itys = (ky >= 0 && ky < ks) ? ky / step : -1;
+  const int uys = (itys >= 0 && (ky % step) % nthr == tid) ? (ky % step) / nthr : -1;
+  int j0 = tid;
+  for (int it = 0; it < nfs; ++it, j0 += step) {
     uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = stash[j0 + (int64_t)u * nthr];
-    const int64_t kr = ky - j0;
-    if (kr >= 0 && kr < step && kr % nthr == 0) fwd_consume<T, U, NP, true>(v, st, (int)(kr / nthr), ey);
+    for (int u = 0; u < U; ++u) v[u] = stash[j0 + u * nthr];
+    if (it == itys) fwd_consume<T, U, NP, true>(v, st, uys, ey);
     else fwd_consume<T, U, NP>(v, st);
   }
-  for (int64_t k = j0; k < ks; k += nthr) {
+  for (int k = j0; k < ks; k += nthr) {
     uint4 v1[1] = {stash[k]};
     if (k == ky) fwd_consume<T, 1, 0, true>(v1, st, 0, ey);
     else fwd_consume<T, 1>(v1, st);
