@@ -183,8 +183,10 @@ int tba_tb_loss_pipelined(const tba_rows* x, const tba_tb_opts* opts, const doub
  *   grad_unscaled[s,t,v] = mu_{s,t} * inv_temp * (1[v = y] - softmax(inv_temp z)_v)
  * so that dL/dz = grad_scale * g * resid_s * grad_unscaled with grad_scale = 2 / n_seq_global.
  * The consumer (the LM-head backward) applies that per-sequence factor as a row scale. Each
- * valid row is read from HBM once and re-read from L2 (one CTA per SM keeps ~148 rows in
- * flight): 4V HBM bytes per token instead of 6V. grad_unscaled must not alias logits. */
+ * valid row is read from HBM once and re-read on chip: one CTA per row, two per SM, the row's
+ * first 96 KB kept in shared memory and the rest re-read from L2 (rows <= 128 KB: four CTAs per
+ * SM, all from L2): 4V HBM bytes per token instead of 6V, plus the re-reads that miss L2
+ * (DESIGN.md §5.4). grad_unscaled must not overlap logits at all (TBA_ERR_INVALID_ARG). */
 int tba_tb_loss_fwd_deferred(const tba_rows* x, const tba_tb_opts* opts, const double* ref_logp,
                              const double* log_reward, double beta, int32_t K, double n_seq_global,
                              void* workspace, double* seq_logp, int32_t* n_tokens, double* log_z,
