@@ -279,3 +279,32 @@ def test_variants_full_size_temperature_and_learned_log_z():
     n, ma, mr = H.compare_dlogits_rows(d, w, seed, rows, 0, ref["tokens"].reshape(-1), np.repeat(eps, w.T), w.N,
                                        what=f"{test} dlogits", inv_temp=a)
     H.record(test, w.name, seed, "dlogits (group 3 whole + 4096 random rows)", n, ma, mr, tol="1 bf16 ulp")
+
+
+@pytest.mark.parametrize("name,seed,groups", [("qwen_shard", 1, [0, 5]), ("rhomath", 1, [3, 30]),
+                                              ("pythia_fp32", 0, [0, 63])])
+def test_deferred_full_size(name, seed, groups):
+    """The deferred-scale pass (NEXT 2 (ii)) at full size in the bench's launch configuration: every
+    per-sequence value against the oracle, and G = inv_temp (onehot - softmax) — the oracle's
+    dlogits_row at c = 1 — on 4096 seeded random valid rows plus every row of two whole groups
+    (bf16 G within 1 bf16 ulp, fp32 G within 2e-6; App. A)."""
+    w = syn.WORKLOADS[name]
+    test = f"deferred_{name}"
+    inp = H.device_inputs(w, seed)
+    gdt = torch.float32 if w.dtype == "fp32" else torch.bfloat16
+    o, _, G = tba.vargrad_fwd_deferred(inp["logits"], inp["tokens"], inp["mask"], inp["ref_logp"],
+                                       inp["log_reward"], w.beta, w.K, float(w.N), g_dtype=gdt, check_status=True)
+    torch.cuda.synchronize()
+    ref = check_seq_values(test, w, seed, o, 0, w.B, w.N)
+    mask_flat = ref["mask"].reshape(-1)
+    rows = _row_plan(w, seed, mask_flat, groups, 4096)
+    unit = np.full(w.N * w.T, w.N / 2.0)  # eps = N/2 makes the oracle's c = 2 eps / N = 1: dlogits_row = G
+    n, ma, mr = H.compare_dlogits_rows(G, w, seed, rows, 0, ref["tokens"].reshape(-1), unit, w.N,
+                                       what=f"{test} G, groups {groups} whole + 4096 random rows")
+    H.record(test, w.name, seed, f"G (groups {groups} whole + 4096 random rows)", n, ma, mr,
+             tol="1 bf16 ulp" if gdt == torch.bfloat16 else "2e-6")
+    masked = np.flatnonzero(mask_flat == 0)
+    flat = G.view(-1, w.V)
+    for i in range(0, len(masked), 4096):                                     # every masked row is +0
+        idx = torch.from_numpy(masked[i:i + 4096]).to(G.device)
+        assert torch.count_nonzero(flat.index_select(0, idx)).item() == 0
