@@ -94,6 +94,25 @@ def main(tag):
             lines.append(f"| {k} | {r / 1e9:.3f} | {w / 1e9:.3f} | {t / 1e3:.1f} | {(r + w) / t:.0f} |")
             traffic[k] = r + w
         lines.append("")
+    ddp = os.path.join(G, f"dram_deferred_{tag}.csv")
+    if os.path.exists(ddp):  # the deferred-scale pass on the full shard (4V algorithmic bytes per valid row)
+        D = read_metric_csv(ddp)
+        agg = {}
+        for d in D:
+            agg.setdefault(d["ID"], {})[d["Metric Name"]] = float(d["Metric Value"])
+        alg = 65536 * 152064 * 2 * 2
+        lines += ["## Deferred-scale pass `row_single1`, full Qwen shard (DRAM bytes per launch)", "",
+                  "| launch | read GB | write GB | time µs | algorithmic 4V GB | algorithmic GB/s | DRAM GB/s |",
+                  "|---|---|---|---|---|---|---|"]
+        tot = []
+        for k, m in agg.items():
+            r, w, t = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"], m["gpu__time_duration.sum"]
+            lines.append(f"| {k} | {r / 1e9:.2f} | {w / 1e9:.2f} | {t / 1e3:.0f} | {alg / 1e9:.2f} | {alg / t:.0f} | "
+                         f"{(r + w) / t:.0f} |")
+            tot.append(r + w)
+        traffic["row_single"] = statistics.mean(tot)
+        lines += ["", "Unique logits are 19.93 GB; reads above that are pass-2 re-reads that missed L2. ncu launches "
+                  "are cold and alone; the bench's back-to-back steps run under the board power cap (DESIGN.md §5.4).", ""]
     lmp = os.path.join(G, f"lmhead_launches_{tag}.csv")
     if os.path.exists(lmp):
         M = read_metric_csv(lmp)
