@@ -103,25 +103,13 @@ __global__ void __launch_bounds__(256) tb_fused(FusedArgs a) {
         const int64_t s0 = (int64_t)g * a.K;
         seq_sums(a.lp, a.mask, a.n_seq, a.T, s0, a.K, a.seq_logp, a.n_tokens, nullptr);
         __syncthreads();
+        if (threadIdx.x < 32) {  // warp 0: the group head, as seq_head
+          tb_group_head((int64_t)g, a.K, a.ref_logp, a.log_reward, a.log_z_param, a.inv_beta, a.seq_logp, a.log_z,
+                        a.resid, a.group_sq, (int)threadIdx.x);
+          __threadfence();
+          __syncwarp();
+        }
         if (threadIdx.x == 0) {
-          double lz;
-          if (a.log_z_param) {
-            lz = a.log_z_param[g];
-          } else {
-            double sum = 0.0;
-            for (int q = 0; q < a.K; ++q)
-              sum += a.ref_logp[s0 + q] - __ldcg(a.seq_logp + s0 + q) + a.log_reward[s0 + q] * a.inv_beta;
-            lz = sum / (double)a.K;
-          }
-          double sq = 0.0;
-          for (int q = 0; q < a.K; ++q) {
-            const double delta = a.ref_logp[s0 + q] - __ldcg(a.seq_logp + s0 + q) + a.log_reward[s0 + q] * a.inv_beta;
-            const double e = lz - delta;
-            a.resid[s0 + q] = e;
-            sq += e * e;
-          }
-          a.log_z[g] = lz;
-          a.group_sq[g] = sq;
           __threadfence();
           st_release(&a.ready[g], 1u);
           if (atomicAdd(a.groups_done, 1u) == (unsigned)a.groups - 1) {

@@ -25,13 +25,15 @@ __global__ void __launch_bounds__(1024) seq_head(const double* __restrict__ lp, 
   if (!HEAD) return;
   __syncthreads();
   __shared__ bool am_last;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: the group head
     tb_group_head((int64_t)blockIdx.x, K, ref_logp, log_reward, log_z_param, inv_beta, seq_logp, log_z, resid,
-                  group_sq);
-    am_last = false;
-    if (counter) {  // counter == NULL: a chunk of a larger batch; tb_finish_kernel reduces later
-      __threadfence();
-      am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+                  group_sq, (int)threadIdx.x);
+    __threadfence();  // every lane's residuals before the counter moves
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      am_last = false;
+      if (counter)  // counter == NULL: a chunk of a larger batch; tb_finish_kernel reduces later
+        am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
     }
   }
   __syncthreads();

@@ -463,7 +463,7 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
     // t order: bitwise the plain one-position loop (the tail), without one load latency per
     // position. (Predicating the tail into the same batches measured slower: 13.9-15.0 vs 12.3-12.9 us.)
     // (lp is read L2-coherent: it may have been written by other CTAs of this grid)
-    for (; t + 32 * 7 < T; t += 32 * 8) {
+    for (; t + 32 * (7) < T; t += 32 * 8) {
       uint8_t mk[8];
       double v[8];
 #pragma unroll
@@ -498,47 +498,42 @@ __device__ __forceinline__ void seq_sums(const double* __restrict__ lp, const ui
   if (my_count) *my_count = tot;
 }
 
-// Eq. 4 (or the learned log Z of Eq. 3) and the Eq. 5 residuals of group g, by one thread.
+// Eq. 4 (or the learned log Z of Eq. 3) and the Eq. 5 residuals of group g, by one whole warp: lane l
+// takes sequences l, l+32, ... (partial sums in j order), then a fixed xor butterfly — every lane ends
+// with the same log Z (fp64 addition is commutative, so both partners of a butterfly step compute the
+// same sum); every schedule (two-call, pipelined, fused, deferred, LM-head) forms the head here.
 __device__ __forceinline__ void tb_group_head(int64_t g, int K, const double* __restrict__ ref_logp,
                                               const double* __restrict__ log_reward,
                                               const double* __restrict__ log_z_param, double inv_beta,
                                               const double* seq_logp, double* __restrict__ log_z,
-                                              double* __restrict__ resid, double* __restrict__ group_sq) {
+                                              double* __restrict__ resid, double* __restrict__ group_sq,
+                                              int lane) {
   const int64_t s0 = g * K;
-  // delta_j for 8 sequences at a time (loads in flight together); sums in j order as before
-  auto delta8 = [&](int j0, double (&d)[8]) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (j0 + u < K) d[u] = ref_logp[s0 + j0 + u] - __ldcg(seq_logp + s0 + j0 + u) + log_reward[s0 + j0 + u] * inv_beta;
+  auto delta = [&](int j) {
+    return ref_logp[s0 + j] - __ldcg(seq_logp + s0 + j) + log_reward[s0 + j] * inv_beta;
   };
   double lz;
   if (log_z_param) {
     lz = log_z_param[g];
   } else {
-    double sum = 0.0;
-    for (int j0 = 0; j0 < K; j0 += 8) {
-      double d[8];
-      delta8(j0, d);
+    double part = 0.0;
+    for (int j = lane; j < K; j += 32) part += delta(j);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j0 + u < K) sum += d[u];
-    }
-    lz = sum / (double)K;
+    for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    lz = part / (double)K;
   }
   double sq = 0.0;
-  for (int j0 = 0; j0 < K; j0 += 8) {
-    double d[8];
-    delta8(j0, d);
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (j0 + u < K) {
-        const double e = lz - d[u];
-        resid[s0 + j0 + u] = e;
-        sq += e * e;
-      }
+  for (int j = lane; j < K; j += 32) {
+    const double e = lz - delta(j);
+    resid[s0 + j] = e;
+    sq += e * e;
   }
-  log_z[g] = lz;
-  group_sq[g] = sq;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0) {
+    log_z[g] = lz;
+    group_sq[g] = sq;
+  }
 }
 
 // Final fixed-order reduction of the per-group sums of squares.
