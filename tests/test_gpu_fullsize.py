@@ -143,10 +143,10 @@ def test_large_all_sequences_plus_rows(name, seed, groups):
 
 
 @pytest.mark.parametrize("name,seed", [("pythia", 1), ("pythia", 2), ("redteam", 0), ("redteam", 2),
-                                       ("rhomath", 0), ("rhomath", 1)])
+                                       ("rhomath", 0), ("rhomath", 1), ("qwen_shard", 1), ("qwen_shard", 2)])
 def test_parity_seeds_sequence_values(name, seed):
     """Parity seeds {0, 1, 2}: every per-sequence value and the loss, plus 512
-    random dlogits rows, on the other seeds of the smaller configs."""
+    random dlogits rows, on the other seeds (the Qwen shard's seed 0 is test_large_all_sequences_plus_rows)."""
     w = syn.WORKLOADS[name]
     test = f"seeds_{name}"
     inp, o, d = run_full(w, seed)
